@@ -1,0 +1,319 @@
+"""Benchmark: BASELINE.json's metric on its configuration 2 (bit-depth sweep).
+
+One step = the hot path (quantise -> exact full-lag integer cross-correlation
+-> argmax) over the whole C2 batch at every bit depth: 64 float32 pairs of
+2^18 samples at b = 1, 2, 4, 8, i.e. 256 lag estimates.  Inputs are seeded
+synthetic data with BASELINE's shapes and statistics (workloads.c2); they are
+resident in HBM before timing (`value`) or copied from pinned host memory
+inside the timed region through the C ABI's host entry point (`e2e`).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun every rank processes its own 64-pair batch (weak scaling; the
+pairs are independent, so there is no data-path collective); the timed region
+is bracketed by a barrier + synchronize and the max over ranks is reported.
+`--impl reference` times the reference algorithm's CPU implementation (the C
+oracle: float64 quantise, Kronecker substitution with GMP, argmax; all host
+threads) on a bounded sample of the same workload; rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lag estimates/sec (quantize+int xcorr+argmax)"
+UNIT = "estimates/s"
+BITS = (1, 2, 4, 8)
+L2_BYTES = 126 * (1 << 20)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pairs", type=int, default=64)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def config_desc(pairs, world):
+    from paper_2509_19974_b200 import workloads as W
+
+    return {"workload": "BASELINE config 2: bit-depth sweep", "pairs_per_gpu": pairs, "n": W.C2_N,
+            "bits": list(BITS), "lags": "full -(N-1)..(N-1)", "dtype_in": "float32",
+            "quantizers": "b=1 sign(); b>=2 uniform(2^(b-1)-1, 6*sigma/2^b)",
+            "estimates_per_step": pairs * len(BITS) * world,
+            "l2": "flushed between timed steps (512 MiB write), per-step CUDA events",
+            "parallelism": f"pairs x{world} ranks (weak)"}
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons while the timed region runs."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self.stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # noqa: BLE001
+            self.nv = None
+            self.err = str(exc)
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- CPU (oracle)
+def cpu_arm(pairs_sample, threads, xs, ys):
+    """Reference algorithm on the host: the C oracle (quantise in float64,
+    Kronecker substitution + GMP multiply, argmax) for every bit depth on
+    `pairs_sample` pairs, threaded over pairs.  Returns (estimates/s, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    from paper_2509_19974_b200 import workloads as W
+
+    O.build()
+    t0 = time.perf_counter()
+    n_est = 0
+    for b in BITS:
+        q = W.bit_quantizer(b, W.C2_SIGMA)
+        rec = O.estimate_batch_f32(xs[:pairs_sample], ys[:pairs_sample], q, q, threads=threads)
+        n_est += len(rec)
+    dt = time.perf_counter() - t0
+    return n_est / dt, dt
+
+
+def reference_arm(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return
+    from paper_2509_19974_b200 import workloads as W
+
+    threads = os.cpu_count() or 1
+    sample = max(1, min(args.pairs, 2 * threads))
+    xs, ys, lag = W.c2(pairs=sample)
+    times = []
+    for i in range(args.warmup + args.steps):
+        rate, dt = cpu_arm(sample, threads, xs, ys)
+        if i >= args.warmup:
+            times.append(dt)
+    per_step = sum(times) / len(times)
+    value = sample * len(BITS) / per_step
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_step * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded, BASELINE config 2 shapes)",
+            "config": config_desc(sample, 1) | {"sample": f"{sample} pairs x 4 bit depths per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{sample} pairs x {len(BITS)} bit depths of config 2 per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return reference_arm(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_19974_b200 as P
+    from paper_2509_19974_b200 import _native, workloads as W
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    pairs = args.pairs
+    xs, ys, lag = W.c2(pairs=pairs, first=rank * pairs)
+    xd = torch.from_numpy(xs).to(dev)
+    yd = torch.from_numpy(ys).to(dev)
+    qs = [W.bit_quantizer(b, W.C2_SIGMA) for b in BITS]
+    outs = [torch.empty((pairs, 8), dtype=torch.int64, device=dev) for _ in BITS]
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        for q, o in zip(qs, outs):
+            P.estimate_batch(xd, yd, q, q, out=o)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # correctness of the benchmarked work: every pair finds its delay
+    for o in outs:
+        got = o[:, 1].cpu().numpy()
+        assert np.array_equal(got, lag), "benchmark results disagree with the planted delays"
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk, _native.profile(timed=True) as prof:
+        for a, b in evs:
+            flush.zero_()
+            a.record()
+            step()
+            b.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(total_ms.item())
+    est_per_step = pairs * len(BITS) * world
+    value = est_per_step * args.steps / (total_ms / 1e3)
+    samples_per_step = est_per_step * 2 * W.C2_N
+    ms_per_step = total_ms / args.steps
+
+    # dominant kernel and its roofline (live event timing of every launch)
+    P2 = 1 << 19
+    n_pairs_total = pairs * len(BITS) * args.steps
+    alg_bytes = {  # compulsory bytes per kind over the timed region (prime 0)
+        "ntt_pass1": n_pairs_total * (2 * W.C2_N * 4 + 2 * P2 * 4),
+        "ntt_pass2": n_pairs_total * (3 * P2 * 4),
+        "ntt_pass3": n_pairs_total * (P2 * 4),
+    }
+    bflies = {"ntt_pass1": n_pairs_total * 2 * (P2 // 2) * 10, "ntt_pass2": n_pairs_total * 3 * (P2 // 2) * 9,
+              "ntt_pass3": n_pairs_total * (P2 // 2) * 10}
+    kinds = prof.result
+    dom = max(kinds, key=lambda k: kinds[k][1])
+    dom_ms = kinds[dom][1]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg_bytes.get(dom, 0) / (dom_ms / 1e3) / 1e9 if dom_ms else None
+    traffic = None
+    ncu_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(ncu_path):
+        traffic = json.load(open(ncu_path)).get("kernels", {}).get(dom, {}).get("dram_bytes_per_launch")
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+            "frac": (achieved / hbm_peak) if achieved else None, "traffic": traffic,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s",
+            "kernel_ms_share": dom_ms / total_ms if total_ms else None}
+    int_peak_path = os.path.join(ROOT, "profiles", "int_peaks.json")
+    int_roof = {"kernel": dom, "butterflies_per_s": bflies.get(dom, 0) / (dom_ms / 1e3) if dom_ms else None}
+    if os.path.exists(int_peak_path):
+        ip = json.load(open(int_peak_path))
+        if ip.get("butterflies_per_s"):
+            int_roof["peak"] = ip["butterflies_per_s"]
+            int_roof["frac"] = int_roof["butterflies_per_s"] / ip["butterflies_per_s"]
+    all_bfly = sum(bflies.values())
+    ntt_ms = sum(kinds[k][1] for k in bflies if k in kinds)
+    int_roof["all_ntt_butterflies_per_s"] = all_bfly / (ntt_ms / 1e3) if ntt_ms else None
+    if "peak" in int_roof and int_roof["all_ntt_butterflies_per_s"]:
+        int_roof["all_ntt_frac"] = int_roof["all_ntt_butterflies_per_s"] / int_roof["peak"]
+
+    # e2e through the C ABI host entry point (pinned host buffers, H2D+D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        hx = torch.from_numpy(xs).pin_memory()
+        hy = torch.from_numpy(ys).pin_memory()
+        hxn, hyn = hx.numpy(), hy.numpy()
+        n_e2e = max(3, args.steps // 3)
+        for q in qs:
+            P.estimate_batch_host(hxn, hyn, q, q, device=local)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            for q in qs:
+                res = P.estimate_batch_host(hxn, hyn, q, q, device=local)
+        t1 = time.perf_counter()
+        e2e_s = torch.tensor([t1 - t0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        assert np.array_equal(res["lag"], lag)
+        e2e = {"value": est_per_step * n_e2e / float(e2e_s.item()), "unit": UNIT,
+               "h2d_bytes_per_step": int(len(BITS) * (xs.nbytes + ys.nbytes)),
+               "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e,
+               "path": "qx_estimate_batch_host (C ABI, host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        sample = min(pairs, max(8, threads))
+        rate, dt = cpu_arm(sample, threads, xs, ys)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{sample} pairs x {len(BITS)} bit depths of config 2 ({dt:.1f} s): "
+                         "C oracle = reference algorithm (float64 quantise, KS + GMP mpn_mul, argmax)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32 mod-p NTT (exact int64 results)",
+                "data": "synthetic (seeded numpy, BASELINE config 2 shapes/SNR); inputs resident in HBM",
+                "config": config_desc(pairs, world),
+                "gsamples_per_s": samples_per_step * args.steps / (total_ms / 1e3) / 1e9,
+                "gpu_launches": prof.launches, "kernels": {k: {"launches": c, "ms": m} for k, (c, m) in kinds.items()},
+                "roofline": roof, "int_roofline": int_roof, "clocks": clk.summary(), "e2e": e2e,
+                "cpu_baseline": cpu, "step_ms_median": statistics.median(step_ms)}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,158 @@
+/*
+ * qxcorr_b200.h -- C ABI of the B200-native quantise -> integer
+ * cross-correlation -> argmax engine (libqxcorr_b200.so).
+ *
+ * Plain C types only (no torch, no C++): a ctypes / cffi / cgo / JNI binding
+ * can bind every symbol directly.  The entry points replace the reference
+ * `qxcorr` hot path (/root/reference/pkg/src/qxcorr):
+ *
+ *   qx_quantize              <- quantize.apply / Quantizer.__call__
+ *                               (quantize.py:53-65, 105-107)
+ *   qx_quantizer_thresholds  <- the same map, as an exact threshold table
+ *                               (quantize.py:53-65)
+ *   qx_xcorr_full            <- xcorr_int_bf / xcorr_int_ks
+ *                               (intxcorr.py:96-100, 259-265): the full
+ *                               correlogram, bit-identical int64 values
+ *   qx_estimate_batch        <- estimate() lines 1-5 + argmax_set summary
+ *                               (estimator.py:60-94, 50-57), batched, with an
+ *                               optional lag window (new; parity = the full
+ *                               reference correlogram sliced to the window)
+ *   qx_estimate_batch_host   <- the same from host buffers (H2D/D2H inside)
+ *
+ * Conventions
+ *   - Device pointers are caller-owned; `stream` is a cudaStream_t (NULL =
+ *     legacy default stream).  Calls only enqueue work, except the *_host
+ *     variants which synchronise.
+ *   - Correlation index t in [0, n_x + n_y - 1) holds lag
+ *     first_lag + t with first_lag = y.start - (x.start + n_x - 1)
+ *     (signals.py:100-105, intxcorr.py:85-86); value(t) =
+ *     sum_m u[m] * v[m + lag] on the quantised codes u = q_x(x), v = q_y(y).
+ *   - Errors map 1:1 onto the reference's exceptions (see qx_status).
+ */
+#ifndef QXCORR_B200_H
+#define QXCORR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QX_ABI_VERSION 1
+
+typedef enum qx_status {
+    QX_OK = 0,
+    QX_ERR_INVALID = 1,              /* ValueError: bad argument */
+    QX_DEGENERATE_QUANTIZATION = 2,  /* errors.DegenerateQuantization (estimator.py:83-86) */
+    QX_DEGENERATE_INPUT = 3,         /* errors.DegenerateInput (intxcorr.py:109-110) */
+    QX_BOUND_EXCEEDED = 4,           /* ValueError, N_min*K_u*K_v > 2^59 (intxcorr.py:89-93) */
+    QX_INTERNAL_OVERFLOW = 5,        /* errors.InternalOverflow (intxcorr.py:140-141, 254-255) */
+    QX_ERR_CUDA = 6,                 /* RuntimeError: CUDA failure */
+    QX_ERR_UNSUPPORTED = 7,          /* shape/parameter outside this build's kernels */
+    QX_ERR_NOMEM = 8,
+    QX_ERR_NONFINITE = 9             /* NaN input (reference behaviour undefined) */
+} qx_status;
+
+typedef enum qx_dtype { QX_F32 = 0, QX_F64 = 1, QX_I64 = 2 } qx_dtype;
+
+typedef enum qx_qkind {
+    QX_Q_SIGN = 0,     /* quantize.sign()            (quantize.py:76-78) */
+    QX_Q_UNIFORM = 1,  /* quantize.uniform(k, step)  (quantize.py:81-82) */
+    QX_Q_CUSTOM = 2,   /* quantize.custom(thresholds)(quantize.py:85-89) */
+    QX_Q_CODES = 3     /* input is already integer codes, |c| <= k (IntSignal) */
+} qx_qkind;
+
+typedef struct qx_quantizer {
+    int32_t kind;              /* qx_qkind */
+    int32_t reserved;
+    int64_t k;                 /* level bound K (>= 1) */
+    double step;               /* uniform step (> 0) */
+    const double *thresholds;  /* custom: 2k strictly increasing, host memory */
+} qx_quantizer;
+
+typedef struct qx_signals {
+    const void *data;  /* batch rows; row b starts at element b*ld */
+    int32_t dtype;     /* qx_dtype */
+    int32_t reserved;
+    int64_t n;         /* samples per row (>= 1) */
+    int64_t ld;        /* row stride in elements (>= n) */
+    int64_t start;     /* Signal.start of every row */
+} qx_signals;
+
+typedef enum qx_path { QX_PATH_AUTO = 0, QX_PATH_NTT = 1, QX_PATH_DIRECT = 2 } qx_path;
+
+/* per-pair flags in qx_result.flags */
+#define QX_RF_DEGENERATE_X 1 /* x quantizes to all zeros */
+#define QX_RF_DEGENERATE_Y 2
+#define QX_RF_NONFINITE 4    /* NaN seen in x or y */
+#define QX_RF_CODE_RANGE 8   /* integer codes outside [-k, k] */
+
+typedef struct qx_result {
+    int64_t value;   /* peak integer correlation (EstimationResult.peak_value_int) */
+    int64_t lag;     /* smallest lag attaining it (argmax_set()[0]) */
+    int64_t ties;    /* number of lags attaining it (len(argmax_set)) */
+    int64_t sumsq_x; /* sum of squared codes of x: l2_norm(u)**2 */
+    int64_t sumsq_y;
+    int64_t nnz_x;   /* nonzero codes in x */
+    int64_t nnz_y;
+    int32_t flags;   /* QX_RF_* */
+    int32_t status;  /* qx_status for this pair */
+} qx_result;
+
+typedef struct qx_context qx_context;
+
+qx_status qx_context_create(int device, qx_context **out);
+void qx_context_destroy(qx_context *ctx);
+const char *qx_status_string(qx_status s);
+const char *qx_context_last_error(const qx_context *ctx);
+int qx_abi_version(void);
+
+/* Exact threshold table of a quantiser for inputs of `dtype` (F32/F64):
+ * out[i], i < 2k, is the smallest value of that type whose level is
+ * >= i - k + 1, so level(v) = -k + #{i : v >= out[i]}.  out is 2k doubles
+ * (float32 tables hold exactly representable floats). Host only. */
+qx_status qx_quantizer_thresholds(const qx_quantizer *q, qx_dtype dtype, double *out);
+
+/* codes[b*n + i] = q(x[b*ld + i]) as int64 (quantize.apply), plus per-row
+ * sum of squares and nonzero counts (sumsq/nnz may be NULL). Device pointers. */
+qx_status qx_quantize(qx_context *ctx, const qx_quantizer *q, const qx_signals *x, int64_t batch,
+                      int64_t *codes, int64_t *sumsq, int64_t *nnz, void *stream);
+
+/* Full correlograms values[b*(nx+ny-1) + t] of q_x(x_b) against q_y(y_b).
+ * stats (optional, device) receives sumsq/nnz/flags per pair. */
+qx_status qx_xcorr_full(qx_context *ctx, const qx_signals *x, const qx_signals *y, int64_t batch,
+                        const qx_quantizer *qx, const qx_quantizer *qy, int64_t *values,
+                        qx_result *stats, qx_path path, void *stream);
+
+/* Peak summary per pair over lags [lag_lo, lag_hi] (clipped to the full
+ * range; INT64_MIN/INT64_MAX = all lags).  results: device, batch entries. */
+qx_status qx_estimate_batch(qx_context *ctx, const qx_signals *x, const qx_signals *y,
+                            int64_t batch, const qx_quantizer *qx, const qx_quantizer *qy,
+                            int64_t lag_lo, int64_t lag_hi, qx_path path, qx_result *results,
+                            void *stream);
+
+/* As qx_estimate_batch, but x/y data and results are HOST pointers; the
+ * library stages the inputs to the device, runs, copies results back and
+ * synchronises.  Returns the first per-pair error status if any. */
+qx_status qx_estimate_batch_host(qx_context *ctx, const qx_signals *x, const qx_signals *y,
+                                 int64_t batch, const qx_quantizer *qx, const qx_quantizer *qy,
+                                 int64_t lag_lo, int64_t lag_hi, qx_path path, qx_result *results);
+
+/* Launch accounting for measurement (bench.py): between begin and end every
+ * kernel the library launches is counted per kind and, when `timed`, bracketed
+ * by CUDA events on its own stream.  qx_profile_end synchronises and returns
+ * summed device milliseconds per kind (names via qx_profile_kind_name). */
+#define QX_PROFILE_KINDS 8
+typedef struct qx_profile {
+    int64_t launches;
+    int64_t count[QX_PROFILE_KINDS];
+    double ms[QX_PROFILE_KINDS];
+} qx_profile;
+qx_status qx_profile_begin(qx_context *ctx, int timed);
+qx_status qx_profile_end(qx_context *ctx, qx_profile *out);
+const char *qx_profile_kind_name(int kind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QXCORR_B200_H */

@@ -1,0 +1,42 @@
+"""B200-native quantise -> exact integer cross-correlation -> argmax engine.
+
+A drop-in for the hot path of the reference package ``qxcorr``
+(arxiv 2509.19974; /root/reference/pkg/src/qxcorr): the same function names,
+argument meanings and exceptions, with the arithmetic in hand-written sm_100a
+kernels behind the C ABI include/qxcorr_b200.h (libqxcorr_b200.so).
+
+    from paper_2509_19974_b200 import Signal, sign, estimate
+    r = estimate(Signal(0, x), Signal(0, y), sign(), sign())
+
+Batched and windowed entry points (new): ``estimate_batch``,
+``estimate_batch_host``.
+"""
+
+from .batch import BatchResult, check_results, estimate_batch, estimate_batch_host
+from .errors import (
+    BadLength,
+    ConfigError,
+    DegenerateInput,
+    DegenerateQuantization,
+    InternalOverflow,
+    ParseError,
+    QxcorrError,
+    UnsupportedFormat,
+)
+from .estimator import EstimationResult, argmax_set, estimate
+from .intxcorr import xcorr_int_bf, xcorr_int_gpu, xcorr_int_ks
+from .quantize import Quantizer, apply, custom, from_spec, sign, uniform
+from .realxcorr import xcorr_real_at
+from .signals import Correlogram, IntSignal, Signal, l2_norm, reverse, shift
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "QxcorrError", "DegenerateInput", "DegenerateQuantization", "InternalOverflow", "BadLength",
+    "ParseError", "UnsupportedFormat", "ConfigError",
+    "Signal", "IntSignal", "Correlogram", "reverse", "shift", "l2_norm",
+    "Quantizer", "sign", "uniform", "custom", "from_spec", "apply",
+    "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at",
+    "EstimationResult", "argmax_set", "estimate",
+    "BatchResult", "estimate_batch", "estimate_batch_host", "check_results",
+]

@@ -1,0 +1,61 @@
+"""Device plumbing: torch supplies CUDA memory and the current stream; the
+kernels themselves live in libqxcorr_b200.so (see _native.py)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+
+def torch():
+    import torch as _t
+
+    if not _t.cuda.is_available():
+        raise RuntimeError("paper_2509_19974_b200 needs a CUDA device (no CPU fallback)")
+    return _t
+
+
+def as_device(a, dtype=None):
+    """numpy array / torch tensor -> contiguous CUDA tensor (no copy if already one)."""
+    t = torch()
+    if isinstance(a, t.Tensor):
+        x = a
+        if dtype is not None and x.dtype != dtype:
+            x = x.to(dtype)
+        if not x.is_cuda:
+            x = x.to("cuda", non_blocking=False)
+        return x.contiguous()
+    arr = np.ascontiguousarray(a)
+    x = t.from_numpy(arr)
+    if dtype is not None and x.dtype != dtype:
+        x = x.to(dtype)
+    return x.to("cuda").contiguous()
+
+
+def stream_handle() -> int:
+    return torch().cuda.current_stream().cuda_stream
+
+
+DTYPE_CODE = {"float32": N.QX_F32, "float64": N.QX_F64, "int64": N.QX_I64}
+
+
+def dtype_code(x) -> int:
+    name = str(x.dtype).replace("torch.", "")
+    try:
+        return DTYPE_CODE[name]
+    except KeyError:
+        raise ValueError(f"unsupported sample dtype {x.dtype} (float32, float64 or int64)") from None
+
+
+def signals(x, start: int = 0) -> N.QxSignals:
+    """QxSignals descriptor of a CUDA tensor shaped (n,) or (batch, n)."""
+    if x.dim() == 1:
+        n, ld = x.shape[0], x.shape[0]
+    elif x.dim() == 2:
+        n, ld = x.shape[1], x.stride(0)
+        if x.stride(1) != 1:
+            raise ValueError("rows must be contiguous")
+    else:
+        raise ValueError("signals must be 1-D or (batch, n)")
+    return N.QxSignals(x.data_ptr(), dtype_code(x), 0, int(n), int(ld), int(start))

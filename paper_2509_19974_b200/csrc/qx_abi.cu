@@ -1,0 +1,521 @@
+// qx_abi.cu -- the C ABI (include/qxcorr_b200.h): argument validation with the
+// reference's error semantics, quantiser tables, transform-plan cache,
+// per-context scratch, and dispatch to the kernels.
+#include <climits>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/qxcorr_b200.h"
+#include "qx_internal.h"
+
+namespace qx {
+int thresholds(int kind, long long k, double step, const double* thr, int dtype, double* out);
+cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
+                            int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s);
+cudaError_t stats_to_results(const unsigned long long* stats, void* results, int64_t batch, cudaStream_t s);
+}  // namespace qx
+
+using namespace qx;
+
+// NTT primes p < 2^30 (lazy [0,4p) arithmetic) with their 2-adicity and a
+// primitive root, largest first.
+struct PrimeInfo {
+    uint32_t p, g;
+    int adicity;
+};
+static const PrimeInfo kPrimes[] = {
+    {1012924417u, 5, 21}, {1004535809u, 3, 21}, {998244353u, 3, 23},
+    {985661441u, 3, 22},  {469762049u, 3, 26},  {167772161u, 3, 25},
+};
+
+struct Arena {
+    void* ptr = nullptr;
+    size_t size = 0;
+};
+
+struct qx_context {
+    int device = 0;
+    std::recursive_mutex mu;
+    std::map<std::pair<uint32_t, int>, std::pair<NttTables, void*>> tables;
+    std::map<std::string, std::vector<double>> thr_cache;
+    Arena scratch;     // Y/R/stats/partials
+    Arena counters;    // zero-initialised ints, reset by the kernels
+    Arena stage;       // host-API staging (x, y, results)
+    cudaStream_t host_stream = nullptr;
+    Profiler prof;
+    std::string last_error;
+};
+
+static qx_status fail(qx_context* ctx, qx_status s, const std::string& msg)
+{
+    if (ctx) ctx->last_error = msg;
+    return s;
+}
+
+static qx_status cuda_fail(qx_context* ctx, cudaError_t e, const char* where)
+{
+    return fail(ctx, QX_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+static cudaError_t arena_reserve(Arena& a, size_t bytes, bool zero)
+{
+    if (a.size >= bytes) return cudaSuccess;
+    if (a.ptr) {
+        cudaError_t e = cudaFree(a.ptr);  // synchronising: prior users are done
+        if (e != cudaSuccess) return e;
+        a.ptr = nullptr;
+        a.size = 0;
+    }
+    size_t want = bytes + bytes / 4;
+    cudaError_t e = cudaMalloc(&a.ptr, want);
+    if (e != cudaSuccess) return e;
+    a.size = want;
+    if (zero) return cudaMemset(a.ptr, 0, want);
+    return cudaSuccess;
+}
+
+extern "C" {
+
+int qx_abi_version(void) { return QX_ABI_VERSION; }
+
+const char* qx_status_string(qx_status s)
+{
+    switch (s) {
+    case QX_OK: return "ok";
+    case QX_ERR_INVALID: return "invalid argument";
+    case QX_DEGENERATE_QUANTIZATION: return "quantizes to all zeros";
+    case QX_DEGENERATE_INPUT: return "all-zero input";
+    case QX_BOUND_EXCEEDED: return "coefficient bound N_min*K_u*K_v exceeds the supported int64 range";
+    case QX_INTERNAL_OVERFLOW: return "internal overflow";
+    case QX_ERR_CUDA: return "CUDA error";
+    case QX_ERR_UNSUPPORTED: return "unsupported shape or parameter";
+    case QX_ERR_NOMEM: return "out of memory";
+    case QX_ERR_NONFINITE: return "NaN input";
+    }
+    return "unknown status";
+}
+
+qx_status qx_context_create(int device, qx_context** out)
+{
+    if (!out) return QX_ERR_INVALID;
+    *out = nullptr;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return QX_ERR_CUDA;
+    qx_context* c = new qx_context();
+    c->device = device;
+    e = cudaStreamCreateWithFlags(&c->host_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return QX_ERR_CUDA;
+    }
+    *out = c;
+    return QX_OK;
+}
+
+void qx_context_destroy(qx_context* c)
+{
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->tables) cudaFree(kv.second.second);
+    for (Arena* a : {&c->scratch, &c->counters, &c->stage})
+        if (a->ptr) cudaFree(a->ptr);
+    if (c->host_stream) cudaStreamDestroy(c->host_stream);
+    delete c;
+}
+
+const char* qx_context_last_error(const qx_context* c) { return c ? c->last_error.c_str() : ""; }
+
+}  // extern "C"
+
+// ------------------------------------------------------------ validation
+
+// Quantizer.__post_init__ (quantize.py:37-51) semantics
+static qx_status check_quantizer(qx_context* ctx, const qx_quantizer* q, int dtype)
+{
+    if (!q) return fail(ctx, QX_ERR_INVALID, "quantizer is NULL");
+    if (q->kind == QX_Q_CODES) {
+        if (dtype != QX_I64) return fail(ctx, QX_ERR_INVALID, "integer codes require dtype int64");
+        if (q->k < 0) return fail(ctx, QX_ERR_INVALID, "bound must be >= 0");
+        return QX_OK;
+    }
+    if (dtype != QX_F32 && dtype != QX_F64)
+        return fail(ctx, QX_ERR_INVALID, "quantised inputs must be float32 or float64");
+    if (q->k < 1) return fail(ctx, QX_ERR_INVALID, "level bound k must be >= 1");
+    if (q->kind == QX_Q_SIGN) {
+        if (q->k != 1) return fail(ctx, QX_ERR_INVALID, "sign quantizer has k == 1");
+    } else if (q->kind == QX_Q_UNIFORM) {
+        if (!(q->step > 0)) return fail(ctx, QX_ERR_INVALID, "uniform step must be > 0");
+    } else if (q->kind == QX_Q_CUSTOM) {
+        if (!q->thresholds) return fail(ctx, QX_ERR_INVALID, "custom quantizer needs thresholds");
+        for (int64_t i = 1; i < 2 * q->k; ++i)
+            if (!(q->thresholds[i] > q->thresholds[i - 1]))
+                return fail(ctx, QX_ERR_INVALID, "thresholds must be strictly increasing");
+        if (!(q->thresholds[q->k - 1] <= 0.0 && 0.0 < q->thresholds[q->k]))
+            return fail(ctx, QX_ERR_INVALID, "level 0 must contain the input 0");
+    } else {
+        return fail(ctx, QX_ERR_INVALID, "unknown quantizer kind");
+    }
+    if (q->k > kMaxThr / 2) return fail(ctx, QX_ERR_UNSUPPORTED, "quantizer level bound k > 128");
+    return QX_OK;
+}
+
+static qx_status make_qtable(qx_context* ctx, const qx_quantizer* q, int dtype, QTable* t)
+{
+    memset(t, 0, sizeof(*t));
+    t->k = (int)(q->kind == QX_Q_CODES ? q->k : q->k);
+    if (q->kind == QX_Q_CODES) {
+        t->mode = QM_CODES;
+        t->tsize = 0;
+        return QX_OK;
+    }
+    t->mode = q->k == 1 ? QM_K1 : (q->kind == QX_Q_UNIFORM ? QM_UNIFORM : QM_BSEARCH);
+    int ts = 1, tb = 0;
+    while (ts < 2 * q->k) {
+        ts <<= 1;
+        ++tb;
+    }
+    t->tsize = ts;
+    t->tbits = tb;
+    t->inv_step = q->kind == QX_Q_UNIFORM ? 1.0 / q->step : 1.0;
+    // cache key: every parameter byte
+    std::string key((const char*)&q->kind, 4);
+    key.append((const char*)&q->k, 8);
+    key.append((const char*)&q->step, 8);
+    key.append((const char*)&dtype, 4);
+    if (q->kind == QX_Q_CUSTOM) key.append((const char*)q->thresholds, (size_t)(16 * q->k));
+    auto it = ctx->thr_cache.find(key);
+    if (it == ctx->thr_cache.end()) {
+        std::vector<double> v((size_t)(2 * q->k));
+        thresholds(q->kind, q->k, q->step, q->thresholds, dtype == QX_F32 ? DT_F32 : DT_F64, v.data());
+        it = ctx->thr_cache.emplace(key, std::move(v)).first;
+    }
+    for (int i = 0; i < ts; ++i) t->thr[i] = i < 2 * q->k ? it->second[i] : NAN;
+    return QX_OK;
+}
+
+static qx_status check_signals(qx_context* ctx, const qx_signals* s, const char* name)
+{
+    if (!s || !s->data) return fail(ctx, QX_ERR_INVALID, std::string(name) + " is NULL");
+    if (s->n < 1) return fail(ctx, QX_ERR_INVALID, "samples must be a non-empty 1-D sequence");
+    if (s->ld < s->n) return fail(ctx, QX_ERR_INVALID, std::string(name) + ": ld < n");
+    if (s->dtype < QX_F32 || s->dtype > QX_I64) return fail(ctx, QX_ERR_INVALID, "bad dtype");
+    return QX_OK;
+}
+
+static int ceil_log2(int64_t v)
+{
+    int l = 0;
+    while ((1ll << l) < v) ++l;
+    return l;
+}
+
+static qx_status get_tables(qx_context* ctx, const PrimeInfo& pi, int lp, NttTables* out)
+{
+    auto key = std::make_pair(pi.p, lp);
+    auto it = ctx->tables.find(key);
+    if (it == ctx->tables.end()) {
+        NttTables t;
+        void* blk = nullptr;
+        cudaError_t e = ntt_make_tables(pi.p, pi.g, lp, &t, &blk);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "twiddle tables");
+        it = ctx->tables.emplace(key, std::make_pair(t, blk)).first;
+    }
+    *out = it->second.first;
+    return QX_OK;
+}
+
+static uint64_t powmod64(uint64_t a, uint64_t e, uint64_t p)
+{
+    uint64_t r = 1;
+    a %= p;
+    while (e) {
+        if (e & 1) r = (unsigned __int128)r * a % p;
+        a = (unsigned __int128)a * a % p;
+        e >>= 1;
+    }
+    return r;
+}
+
+// Common front half: validate, build the call, reserve scratch.
+struct Prepared {
+    NttCall call;
+    int64_t nx, ny;
+    int path;
+};
+
+static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                         const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
+                         bool argmax, qx_path path, Prepared* out)
+{
+    qx_status st;
+    if (batch < 1) return fail(ctx, QX_ERR_INVALID, "batch must be >= 1");
+    if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
+    if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, qx_, x->dtype)) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, qy_, y->dtype)) != QX_OK) return st;
+    const int64_t nx = x->n, ny = y->n;
+    const int64_t ku = qx_->k > 1 ? qx_->k : 1, kv = qy_->k > 1 ? qy_->k : 1;
+    const int64_t nmin = nx < ny ? nx : ny;
+    // _check_coeff_bound (intxcorr.py:89-93)
+    const unsigned __int128 bound = (unsigned __int128)nmin * (uint64_t)ku * (uint64_t)kv;
+    if (bound > ((unsigned __int128)1 << 59))
+        return fail(ctx, QX_BOUND_EXCEEDED, "coefficient bound N_min*K_u*K_v exceeds the supported int64 range");
+    const int64_t nout = nx + ny - 1;
+    const int64_t first_lag = y->start - (x->start + nx - 1);
+    int64_t t_lo = 0, t_hi = nout - 1;
+    if (argmax) {
+        // window in t, computed without overflow
+        if (lag_lo != INT64_MIN) {
+            __int128 v = (__int128)lag_lo - first_lag;
+            if (v > t_lo) t_lo = v > (__int128)t_hi ? t_hi + 1 : (int64_t)v;
+        }
+        if (lag_hi != INT64_MAX) {
+            __int128 v = (__int128)lag_hi - first_lag;
+            if (v < t_hi) t_hi = v < 0 ? -1 : (int64_t)v;
+        }
+        if (t_lo > t_hi) return fail(ctx, QX_ERR_INVALID, "lag window does not intersect the overlap range");
+    }
+    NttCall& c = out->call;
+    memset(&c, 0, sizeof(c));
+    c.op[0].data = x->data;
+    c.op[0].ld = x->ld;
+    c.op[0].n = nx;
+    c.op[0].reverse = 1;
+    c.op[0].dtype = x->dtype == QX_F32 ? DT_F32 : (x->dtype == QX_F64 ? DT_F64 : DT_I64);
+    c.op[1].data = y->data;
+    c.op[1].ld = y->ld;
+    c.op[1].n = ny;
+    c.op[1].reverse = 0;
+    c.op[1].dtype = y->dtype == QX_F32 ? DT_F32 : (y->dtype == QX_F64 ? DT_F64 : DT_I64);
+    if ((st = make_qtable(ctx, qx_, x->dtype, &c.op[0].q)) != QX_OK) return st;
+    if ((st = make_qtable(ctx, qy_, y->dtype, &c.op[1].q)) != QX_OK) return st;
+    c.batch = batch;
+    c.nout = nout;
+    c.am.first_lag = first_lag;
+    c.am.t_lo = t_lo;
+    c.am.t_hi = t_hi;
+    out->nx = nx;
+    out->ny = ny;
+    out->path = path == QX_PATH_AUTO ? QX_PATH_NTT : path;
+    if (out->path != QX_PATH_NTT) return fail(ctx, QX_ERR_UNSUPPORTED, "path not available in this build");
+
+    const int lp = ceil_log2(nout) < 10 ? 10 : ceil_log2(nout);
+    if (lp > 19) return fail(ctx, QX_ERR_UNSUPPORTED, "full-lag correlation longer than 2^19 points");
+    // primes: product must exceed 2*bound + 1 (centred lift)
+    std::vector<const PrimeInfo*> ps;
+    for (const PrimeInfo& pi : kPrimes)
+        if (pi.adicity >= lp) ps.push_back(&pi);
+    int np = 0;
+    unsigned __int128 M = 1;
+    while (np < (int)ps.size() && np < 3) {
+        M *= ps[np]->p;
+        ++np;
+        if ((M - 1) / 2 >= bound) break;
+    }
+    if ((M - 1) / 2 < bound) return fail(ctx, QX_ERR_UNSUPPORTED, "no prime set covers this coefficient bound");
+    c.np = np;
+    for (int i = 0; i < np; ++i) {
+        if ((st = get_tables(ctx, *ps[i], lp, &c.tab[i])) != QX_OK) return st;
+        uint64_t mprev = 1;
+        for (int j = 0; j < i; ++j) mprev = (unsigned __int128)mprev * ps[j]->p % ps[i]->p;
+        c.garner_inv[i] = i ? powmod64(mprev, ps[i]->p - 2, ps[i]->p) : 1;
+    }
+    const int64_t P = 1ll << lp;
+    c.zero_upper = (nx <= P / 2 && ny <= P / 2);
+    // chunk of pairs per launch group: keep Y (2 operands) within ~64 MiB
+    int64_t chunk = (64ll << 20) / (2 * P * 4);
+    if (const char* ev = getenv("QX_CHUNK_PAIRS")) chunk = atoll(ev);
+    if (chunk < 1) chunk = 1;
+    if (chunk > batch) chunk = batch;
+    c.chunk = chunk;
+    // scratch: Y | R | stats | partials
+    const size_t yb = (size_t)chunk * 2 * P * 4;
+    const size_t rb = np > 1 ? (size_t)chunk * np * P * 4 : 0;
+    const size_t sb = (size_t)batch * 8 * 8;
+    const size_t pb = argmax ? (size_t)batch * kMaxPartials * 3 * 8 : 0;
+    cudaError_t e = arena_reserve(ctx->scratch, yb + rb + sb + pb + 256, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
+    e = arena_reserve(ctx->counters, (size_t)batch * 4, true);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "counters");
+    char* base = (char*)ctx->scratch.ptr;
+    c.Y = (uint32_t*)base;
+    c.R = rb ? (uint32_t*)(base + yb) : nullptr;
+    c.stats = (unsigned long long*)(base + yb + rb);
+    c.am.partials = argmax ? (long long*)(base + yb + rb + sb) : nullptr;
+    c.am.counters = (int*)ctx->counters.ptr;
+    c.prof = &ctx->prof;
+    return QX_OK;
+}
+
+extern "C" {
+
+qx_status qx_quantizer_thresholds(const qx_quantizer* q, qx_dtype dtype, double* out)
+{
+    if (!out) return QX_ERR_INVALID;
+    qx_status st = check_quantizer(nullptr, q, dtype);
+    if (st != QX_OK) return st;
+    if (q->kind == QX_Q_CODES) return QX_ERR_INVALID;
+    thresholds(q->kind, q->k, q->step, q->thresholds, dtype == QX_F32 ? DT_F32 : DT_F64, out);
+    return QX_OK;
+}
+
+qx_status qx_quantize(qx_context* ctx, const qx_quantizer* q, const qx_signals* x, int64_t batch, int64_t* codes,
+                      int64_t* sumsq, int64_t* nnz, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    qx_status st;
+    if (batch < 1 || !codes) return fail(ctx, QX_ERR_INVALID, "bad batch or output");
+    if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, q, x->dtype)) != QX_OK) return st;
+    if (q->kind == QX_Q_CODES) return fail(ctx, QX_ERR_INVALID, "input already quantised");
+    QTable t;
+    if ((st = make_qtable(ctx, q, x->dtype, &t)) != QX_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = arena_reserve(ctx->scratch, (size_t)batch * 16 + 64, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
+    unsigned long long* sums = (unsigned long long*)ctx->scratch.ptr;
+    unsigned* flags = (unsigned*)((char*)ctx->scratch.ptr + batch * 16);
+    e = cudaMemsetAsync(ctx->scratch.ptr, 0, (size_t)batch * 16 + 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset");
+    ctx->prof.pre(KK_QUANT, s);
+    e = quantize_launch(x->data, x->ld, x->n, batch, x->dtype == QX_F32 ? DT_F32 : DT_F64, t, codes, sums, flags, s);
+    ctx->prof.post(KK_QUANT, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "quantize");
+    if (sumsq) {
+        e = cudaMemcpy2DAsync(sumsq, 8, sums, 16, 8, (size_t)batch, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "copy sums");
+    }
+    if (nnz) {
+        e = cudaMemcpy2DAsync(nnz, 8, sums + 1, 16, 8, (size_t)batch, cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "copy nnz");
+    }
+    return QX_OK;
+}
+
+qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                            const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
+                            qx_path path, qx_result* results, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!results) return fail(ctx, QX_ERR_INVALID, "results is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    Prepared pr;
+    qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr);
+    if (st != QX_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    pr.call.am.results = results;
+    cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
+    e = ntt_run(pr.call, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "ntt launch");
+    return QX_OK;
+}
+
+qx_status qx_xcorr_full(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                        const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t* values, qx_result* stats,
+                        qx_path path, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!values) return fail(ctx, QX_ERR_INVALID, "values is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    Prepared pr;
+    qx_status st = prepare(ctx, x, y, batch, qx_, qy_, INT64_MIN, INT64_MAX, false, path, &pr);
+    if (st != QX_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    pr.call.values = values;
+    cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
+    e = ntt_run(pr.call, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "ntt launch");
+    if (stats) {
+        e = stats_to_results(pr.call.stats, stats, batch, s);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "stats");
+    }
+    return QX_OK;
+}
+
+static const char* kKindNames[QX_PROFILE_KINDS] = {"ntt_pass1", "ntt_pass2", "ntt_pass3", "crt_combine",
+                                                    "quantize", "direct", "other", ""};
+
+const char* qx_profile_kind_name(int kind)
+{
+    return (kind >= 0 && kind < QX_PROFILE_KINDS) ? kKindNames[kind] : "";
+}
+
+qx_status qx_profile_begin(qx_context* ctx, int timed)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    Profiler& p = ctx->prof;
+    p.on = true;
+    p.timed = timed != 0;
+    p.launches = 0;
+    for (long long& c : p.count) c = 0;
+    p.nrec = 0;
+    return QX_OK;
+}
+
+qx_status qx_profile_end(qx_context* ctx, qx_profile* out)
+{
+    if (!ctx || !out) return QX_ERR_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    Profiler& p = ctx->prof;
+    memset(out, 0, sizeof(*out));
+    out->launches = p.launches;
+    for (int i = 0; i < QX_PROFILE_KINDS; ++i) out->count[i] = p.count[i];
+    for (int i = 0; i < p.nrec; ++i) {
+        cudaError_t e = cudaEventSynchronize(p.recs[i].b);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "profile sync");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, p.recs[i].a, p.recs[i].b);
+        out->ms[p.recs[i].kind] += ms;
+    }
+    p.on = false;
+    p.nrec = 0;
+    return QX_OK;
+}
+
+qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                                 const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo,
+                                 int64_t lag_hi, qx_path path, qx_result* results)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!results) return fail(ctx, QX_ERR_INVALID, "results is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    qx_status st;
+    if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
+    if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
+    static const size_t esz[] = {4, 8, 8};
+    const size_t xb = (size_t)batch * x->ld * esz[x->dtype], yb = (size_t)batch * y->ld * esz[y->dtype];
+    const size_t xa = (xb + 255) & ~(size_t)255, ya = (yb + 255) & ~(size_t)255;
+    const size_t rb = (size_t)batch * sizeof(qx_result);
+    cudaError_t e = arena_reserve(ctx->stage, xa + ya + rb, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "staging");
+    char* d = (char*)ctx->stage.ptr;
+    cudaStream_t s = ctx->host_stream;
+    e = cudaMemcpyAsync(d, x->data, xb, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + xa, y->data, yb, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D");
+    qx_signals xd = *x, yd = *y;
+    xd.data = d;
+    yd.data = d + xa;
+    qx_result* rd = (qx_result*)(d + xa + ya);
+    st = qx_estimate_batch(ctx, &xd, &yd, batch, qx_, qy_, lag_lo, lag_hi, path, rd, s);
+    if (st != QX_OK) return st;
+    e = cudaMemcpyAsync(results, rd, rb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
+    for (int64_t b = 0; b < batch; ++b)
+        if (results[b].status) return (qx_status)results[b].status;
+    return QX_OK;
+}
+
+}  // extern "C"

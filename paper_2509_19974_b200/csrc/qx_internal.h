@@ -1,0 +1,102 @@
+// qx_internal.h -- host/device argument blocks shared by the kernels and
+// the C-ABI implementation (not part of the public ABI; see
+// include/qxcorr_b200.h for that).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "qx_common.cuh"
+
+namespace qx {
+
+constexpr int kMaxThr = 256;  // threshold table capacity (k <= 128)
+
+// Quantiser as the kernels see it: mode + table, passed by value (kernel
+// parameter space) and staged into shared memory by each CTA.
+struct QTable {
+    int mode;       // QMode
+    int k;          // level bound K
+    int tsize;      // padded table size (power of two >= 2k)
+    int tbits;
+    double inv_step;
+    double thr[kMaxThr];  // T[i], +inf padded; float32 tables hold exact floats
+};
+
+enum DType : int { DT_F32 = 0, DT_F64 = 1, DT_I64 = 2 };
+
+struct OperandDesc {
+    const void* data;  // batch rows, row b at data + b*ld elements
+    int64_t ld;
+    int64_t n;         // samples per row
+    int reverse;       // 1: operand is time-reversed (the x side)
+    int dtype;         // DType
+    QTable q;
+};
+
+// Per-pair statistics filled by pass 1: [pair][op][4] =
+//   {sum of code^2, nonzero count, flag bits, unused}
+enum StatFlag : unsigned { SF_NONFINITE = 1u, SF_CODE_RANGE = 2u };
+
+struct ArgmaxOut {
+    // device result records (public layout qx_result, see qxcorr_b200.h)
+    void* results;
+    int64_t first_lag;   // lag of correlogram index t = 0
+    int64_t t_lo, t_hi;  // inclusive window on t
+    long long* partials; // [batch][kMaxPartials][3]
+    int* counters;       // [batch]
+};
+constexpr int kMaxPartials = 64;
+
+// Tables for one (prime, log2 P) transform plan, device pointers.
+struct NttTables {
+    ModP m;
+    uint32_t p;
+    int lp, l1, l2;
+    const uint2* tw1f;  // DIF stage twiddles for N1 = 2^l1 (Shoup pairs)
+    const uint2* tw1i;  // inverse (DIT) stage twiddles for N1
+    const uint2* tw2f;
+    const uint2* tw2i;
+    const uint32_t* twf;  // forward four-step twiddles [P] (Montgomery form)
+    const uint32_t* twi;  // inverse four-step twiddles [P] incl. R^2/P
+};
+
+// Optional per-launch accounting (qx_profile_begin/end): counts every kernel
+// launch and, when timed, brackets it with CUDA events on its stream.
+enum KernelKind : int { KK_PASS1 = 0, KK_PASS2, KK_PASS3, KK_COMBINE, KK_QUANT, KK_DIRECT, KK_OTHER, KK_N };
+struct Profiler {
+    bool on = false, timed = false;
+    long long launches = 0;
+    long long count[8] = {0};
+    struct Rec { int kind; cudaEvent_t a, b; };
+    Rec* recs = nullptr;
+    int nrec = 0, cap = 0;
+    cudaEvent_t pending = nullptr;
+    void pre(int kind, cudaStream_t s);
+    void post(int kind, cudaStream_t s);
+};
+
+struct NttCall {
+    OperandDesc op[2];
+    int64_t batch;
+    int64_t nout;           // n_u + n_v - 1
+    int np;                 // number of primes (1..3)
+    NttTables tab[3];
+    uint64_t garner_inv[3]; // inv(p0*..*p_{i-1}) mod p_i
+    int zero_upper;         // both operands fit the lower half of P
+    // scratch (device)
+    uint32_t* Y;              // [chunk][2][P]
+    uint32_t* R;              // [chunk][np][P] residues (np > 1)
+    unsigned long long* stats;  // [batch][2][4]
+    // outputs: exactly one of
+    ArgmaxOut am;             // argmax mode (am.results != nullptr)
+    int64_t* values;          // full correlogram mode [batch][nout]
+    int64_t chunk;            // pairs per launch group
+    Profiler* prof;           // may be null
+};
+
+// launches every pass of the NTT correlation for all pairs on `stream`
+cudaError_t ntt_run(const NttCall& c, cudaStream_t stream);
+// builds host-side twiddle tables for (p, lp) and uploads them
+cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block);
+
+}  // namespace qx

@@ -1,0 +1,925 @@
+// qx_ntt.cu -- exact full-lag integer cross-correlation by number-theoretic
+// transform (the GPU replacement of the reference's Kronecker-substitution
+// path, intxcorr.py:259-265: pack -> one big multiply -> unpack; here the
+// "big multiply" is a cyclic convolution mod word-sized primes, which is what
+// KS + GMP's FFT multiply compute underneath).
+//
+// Layout: P = 2^lp = N1 * N2 points, element n stored
+// at row n1 = n / N2, column n2 = n % N2 of a row-major N1 x N2 matrix.
+//   pass 1  per operand, tiles of 32 columns: load floats, quantise, column
+//           DIF NTT over n1 (length N1), forward four-step twiddle -> Y
+//   pass 2  tiles of 32 rows: row DIF of both operands (length N2),
+//           pointwise product, row DIT (inverse), inverse twiddle * R^2/P -> Z
+//   pass 3  tiles of 32 columns: column DIT (inverse) -> exact residues in
+//           natural order -> centred lift -> argmax / values / residues
+// Forward transforms are DIF (natural in, bit-reversed out), inverses DIT
+// (bit-reversed in, natural out) so no permutation pass exists.  Inside a
+// tile each lane owns one vector (column or row) and the 32 vectors sit in
+// shared memory with an XOR swizzle, conflict-free both for the transform
+// (lane = vector) and for row-contiguous global I/O (lane = element).
+// tools/ntt_model.py is an exact-arithmetic model of the same index math.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "qx_internal.h"
+
+namespace qx {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+
+__device__ __forceinline__ int sidx(int e, int c) { return (e << 5) + (c ^ (e & 31)); }
+
+// register-group schedule of a length-2^LOG transform: ceil(LOG/4) groups,
+// radices 2^3..2^4, larger first (DIF order; DIT uses the reverse).
+template <int LOG>
+struct Sched {
+    static constexpr int NG = (LOG + 3) / 4;
+    static constexpr int BASE = LOG / NG;
+    static constexpr int EXTRA = LOG % NG;
+    static constexpr int r(int i) { return i < EXTRA ? BASE + 1 : BASE; }
+    static constexpr int s0(int i) { return i == 0 ? 0 : s0(i - 1) + r(i - 1); }
+    // DIT group i = DIF group NG-1-i
+    static constexpr int rd(int i) { return r(NG - 1 - i); }
+    static constexpr int s0d(int i) { return i == 0 ? 0 : s0d(i - 1) + rd(i - 1); }
+};
+
+// ---------------------------------------------------------------- groups
+
+// R DIF stages on 2^R registers; element k of the group sits at position
+// j0 + k*S of a block of size S*2^R whose first stage is global stage S0.
+template <int R, int S0>
+__device__ __forceinline__ void dif_regs(uint32_t (&x)[1 << R], int j0, int S,
+                                         const uint2* __restrict__ tw, const ModP& m)
+{
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int h = 1 << (R - 1 - t);
+#pragma unroll
+        for (int kp = 0; kp < h; ++kp) {
+            const uint2 w = __ldg(&tw[(j0 + kp * S) << (S0 + t)]);
+#pragma unroll
+            for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dif(x[blk + kp], x[blk + kp + h], w, m);
+        }
+    }
+}
+
+// R DIT stages; element k sits at j0 + (k << S0) of a block of size 2^(S0+R).
+template <int R, int S0, int LOG>
+__device__ __forceinline__ void dit_regs(uint32_t (&x)[1 << R], int j0,
+                                         const uint2* __restrict__ tw, const ModP& m)
+{
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int h = 1 << t;
+#pragma unroll
+        for (int kp = 0; kp < h; ++kp) {
+            const int j = j0 + (kp << S0);
+            const uint2 w = __ldg(&tw[j << (LOG - S0 - t - 1)]);
+#pragma unroll
+            for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dit(x[blk + kp], x[blk + kp + h], w, m);
+        }
+    }
+}
+
+// one DIF group pass over a swizzled smem tile (all warps)
+template <int LOG, int S0, int R>
+__device__ __forceinline__ void dif_pass(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+{
+    constexpr int L = 1 << LOG, B = L >> S0, S = B >> R, NGRP = L >> R;
+    const int lane = threadIdx.x & 31;
+    for (int g = threadIdx.x >> 5; g < NGRP; g += kWarps) {
+        const int j0 = g & (S - 1);
+        const int base = (g / S) * B + j0;
+        uint32_t x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); ++k) x[k] = s[sidx(base + k * S, lane)];
+        dif_regs<R, S0>(x, j0, S, tw, m);
+#pragma unroll
+        for (int k = 0; k < (1 << R); ++k) s[sidx(base + k * S, lane)] = x[k];
+    }
+}
+
+template <int LOG, int S0, int R>
+__device__ __forceinline__ void dit_pass(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+{
+    constexpr int L = 1 << LOG, NGRP = L >> R;
+    const int lane = threadIdx.x & 31;
+    for (int g = threadIdx.x >> 5; g < NGRP; g += kWarps) {
+        const int j0 = g & ((1 << S0) - 1);
+        const int base = (g >> S0) * (1 << (S0 + R)) + j0;
+        uint32_t x[1 << R];
+#pragma unroll
+        for (int k = 0; k < (1 << R); ++k) x[k] = s[sidx(base + (k << S0), lane)];
+        dit_regs<R, S0, LOG>(x, j0, tw, m);
+#pragma unroll
+        for (int k = 0; k < (1 << R); ++k) s[sidx(base + (k << S0), lane)] = x[k];
+    }
+}
+
+// DIF groups [I, NG-1) (all but the first and last), syncs after each
+template <int LOG, int I>
+__device__ __forceinline__ void dif_middle(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+{
+    if constexpr (I < Sched<LOG>::NG - 1) {
+        dif_pass<LOG, Sched<LOG>::s0(I), Sched<LOG>::r(I)>(s, tw, m);
+        __syncthreads();
+        dif_middle<LOG, I + 1>(s, tw, m);
+    }
+}
+
+template <int LOG, int I>
+__device__ __forceinline__ void dit_middle(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+{
+    if constexpr (I < Sched<LOG>::NG - 1) {
+        dit_pass<LOG, Sched<LOG>::s0d(I), Sched<LOG>::rd(I)>(s, tw, m);
+        __syncthreads();
+        dit_middle<LOG, I + 1>(s, tw, m);
+    }
+}
+
+// ------------------------------------------------------------ statistics
+
+__device__ __forceinline__ bool cs_single(const unsigned long long* stats, int64_t pair, uint32_t p0)
+{
+    // |c| <= sqrt(Su*Sv) (Cauchy-Schwarz on the codes); a single prime
+    // suffices when that is <= (p0-1)/2.
+    const unsigned long long su = stats[pair * 8 + 0], sv = stats[pair * 8 + 4];
+    const unsigned long long h = (p0 - 1) / 2;
+    return (unsigned __int128)su * sv <= (unsigned __int128)h * h;
+}
+
+// ------------------------------------------------------------ quantiser
+
+template <typename T, int QM>
+__device__ __forceinline__ int quant_level(T v, const T* sthr, int k, int tbits, T inv_step, T t0, T t1)
+{
+    if constexpr (QM == QM_K1) return level_k1(v, t0, t1);
+    else if constexpr (QM == QM_UNIFORM) return level_uniform(v, sthr, k, inv_step);
+    else return level_bsearch(v, sthr, tbits) - k;
+}
+
+template <typename T, int QM>
+__device__ __forceinline__ int load_code(const T* __restrict__ src, int64_t i, const T* sthr, int k,
+                                         int tbits, T inv_step, T t0, T t1, unsigned& flags)
+{
+    if constexpr (QM == QM_CODES) {
+        const long long c = src[i];
+        if (c > k || c < -k) flags |= SF_CODE_RANGE;
+        return (int)c;
+    } else {
+        const T v = __ldg(&src[i]);
+        if (v != v) flags |= SF_NONFINITE;
+        return quant_level<T, QM>(v, sthr, k, tbits, inv_step, t0, t1);
+    }
+}
+
+// ------------------------------------------------------------------ pass 1
+
+struct Pass1Args {
+    OperandDesc op[2];
+    uint32_t* Y;
+    const uint2* tw;
+    const uint32_t* twf;
+    unsigned long long* stats;
+    ModP m;
+    uint32_t p0;
+    int N2;
+    int zero_upper;
+    int skip_cs;
+    int op_base;  // operand index of blockIdx.y == 0 (1 when launched per operand)
+    int64_t pair0;
+};
+
+template <int LOG1, typename T, int QM>
+__global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ Pass1Args a)
+{
+    constexpr int N1 = 1 << LOG1;
+    using SC = Sched<LOG1>;
+    constexpr int R0 = SC::r(0), S = N1 >> R0, RAD0 = 1 << R0;
+    constexpr int RL = SC::r(SC::NG - 1), S0L = SC::s0(SC::NG - 1), RADL = 1 << RL;
+    extern __shared__ __align__(16) uint32_t smem[];
+
+    const int op = a.op_base + blockIdx.y;
+    const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
+    if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
+    const OperandDesc& d = a.op[blockIdx.y];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N2 = a.N2;
+    const int col = blockIdx.x * 32 + lane;
+    const ModP m = a.m;
+
+    // thresholds -> smem (after the tile)
+    T* sthr = reinterpret_cast<T*>(smem + N1 * 32);
+    if constexpr (QM != QM_CODES) {
+        for (int i = threadIdx.x; i < d.q.tsize; i += kThreads) sthr[i] = (T)d.q.thr[i];
+    }
+    __syncthreads();
+    T t0 = T(0), t1 = T(0);
+    if constexpr (QM == QM_K1) { t0 = sthr[0]; t1 = sthr[1]; }
+    const T inv_step = (T)d.q.inv_step;
+    const int k = d.q.k, tbits = d.q.tbits;
+    const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld;
+    const int64_t n = d.n;
+    const bool rev = d.reverse;
+
+    unsigned long long ssq = 0, nnz = 0;
+    unsigned flags = 0;
+    // first DIF group straight from global memory (coalesced: lane = column)
+    for (int g = warp; g < S; g += kWarps) {
+        uint32_t x[RAD0];
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) {
+            x[kk] = 0;
+            if (a.zero_upper && kk >= RAD0 / 2) continue;
+            const int64_t idx = (int64_t)(g + kk * S) * N2 + col;
+            if (idx < n) {
+                const int c = load_code<T, QM>(src, rev ? n - 1 - idx : idx, sthr, k, tbits, inv_step,
+                                               t0, t1, flags);
+                ssq += (unsigned long long)((long long)c * c);
+                nnz += (c != 0);
+                x[kk] = c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
+            }
+        }
+        dif_regs<R0, 0>(x, g, S, a.tw, m);
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) smem[sidx(g + kk * S, lane)] = x[kk];
+    }
+    // statistics: warp reduce, one atomic per warp
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if (lane == 0 && a.p0 == m.p) {  // only the first prime's pass counts
+        unsigned long long* st = a.stats + (pair * 2 + op) * 4;
+        if (ssq) atomicAdd(st + 0, ssq);
+        if (nnz) atomicAdd(st + 1, nnz);
+        if (flags) atomicOr(st + 2, (unsigned long long)flags);
+    }
+    __syncthreads();
+    dif_middle<LOG1, 1>(smem, a.tw, m);
+    // last DIF group, forward four-step twiddle, store (coalesced)
+    uint32_t* Y = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
+    for (int g = warp; g < (N1 >> RL); g += kWarps) {
+        uint32_t x[RADL];
+        const int base = g * RADL;
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = smem[sidx(base + kk, lane)];
+        dif_regs<RL, S0L>(x, 0, 1, a.tw, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) {
+            const int64_t o = (int64_t)(base + kk) * N2 + col;
+            Y[o] = montmul(x[kk], __ldg(&a.twf[o]), m.p, m.pinv);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ pass 2
+
+struct Pass2Args {
+    uint32_t* Y;
+    const uint2* twf;  // DIF stage table for N2
+    const uint2* twi;  // DIT stage table for N2
+    const uint32_t* twinv;  // inverse four-step twiddles [P]
+    const unsigned long long* stats;
+    ModP m;
+    uint32_t p0;
+    int N1;
+    int skip_cs;
+    int64_t pair0;
+};
+
+template <int LOG2>
+__global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ Pass2Args a)
+{
+    constexpr int N2 = 1 << LOG2;
+    using SC = Sched<LOG2>;
+    constexpr int RL = SC::r(SC::NG - 1), S0L = SC::s0(SC::NG - 1), RADL = 1 << RL;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* su = smem;
+    uint32_t* sv = smem + N2 * 32;
+
+    const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
+    if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r0 = blockIdx.x * 32;
+    const ModP m = a.m;
+    const int64_t P = (int64_t)a.N1 * N2;
+    uint32_t* Yu = a.Y + pl * 2 * P;
+    const uint32_t* Yv = Yu + P;
+
+    // transposed load: warp reads row c contiguously, lane = element
+    for (int c = warp; c < 32; c += kWarps) {
+        const int64_t rb = (int64_t)(r0 + c) * N2;
+        for (int e = lane; e < N2; e += 32) {
+            su[sidx(e, c)] = Yu[rb + e];
+            sv[sidx(e, c)] = Yv[rb + e];
+        }
+    }
+    __syncthreads();
+    // forward DIF groups except the last, both operands
+    if constexpr (SC::NG > 1) {
+        dif_middle<LOG2, 0>(su, a.twf, m);
+        dif_middle<LOG2, 0>(sv, a.twf, m);
+    }
+    // last DIF group of both, pointwise product, first DIT group (same
+    // element grouping: consecutive blocks of 2^RL)
+    for (int g = warp; g < (N2 >> RL); g += kWarps) {
+        uint32_t xu[RADL], xv[RADL];
+        const int base = g * RADL;
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) {
+            xu[kk] = su[sidx(base + kk, lane)];
+            xv[kk] = sv[sidx(base + kk, lane)];
+        }
+        dif_regs<RL, S0L>(xu, 0, 1, a.twf, m);
+        dif_regs<RL, S0L>(xv, 0, 1, a.twf, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) xu[kk] = montmul(xu[kk], xv[kk], m.p, m.pinv);
+        dit_regs<RL, 0, LOG2>(xu, 0, a.twi, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) su[sidx(base + kk, lane)] = xu[kk];
+    }
+    __syncthreads();
+    // remaining DIT groups (1 .. NG-1)
+    if constexpr (SC::NG > 1) {
+        dit_middle<LOG2, 1>(su, a.twi, m);
+        dit_pass<LOG2, SC::s0d(SC::NG - 1), SC::rd(SC::NG - 1)>(su, a.twi, m);
+        __syncthreads();
+    }
+    // transposed store with the inverse four-step twiddle (includes R^2/P)
+    for (int c = warp; c < 32; c += kWarps) {
+        const int64_t rb = (int64_t)(r0 + c) * N2;
+        for (int e = lane; e < N2; e += 32)
+            Yu[rb + e] = montmul(su[sidx(e, c)], __ldg(&a.twinv[rb + e]), m.p, m.pinv);
+    }
+}
+
+// ------------------------------------------------------ argmax reduction
+
+struct Best {
+    long long v, t, c;
+};
+
+__device__ __forceinline__ void best_merge(Best& a, const Best& b)
+{
+    if (b.v > a.v) a = b;
+    else if (b.v == a.v) { a.t = min(a.t, b.t); a.c += b.c; }
+}
+
+__device__ __forceinline__ void best_add(Best& a, long long v, long long t)
+{
+    if (v > a.v) { a.v = v; a.t = t; a.c = 1; }
+    else if (v == a.v) { a.t = min(a.t, t); a.c += 1; }
+}
+
+__device__ __forceinline__ Best best_init() { return Best{LLONG_MIN, LLONG_MAX, 0}; }
+
+// one qx_result record (include/qxcorr_b200.h) from the peak summary and the
+// pass-1 statistics of a pair
+__device__ void write_result(long long* res, const Best& r, long long first_lag, const unsigned long long* st)
+{
+    const long long nzx = (long long)st[1], nzy = (long long)st[5];
+    const unsigned f = (unsigned)(st[2] | st[6]);
+    int flags = 0;
+    if (nzx == 0) flags |= 1;
+    if (nzy == 0) flags |= 2;
+    if (f & SF_NONFINITE) flags |= 4;
+    if (f & SF_CODE_RANGE) flags |= 8;
+    int status = 0;
+    if (flags & 4) status = 9;       // QX_ERR_NONFINITE
+    else if (flags & 8) status = 1;  // QX_ERR_INVALID (codes exceed bound)
+    else if (flags & 3) status = 2;  // QX_DEGENERATE_QUANTIZATION
+    res[0] = r.v;
+    res[1] = first_lag + r.t;
+    res[2] = r.c;
+    res[3] = (long long)st[0];
+    res[4] = (long long)st[4];
+    res[5] = nzx;
+    res[6] = nzy;
+    res[7] = ((long long)status << 32) | (unsigned)flags;
+}
+
+__global__ void k_stats_to_results(const unsigned long long* stats, long long* res, int64_t batch)
+{
+    const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (b < batch) write_result(res + b * 8, Best{0, 0, 0}, 0, stats + b * 8);
+}
+
+cudaError_t stats_to_results(const unsigned long long* stats, void* results, int64_t batch, cudaStream_t s)
+{
+    k_stats_to_results<<<(unsigned)((batch + 127) / 128), 128, 0, s>>>(stats, (long long*)results, batch);
+    return cudaGetLastError();
+}
+
+// block-wide reduce, per-block partial, last block writes the qx_result
+__device__ void argmax_finish(Best b, const ArgmaxOut& am, const unsigned long long* stats, int64_t pair,
+                              int nblk, int blk)
+{
+    __shared__ Best sb[kWarps];
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        Best o2{__shfl_xor_sync(0xffffffffu, b.v, o), __shfl_xor_sync(0xffffffffu, b.t, o),
+                __shfl_xor_sync(0xffffffffu, b.c, o)};
+        best_merge(b, o2);
+    }
+    if (lane == 0) sb[warp] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        Best r = sb[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(r, sb[w]);
+        long long* pp = am.partials + (pair * kMaxPartials + blk) * 3;
+        pp[0] = r.v; pp[1] = r.t; pp[2] = r.c;
+        __threadfence();
+        const int ticket = atomicAdd(am.counters + pair, 1);
+        s_last = (ticket == nblk - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        Best r = best_init();
+        const volatile long long* pp = am.partials + pair * kMaxPartials * 3;
+        for (int i = 0; i < nblk; ++i) best_merge(r, Best{pp[3 * i], pp[3 * i + 1], pp[3 * i + 2]});
+        write_result(reinterpret_cast<long long*>(am.results) + pair * 8, r, am.first_lag, stats + pair * 8);
+        am.counters[pair] = 0;
+    }
+}
+
+// ------------------------------------------------------------------ pass 3
+
+struct Pass3Args {
+    uint32_t* Y;      // Z lives in the u slot of Y
+    uint32_t* R;      // residue output (multi-prime)
+    const uint2* twi;  // DIT stage table for N1
+    const unsigned long long* stats;
+    ArgmaxOut am;
+    int64_t* values;
+    int64_t nout;
+    int64_t vld;       // row stride of values
+    ModP m;
+    uint32_t p0;
+    int N2;
+    int np;
+    int pi;            // prime index
+    int64_t pair0;
+};
+
+enum { OUT_ARGMAX = 0, OUT_VALUES = 1 };
+
+template <int LOG1, int OUT>
+__global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ Pass3Args a)
+{
+    constexpr int N1 = 1 << LOG1;
+    using SC = Sched<LOG1>;
+    constexpr int R0 = SC::rd(0), RAD0 = 1 << R0;
+    constexpr int RL = SC::rd(SC::NG - 1), S0L = SC::s0d(SC::NG - 1), RADL = 1 << RL;
+    extern __shared__ __align__(16) uint32_t smem[];
+
+    const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
+    const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
+    if (a.pi > 0 && cs) return;
+    const bool final_out = (a.np == 1) || cs;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N2 = a.N2;
+    const int col = blockIdx.x * 32 + lane;
+    const ModP m = a.m;
+    const int64_t P = (int64_t)N1 * N2;
+    const uint32_t* Z = a.Y + pl * 2 * P;
+
+    // first DIT group from global (positions g*RAD0 + k, lane = column)
+    for (int g = warp; g < (N1 >> R0); g += kWarps) {
+        uint32_t x[RAD0];
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) x[kk] = Z[(int64_t)(g * RAD0 + kk) * N2 + col];
+        dit_regs<R0, 0, LOG1>(x, 0, a.twi, m);
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) smem[sidx(g * RAD0 + kk, lane)] = x[kk];
+    }
+    __syncthreads();
+    dit_middle<LOG1, 1>(smem, a.twi, m);
+    // last DIT group: natural-order n1 = j0 + (k << S0L)
+    Best b = best_init();
+    const uint32_t half = (m.p - 1) / 2;
+    uint32_t* Rout = a.R + (pl * a.np + a.pi) * P;
+    for (int g = warp; g < (1 << S0L); g += kWarps) {
+        uint32_t x[RADL];
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = smem[sidx(g + (kk << S0L), lane)];
+        dit_regs<RL, S0L, LOG1>(x, g, a.twi, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) {
+            const int64_t t = (int64_t)(g + (kk << S0L)) * N2 + col;
+            const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
+            if (!final_out) {
+                Rout[t] = r;
+                continue;
+            }
+            const long long v = r > half ? (long long)r - (long long)m.p : (long long)r;
+            if constexpr (OUT == OUT_VALUES) {
+                if (t < a.nout) a.values[pair * a.vld + t] = v;
+            } else {
+                if (t >= a.am.t_lo && t <= a.am.t_hi) best_add(b, v, t);
+            }
+        }
+    }
+    if constexpr (OUT == OUT_ARGMAX) {
+        if (final_out) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+    }
+}
+
+// ----------------------------------------------------- multi-prime combine
+
+struct CombineArgs {
+    const uint32_t* R;
+    const unsigned long long* stats;
+    ArgmaxOut am;
+    int64_t* values;
+    int64_t nout, vld, P;
+    uint32_t p[3];
+    uint64_t ginv[3];
+    uint32_t p0;
+    int np;
+    int64_t pair0;
+};
+
+template <int OUT>
+__global__ void __launch_bounds__(256) k_combine(const __grid_constant__ CombineArgs a)
+{
+    const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
+    if (cs_single(a.stats, pair, a.p0)) return;
+    const uint32_t* R = a.R + pl * a.np * a.P;
+    // centred lift of the mixed-radix (Garner) reconstruction
+    unsigned __int128 M = a.p[0];
+    for (int i = 1; i < a.np; ++i) M *= a.p[i];
+    const unsigned __int128 Mh = M / 2;
+    Best b = best_init();
+    int64_t lo = 0, hi = a.nout - 1;
+    if (OUT == OUT_ARGMAX) { lo = a.am.t_lo; hi = a.am.t_hi; }
+    for (int64_t t = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t <= hi;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        unsigned __int128 x = R[t];
+        unsigned __int128 Mi = a.p[0];
+        for (int i = 1; i < a.np; ++i) {
+            const uint64_t pi = a.p[i];
+            const uint64_t xm = (uint64_t)(x % pi);
+            const uint64_t ri = R[(int64_t)i * a.P + t];
+            const uint64_t di = (ri + pi - xm) % pi;
+            const uint64_t ai = (di * a.ginv[i]) % pi;
+            x += (unsigned __int128)ai * Mi;
+            Mi *= pi;
+        }
+        const long long v = x > Mh ? -(long long)(uint64_t)(M - x) : (long long)(uint64_t)x;
+        if (OUT == OUT_VALUES) a.values[pair * a.vld + t] = v;
+        else best_add(b, v, t);
+    }
+    if (OUT == OUT_ARGMAX) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+}
+
+// ================================================================== host
+
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (unsigned __int128)a * b % p; }
+static uint64_t powmod(uint64_t a, uint64_t e, uint64_t p)
+{
+    uint64_t r = 1;
+    a %= p;
+    while (e) {
+        if (e & 1) r = mulmod(r, a, p);
+        a = mulmod(a, a, p);
+        e >>= 1;
+    }
+    return r;
+}
+static uint32_t bitrev(uint32_t x, int bits)
+{
+    uint32_t r = 0;
+    for (int i = 0; i < bits; ++i) r |= ((x >> i) & 1u) << (bits - 1 - i);
+    return r;
+}
+
+cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block)
+{
+    const int l1 = (lp + 1) / 2, l2 = lp / 2;
+    const uint64_t P = 1ull << lp, N1 = 1ull << l1, N2 = 1ull << l2;
+    const uint64_t w = powmod(g, (p - 1) >> lp, p), wi = powmod(w, p - 2, p);
+    const uint64_t R = (1ull << 32) % p, R2 = mulmod(R, R, p);
+    const uint64_t invP = powmod(P, p - 2, p);
+    // layout: tw1f | tw1i | tw2f | tw2i | twf | twi
+    const size_t n1h = N1 / 2, n2h = N2 / 2;
+    const size_t bytes = (2 * n1h + 2 * n2h) * sizeof(uint2) + 2 * P * sizeof(uint32_t);
+    std::vector<unsigned char> host(bytes);
+    uint2* h1f = reinterpret_cast<uint2*>(host.data());
+    uint2* h1i = h1f + n1h;
+    uint2* h2f = h1i + n1h;
+    uint2* h2i = h2f + n2h;
+    uint32_t* hf = reinterpret_cast<uint32_t*>(h2i + n2h);
+    uint32_t* hi = hf + P;
+    auto shoup_pair = [&](uint64_t v) { return make_uint2((uint32_t)v, (uint32_t)((v << 32) / p)); };
+    const uint64_t w1 = powmod(w, N2, p), w2 = powmod(w, N1, p);
+    const uint64_t w1i = powmod(w1, p - 2, p), w2i = powmod(w2, p - 2, p);
+    for (uint64_t e = 0, a = 1, b = 1; e < n1h; ++e, a = mulmod(a, w1, p), b = mulmod(b, w1i, p)) {
+        h1f[e] = shoup_pair(a);
+        h1i[e] = shoup_pair(b);
+    }
+    for (uint64_t e = 0, a = 1, b = 1; e < n2h; ++e, a = mulmod(a, w2, p), b = mulmod(b, w2i, p)) {
+        h2f[e] = shoup_pair(a);
+        h2i[e] = shoup_pair(b);
+    }
+    const uint64_t ci = mulmod(invP, R2, p);
+    for (uint64_t pos = 0; pos < N1; ++pos) {
+        const uint64_t k1 = bitrev((uint32_t)pos, l1);
+        const uint64_t step_f = powmod(w, k1, p), step_i = powmod(wi, k1, p);
+        uint64_t f = R, iv = ci;  // n2 = 0
+        for (uint64_t n2 = 0; n2 < N2; ++n2) {
+            hf[pos * N2 + n2] = (uint32_t)f;
+            hi[pos * N2 + n2] = (uint32_t)iv;
+            f = mulmod(f, step_f, p);
+            iv = mulmod(iv, step_i, p);
+        }
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, bytes);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(d, host.data(), bytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(d); return e; }
+    uint2* d1f = reinterpret_cast<uint2*>(d);
+    out->p = p;
+    out->m.p = p;
+    out->m.p2 = 2 * p;
+    uint32_t inv = 1;  // p^-1 mod 2^32 by Newton
+    for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
+    out->m.pinv = inv;
+    out->lp = lp;
+    out->l1 = l1;
+    out->l2 = l2;
+    out->tw1f = d1f;
+    out->tw1i = d1f + n1h;
+    out->tw2f = d1f + 2 * n1h;
+    out->tw2i = d1f + 2 * n1h + n2h;
+    out->twf = reinterpret_cast<const uint32_t*>(d1f + 2 * n1h + 2 * n2h);
+    out->twi = out->twf + P;
+    *dev_block = d;
+    return cudaSuccess;
+}
+
+// ---- kernel dispatch tables
+
+template <int LOG1, typename T, int QM>
+static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, size_t smem, cudaStream_t s)
+{
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass1<LOG1, T, QM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_pass1<LOG1, T, QM><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int LOG1>
+static cudaError_t dispatch_p1_mode(const Pass1Args& a, int dtype, int qm, dim3 grid, size_t smem,
+                                    cudaStream_t s)
+{
+    if (dtype == DT_I64) return launch_p1<LOG1, long long, QM_CODES>(a, grid, smem, s);
+    if (dtype == DT_F32) {
+        if (qm == QM_K1) return launch_p1<LOG1, float, QM_K1>(a, grid, smem, s);
+        if (qm == QM_UNIFORM) return launch_p1<LOG1, float, QM_UNIFORM>(a, grid, smem, s);
+        return launch_p1<LOG1, float, QM_BSEARCH>(a, grid, smem, s);
+    }
+    if (qm == QM_K1) return launch_p1<LOG1, double, QM_K1>(a, grid, smem, s);
+    if (qm == QM_UNIFORM) return launch_p1<LOG1, double, QM_UNIFORM>(a, grid, smem, s);
+    return launch_p1<LOG1, double, QM_BSEARCH>(a, grid, smem, s);
+}
+
+static cudaError_t dispatch_p1(int log1, const Pass1Args& a, int dtype, int qm, dim3 grid, size_t smem,
+                               cudaStream_t s)
+{
+    switch (log1) {
+    case 5: return dispatch_p1_mode<5>(a, dtype, qm, grid, smem, s);
+    case 6: return dispatch_p1_mode<6>(a, dtype, qm, grid, smem, s);
+    case 7: return dispatch_p1_mode<7>(a, dtype, qm, grid, smem, s);
+    case 8: return dispatch_p1_mode<8>(a, dtype, qm, grid, smem, s);
+    case 9: return dispatch_p1_mode<9>(a, dtype, qm, grid, smem, s);
+    case 10: return dispatch_p1_mode<10>(a, dtype, qm, grid, smem, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LOG2>
+static cudaError_t launch_p2(const Pass2Args& a, dim3 grid, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = (size_t)2 * 32 * (1 << LOG2) * 4;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass2<LOG2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_pass2<LOG2><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+static cudaError_t dispatch_p2(int log2, const Pass2Args& a, dim3 grid, cudaStream_t s)
+{
+    switch (log2) {
+    case 5: return launch_p2<5>(a, grid, s);
+    case 6: return launch_p2<6>(a, grid, s);
+    case 7: return launch_p2<7>(a, grid, s);
+    case 8: return launch_p2<8>(a, grid, s);
+    case 9: return launch_p2<9>(a, grid, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LOG1, int OUT>
+static cudaError_t launch_p3(const Pass3Args& a, dim3 grid, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = (size_t)32 * (1 << LOG1) * 4;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_pass3<LOG1, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_pass3<LOG1, OUT><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int OUT>
+static cudaError_t dispatch_p3_out(int log1, const Pass3Args& a, dim3 grid, cudaStream_t s)
+{
+    switch (log1) {
+    case 5: return launch_p3<5, OUT>(a, grid, s);
+    case 6: return launch_p3<6, OUT>(a, grid, s);
+    case 7: return launch_p3<7, OUT>(a, grid, s);
+    case 8: return launch_p3<8, OUT>(a, grid, s);
+    case 9: return launch_p3<9, OUT>(a, grid, s);
+    case 10: return launch_p3<10, OUT>(a, grid, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+void Profiler::pre(int kind, cudaStream_t s)
+{
+    if (!on) return;
+    ++launches;
+    ++count[kind];
+    if (!timed) return;
+    if (nrec == cap) {
+        int ncap = cap ? 2 * cap : 256;
+        Rec* n = new Rec[ncap];
+        for (int i = 0; i < nrec; ++i) n[i] = recs[i];
+        for (int i = nrec; i < ncap; ++i) {
+            n[i].a = n[i].b = nullptr;
+        }
+        delete[] recs;
+        recs = n;
+        cap = ncap;
+    }
+    Rec& r = recs[nrec];
+    if (!r.a) {
+        cudaEventCreate(&r.a);
+        cudaEventCreate(&r.b);
+    }
+    r.kind = kind;
+    cudaEventRecord(r.a, s);
+}
+
+void Profiler::post(int kind, cudaStream_t s)
+{
+    if (!on || !timed) return;
+    (void)kind;
+    cudaEventRecord(recs[nrec].b, s);
+    ++nrec;
+}
+
+cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
+{
+    const NttTables& t0 = c.tab[0];
+    const int l1 = t0.l1, l2 = t0.l2;
+    const int N1 = 1 << l1, N2 = 1 << l2;
+    const int64_t P = (int64_t)N1 * N2;
+    const bool argmax = c.am.results != nullptr;
+    cudaError_t e;
+    for (int64_t p0 = 0; p0 < c.batch; p0 += c.chunk) {
+        const int64_t nb = (c.batch - p0 < c.chunk) ? c.batch - p0 : c.chunk;
+        for (int pi = 0; pi < c.np; ++pi) {
+            const NttTables& T = c.tab[pi];
+            Pass1Args a1;
+            memset(&a1, 0, sizeof(a1));
+            a1.op[0] = c.op[0];
+            a1.op[1] = c.op[1];
+            a1.Y = c.Y;
+            a1.tw = T.tw1f;
+            a1.twf = T.twf;
+            a1.stats = c.stats;
+            a1.m = T.m;
+            a1.p0 = t0.p;
+            a1.N2 = N2;
+            a1.zero_upper = c.zero_upper;
+            a1.skip_cs = pi > 0;
+            a1.pair0 = p0;
+            // both operands must use the same kernel instantiation (grid.y = 2)
+            const int dt = c.op[0].dtype, qm = c.op[0].q.mode;
+            const size_t tsz = (dt == DT_F32) ? 4 : 8;
+            const size_t smem1 = (size_t)32 * N1 * 4 + (size_t)kMaxThr * tsz;
+            if (c.op[1].dtype == dt && c.op[1].q.mode == qm) {
+                if (c.prof) c.prof->pre(KK_PASS1, s);
+                e = dispatch_p1(l1, a1, dt, qm, dim3(N2 / 32, 2, (unsigned)nb), smem1, s);
+                if (c.prof) c.prof->post(KK_PASS1, s);
+                if (e != cudaSuccess) return e;
+            } else {
+                // mixed quantiser modes: one launch per operand (grid.y = 1)
+                for (int op = 0; op < 2; ++op) {
+                    Pass1Args b1 = a1;
+                    b1.op[0] = c.op[op];
+                    b1.op[1] = c.op[op];
+                    b1.op_base = op;
+                    const int dto = c.op[op].dtype, qmo = c.op[op].q.mode;
+                    const size_t smo = (size_t)32 * N1 * 4 + (size_t)kMaxThr * (dto == DT_F32 ? 4 : 8);
+                    if (c.prof) c.prof->pre(KK_PASS1, s);
+                    e = dispatch_p1(l1, b1, dto, qmo, dim3(N2 / 32, 1, (unsigned)nb), smo, s);
+                    if (c.prof) c.prof->post(KK_PASS1, s);
+                    if (e != cudaSuccess) return e;
+                }
+            }
+            Pass2Args a2;
+            memset(&a2, 0, sizeof(a2));
+            a2.Y = c.Y;
+            a2.twf = T.tw2f;
+            a2.twi = T.tw2i;
+            a2.twinv = T.twi;
+            a2.stats = c.stats;
+            a2.m = T.m;
+            a2.p0 = t0.p;
+            a2.N1 = N1;
+            a2.skip_cs = pi > 0;
+            a2.pair0 = p0;
+            if (c.prof) c.prof->pre(KK_PASS2, s);
+            e = dispatch_p2(l2, a2, dim3(N1 / 32, (unsigned)nb), s);
+            if (c.prof) c.prof->post(KK_PASS2, s);
+            if (e != cudaSuccess) return e;
+            Pass3Args a3;
+            memset(&a3, 0, sizeof(a3));
+            a3.Y = c.Y;
+            a3.R = c.R;
+            a3.twi = T.tw1i;
+            a3.stats = c.stats;
+            a3.am = c.am;
+            a3.values = c.values;
+            a3.nout = c.nout;
+            a3.vld = c.nout;
+            a3.m = T.m;
+            a3.p0 = t0.p;
+            a3.N2 = N2;
+            a3.np = c.np;
+            a3.pi = pi;
+            a3.pair0 = p0;
+            if (c.prof) c.prof->pre(KK_PASS3, s);
+            e = argmax ? dispatch_p3_out<OUT_ARGMAX>(l1, a3, dim3(N2 / 32, (unsigned)nb), s)
+                       : dispatch_p3_out<OUT_VALUES>(l1, a3, dim3(N2 / 32, (unsigned)nb), s);
+            if (c.prof) c.prof->post(KK_PASS3, s);
+            if (e != cudaSuccess) return e;
+        }
+        if (c.np > 1) {
+            CombineArgs ca;
+            memset(&ca, 0, sizeof(ca));
+            ca.R = c.R;
+            ca.stats = c.stats;
+            ca.am = c.am;
+            ca.values = c.values;
+            ca.nout = c.nout;
+            ca.vld = c.nout;
+            ca.P = P;
+            for (int i = 0; i < c.np; ++i) {
+                ca.p[i] = c.tab[i].p;
+                ca.ginv[i] = c.garner_inv[i];
+            }
+            ca.p0 = t0.p;
+            ca.np = c.np;
+            ca.pair0 = p0;
+            int64_t span = argmax ? (c.am.t_hi - c.am.t_lo + 1) : c.nout;
+            int nblk = (int)((span + 256 * 8 - 1) / (256 * 8));
+            if (nblk > kMaxPartials) nblk = kMaxPartials;
+            if (nblk < 1) nblk = 1;
+            if (c.prof) c.prof->pre(KK_COMBINE, s);
+            if (argmax) k_combine<OUT_ARGMAX><<<dim3(nblk, (unsigned)nb), 256, 0, s>>>(ca);
+            else k_combine<OUT_VALUES><<<dim3(nblk, (unsigned)nb), 256, 0, s>>>(ca);
+            e = cudaGetLastError();
+            if (c.prof) c.prof->post(KK_COMBINE, s);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
+}  // namespace qx

@@ -1,0 +1,169 @@
+// qx_quant.cu -- quantiser support: exact threshold tables (host) and the
+// standalone quantise kernel behind quantize.apply (quantize.py:105-107).
+//
+// The reference evaluates Quantizer.__call__ (quantize.py:53-65) in float64
+// after upcasting every sample (signals.py:46).  Every reference quantiser is
+// monotone non-decreasing in its input, so for a given input type the map is
+// fully described by 2k thresholds T[i] = min{ v : q(v) >= i - k + 1 }, found
+// here by bisection over the totally ordered bit patterns of that type while
+// evaluating the reference formula in float64.  The kernels then compute
+// level(v) = -k + #{i : v >= T[i]}, which is exact for every finite or
+// infinite input (NaN is reported, the reference's result for it is
+// undefined).  This file is compiled without fast-math or FMA contraction.
+#include <cmath>
+#include <cstring>
+
+#include "qx_internal.h"
+
+namespace qx {
+
+// reference map, float64 (quantize.py:53-65)
+static long long ref_level(double v, int kind, long long k, double step, const double* thr)
+{
+    if (kind == 0) return v > 0.0 ? 1 : (v < 0.0 ? -1 : 0);  // np.sign
+    if (kind == 1) {
+        volatile double a = std::fabs(v) / step;  // volatile: no contraction
+        double s = v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0);
+        double o = s * std::floor(a + 0.5);
+        if (o > (double)k) o = (double)k;
+        if (o < -(double)k) o = -(double)k;
+        return (long long)o;
+    }
+    long long lo = 0, hi = 2 * k;  // searchsorted(t, v, side="right")
+    while (lo < hi) {
+        long long mid = (lo + hi) >> 1;
+        if (thr[mid] <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo - k;
+}
+
+static inline uint32_t f32_key(float f)
+{
+    uint32_t b;
+    std::memcpy(&b, &f, 4);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+static inline float f32_from_key(uint32_t k)
+{
+    uint32_t b = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+    float f;
+    std::memcpy(&f, &b, 4);
+    return f;
+}
+static inline uint64_t f64_key(double f)
+{
+    uint64_t b;
+    std::memcpy(&b, &f, 8);
+    return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+static inline double f64_from_key(uint64_t k)
+{
+    uint64_t b = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+    double f;
+    std::memcpy(&f, &b, 8);
+    return f;
+}
+
+// out[i] (i < 2k) = smallest value of the input type with level >= i-k+1
+int thresholds(int kind, long long k, double step, const double* thr, int dtype, double* out)
+{
+    for (long long i = 0; i < 2 * k; ++i) {
+        const long long want = i - k + 1;
+        if (dtype == DT_F32) {
+            uint32_t lo = f32_key(-INFINITY), hi = f32_key(INFINITY);
+            while (lo < hi) {
+                uint32_t mid = lo + (hi - lo) / 2;
+                if (ref_level((double)f32_from_key(mid), kind, k, step, thr) >= want) hi = mid;
+                else lo = mid + 1;
+            }
+            out[i] = (double)f32_from_key(lo);
+        } else {
+            uint64_t lo = f64_key(-INFINITY), hi = f64_key(INFINITY);
+            while (lo < hi) {
+                uint64_t mid = lo + (hi - lo) / 2;
+                if (ref_level(f64_from_key(mid), kind, k, step, thr) >= want) hi = mid;
+                else lo = mid + 1;
+            }
+            out[i] = f64_from_key(lo);
+        }
+    }
+    return 0;
+}
+
+// standalone quantise (apply): codes[b*n + i] = level(x[b*ld + i])
+struct QuantArgs {
+    const void* x;
+    int64_t ld, n, batch;
+    int64_t* codes;
+    unsigned long long* sums;  // [batch][2]: sumsq, nnz
+    unsigned* flags;
+    QTable q;
+};
+
+template <typename T, int QM>
+__global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QuantArgs a)
+{
+    __shared__ T sthr[kMaxThr];
+    for (int i = threadIdx.x; i < a.q.tsize; i += blockDim.x) sthr[i] = (T)a.q.thr[i];
+    __syncthreads();
+    const int64_t b = blockIdx.y;
+    const T* x = reinterpret_cast<const T*>(a.x) + b * a.ld;
+    const T t0 = sthr[0], t1 = sthr[1], inv_step = (T)a.q.inv_step;
+    unsigned long long ssq = 0, nnz = 0;
+    unsigned fl = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * blockDim.x) {
+        const T v = x[i];
+        if (v != v) fl |= SF_NONFINITE;
+        int c;
+        if constexpr (QM == QM_K1) c = level_k1(v, t0, t1);
+        else if constexpr (QM == QM_UNIFORM) c = level_uniform(v, sthr, a.q.k, inv_step);
+        else c = level_bsearch(v, sthr, a.q.tbits) - a.q.k;
+        a.codes[b * a.n + i] = c;
+        ssq += (unsigned long long)((long long)c * c);
+        nnz += (c != 0);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (a.sums) {
+            atomicAdd(a.sums + 2 * b, ssq);
+            atomicAdd(a.sums + 2 * b + 1, nnz);
+        }
+        if (fl) atomicOr(a.flags, fl);
+    }
+}
+
+
+cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
+                            int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s)
+{
+    QuantArgs a;
+    a.x = x;
+    a.ld = ld;
+    a.n = n;
+    a.batch = batch;
+    a.codes = codes;
+    a.sums = sums;
+    a.flags = flags;
+    a.q = q;
+    int gx = (int)((n + 255) / 256);
+    if (gx > 1184) gx = 1184;
+    dim3 grid(gx, (unsigned)batch);
+    if (dtype == DT_F32) {
+        if (q.mode == QM_K1) k_quantize<float, QM_K1><<<grid, 256, 0, s>>>(a);
+        else if (q.mode == QM_UNIFORM) k_quantize<float, QM_UNIFORM><<<grid, 256, 0, s>>>(a);
+        else k_quantize<float, QM_BSEARCH><<<grid, 256, 0, s>>>(a);
+    } else {
+        if (q.mode == QM_K1) k_quantize<double, QM_K1><<<grid, 256, 0, s>>>(a);
+        else if (q.mode == QM_UNIFORM) k_quantize<double, QM_UNIFORM><<<grid, 256, 0, s>>>(a);
+        else k_quantize<double, QM_BSEARCH><<<grid, 256, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace qx

@@ -1,0 +1,75 @@
+"""C ABI checks that need no GPU: the library loads, exports every symbol
+include/qxcorr_b200.h declares, and its host-side exact threshold tables
+reproduce the reference quantisers on the golden vectors."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_every_declared_symbol():
+    from paper_2509_19974_b200 import _native as N
+
+    L = N.load()
+    header = open(os.path.join(ROOT, "include", "qxcorr_b200.h")).read()
+    declared = set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(qx_[a-z_0-9]+)\s*\(", header, re.M))
+    assert declared == set(N.EXPORTS), declared ^ set(N.EXPORTS)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert L.qx_abi_version() == 1
+    assert L.qx_status_string(2) == b"quantizes to all zeros"
+
+
+def _levels(thr, vals, k):
+    # level(v) = -k + #{i : v >= T[i]}
+    return np.searchsorted(thr, vals, side="right") - k
+
+
+def test_thresholds_reproduce_reference(golden, qrec):
+    from paper_2509_19974_b200 import quantize
+
+    meta, arr = golden
+    for i, qd in enumerate(meta["quant"]):
+        q = qrec(qd)
+        vals, want = arr[f"q{i}_in"], arr[f"q{i}_out"]
+        dt = "float32" if vals.dtype == np.float32 else "float64"
+        thr = quantize.thresholds(q, dt)
+        assert thr.size == 2 * q.k and np.all(np.diff(thr) >= 0)
+        got = _levels(thr.astype(vals.dtype), vals, q.k)
+        assert np.array_equal(got, want), (i, qd)
+
+
+def test_thresholds_exhaustive_float32_sample():
+    """Dense sweep over float32 bit patterns for the C2 b=4 quantiser: the
+    threshold map equals the reference formula in float64 on every sample."""
+    from paper_2509_19974_b200 import quantize, workloads as W
+
+    q = W.bit_quantizer(4, W.C2_SIGMA)
+    thr = quantize.thresholds(q, "float32").astype(np.float32)
+    bits = np.arange(0, 1 << 32, 4099, dtype=np.uint64).astype(np.uint32)
+    v = bits.view(np.float32)
+    v = v[~np.isnan(v)]
+    ref = np.clip(np.sign(v.astype(np.float64)) * np.floor(np.abs(v.astype(np.float64)) / q.step + 0.5),
+                  -q.k, q.k).astype(np.int64)
+    assert np.array_equal(_levels(thr, v, q.k), ref)
+
+
+def test_quantizer_validation_errors():
+    from paper_2509_19974_b200 import _native as N
+    from paper_2509_19974_b200 import quantize
+
+    import pytest
+
+    with pytest.raises(ValueError):
+        quantize.custom([0.5, 1.0])
+    with pytest.raises(ValueError):
+        quantize.custom([1.0, -1.0])
+    with pytest.raises(ValueError):
+        quantize.Quantizer(kind="uniform", k=0)
+    bad = N.QxQuantizer(N.QX_Q_UNIFORM, 0, 3, -1.0, None)
+    out = np.empty(6)
+    assert N.load().qx_quantizer_thresholds(ctypes.byref(bad), N.QX_F32, out.ctypes.data) == N.QX_ERR_INVALID

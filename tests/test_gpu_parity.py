@@ -1,0 +1,302 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Integer results must be bit-exact."""
+
+import hashlib
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.int64).tobytes()).hexdigest()[:16]
+
+
+@pytest.fixture(scope="module")
+def qx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2509_19974_b200 as P
+
+    return P
+
+
+def test_native_library_loaded(qx):
+    from paper_2509_19974_b200 import _native as N
+
+    N.context()
+    import os
+
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert "libqxcorr_b200.so" in maps
+
+
+def test_quantize_kernel_matches_reference(qx, golden, qrec):
+    import torch
+
+    from paper_2509_19974_b200.quantize import quantize_device
+
+    meta, arr = golden
+    for i, qd in enumerate(meta["quant"]):
+        vals, want = arr[f"q{i}_in"], arr[f"q{i}_out"]
+        x = torch.from_numpy(vals).cuda()
+        codes, sums = quantize_device(qrec(qd), x, with_stats=True)
+        assert np.array_equal(codes.cpu().numpy(), want), (i, qd)
+        assert int(sums[0, 0]) == int(np.sum(want * want))
+        assert int(sums[1, 0]) == int(np.count_nonzero(want))
+
+
+def test_apply_and_call(qx):
+    q = qx.uniform(4, 1.0)
+    assert q([0.49, 0.5, 1.49, 1.5, -0.5, -1.5]).tolist() == [0, 1, 1, 2, -1, -2]
+    assert qx.sign()([-3.5, -0.0, 0.0, 1e-12, 2.0]).tolist() == [-1, 0, 0, 1, 1]
+    s = qx.Signal(-3, [0.2, -1.7, 0.0])
+    out = qx.apply(qx.uniform(2, 1.0), s)
+    assert out.start == -3 and out.samples.tolist() == [0, -2, 0] and out.bound == 2
+
+
+def test_xcorr_full_matches_reference(qx, golden):
+    meta, arr = golden
+    for i, d in enumerate(meta["xcorr"]):
+        u = qx.IntSignal(d["u_start"], arr[f"x{i}_u"], d["ku"])
+        v = qx.IntSignal(d["v_start"], arr[f"x{i}_v"], d["kv"])
+        c = qx.xcorr_int_bf(u, v)
+        assert c.first_lag == d["first_lag"], i
+        assert np.array_equal(c.values, arr[f"x{i}_c"]), i
+        assert c.norm_x == d["norm_x"] and c.norm_y == d["norm_y"]
+        assert qx.argmax_set(c) == d["argmax"]
+
+
+def test_acceptance_criterion2_on_gpu(qx, golden):
+    """The 1000 seeded pairs of the reference's acceptance criterion 2,
+    correlated on the GPU, hash to the reference's brute-force digests."""
+    import test_oracle_golden as T
+
+    meta, _ = golden
+    acc = meta["acceptance_c2"]
+    fixed = T._edge_pairs()
+    for rec in acc["records"]:
+        if "skipped" in rec:
+            continue
+        (su, u, ku), (sv, v, kv) = T._acceptance_pair(acc["seed"], rec["case"], fixed)
+        c = qx.xcorr_int_gpu(qx.IntSignal(su, u, ku), qx.IntSignal(sv, v, kv))
+        assert sha(c.values) == rec["sha"] and c.first_lag == rec["first_lag"], rec
+
+
+def _q(qx, d):
+    if d["kind"] == "sign":
+        return qx.sign()
+    if d["kind"] == "uniform":
+        return qx.uniform(d["k"], d["step"])
+    return qx.custom(d["thresholds"])
+
+
+def test_estimate_matches_reference(qx, golden):
+    meta, arr = golden
+    for i, d in enumerate(meta["estimate"]):
+        x = qx.Signal(d["x_start"], arr[f"e{i}_x"])
+        y = qx.Signal(d["y_start"], arr[f"e{i}_y"])
+        want = d["result"]
+        kw = dict(d["kw"])
+        if "raises" in want:
+            with pytest.raises(Exception) as ei:
+                qx.estimate(x, y, _q(qx, d["qx"]), _q(qx, d["qy"]), **kw)
+            assert type(ei.value).__name__ == want["raises"], (i, want)
+            continue
+        r = qx.estimate(x, y, _q(qx, d["qx"]), _q(qx, d["qy"]), **kw)
+        assert list(r.lags) == want["lags"], (i, r, want)
+        assert r.peak_value_int == want["peak"]
+        assert r.tie_broken == want["tie_broken"]
+        assert [[a, b] for a, b in r.tie_break_values] == want["tie_break_values"]
+        assert r.method == want["method"]
+
+
+def test_c1(qx, golden):
+    from paper_2509_19974_b200 import workloads as W
+
+    meta, _ = golden
+    x, y = W.c1(0)
+    r = qx.estimate(qx.Signal(0, x), qx.Signal(0, y), qx.sign(), qx.sign())
+    g = meta["configs"]["c1"]
+    assert list(r.lags) == g["lags"] == [-137] and r.peak_value_int == g["peak"] == 14839
+
+
+def test_c2_golden_pairs(qx, golden):
+    import torch
+
+    from paper_2509_19974_b200 import workloads as W
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    meta, _ = golden
+    xs, ys, lag = W.c2(pairs=3)
+    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    for b in (1, 2, 4, 8):
+        q = W.bit_quantizer(b, W.C2_SIGMA)
+        res = qx.estimate_batch(xd, yd, q, q).numpy()
+        vals, _ = xcorr_full_device(xd, yd, q, q)
+        for g in [g for g in meta["configs"]["c2"] if g["b"] == b]:
+            p = g["pair"]
+            assert res["value"][p] == g["peak"] and res["lag"][p] == g["lags"][0]
+            assert res["ties"][p] == len(g["lags"])
+            assert res["sumsq_x"][p] == g["sumsq_u"] and res["sumsq_y"][p] == g["sumsq_v"]
+            assert sha(vals[p].cpu().numpy()) == g["sha"], (b, p)
+            assert g["lags"][0] == g["expected"]
+
+
+def test_c3_golden_window(qx, golden):
+    import torch
+
+    from paper_2509_19974_b200 import workloads as W
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    meta, _ = golden
+    xs, ys, lag = W.c3(pairs=256)
+    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    for b in (2, 4):
+        q = W.bit_quantizer(b, W.C3_SIGMA)
+        res = qx.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512).numpy()
+        vals, _ = xcorr_full_device(xd, yd, q, q)
+        first = -(W.C3_N - 1)
+        win = vals[:, -512 - first:-512 - first + 1025].cpu().numpy()
+        for g in [g for g in meta["configs"]["c3"] if g["b"] == b]:
+            p = g["pair"]
+            assert res["value"][p] == g["peak"] and res["lag"][p] == g["lags"][0], (b, p)
+            assert res["ties"][p] == len(g["lags"])
+            assert sha(win[p]) == g["sha"]
+
+
+def test_c4_small_and_c5_small(qx, golden):
+    import torch
+
+    from paper_2509_19974_b200 import workloads as W
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    meta, _ = golden
+    g = meta["configs"]["c4_small"]
+    x4, y4, l4 = W.c4(n=g["n"], delay=g["delay"])
+    q4 = W.bit_quantizer(4, W.C4_SIGMA)
+    r = qx.estimate(qx.Signal(0, x4), qx.Signal(0, y4), q4, q4)
+    assert list(r.lags) == g["lags"] and r.peak_value_int == g["peak"]
+    vals, _ = xcorr_full_device(torch.from_numpy(x4).cuda(), torch.from_numpy(y4).cuda(), q4, q4)
+    assert sha(vals[0].cpu().numpy()) == g["sha"]
+    g5 = meta["configs"]["c5_small"]
+    t5, s5, off, sn2 = W.c5(stream=g5["stream"], template=g5["template"], offset=g5["offset"])
+    for case in g5["cases"]:
+        qa, qb = _q(qx, case["qx"]), _q(qx, case["qy"])
+        nvalid = g5["stream"] - g5["template"]
+        res = qx.estimate_batch(t5[None], s5[None], qa, qb, lag_lo=0, lag_hi=nvalid).numpy()
+        assert res["value"][0] == case["peak"] and res["lag"][0] == case["lags"][0]
+        assert res["ties"][0] == len(case["lags"]) and case["lags"][0] == off
+
+
+def test_random_pairs_against_oracle(qx, oracle):
+    """Seeded sweep of lengths, quantisers, dtypes and windows vs the oracle."""
+    import torch
+
+    rng = np.random.default_rng(7)
+    quants = [qx.sign(), qx.uniform(1, 0.7), qx.uniform(7, 0.3), qx.uniform(127, 0.02),
+              qx.custom([-1.0, -0.2, 0.3, 1.1]), qx.uniform(40, 0.05)]
+    for trial in range(60):
+        B = int(rng.integers(1, 5))
+        nx = int(rng.integers(1, 3000))
+        ny = int(rng.integers(1, 3000))
+        dt = np.float32 if trial % 2 else np.float64
+        x = (rng.standard_normal((B, nx)) * rng.uniform(0.1, 3)).astype(dt)
+        y = (rng.standard_normal((B, ny)) * rng.uniform(0.1, 3)).astype(dt)
+        qa = quants[int(rng.integers(len(quants)))]
+        qb = quants[int(rng.integers(len(quants)))]
+        nout = nx + ny - 1
+        t_lo = int(rng.integers(0, nout))
+        t_hi = int(rng.integers(t_lo, nout))
+        first = -(nx - 1)
+        res = qx.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), qa, qb,
+                                lag_lo=first + t_lo, lag_hi=first + t_hi).numpy()
+        for b in range(B):
+            u, v = oracle.quantize(qa, x[b]), oracle.quantize(qb, y[b])
+            if not u.any() or not v.any():
+                assert res["status"][b] == 2
+                continue
+            c = oracle.xcorr_bf(u, v, t_lo, t_hi)
+            m, f, n = oracle.argmax(c)
+            assert (res["value"][b], res["lag"][b], res["ties"][b]) == (m, first + t_lo + f, n), trial
+            assert res["sumsq_x"][b] == oracle.sumsq(u) and res["sumsq_y"][b] == oracle.sumsq(v)
+
+
+def test_multiprime_path_saturated(qx, oracle):
+    """Saturated b=8 codes defeat the Cauchy-Schwarz single-prime test, so
+    the 2-prime CRT path must reproduce the exact (large) values."""
+    import torch
+
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    rng = np.random.default_rng(9)
+    n = 1 << 15
+    x = (rng.standard_normal(n) + 30).astype(np.float32)
+    y = (rng.standard_normal(n) + 30).astype(np.float32)
+    y[::7] *= -1
+    q = qx.uniform(127, 0.1)
+    u, v = oracle.quantize(q, x), oracle.quantize(q, y)
+    want = oracle.xcorr_ks(u, v, 127, 127)
+    assert np.abs(want).max() > 600_000_000  # beyond a single prime's centred range
+    vals, _ = xcorr_full_device(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), q, q)
+    assert np.array_equal(vals[0].cpu().numpy(), want)
+    res = qx.estimate_batch(x[None], y[None], q, q).numpy()
+    m, f, cnt = oracle.argmax(want)
+    assert (res["value"][0], res["lag"][0], res["ties"][0]) == (m, -(n - 1) + f, cnt)
+
+
+def test_errors_match_reference(qx):
+    with pytest.raises(qx.DegenerateQuantization, match="x quantizes"):
+        qx.estimate(qx.Signal(0, [0.01, -0.02, 0.03]), qx.Signal(0, [1.0, -1.0, 1.0]), qx.uniform(4, 1.0),
+                    qx.uniform(4, 1.0))
+    with pytest.raises(qx.DegenerateQuantization, match="y quantizes"):
+        qx.estimate(qx.Signal(0, [1.0, -1.0, 1.0]), qx.Signal(0, [0.01, -0.02, 0.03]), qx.uniform(4, 1.0),
+                    qx.uniform(4, 1.0))
+    with pytest.raises(ValueError):
+        qx.estimate(qx.Signal(0, [1.0, -1.0]), qx.Signal(0, [1.0, -1.0]), qx.sign(), qx.sign(), method="phat")
+    huge = qx.IntSignal(0, [1, 1], bound=1 << 40)
+    with pytest.raises(ValueError):
+        qx.xcorr_int_bf(huge, huge)
+    with pytest.raises(qx.DegenerateInput):
+        qx.xcorr_int_ks(qx.IntSignal(0, [0, 0], 1), qx.IntSignal(0, [1], 1))
+    with pytest.raises(ValueError):
+        qx.estimate(qx.Signal(0, [1.0, np.nan]), qx.Signal(0, [1.0, 2.0]), qx.sign(), qx.sign())
+    with pytest.raises(ValueError):
+        qx.estimate_batch(np.ones((1, 8), np.float32), np.ones((1, 8), np.float32), qx.sign(), qx.sign(),
+                          lag_lo=100, lag_hi=200)
+
+
+def test_host_entry_point(qx, oracle):
+    from paper_2509_19974_b200 import workloads as W
+
+    xs, ys, lag = W.c2(pairs=2, n=1 << 14)
+    q = W.bit_quantizer(2, W.C2_SIGMA)
+    res = qx.estimate_batch_host(xs, ys, q, q)
+    want = oracle.estimate_batch_f32(xs, ys, q, q)
+    assert np.array_equal(res["value"], want[:, 0])
+    assert np.array_equal(res["lag"], want[:, 1] - (xs.shape[1] - 1))
+    assert np.array_equal(res["ties"], want[:, 2])
+
+
+def test_c2_full_size_properties(qx, oracle):
+    """BASELINE config 2 at full size (64 pairs x 2^18, b = 1, 2, 4, 8): every
+    pair finds its true delay; a sample of pairs is checked exactly against
+    the oracle's Kronecker-substitution correlation (GMP)."""
+    import torch
+
+    from paper_2509_19974_b200 import workloads as W
+
+    xs, ys, lag = W.c2()
+    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    for b in (1, 2, 4, 8):
+        q = W.bit_quantizer(b, W.C2_SIGMA)
+        res = qx.estimate_batch(xd, yd, q, q).numpy()
+        assert np.array_equal(res["lag"], lag), b
+        assert np.all(res["ties"] == 1) and np.all(res["status"] == 0)
+        sel = [0, 17, 63]
+        want = oracle.estimate_batch_f32(xs[sel], ys[sel], q, q, threads=3)
+        assert np.array_equal(res["value"][sel], want[:, 0])
+        assert np.array_equal(res["lag"][sel], want[:, 1] - (W.C2_N - 1))

@@ -27,6 +27,8 @@ def as_device(a, dtype=None):
             x = x.to("cuda", non_blocking=False)
         return x.contiguous()
     arr = np.ascontiguousarray(a)
+    if not arr.flags.writeable:
+        arr = arr.copy()
     x = t.from_numpy(arr)
     if dtype is not None and x.dtype != dtype:
         x = x.to(dtype)
@@ -53,8 +55,10 @@ def signals(x, start: int = 0) -> N.QxSignals:
     if x.dim() == 1:
         n, ld = x.shape[0], x.shape[0]
     elif x.dim() == 2:
-        n, ld = x.shape[1], x.stride(0)
-        if x.stride(1) != 1:
+        # a size-1 dimension may carry any stride in torch; rows are what matter
+        n = x.shape[1]
+        ld = x.stride(0) if x.shape[0] > 1 else n
+        if x.stride(1) != 1 and n > 1:
             raise ValueError("rows must be contiguous")
     else:
         raise ValueError("signals must be 1-D or (batch, n)")

@@ -233,10 +233,11 @@ def test_multiprime_path_saturated(qx, oracle):
     from paper_2509_19974_b200.intxcorr import xcorr_full_device
 
     rng = np.random.default_rng(9)
-    n = 1 << 15
+    n = 1 << 16
     x = (rng.standard_normal(n) + 30).astype(np.float32)
     y = (rng.standard_normal(n) + 30).astype(np.float32)
-    y[::7] *= -1
+    y[::97] *= -1
+    x[::89] = 0.0
     q = qx.uniform(127, 0.1)
     u, v = oracle.quantize(q, x), oracle.quantize(q, y)
     want = oracle.xcorr_ks(u, v, 127, 127)

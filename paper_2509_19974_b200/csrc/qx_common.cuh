@@ -103,15 +103,16 @@ __device__ __forceinline__ int level_bsearch(T v, const T* s, int tbits)
 template <typename T>
 __device__ __forceinline__ int level_uniform(T v, const T* s, int k, T inv_step)
 {
-    // estimate: round-half-away of |v|/step, clamped (any small error in the
-    // estimate is removed by the exact compares below)
+    // estimate: round-half-away of |v|/step, clamped.  For k <= 128 the
+    // estimate of |v|/step + 0.5 (<= 128.5) is within 2^-16 of the float64
+    // value, so it is off by at most one level; one exact compare in each
+    // direction fixes it: level >= j  <=>  v >= s[j + k - 1].
     T a = v < T(0) ? -v : v;
     T e = a * inv_step + T(0.5);
     int lv = e >= T(k) ? k : (int)e;   // NaN -> 0 (flagged separately)
     if (v < T(0)) lv = -lv;
-    // exact fix-up: level >= j  <=>  v >= s[j + k - 1]
-    while (lv < k && v >= s[lv + k]) ++lv;
-    while (lv > -k && !(v >= s[lv + k - 1])) --lv;
+    if (lv < k && v >= s[lv + k]) ++lv;
+    if (lv > -k && !(v >= s[lv + k - 1])) --lv;
     return lv;
 }
 

@@ -52,10 +52,10 @@ struct NttTables {
     ModP m;
     uint32_t p;
     int lp, l1, l2;
-    const uint2* tw1f;  // DIF stage twiddles for N1 = 2^l1 (Shoup pairs)
-    const uint2* tw1i;  // inverse (DIT) stage twiddles for N1
-    const uint2* tw2f;
-    const uint2* tw2i;
+    const uint2* g1f;  // DIF group twiddles for N1 = 2^l1 (Shoup pairs, Sched layout)
+    const uint2* g1i;  // DIT (inverse) group twiddles for N1
+    const uint2* g2f;  // same for N2
+    const uint2* g2i;
     const uint32_t* twf;  // forward four-step twiddles [P] (Montgomery form)
     const uint32_t* twi;  // inverse four-step twiddles [P] incl. R^2/P
 };

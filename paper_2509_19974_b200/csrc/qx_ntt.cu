@@ -14,27 +14,38 @@
 //           natural order -> centred lift -> argmax / values / residues
 // Forward transforms are DIF (natural in, bit-reversed out), inverses DIT
 // (bit-reversed in, natural out) so no permutation pass exists.  Inside a
-// tile each lane owns one vector (column or row) and the 32 vectors sit in
-// shared memory with an XOR swizzle, conflict-free both for the transform
-// (lane = vector) and for row-contiguous global I/O (lane = element).
+// tile each lane owns one vector (column or row); the 32 vectors of element e
+// sit at shared words e*33 + lane (one pad word per row), which is
+// bank-conflict-free both for the transform (lane = vector) and for
+// row-contiguous global I/O (lane = element), and turns every register-group
+// access into base + compile-time offset.  Each register group of R radix-2
+// stages reads its 2^R - 1 twiddles (Shoup pairs) as a contiguous block of a
+// per-transform table staged in shared memory (warp-broadcast loads).
 // tools/ntt_model.py is an exact-arithmetic model of the same index math.
+#include <climits>
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#include <type_traits>
 
 #include "qx_internal.h"
 
+#ifndef QX_NTT_THREADS
+#define QX_NTT_THREADS 512
+#endif
+
 namespace qx {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = QX_NTT_THREADS;
 constexpr int kWarps = kThreads / 32;
-
-__device__ __forceinline__ int sidx(int e, int c) { return (e << 5) + (c ^ (e & 31)); }
+constexpr int kPad = 33;  // words per element row of a 32-vector tile
 
 // register-group schedule of a length-2^LOG transform: ceil(LOG/4) groups,
-// radices 2^3..2^4, larger first (DIF order; DIT uses the reverse).
+// radices 2^3..2^4, larger first (DIF order; DIT uses the reverse), and the
+// layout of the per-group twiddle blocks.
 template <int LOG>
 struct Sched {
+    static constexpr int L = 1 << LOG;
     static constexpr int NG = (LOG + 3) / 4;
     static constexpr int BASE = LOG / NG;
     static constexpr int EXTRA = LOG % NG;
@@ -43,100 +54,133 @@ struct Sched {
     // DIT group i = DIF group NG-1-i
     static constexpr int rd(int i) { return r(NG - 1 - i); }
     static constexpr int s0d(int i) { return i == 0 ? 0 : s0d(i - 1) + rd(i - 1); }
+    // distinct j0 values per group and twiddle-block offsets (uint2 units)
+    static constexpr int nj_dif(int i) { return L >> (s0(i) + r(i)); }
+    static constexpr int nj_dit(int i) { return 1 << s0d(i); }
+    static constexpr int twoff_dif(int i) { return i == 0 ? 0 : twoff_dif(i - 1) + nj_dif(i - 1) * (1 << r(i - 1)); }
+    static constexpr int twoff_dit(int i) { return i == 0 ? 0 : twoff_dit(i - 1) + nj_dit(i - 1) * (1 << rd(i - 1)); }
+    static constexpr int TW_DIF = twoff_dif(NG);
+    static constexpr int TW_DIT = twoff_dit(NG);
 };
 
 // ---------------------------------------------------------------- groups
 
-// R DIF stages on 2^R registers; element k of the group sits at position
-// j0 + k*S of a block of size S*2^R whose first stage is global stage S0.
-template <int R, int S0>
-__device__ __forceinline__ void dif_regs(uint32_t (&x)[1 << R], int j0, int S,
-                                         const uint2* __restrict__ tw, const ModP& m)
+// DIF group I on 2^R registers (element k at j0 + k*S of its block).
+// Twiddles: block j0 of group I, stage t at [2^R - 2^(R-t), +2^(R-1-t)).
+template <int LOG, int I>
+__device__ __forceinline__ void dif_regs(uint32_t (&x)[1 << Sched<LOG>::r(I)], int j0, const uint2* stw,
+                                         const ModP& m)
 {
+    constexpr int R = Sched<LOG>::r(I);
+    const uint2* tw = stw + Sched<LOG>::twoff_dif(I) + j0 * (1 << R);
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int h = 1 << (R - 1 - t);
+        const int off = (1 << R) - (1 << (R - t));
 #pragma unroll
         for (int kp = 0; kp < h; ++kp) {
-            const uint2 w = __ldg(&tw[(j0 + kp * S) << (S0 + t)]);
+            const uint2 w = tw[off + kp];
 #pragma unroll
             for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dif(x[blk + kp], x[blk + kp + h], w, m);
         }
     }
 }
 
-// R DIT stages; element k sits at j0 + (k << S0) of a block of size 2^(S0+R).
-template <int R, int S0, int LOG>
-__device__ __forceinline__ void dit_regs(uint32_t (&x)[1 << R], int j0,
-                                         const uint2* __restrict__ tw, const ModP& m)
+// DIT group I (element k at j0 + (k << S0) of its block); stage t twiddles
+// at [2^t - 1, +2^t).
+template <int LOG, int I>
+__device__ __forceinline__ void dit_regs(uint32_t (&x)[1 << Sched<LOG>::rd(I)], int j0, const uint2* stw,
+                                         const ModP& m)
 {
+    constexpr int R = Sched<LOG>::rd(I);
+    const uint2* tw = stw + Sched<LOG>::twoff_dit(I) + j0 * (1 << R);
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int h = 1 << t;
 #pragma unroll
         for (int kp = 0; kp < h; ++kp) {
-            const int j = j0 + (kp << S0);
-            const uint2 w = __ldg(&tw[j << (LOG - S0 - t - 1)]);
+            const uint2 w = tw[h - 1 + kp];
 #pragma unroll
             for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dit(x[blk + kp], x[blk + kp + h], w, m);
         }
     }
 }
 
-// one DIF group pass over a swizzled smem tile (all warps)
-template <int LOG, int S0, int R>
-__device__ __forceinline__ void dif_pass(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+// DIF group I over one or two smem tiles (two share the twiddle loads)
+template <int LOG, int I, int NT>
+__device__ __forceinline__ void dif_group_smem(uint32_t* s0, uint32_t* s1, const uint2* stw, const ModP& m)
 {
-    constexpr int L = 1 << LOG, B = L >> S0, S = B >> R, NGRP = L >> R;
+    using SC = Sched<LOG>;
+    constexpr int R = SC::r(I), S0 = SC::s0(I), B = SC::L >> S0, S = B >> R, NGRP = SC::L >> R;
     const int lane = threadIdx.x & 31;
+#pragma unroll 1
     for (int g = threadIdx.x >> 5; g < NGRP; g += kWarps) {
         const int j0 = g & (S - 1);
-        const int base = (g / S) * B + j0;
+        const int off = ((g / S) * B + j0) * kPad + lane;
         uint32_t x[1 << R];
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) x[k] = s[sidx(base + k * S, lane)];
-        dif_regs<R, S0>(x, j0, S, tw, m);
+        for (int k = 0; k < (1 << R); ++k) x[k] = s0[off + k * S * kPad];
+        if constexpr (NT == 2) {
+            uint32_t y[1 << R];
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) s[sidx(base + k * S, lane)] = x[k];
+            for (int k = 0; k < (1 << R); ++k) y[k] = s1[off + k * S * kPad];
+            dif_regs<LOG, I>(y, j0, stw, m);
+#pragma unroll
+            for (int k = 0; k < (1 << R); ++k) s1[off + k * S * kPad] = y[k];
+        }
+        dif_regs<LOG, I>(x, j0, stw, m);
+#pragma unroll
+        for (int k = 0; k < (1 << R); ++k) s0[off + k * S * kPad] = x[k];
     }
 }
 
-template <int LOG, int S0, int R>
-__device__ __forceinline__ void dit_pass(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+template <int LOG, int I>
+__device__ __forceinline__ void dit_group_smem(uint32_t* s, const uint2* stw, const ModP& m)
 {
-    constexpr int L = 1 << LOG, NGRP = L >> R;
+    using SC = Sched<LOG>;
+    constexpr int R = SC::rd(I), S0 = SC::s0d(I), NGRP = SC::L >> R;
     const int lane = threadIdx.x & 31;
+#pragma unroll 1
     for (int g = threadIdx.x >> 5; g < NGRP; g += kWarps) {
         const int j0 = g & ((1 << S0) - 1);
-        const int base = (g >> S0) * (1 << (S0 + R)) + j0;
+        const int off = ((g >> S0) * (1 << (S0 + R)) + j0) * kPad + lane;
         uint32_t x[1 << R];
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) x[k] = s[sidx(base + (k << S0), lane)];
-        dit_regs<R, S0, LOG>(x, j0, tw, m);
+        for (int k = 0; k < (1 << R); ++k) x[k] = s[off + (k << S0) * kPad];
+        dit_regs<LOG, I>(x, j0, stw, m);
 #pragma unroll
-        for (int k = 0; k < (1 << R); ++k) s[sidx(base + (k << S0), lane)] = x[k];
+        for (int k = 0; k < (1 << R); ++k) s[off + (k << S0) * kPad] = x[k];
     }
 }
 
-// DIF groups [I, NG-1) (all but the first and last), syncs after each
-template <int LOG, int I>
-__device__ __forceinline__ void dif_middle(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+// DIF groups [I, NG-1) with a barrier after each
+template <int LOG, int I, int NT>
+__device__ __forceinline__ void dif_middle(uint32_t* s0, uint32_t* s1, const uint2* stw, const ModP& m)
 {
     if constexpr (I < Sched<LOG>::NG - 1) {
-        dif_pass<LOG, Sched<LOG>::s0(I), Sched<LOG>::r(I)>(s, tw, m);
+        dif_group_smem<LOG, I, NT>(s0, s1, stw, m);
         __syncthreads();
-        dif_middle<LOG, I + 1>(s, tw, m);
+        dif_middle<LOG, I + 1, NT>(s0, s1, stw, m);
     }
 }
 
+// DIT groups [I, NG-1)
 template <int LOG, int I>
-__device__ __forceinline__ void dit_middle(uint32_t* s, const uint2* __restrict__ tw, const ModP& m)
+__device__ __forceinline__ void dit_middle(uint32_t* s, const uint2* stw, const ModP& m)
 {
     if constexpr (I < Sched<LOG>::NG - 1) {
-        dit_pass<LOG, Sched<LOG>::s0d(I), Sched<LOG>::rd(I)>(s, tw, m);
+        dit_group_smem<LOG, I>(s, stw, m);
         __syncthreads();
-        dit_middle<LOG, I + 1>(s, tw, m);
+        dit_middle<LOG, I + 1>(s, stw, m);
     }
+}
+
+// copy a twiddle table (uint2) into shared memory, all threads
+__device__ __forceinline__ void stage_table(uint2* dst, const uint2* __restrict__ src, int n)
+{
+    const uint4* s4 = reinterpret_cast<const uint4*>(src);
+    uint4* d4 = reinterpret_cast<uint4*>(dst);
+    for (int i = threadIdx.x; i < n / 2; i += kThreads) d4[i] = __ldg(&s4[i]);
 }
 
 // ------------------------------------------------------------ statistics
@@ -180,8 +224,8 @@ __device__ __forceinline__ int load_code(const T* __restrict__ src, int64_t i, c
 struct Pass1Args {
     OperandDesc op[2];
     uint32_t* Y;
-    const uint2* tw;
-    const uint32_t* twf;
+    const uint2* gtw;     // DIF group twiddles for N1
+    const uint32_t* twf;  // forward four-step twiddles [P]
     unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -192,14 +236,22 @@ struct Pass1Args {
     int64_t pair0;
 };
 
-template <int LOG1, typename T, int QM>
+template <int LOG1>
+constexpr size_t pass1_smem(size_t tsz)
+{
+    return (size_t)(1 << LOG1) * kPad * 4 + (size_t)Sched<LOG1>::TW_DIF * 8 + (size_t)kMaxThr * tsz;
+}
+
+template <int LOG1, typename T, int QM, bool ZU>
 __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ Pass1Args a)
 {
     constexpr int N1 = 1 << LOG1;
     using SC = Sched<LOG1>;
     constexpr int R0 = SC::r(0), S = N1 >> R0, RAD0 = 1 << R0;
-    constexpr int RL = SC::r(SC::NG - 1), S0L = SC::s0(SC::NG - 1), RADL = 1 << RL;
+    constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
     extern __shared__ __align__(16) uint32_t smem[];
+    uint2* stw = reinterpret_cast<uint2*>(smem + N1 * kPad);
+    T* sthr = reinterpret_cast<T*>(stw + SC::TW_DIF);
 
     const int op = a.op_base + blockIdx.y;
     const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
@@ -210,8 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     const int col = blockIdx.x * 32 + lane;
     const ModP m = a.m;
 
-    // thresholds -> smem (after the tile)
-    T* sthr = reinterpret_cast<T*>(smem + N1 * 32);
+    stage_table(stw, a.gtw, SC::TW_DIF);
     if constexpr (QM != QM_CODES) {
         for (int i = threadIdx.x; i < d.q.tsize; i += kThreads) sthr[i] = (T)d.q.thr[i];
     }
@@ -223,28 +274,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld;
     const int64_t n = d.n;
     const bool rev = d.reverse;
+    // every element of this tile's loaded rows is in range (no per-element checks)
+    const int rows_loaded = ZU ? N1 / 2 : N1;
+    const bool full = (int64_t)(rows_loaded - 1) * N2 + blockIdx.x * 32 + 31 < n;
+    const T* base = rev ? src + (n - 1 - col) : src + col;
+    const int rstride = rev ? -N2 : N2;
+    constexpr int NLD = ZU ? RAD0 / 2 : RAD0;  // rows actually loaded per group
 
-    unsigned long long ssq = 0, nnz = 0;
+    // per-thread sums stay far below 2^32 (<= 64 samples of k^2 <= 2^14)
+    unsigned ssq = 0, nnz = 0;
     unsigned flags = 0;
+    auto to_res = [&](int c) -> uint32_t {
+        ssq += (unsigned)(c * c);
+        nnz += (c != 0);
+        return c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
+    };
     // first DIF group straight from global memory (coalesced: lane = column)
-    for (int g = warp; g < S; g += kWarps) {
-        uint32_t x[RAD0];
+    if (full) {
+        // register double buffer: the next group's raw samples are in flight
+        // while this group is quantised and transformed
+        using Raw = typename std::conditional<QM == QM_CODES, long long, T>::type;
+        Raw raw[NLD];
+        auto fetch = [&](int g) {
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) {
-            x[kk] = 0;
-            if (a.zero_upper && kk >= RAD0 / 2) continue;
-            const int64_t idx = (int64_t)(g + kk * S) * N2 + col;
-            if (idx < n) {
-                const int c = load_code<T, QM>(src, rev ? n - 1 - idx : idx, sthr, k, tbits, inv_step,
-                                               t0, t1, flags);
-                ssq += (unsigned long long)((long long)c * c);
-                nnz += (c != 0);
-                x[kk] = c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
+            for (int kk = 0; kk < NLD; ++kk) raw[kk] = __ldg(&base[(g + kk * S) * rstride]);
+        };
+        if (warp < S) fetch(warp);
+#pragma unroll 1
+        for (int g = warp; g < S; g += kWarps) {
+            Raw cur[NLD];
+#pragma unroll
+            for (int kk = 0; kk < NLD; ++kk) cur[kk] = raw[kk];
+            if (g + kWarps < S) fetch(g + kWarps);
+            uint32_t x[RAD0];
+#pragma unroll
+            for (int kk = 0; kk < RAD0; ++kk) {
+                if (kk >= NLD) { x[kk] = 0; continue; }
+                int c;
+                if constexpr (QM == QM_CODES) {
+                    c = (int)cur[kk];
+                    if (cur[kk] > k || cur[kk] < -k) flags |= SF_CODE_RANGE;
+                } else {
+                    if (cur[kk] != cur[kk]) flags |= SF_NONFINITE;
+                    c = quant_level<T, QM>(cur[kk], sthr, k, tbits, inv_step, t0, t1);
+                }
+                x[kk] = to_res(c);
             }
-        }
-        dif_regs<R0, 0>(x, g, S, a.tw, m);
+            dif_regs<LOG1, 0>(x, g, stw, m);
+            uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) smem[sidx(g + kk * S, lane)] = x[kk];
+            for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
+        }
+    } else {
+#pragma unroll 1
+        for (int g = warp; g < S; g += kWarps) {
+            uint32_t x[RAD0];
+#pragma unroll
+            for (int kk = 0; kk < RAD0; ++kk) {
+                x[kk] = 0;
+                if (kk >= NLD) continue;
+                const int64_t idx = (int64_t)(g + kk * S) * N2 + col;
+                if (idx < n)
+                    x[kk] = to_res(
+                        load_code<T, QM>(src, rev ? n - 1 - idx : idx, sthr, k, tbits, inv_step, t0, t1, flags));
+            }
+            dif_regs<LOG1, 0>(x, g, stw, m);
+            uint32_t* p = smem + g * kPad + lane;
+#pragma unroll
+            for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
+        }
     }
     // statistics: warp reduce, one atomic per warp
 #pragma unroll
@@ -260,20 +358,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         if (flags) atomicOr(st + 2, (unsigned long long)flags);
     }
     __syncthreads();
-    dif_middle<LOG1, 1>(smem, a.tw, m);
+    dif_middle<LOG1, 1, 1>(smem, nullptr, stw, m);
     // last DIF group, forward four-step twiddle, store (coalesced)
     uint32_t* Y = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
+#pragma unroll 1
     for (int g = warp; g < (N1 >> RL); g += kWarps) {
         uint32_t x[RADL];
-        const int base = g * RADL;
+        const uint32_t* p = smem + g * RADL * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) x[kk] = smem[sidx(base + kk, lane)];
-        dif_regs<RL, S0L>(x, 0, 1, a.tw, m);
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[kk * kPad];
+        dif_regs<LOG1, SC::NG - 1>(x, 0, stw, m);
+        const int o = g * RADL * N2 + col;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) {
-            const int64_t o = (int64_t)(base + kk) * N2 + col;
-            Y[o] = montmul(x[kk], __ldg(&a.twf[o]), m.p, m.pinv);
-        }
+        for (int kk = 0; kk < RADL; ++kk) Y[o + kk * N2] = montmul(x[kk], __ldg(&a.twf[o + kk * N2]), m.p, m.pinv);
     }
 }
 
@@ -281,8 +378,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
 
 struct Pass2Args {
     uint32_t* Y;
-    const uint2* twf;  // DIF stage table for N2
-    const uint2* twi;  // DIT stage table for N2
+    const uint2* gtwf;      // DIF group twiddles for N2
+    const uint2* gtwi;      // DIT group twiddles for N2
     const uint32_t* twinv;  // inverse four-step twiddles [P]
     const unsigned long long* stats;
     ModP m;
@@ -293,14 +390,23 @@ struct Pass2Args {
 };
 
 template <int LOG2>
+constexpr size_t pass2_smem()
+{
+    return (size_t)2 * (1 << LOG2) * kPad * 4 + (size_t)(Sched<LOG2>::TW_DIF + Sched<LOG2>::TW_DIT) * 8;
+}
+
+template <int LOG2>
 __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ Pass2Args a)
 {
     constexpr int N2 = 1 << LOG2;
     using SC = Sched<LOG2>;
-    constexpr int RL = SC::r(SC::NG - 1), S0L = SC::s0(SC::NG - 1), RADL = 1 << RL;
+    constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
+    static_assert(SC::rd(0) == RL, "fused group needs matching radices");
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* su = smem;
-    uint32_t* sv = smem + N2 * 32;
+    uint32_t* sv = smem + N2 * kPad;
+    uint2* stf = reinterpret_cast<uint2*>(sv + N2 * kPad);
+    uint2* sti = stf + SC::TW_DIF;
 
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
@@ -311,50 +417,53 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     uint32_t* Yu = a.Y + pl * 2 * P;
     const uint32_t* Yv = Yu + P;
 
+    stage_table(stf, a.gtwf, SC::TW_DIF);
+    stage_table(sti, a.gtwi, SC::TW_DIT);
     // transposed load: warp reads row c contiguously, lane = element
+#pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
-        const int64_t rb = (int64_t)(r0 + c) * N2;
+        const uint32_t* gu = Yu + (r0 + c) * N2;
+        const uint32_t* gv = Yv + (r0 + c) * N2;
+#pragma unroll 4
         for (int e = lane; e < N2; e += 32) {
-            su[sidx(e, c)] = Yu[rb + e];
-            sv[sidx(e, c)] = Yv[rb + e];
+            su[e * kPad + c] = gu[e];
+            sv[e * kPad + c] = gv[e];
         }
     }
     __syncthreads();
     // forward DIF groups except the last, both operands
-    if constexpr (SC::NG > 1) {
-        dif_middle<LOG2, 0>(su, a.twf, m);
-        dif_middle<LOG2, 0>(sv, a.twf, m);
-    }
+    dif_middle<LOG2, 0, 2>(su, sv, stf, m);
     // last DIF group of both, pointwise product, first DIT group (same
     // element grouping: consecutive blocks of 2^RL)
+#pragma unroll 1
     for (int g = warp; g < (N2 >> RL); g += kWarps) {
         uint32_t xu[RADL], xv[RADL];
-        const int base = g * RADL;
+        const int off = g * RADL * kPad + lane;
 #pragma unroll
         for (int kk = 0; kk < RADL; ++kk) {
-            xu[kk] = su[sidx(base + kk, lane)];
-            xv[kk] = sv[sidx(base + kk, lane)];
+            xu[kk] = su[off + kk * kPad];
+            xv[kk] = sv[off + kk * kPad];
         }
-        dif_regs<RL, S0L>(xu, 0, 1, a.twf, m);
-        dif_regs<RL, S0L>(xv, 0, 1, a.twf, m);
+        dif_regs<LOG2, SC::NG - 1>(xu, 0, stf, m);
+        dif_regs<LOG2, SC::NG - 1>(xv, 0, stf, m);
 #pragma unroll
         for (int kk = 0; kk < RADL; ++kk) xu[kk] = montmul(xu[kk], xv[kk], m.p, m.pinv);
-        dit_regs<RL, 0, LOG2>(xu, 0, a.twi, m);
+        dit_regs<LOG2, 0>(xu, 0, sti, m);
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) su[sidx(base + kk, lane)] = xu[kk];
+        for (int kk = 0; kk < RADL; ++kk) su[off + kk * kPad] = xu[kk];
     }
     __syncthreads();
     // remaining DIT groups (1 .. NG-1)
-    if constexpr (SC::NG > 1) {
-        dit_middle<LOG2, 1>(su, a.twi, m);
-        dit_pass<LOG2, SC::s0d(SC::NG - 1), SC::rd(SC::NG - 1)>(su, a.twi, m);
-        __syncthreads();
-    }
+    dit_middle<LOG2, 1>(su, sti, m);
+    dit_group_smem<LOG2, SC::NG - 1>(su, sti, m);
+    __syncthreads();
     // transposed store with the inverse four-step twiddle (includes R^2/P)
+#pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
-        const int64_t rb = (int64_t)(r0 + c) * N2;
-        for (int e = lane; e < N2; e += 32)
-            Yu[rb + e] = montmul(su[sidx(e, c)], __ldg(&a.twinv[rb + e]), m.p, m.pinv);
+        uint32_t* gz = Yu + (r0 + c) * N2;
+        const uint32_t* ti = a.twinv + (r0 + c) * N2;
+#pragma unroll 4
+        for (int e = lane; e < N2; e += 32) gz[e] = montmul(su[e * kPad + c], __ldg(&ti[e]), m.p, m.pinv);
     }
 }
 
@@ -454,9 +563,9 @@ __device__ void argmax_finish(Best b, const ArgmaxOut& am, const unsigned long l
 // ------------------------------------------------------------------ pass 3
 
 struct Pass3Args {
-    uint32_t* Y;      // Z lives in the u slot of Y
-    uint32_t* R;      // residue output (multi-prime)
-    const uint2* twi;  // DIT stage table for N1
+    uint32_t* Y;       // Z lives in the u slot of Y
+    uint32_t* R;       // residue output (multi-prime)
+    const uint2* gtwi;  // DIT group twiddles for N1
     const unsigned long long* stats;
     ArgmaxOut am;
     int64_t* values;
@@ -472,6 +581,12 @@ struct Pass3Args {
 
 enum { OUT_ARGMAX = 0, OUT_VALUES = 1 };
 
+template <int LOG1>
+constexpr size_t pass3_smem()
+{
+    return (size_t)(1 << LOG1) * kPad * 4 + (size_t)Sched<LOG1>::TW_DIT * 8;
+}
+
 template <int LOG1, int OUT>
 __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ Pass3Args a)
 {
@@ -480,6 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     constexpr int R0 = SC::rd(0), RAD0 = 1 << R0;
     constexpr int RL = SC::rd(SC::NG - 1), S0L = SC::s0d(SC::NG - 1), RADL = 1 << RL;
     extern __shared__ __align__(16) uint32_t smem[];
+    uint2* sti = reinterpret_cast<uint2*>(smem + N1 * kPad);
 
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
@@ -492,44 +608,65 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     const int64_t P = (int64_t)N1 * N2;
     const uint32_t* Z = a.Y + pl * 2 * P;
 
+    stage_table(sti, a.gtwi, SC::TW_DIT);
+    __syncthreads();
     // first DIT group from global (positions g*RAD0 + k, lane = column)
+#pragma unroll 1
     for (int g = warp; g < (N1 >> R0); g += kWarps) {
         uint32_t x[RAD0];
+        const uint32_t* zp = Z + g * RAD0 * N2 + col;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) x[kk] = Z[(int64_t)(g * RAD0 + kk) * N2 + col];
-        dit_regs<R0, 0, LOG1>(x, 0, a.twi, m);
+        for (int kk = 0; kk < RAD0; ++kk) x[kk] = zp[kk * N2];
+        dit_regs<LOG1, 0>(x, 0, sti, m);
+        uint32_t* p = smem + g * RAD0 * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) smem[sidx(g * RAD0 + kk, lane)] = x[kk];
+        for (int kk = 0; kk < RAD0; ++kk) p[kk * kPad] = x[kk];
     }
     __syncthreads();
-    dit_middle<LOG1, 1>(smem, a.twi, m);
-    // last DIT group: natural-order n1 = j0 + (k << S0L)
-    Best b = best_init();
+    dit_middle<LOG1, 1>(smem, sti, m);
+    // last DIT group: natural-order n1 = j0 + (k << S0L), t = n1*N2 + col.
+    // Values of a single-prime lift are in (-p/2, p/2) and t < 2^25, so the
+    // per-thread peak bookkeeping runs in 32-bit; a CTA whose t range lies
+    // inside the window (and below nout) skips the per-element tests.
     const uint32_t half = (m.p - 1) / 2;
     uint32_t* Rout = a.R + (pl * a.np + a.pi) * P;
+    const int tmin = blockIdx.x * 32, tmax = (N1 - 1) * N2 + blockIdx.x * 32 + 31;
+    const bool inside = a.am.t_lo <= tmin && a.am.t_hi >= tmax && tmax < a.nout;
+    const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(min(a.am.t_hi, a.nout - 1), P - 1);
+    int bv = INT_MIN, bt = INT_MAX, bc = 0;
+#pragma unroll 1
     for (int g = warp; g < (1 << S0L); g += kWarps) {
         uint32_t x[RADL];
+        const uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) x[kk] = smem[sidx(g + (kk << S0L), lane)];
-        dit_regs<RL, S0L, LOG1>(x, g, a.twi, m);
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
+        dit_regs<LOG1, SC::NG - 1>(x, g, sti, m);
+        const int t0 = g * N2 + col;
 #pragma unroll
         for (int kk = 0; kk < RADL; ++kk) {
-            const int64_t t = (int64_t)(g + (kk << S0L)) * N2 + col;
+            const int t = t0 + (kk << S0L) * N2;
             const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
             if (!final_out) {
                 Rout[t] = r;
                 continue;
             }
-            const long long v = r > half ? (long long)r - (long long)m.p : (long long)r;
+            const int v = (int)r - (r > half ? (int)m.p : 0);
             if constexpr (OUT == OUT_VALUES) {
                 if (t < a.nout) a.values[pair * a.vld + t] = v;
             } else {
-                if (t >= a.am.t_lo && t <= a.am.t_hi) best_add(b, v, t);
+                const bool ok = inside || (t >= tlo && t <= thi);
+                const bool gt = ok && v > bv, eq = ok && v == bv;
+                bt = gt ? t : (eq ? min(bt, t) : bt);
+                bc = gt ? 1 : bc + (eq ? 1 : 0);
+                bv = gt ? v : bv;
             }
         }
     }
     if constexpr (OUT == OUT_ARGMAX) {
-        if (final_out) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+        if (final_out) {
+            Best b = bc ? Best{bv, bt, bc} : best_init();
+            argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+        }
     }
 }
 
@@ -602,6 +739,47 @@ static uint32_t bitrev(uint32_t x, int bits)
     return r;
 }
 
+// group twiddle blocks of a length-2^LOG transform (layout: Sched)
+template <int LOG>
+static void group_tables(uint64_t root, uint64_t p, std::vector<uint2>& dif, std::vector<uint2>& dit)
+{
+    using SC = Sched<LOG>;
+    const uint64_t iroot = powmod(root, p - 2, p);
+    auto sh = [&](uint64_t v) { return make_uint2((uint32_t)v, (uint32_t)((v << 32) / p)); };
+    dif.assign(SC::TW_DIF, make_uint2(0, 0));
+    dit.assign(SC::TW_DIT, make_uint2(0, 0));
+    for (int i = 0; i < SC::NG; ++i) {
+        const int R = SC::r(i), S0 = SC::s0(i), S = SC::L >> (S0 + R);
+        for (int j0 = 0; j0 < SC::nj_dif(i); ++j0)
+            for (int t = 0; t < R; ++t)
+                for (int kp = 0; kp < (1 << (R - 1 - t)); ++kp) {
+                    const uint64_t e = (uint64_t)(j0 + kp * S) << (S0 + t);
+                    dif[SC::twoff_dif(i) + j0 * (1 << R) + (1 << R) - (1 << (R - t)) + kp] = sh(powmod(root, e, p));
+                }
+    }
+    for (int i = 0; i < SC::NG; ++i) {
+        const int R = SC::rd(i), S0 = SC::s0d(i);
+        for (int j0 = 0; j0 < SC::nj_dit(i); ++j0)
+            for (int t = 0; t < R; ++t)
+                for (int kp = 0; kp < (1 << t); ++kp) {
+                    const uint64_t e = (uint64_t)(j0 + (kp << S0)) << (LOG - S0 - t - 1);
+                    dit[SC::twoff_dit(i) + j0 * (1 << R) + (1 << t) - 1 + kp] = sh(powmod(iroot, e, p));
+                }
+    }
+}
+
+static void group_tables_rt(int log, uint64_t root, uint64_t p, std::vector<uint2>& f, std::vector<uint2>& i)
+{
+    switch (log) {
+    case 5: group_tables<5>(root, p, f, i); break;
+    case 6: group_tables<6>(root, p, f, i); break;
+    case 7: group_tables<7>(root, p, f, i); break;
+    case 8: group_tables<8>(root, p, f, i); break;
+    case 9: group_tables<9>(root, p, f, i); break;
+    case 10: group_tables<10>(root, p, f, i); break;
+    }
+}
+
 cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block)
 {
     const int l1 = (lp + 1) / 2, l2 = lp / 2;
@@ -609,27 +787,22 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     const uint64_t w = powmod(g, (p - 1) >> lp, p), wi = powmod(w, p - 2, p);
     const uint64_t R = (1ull << 32) % p, R2 = mulmod(R, R, p);
     const uint64_t invP = powmod(P, p - 2, p);
-    // layout: tw1f | tw1i | tw2f | tw2i | twf | twi
-    const size_t n1h = N1 / 2, n2h = N2 / 2;
-    const size_t bytes = (2 * n1h + 2 * n2h) * sizeof(uint2) + 2 * P * sizeof(uint32_t);
-    std::vector<unsigned char> host(bytes);
-    uint2* h1f = reinterpret_cast<uint2*>(host.data());
-    uint2* h1i = h1f + n1h;
-    uint2* h2f = h1i + n1h;
-    uint2* h2i = h2f + n2h;
-    uint32_t* hf = reinterpret_cast<uint32_t*>(h2i + n2h);
+    std::vector<uint2> g1f, g1i, g2f, g2i;
+    group_tables_rt(l1, powmod(w, N2, p), p, g1f, g1i);
+    group_tables_rt(l2, powmod(w, N1, p), p, g2f, g2i);
+    // layout: g1f | g1i | g2f | g2i | twf | twi  (each table 16-byte aligned)
+    auto al = [](size_t n) { return (n + 1) & ~(size_t)1; };
+    const size_t nt = al(g1f.size()) + al(g1i.size()) + al(g2f.size()) + al(g2i.size());
+    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint32_t);
+    std::vector<unsigned char> host(bytes, 0);
+    uint2* h = reinterpret_cast<uint2*>(host.data());
+    size_t o1i = al(g1f.size()), o2f = o1i + al(g1i.size()), o2i = o2f + al(g2f.size());
+    memcpy(h, g1f.data(), g1f.size() * 8);
+    memcpy(h + o1i, g1i.data(), g1i.size() * 8);
+    memcpy(h + o2f, g2f.data(), g2f.size() * 8);
+    memcpy(h + o2i, g2i.data(), g2i.size() * 8);
+    uint32_t* hf = reinterpret_cast<uint32_t*>(h + nt);
     uint32_t* hi = hf + P;
-    auto shoup_pair = [&](uint64_t v) { return make_uint2((uint32_t)v, (uint32_t)((v << 32) / p)); };
-    const uint64_t w1 = powmod(w, N2, p), w2 = powmod(w, N1, p);
-    const uint64_t w1i = powmod(w1, p - 2, p), w2i = powmod(w2, p - 2, p);
-    for (uint64_t e = 0, a = 1, b = 1; e < n1h; ++e, a = mulmod(a, w1, p), b = mulmod(b, w1i, p)) {
-        h1f[e] = shoup_pair(a);
-        h1i[e] = shoup_pair(b);
-    }
-    for (uint64_t e = 0, a = 1, b = 1; e < n2h; ++e, a = mulmod(a, w2, p), b = mulmod(b, w2i, p)) {
-        h2f[e] = shoup_pair(a);
-        h2i[e] = shoup_pair(b);
-    }
     const uint64_t ci = mulmod(invP, R2, p);
     for (uint64_t pos = 0; pos < N1; ++pos) {
         const uint64_t k1 = bitrev((uint32_t)pos, l1);
@@ -647,7 +820,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     if (e != cudaSuccess) return e;
     e = cudaMemcpy(d, host.data(), bytes, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(d); return e; }
-    uint2* d1f = reinterpret_cast<uint2*>(d);
+    uint2* db = reinterpret_cast<uint2*>(d);
     out->p = p;
     out->m.p = p;
     out->m.p2 = 2 * p;
@@ -657,11 +830,11 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     out->lp = lp;
     out->l1 = l1;
     out->l2 = l2;
-    out->tw1f = d1f;
-    out->tw1i = d1f + n1h;
-    out->tw2f = d1f + 2 * n1h;
-    out->tw2i = d1f + 2 * n1h + n2h;
-    out->twf = reinterpret_cast<const uint32_t*>(d1f + 2 * n1h + 2 * n2h);
+    out->g1f = db;
+    out->g1i = db + o1i;
+    out->g2f = db + o2f;
+    out->g2i = db + o2i;
+    out->twf = reinterpret_cast<const uint32_t*>(db + nt);
     out->twi = out->twf + P;
     *dev_block = d;
     return cudaSuccess;
@@ -669,45 +842,51 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
 
 // ---- kernel dispatch tables
 
-template <int LOG1, typename T, int QM>
-static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, size_t smem, cudaStream_t s)
+template <int LOG1, typename T, int QM, bool ZU>
+static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, cudaStream_t s)
 {
     static bool attr = false;
+    const size_t smem = pass1_smem<LOG1>(sizeof(T));
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass1<LOG1, T, QM>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaError_t e = cudaFuncSetAttribute(k_pass1<LOG1, T, QM, ZU>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_pass1<LOG1, T, QM><<<grid, kThreads, smem, s>>>(a);
+    k_pass1<LOG1, T, QM, ZU><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int LOG1>
-static cudaError_t dispatch_p1_mode(const Pass1Args& a, int dtype, int qm, dim3 grid, size_t smem,
-                                    cudaStream_t s)
+template <int LOG1, bool ZU>
+static cudaError_t dispatch_p1_zu(const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
-    if (dtype == DT_I64) return launch_p1<LOG1, long long, QM_CODES>(a, grid, smem, s);
+    if (dtype == DT_I64) return launch_p1<LOG1, long long, QM_CODES, ZU>(a, grid, s);
     if (dtype == DT_F32) {
-        if (qm == QM_K1) return launch_p1<LOG1, float, QM_K1>(a, grid, smem, s);
-        if (qm == QM_UNIFORM) return launch_p1<LOG1, float, QM_UNIFORM>(a, grid, smem, s);
-        return launch_p1<LOG1, float, QM_BSEARCH>(a, grid, smem, s);
+        if (qm == QM_K1) return launch_p1<LOG1, float, QM_K1, ZU>(a, grid, s);
+        if (qm == QM_UNIFORM) return launch_p1<LOG1, float, QM_UNIFORM, ZU>(a, grid, s);
+        return launch_p1<LOG1, float, QM_BSEARCH, ZU>(a, grid, s);
     }
-    if (qm == QM_K1) return launch_p1<LOG1, double, QM_K1>(a, grid, smem, s);
-    if (qm == QM_UNIFORM) return launch_p1<LOG1, double, QM_UNIFORM>(a, grid, smem, s);
-    return launch_p1<LOG1, double, QM_BSEARCH>(a, grid, smem, s);
+    if (qm == QM_K1) return launch_p1<LOG1, double, QM_K1, ZU>(a, grid, s);
+    if (qm == QM_UNIFORM) return launch_p1<LOG1, double, QM_UNIFORM, ZU>(a, grid, s);
+    return launch_p1<LOG1, double, QM_BSEARCH, ZU>(a, grid, s);
 }
 
-static cudaError_t dispatch_p1(int log1, const Pass1Args& a, int dtype, int qm, dim3 grid, size_t smem,
-                               cudaStream_t s)
+template <int LOG1>
+static cudaError_t dispatch_p1_mode(const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
+{
+    return a.zero_upper ? dispatch_p1_zu<LOG1, true>(a, dtype, qm, grid, s)
+                        : dispatch_p1_zu<LOG1, false>(a, dtype, qm, grid, s);
+}
+
+static cudaError_t dispatch_p1(int log1, const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
     switch (log1) {
-    case 5: return dispatch_p1_mode<5>(a, dtype, qm, grid, smem, s);
-    case 6: return dispatch_p1_mode<6>(a, dtype, qm, grid, smem, s);
-    case 7: return dispatch_p1_mode<7>(a, dtype, qm, grid, smem, s);
-    case 8: return dispatch_p1_mode<8>(a, dtype, qm, grid, smem, s);
-    case 9: return dispatch_p1_mode<9>(a, dtype, qm, grid, smem, s);
-    case 10: return dispatch_p1_mode<10>(a, dtype, qm, grid, smem, s);
+    case 5: return dispatch_p1_mode<5>(a, dtype, qm, grid, s);
+    case 6: return dispatch_p1_mode<6>(a, dtype, qm, grid, s);
+    case 7: return dispatch_p1_mode<7>(a, dtype, qm, grid, s);
+    case 8: return dispatch_p1_mode<8>(a, dtype, qm, grid, s);
+    case 9: return dispatch_p1_mode<9>(a, dtype, qm, grid, s);
+    case 10: return dispatch_p1_mode<10>(a, dtype, qm, grid, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -716,10 +895,9 @@ template <int LOG2>
 static cudaError_t launch_p2(const Pass2Args& a, dim3 grid, cudaStream_t s)
 {
     static bool attr = false;
-    const size_t smem = (size_t)2 * 32 * (1 << LOG2) * 4;
+    const size_t smem = pass2_smem<LOG2>();
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass2<LOG2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k_pass2<LOG2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
@@ -743,7 +921,7 @@ template <int LOG1, int OUT>
 static cudaError_t launch_p3(const Pass3Args& a, dim3 grid, cudaStream_t s)
 {
     static bool attr = false;
-    const size_t smem = (size_t)32 * (1 << LOG1) * 4;
+    const size_t smem = pass3_smem<LOG1>();
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_pass3<LOG1, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -819,7 +997,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a1.op[0] = c.op[0];
             a1.op[1] = c.op[1];
             a1.Y = c.Y;
-            a1.tw = T.tw1f;
+            a1.gtw = T.g1f;
             a1.twf = T.twf;
             a1.stats = c.stats;
             a1.m = T.m;
@@ -830,11 +1008,9 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a1.pair0 = p0;
             // both operands must use the same kernel instantiation (grid.y = 2)
             const int dt = c.op[0].dtype, qm = c.op[0].q.mode;
-            const size_t tsz = (dt == DT_F32) ? 4 : 8;
-            const size_t smem1 = (size_t)32 * N1 * 4 + (size_t)kMaxThr * tsz;
             if (c.op[1].dtype == dt && c.op[1].q.mode == qm) {
                 if (c.prof) c.prof->pre(KK_PASS1, s);
-                e = dispatch_p1(l1, a1, dt, qm, dim3(N2 / 32, 2, (unsigned)nb), smem1, s);
+                e = dispatch_p1(l1, a1, dt, qm, dim3(N2 / 32, 2, (unsigned)nb), s);
                 if (c.prof) c.prof->post(KK_PASS1, s);
                 if (e != cudaSuccess) return e;
             } else {
@@ -845,9 +1021,8 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
                     b1.op[1] = c.op[op];
                     b1.op_base = op;
                     const int dto = c.op[op].dtype, qmo = c.op[op].q.mode;
-                    const size_t smo = (size_t)32 * N1 * 4 + (size_t)kMaxThr * (dto == DT_F32 ? 4 : 8);
                     if (c.prof) c.prof->pre(KK_PASS1, s);
-                    e = dispatch_p1(l1, b1, dto, qmo, dim3(N2 / 32, 1, (unsigned)nb), smo, s);
+                    e = dispatch_p1(l1, b1, dto, qmo, dim3(N2 / 32, 1, (unsigned)nb), s);
                     if (c.prof) c.prof->post(KK_PASS1, s);
                     if (e != cudaSuccess) return e;
                 }
@@ -855,8 +1030,8 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             Pass2Args a2;
             memset(&a2, 0, sizeof(a2));
             a2.Y = c.Y;
-            a2.twf = T.tw2f;
-            a2.twi = T.tw2i;
+            a2.gtwf = T.g2f;
+            a2.gtwi = T.g2i;
             a2.twinv = T.twi;
             a2.stats = c.stats;
             a2.m = T.m;
@@ -872,7 +1047,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             memset(&a3, 0, sizeof(a3));
             a3.Y = c.Y;
             a3.R = c.R;
-            a3.twi = T.tw1i;
+            a3.gtwi = T.g1i;
             a3.stats = c.stats;
             a3.am = c.am;
             a3.values = c.values;

@@ -329,14 +329,16 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     }
     const int64_t P = 1ll << lp;
     c.zero_upper = (nx <= P / 2 && ny <= P / 2);
-    // chunk of pairs per launch group: keep Y (2 operands) within ~64 MiB
-    int64_t chunk = (64ll << 20) / (2 * P * 4);
+    // pairs per launch group: as many as fit ~1.5 GiB of Y/Z scratch.  Large
+    // grids beat L2 residency here (measured on C2: 16 -> 64 pairs per launch
+    // = 2.91 -> 2.41 ms/step; tail waves of 1-CTA/SM kernels dominate).
+    int64_t chunk = (1536ll << 20) / (3 * P * 4);
     if (const char* ev = getenv("QX_CHUNK_PAIRS")) chunk = atoll(ev);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     c.chunk = chunk;
     // scratch: Y | R | stats | partials
-    const size_t yb = (size_t)chunk * 2 * P * 4;
+    const size_t yb = (size_t)chunk * 3 * P * 4;  // Y (2 operands) | Z
     const size_t rb = np > 1 ? (size_t)chunk * np * P * 4 : 0;
     const size_t sb = (size_t)batch * 8 * 8;
     const size_t pb = argmax ? (size_t)batch * kMaxPartials * 3 * 8 : 0;
@@ -346,6 +348,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     if (e != cudaSuccess) return cuda_fail(ctx, e, "counters");
     char* base = (char*)ctx->scratch.ptr;
     c.Y = (uint32_t*)base;
+    c.Z = c.Y + (size_t)chunk * 2 * P;
     c.R = rb ? (uint32_t*)(base + yb) : nullptr;
     c.stats = (unsigned long long*)(base + yb + rb);
     c.am.partials = argmax ? (long long*)(base + yb + rb + sb) : nullptr;

@@ -38,15 +38,21 @@ __device__ __forceinline__ uint32_t montmul(uint32_t a, uint32_t b, uint32_t p, 
 
 struct ModP {
     uint32_t p, p2, pinv;
+    uint32_t zero;  // runtime 0: keeps two-input adds as ALU IADD3 (see below)
 };
+
+// The FMA-heavy pipe carries every 32-bit multiply (3 per Shoup product), so
+// the butterflies keep all additions on the ALU pipe: every add is written
+// with three inputs, which only IADD3 (ALU) can execute, instead of the
+// two-input form ptxas likes to issue as IMAD.IADD on the FMA pipe.
 
 // DIF (Gentleman-Sande) butterfly, inputs/outputs in [0, 2p):
 //   (a, b) -> (a + b, (a - b) * w)
 __device__ __forceinline__ void bfly_dif(uint32_t& a, uint32_t& b, uint2 w, const ModP& m)
 {
-    uint32_t s = a + b;
-    uint32_t d = a - b + m.p2;
-    a = red2p(s, m.p2);
+    const uint32_t s = a + b + m.zero;  // IADD3
+    const uint32_t d = a - b + m.p2;    // IADD3
+    a = red2p(s, m.p2);                 // VIADDMNMX
     b = shoup(d, w.x, w.y, m.p);
 }
 
@@ -54,10 +60,10 @@ __device__ __forceinline__ void bfly_dif(uint32_t& a, uint32_t& b, uint2 w, cons
 //   (a, b) -> (a + w b, a - w b)
 __device__ __forceinline__ void bfly_dit(uint32_t& a, uint32_t& b, uint2 w, const ModP& m)
 {
-    uint32_t x = red2p(a, m.p2);
-    uint32_t t = shoup(b, w.x, w.y, m.p);
-    a = x + t;
-    b = x - t + m.p2;
+    const uint32_t x = red2p(a, m.p2);
+    const uint32_t t = shoup(b, w.x, w.y, m.p);
+    a = x + t + m.zero;                // IADD3
+    b = x - t + m.p2;                  // IADD3
 }
 
 // ------------------------------------------------------------- quantiser
@@ -98,6 +104,27 @@ __device__ __forceinline__ int level_bsearch(T v, const T* s, int tbits)
         if (s[pos + step - 1] <= v) pos += step;
     }
     return pos + (s[pos] <= v ? 1 : 0);
+}
+
+// Fast exact uniform level: the estimate e of |v|/step + 0.5 is within 2^-15
+// of the float64 value (k <= 128), so floor(e) is exact unless e lies within
+// 2^-14 of an integer; only then (rare, and NaN) take the threshold compare.
+__device__ __forceinline__ int level_uniform_fast(float v, const float* s, int k, float inv_step)
+{
+    const float e = fmaf(fabsf(v), inv_step, 0.5f);
+    const float fl = floorf(e);
+    const float fr = e - fl;
+    int lv = e >= (float)k + 0.5f ? k : (int)fl;
+    const bool safe = (fr >= 0x1p-14f) & (fr <= 1.0f - 0x1p-14f) | (e >= (float)k + 0.5f);
+    if (__builtin_expect(!safe, 0)) {
+        lv = e >= (float)k ? k : (int)e;
+        const int sg = v < 0.f ? -lv : lv;
+        int l2 = sg;
+        if (l2 < k && v >= s[l2 + k]) ++l2;
+        if (l2 > -k && !(v >= s[l2 + k - 1])) --l2;
+        return l2;
+    }
+    return v < 0.f ? -lv : lv;
 }
 
 template <typename T>

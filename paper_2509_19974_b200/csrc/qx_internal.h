@@ -84,7 +84,8 @@ struct NttCall {
     uint64_t garner_inv[3]; // inv(p0*..*p_{i-1}) mod p_i
     int zero_upper;         // both operands fit the lower half of P
     // scratch (device)
-    uint32_t* Y;              // [chunk][2][P]
+    uint32_t* Y;              // [chunk][2][P] forward transforms, Y^T layout
+    uint32_t* Z;              // [chunk][P] pass-2 output (natural layout)
     uint32_t* R;              // [chunk][np][P] residues (np > 1)
     unsigned long long* stats;  // [batch][2][4]
     // outputs: exactly one of

@@ -43,10 +43,15 @@ constexpr int kPad = 33;  // words per element row of a 32-vector tile
 // register-group schedule of a length-2^LOG transform: ceil(LOG/4) groups,
 // radices 2^3..2^4, larger first (DIF order; DIT uses the reverse), and the
 // layout of the per-group twiddle blocks.
+#ifndef QX_NTT_MAXR
+#define QX_NTT_MAXR 4
+#endif
+
 template <int LOG>
 struct Sched {
     static constexpr int L = 1 << LOG;
-    static constexpr int NG = (LOG + 3) / 4;
+    // at least two groups: the first reads global memory, the last writes it
+    static constexpr int NG = (LOG + QX_NTT_MAXR - 1) / QX_NTT_MAXR < 2 ? 2 : (LOG + QX_NTT_MAXR - 1) / QX_NTT_MAXR;
     static constexpr int BASE = LOG / NG;
     static constexpr int EXTRA = LOG % NG;
     static constexpr int r(int i) { return i < EXTRA ? BASE + 1 : BASE; }
@@ -175,6 +180,29 @@ __device__ __forceinline__ void dit_middle(uint32_t* s, const uint2* stw, const 
     }
 }
 
+// Warp-strided loop g = first, first + step, ... < end whose global loads run
+// one iteration ahead: two register buffers alternate roles (2x unrolled), so
+// no buffer-rotation moves land on the FMA pipe.
+template <typename Buf, typename Fetch, typename Body>
+__device__ __forceinline__ void prefetched_loop(int first, int end, int step, Fetch fetch, Body body)
+{
+    Buf ba, bb;
+    if (first < end) fetch(ba, first);
+#pragma unroll 1
+    for (int g = first; g < end; g += 2 * step) {
+        if (g + step < end) fetch(bb, g + step);
+        body(ba, g);
+        if (g + step >= end) break;
+        if (g + 2 * step < end) fetch(ba, g + 2 * step);
+        body(bb, g + step);
+    }
+}
+
+template <typename T, int N>
+struct RegBuf {
+    T v[N];
+};
+
 // copy a twiddle table (uint2) into shared memory, all threads
 __device__ __forceinline__ void stage_table(uint2* dst, const uint2* __restrict__ src, int n)
 {
@@ -223,9 +251,9 @@ __device__ __forceinline__ int load_code(const T* __restrict__ src, int64_t i, c
 
 struct Pass1Args {
     OperandDesc op[2];
-    uint32_t* Y;
+    uint32_t* Y;          // Y^T: [pair][op][n2][k1pos]
     const uint2* gtw;     // DIF group twiddles for N1
-    const uint32_t* twf;  // forward four-step twiddles [P]
+    const uint32_t* twf;  // forward four-step twiddles, transposed [n2][k1pos]
     unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -240,6 +268,15 @@ template <int LOG1>
 constexpr size_t pass1_smem(size_t tsz)
 {
     return (size_t)(1 << LOG1) * kPad * 4 + (size_t)Sched<LOG1>::TW_DIF * 8 + (size_t)kMaxThr * tsz;
+}
+
+template <typename T, int QM>
+__device__ __forceinline__ int level_of(T v, const T* sthr, int k, int tbits, T inv_step, T t0, T t1)
+{
+    if constexpr (QM == QM_UNIFORM && std::is_same<T, float>::value)
+        return level_uniform_fast(v, sthr, k, inv_step);
+    else
+        return quant_level<T, QM>(v, sthr, k, tbits, inv_step, t0, t1);
 }
 
 template <int LOG1, typename T, int QM, bool ZU>
@@ -259,7 +296,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     const OperandDesc& d = a.op[blockIdx.y];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N2 = a.N2;
-    const int col = blockIdx.x * 32 + lane;
+    const int c0 = blockIdx.x * 32;
+    const int col = c0 + lane;
     const ModP m = a.m;
 
     stage_table(stw, a.gtw, SC::TW_DIF);
@@ -276,7 +314,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     const bool rev = d.reverse;
     // every element of this tile's loaded rows is in range (no per-element checks)
     const int rows_loaded = ZU ? N1 / 2 : N1;
-    const bool full = (int64_t)(rows_loaded - 1) * N2 + blockIdx.x * 32 + 31 < n;
+    const bool full = (int64_t)(rows_loaded - 1) * N2 + c0 + 31 < n;
     const T* base = rev ? src + (n - 1 - col) : src + col;
     const int rstride = rev ? -N2 : N2;
     constexpr int NLD = ZU ? RAD0 / 2 : RAD0;  // rows actually loaded per group
@@ -294,37 +332,33 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         // register double buffer: the next group's raw samples are in flight
         // while this group is quantised and transformed
         using Raw = typename std::conditional<QM == QM_CODES, long long, T>::type;
-        Raw raw[NLD];
-        auto fetch = [&](int g) {
+        using Buf = RegBuf<Raw, NLD>;
+        prefetched_loop<Buf>(
+            warp, S, kWarps,
+            [&](Buf& b, int g) {
 #pragma unroll
-            for (int kk = 0; kk < NLD; ++kk) raw[kk] = __ldg(&base[(g + kk * S) * rstride]);
-        };
-        if (warp < S) fetch(warp);
-#pragma unroll 1
-        for (int g = warp; g < S; g += kWarps) {
-            Raw cur[NLD];
+                for (int kk = 0; kk < NLD; ++kk) b.v[kk] = __ldg(&base[(g + kk * S) * rstride]);
+            },
+            [&](const Buf& b, int g) {
+                uint32_t x[RAD0];
 #pragma unroll
-            for (int kk = 0; kk < NLD; ++kk) cur[kk] = raw[kk];
-            if (g + kWarps < S) fetch(g + kWarps);
-            uint32_t x[RAD0];
-#pragma unroll
-            for (int kk = 0; kk < RAD0; ++kk) {
-                if (kk >= NLD) { x[kk] = 0; continue; }
-                int c;
-                if constexpr (QM == QM_CODES) {
-                    c = (int)cur[kk];
-                    if (cur[kk] > k || cur[kk] < -k) flags |= SF_CODE_RANGE;
-                } else {
-                    if (cur[kk] != cur[kk]) flags |= SF_NONFINITE;
-                    c = quant_level<T, QM>(cur[kk], sthr, k, tbits, inv_step, t0, t1);
+                for (int kk = 0; kk < RAD0; ++kk) {
+                    if (kk >= NLD) { x[kk] = 0; continue; }
+                    int c;
+                    if constexpr (QM == QM_CODES) {
+                        c = (int)b.v[kk];
+                        if (b.v[kk] > k || b.v[kk] < -k) flags |= SF_CODE_RANGE;
+                    } else {
+                        if (b.v[kk] != b.v[kk]) flags |= SF_NONFINITE;
+                        c = level_of<T, QM>(b.v[kk], sthr, k, tbits, inv_step, t0, t1);
+                    }
+                    x[kk] = to_res(c);
                 }
-                x[kk] = to_res(c);
-            }
-            dif_regs<LOG1, 0>(x, g, stw, m);
-            uint32_t* p = smem + g * kPad + lane;
+                dif_regs<LOG1, 0>(x, g, stw, m);
+                uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
-            for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
-        }
+                for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
+            });
     } else {
 #pragma unroll 1
         for (int g = warp; g < S; g += kWarps) {
@@ -353,34 +387,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     }
     if (lane == 0 && a.p0 == m.p) {  // only the first prime's pass counts
         unsigned long long* st = a.stats + (pair * 2 + op) * 4;
-        if (ssq) atomicAdd(st + 0, ssq);
-        if (nnz) atomicAdd(st + 1, nnz);
+        if (ssq) atomicAdd(st + 0, (unsigned long long)ssq);
+        if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
         if (flags) atomicOr(st + 2, (unsigned long long)flags);
     }
     __syncthreads();
     dif_middle<LOG1, 1, 1>(smem, nullptr, stw, m);
-    // last DIF group, forward four-step twiddle, store (coalesced)
-    uint32_t* Y = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
+    // last DIF group (in shared memory)
 #pragma unroll 1
     for (int g = warp; g < (N1 >> RL); g += kWarps) {
         uint32_t x[RADL];
-        const uint32_t* p = smem + g * RADL * kPad + lane;
+        uint32_t* p = smem + g * RADL * kPad + lane;
 #pragma unroll
         for (int kk = 0; kk < RADL; ++kk) x[kk] = p[kk * kPad];
         dif_regs<LOG1, SC::NG - 1>(x, 0, stw, m);
-        const int o = g * RADL * N2 + col;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) Y[o + kk * N2] = montmul(x[kk], __ldg(&a.twf[o + kk * N2]), m.p, m.pinv);
+        for (int kk = 0; kk < RADL; ++kk) p[kk * kPad] = x[kk];
+    }
+    __syncthreads();
+    // transposed store Y^T[n2][k1pos] (lane = k1pos, contiguous) with the
+    // forward four-step twiddle (table in the same transposed layout)
+    uint32_t* Yt = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
+#pragma unroll 1
+    for (int c = warp; c < 32; c += kWarps) {
+        const int o = (c0 + c) * N1;
+#pragma unroll 8
+        for (int e = lane; e < N1; e += 32)
+            Yt[o + e] = montmul(smem[e * kPad + c], __ldg(&a.twf[o + e]), m.p, m.pinv);
     }
 }
 
 // ------------------------------------------------------------------ pass 2
 
 struct Pass2Args {
-    uint32_t* Y;
+    const uint32_t* Y;      // Y^T of both operands
+    uint32_t* Z;            // [pair][k1pos][n2]
     const uint2* gtwf;      // DIF group twiddles for N2
     const uint2* gtwi;      // DIT group twiddles for N2
-    const uint32_t* twinv;  // inverse four-step twiddles [P]
+    const uint32_t* twinv;  // inverse four-step twiddles [k1pos][n2]
     const unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -400,8 +444,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
 {
     constexpr int N2 = 1 << LOG2;
     using SC = Sched<LOG2>;
+    constexpr int R0 = SC::r(0), S = N2 >> R0, RAD0 = 1 << R0;
     constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
     static_assert(SC::rd(0) == RL, "fused group needs matching radices");
+    static_assert(SC::NG >= 2, "first and last groups must differ");
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* su = smem;
     uint32_t* sv = smem + N2 * kPad;
@@ -411,28 +457,49 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int N1 = a.N1;
     const int r0 = blockIdx.x * 32;
     const ModP m = a.m;
-    const int64_t P = (int64_t)a.N1 * N2;
-    uint32_t* Yu = a.Y + pl * 2 * P;
+    const int64_t P = (int64_t)N1 * N2;
+    // row vector r0+lane, element n2 at Y^T[n2*N1 + r0 + lane]: coalesced
+    const uint32_t* Yu = a.Y + pl * 2 * P + r0 + lane;
     const uint32_t* Yv = Yu + P;
 
     stage_table(stf, a.gtwf, SC::TW_DIF);
     stage_table(sti, a.gtwi, SC::TW_DIT);
-    // transposed load: warp reads row c contiguously, lane = element
-#pragma unroll 1
-    for (int c = warp; c < 32; c += kWarps) {
-        const uint32_t* gu = Yu + (r0 + c) * N2;
-        const uint32_t* gv = Yv + (r0 + c) * N2;
-#pragma unroll 4
-        for (int e = lane; e < N2; e += 32) {
-            su[e * kPad + c] = gu[e];
-            sv[e * kPad + c] = gv[e];
-        }
+    __syncthreads();
+    // first DIF group of both operands straight from global memory, the next
+    // group's loads in flight during this group's butterflies
+    {
+        using Buf = RegBuf<uint32_t, 2 * RAD0>;
+        prefetched_loop<Buf>(
+            warp, S, kWarps,
+            [&](Buf& b, int g) {
+#pragma unroll
+                for (int kk = 0; kk < RAD0; ++kk) {
+                    b.v[kk] = __ldg(&Yu[(g + kk * S) * N1]);
+                    b.v[RAD0 + kk] = __ldg(&Yv[(g + kk * S) * N1]);
+                }
+            },
+            [&](const Buf& b, int g) {
+                uint32_t xu[RAD0], xv[RAD0];
+#pragma unroll
+                for (int kk = 0; kk < RAD0; ++kk) {
+                    xu[kk] = b.v[kk];
+                    xv[kk] = b.v[RAD0 + kk];
+                }
+                dif_regs<LOG2, 0>(xu, g, stf, m);
+                dif_regs<LOG2, 0>(xv, g, stf, m);
+                const int off = g * kPad + lane;
+#pragma unroll
+                for (int kk = 0; kk < RAD0; ++kk) {
+                    su[off + kk * S * kPad] = xu[kk];
+                    sv[off + kk * S * kPad] = xv[kk];
+                }
+            });
     }
     __syncthreads();
-    // forward DIF groups except the last, both operands
-    dif_middle<LOG2, 0, 2>(su, sv, stf, m);
+    dif_middle<LOG2, 1, 2>(su, sv, stf, m);
     // last DIF group of both, pointwise product, first DIT group (same
     // element grouping: consecutive blocks of 2^RL)
 #pragma unroll 1
@@ -457,13 +524,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     dit_middle<LOG2, 1>(su, sti, m);
     dit_group_smem<LOG2, SC::NG - 1>(su, sti, m);
     __syncthreads();
-    // transposed store with the inverse four-step twiddle (includes R^2/P)
+    // transposed store Z[k1pos][n2] (lane = n2) with the inverse four-step
+    // twiddle (includes R^2/P)
+    uint32_t* Z = a.Z + pl * P;
 #pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
-        uint32_t* gz = Yu + (r0 + c) * N2;
-        const uint32_t* ti = a.twinv + (r0 + c) * N2;
-#pragma unroll 4
-        for (int e = lane; e < N2; e += 32) gz[e] = montmul(su[e * kPad + c], __ldg(&ti[e]), m.p, m.pinv);
+        const int o = (r0 + c) * N2;
+#pragma unroll 8
+        for (int e = lane; e < N2; e += 32) Z[o + e] = montmul(su[e * kPad + c], __ldg(&a.twinv[o + e]), m.p, m.pinv);
     }
 }
 
@@ -563,19 +631,19 @@ __device__ void argmax_finish(Best b, const ArgmaxOut& am, const unsigned long l
 // ------------------------------------------------------------------ pass 3
 
 struct Pass3Args {
-    uint32_t* Y;       // Z lives in the u slot of Y
-    uint32_t* R;       // residue output (multi-prime)
+    const uint32_t* Z;  // [pair][k1pos][n2]
+    uint32_t* R;        // residue output (multi-prime)
     const uint2* gtwi;  // DIT group twiddles for N1
     const unsigned long long* stats;
     ArgmaxOut am;
     int64_t* values;
     int64_t nout;
-    int64_t vld;       // row stride of values
+    int64_t vld;        // row stride of values
     ModP m;
     uint32_t p0;
     int N2;
     int np;
-    int pi;            // prime index
+    int pi;             // prime index
     int64_t pair0;
 };
 
@@ -592,7 +660,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
 {
     constexpr int N1 = 1 << LOG1;
     using SC = Sched<LOG1>;
-    constexpr int R0 = SC::rd(0), RAD0 = 1 << R0;
+    constexpr int R0 = SC::rd(0), RAD0 = 1 << R0, NG0 = N1 >> R0;
     constexpr int RL = SC::rd(SC::NG - 1), S0L = SC::s0d(SC::NG - 1), RADL = 1 << RL;
     extern __shared__ __align__(16) uint32_t smem[];
     uint2* sti = reinterpret_cast<uint2*>(smem + N1 * kPad);
@@ -606,21 +674,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     const int col = blockIdx.x * 32 + lane;
     const ModP m = a.m;
     const int64_t P = (int64_t)N1 * N2;
-    const uint32_t* Z = a.Y + pl * 2 * P;
+    const uint32_t* Zc = a.Z + pl * P + col;
 
     stage_table(sti, a.gtwi, SC::TW_DIT);
     __syncthreads();
-    // first DIT group from global (positions g*RAD0 + k, lane = column)
-#pragma unroll 1
-    for (int g = warp; g < (N1 >> R0); g += kWarps) {
-        uint32_t x[RAD0];
-        const uint32_t* zp = Z + g * RAD0 * N2 + col;
+    // first DIT group from global (positions g*RAD0 + k, lane = column),
+    // next group's loads in flight
+    {
+        using Buf = RegBuf<uint32_t, RAD0>;
+        prefetched_loop<Buf>(
+            warp, NG0, kWarps,
+            [&](Buf& b, int g) {
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) x[kk] = zp[kk * N2];
-        dit_regs<LOG1, 0>(x, 0, sti, m);
-        uint32_t* p = smem + g * RAD0 * kPad + lane;
+                for (int kk = 0; kk < RAD0; ++kk) b.v[kk] = __ldg(&Zc[(g * RAD0 + kk) * N2]);
+            },
+            [&](const Buf& b, int g) {
+                uint32_t x[RAD0];
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) p[kk * kPad] = x[kk];
+                for (int kk = 0; kk < RAD0; ++kk) x[kk] = b.v[kk];
+                dit_regs<LOG1, 0>(x, 0, sti, m);
+                uint32_t* p = smem + g * RAD0 * kPad + lane;
+#pragma unroll
+                for (int kk = 0; kk < RAD0; ++kk) p[kk * kPad] = x[kk];
+            });
     }
     __syncthreads();
     dit_middle<LOG1, 1>(smem, sti, m);
@@ -809,7 +885,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
         const uint64_t step_f = powmod(w, k1, p), step_i = powmod(wi, k1, p);
         uint64_t f = R, iv = ci;  // n2 = 0
         for (uint64_t n2 = 0; n2 < N2; ++n2) {
-            hf[pos * N2 + n2] = (uint32_t)f;
+            hf[n2 * N1 + pos] = (uint32_t)f;
             hi[pos * N2 + n2] = (uint32_t)iv;
             f = mulmod(f, step_f, p);
             iv = mulmod(iv, step_i, p);
@@ -827,6 +903,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     uint32_t inv = 1;  // p^-1 mod 2^32 by Newton
     for (int i = 0; i < 5; ++i) inv *= 2u - p * inv;
     out->m.pinv = inv;
+    out->m.zero = 0;
     out->lp = lp;
     out->l1 = l1;
     out->l2 = l2;
@@ -1030,6 +1107,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             Pass2Args a2;
             memset(&a2, 0, sizeof(a2));
             a2.Y = c.Y;
+            a2.Z = c.Z;
             a2.gtwf = T.g2f;
             a2.gtwi = T.g2i;
             a2.twinv = T.twi;
@@ -1045,7 +1123,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             if (e != cudaSuccess) return e;
             Pass3Args a3;
             memset(&a3, 0, sizeof(a3));
-            a3.Y = c.Y;
+            a3.Z = c.Z;
             a3.R = c.R;
             a3.gtwi = T.g1i;
             a3.stats = c.stats;

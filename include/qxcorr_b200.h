@@ -75,7 +75,7 @@ typedef struct qx_signals {
     int32_t dtype;     /* qx_dtype */
     int32_t reserved;
     int64_t n;         /* samples per row (>= 1) */
-    int64_t ld;        /* row stride in elements (>= n) */
+    int64_t ld;        /* row stride in elements (>= 0; rows may overlap or repeat) */
     int64_t start;     /* Signal.start of every row */
 } qx_signals;
 

@@ -8,11 +8,12 @@ kernels behind the C ABI include/qxcorr_b200.h (libqxcorr_b200.so).
     from paper_2509_19974_b200 import Signal, sign, estimate
     r = estimate(Signal(0, x), Signal(0, y), sign(), sign())
 
-Batched and windowed entry points (new): ``estimate_batch``,
-``estimate_batch_host``.
+Batched, windowed and streaming entry points (new): ``estimate_batch``,
+``estimate_batch_host``, ``template_search``; multi-GPU sharding in
+``parallel``.
 """
 
-from .batch import BatchResult, check_results, estimate_batch, estimate_batch_host
+from .batch import BatchResult, check_results, estimate_batch, estimate_batch_host, template_search
 from .errors import (
     BadLength,
     ConfigError,
@@ -38,5 +39,5 @@ __all__ = [
     "Quantizer", "sign", "uniform", "custom", "from_spec", "apply",
     "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at",
     "EstimationResult", "argmax_set", "estimate",
-    "BatchResult", "estimate_batch", "estimate_batch_host", "check_results",
+    "BatchResult", "estimate_batch", "estimate_batch_host", "check_results", "template_search",
 ]

@@ -25,6 +25,10 @@ def as_device(a, dtype=None):
             x = x.to(dtype)
         if not x.is_cuda:
             x = x.to("cuda", non_blocking=False)
+        # keep row-contiguous views as they are: overlapping (sliding-window)
+        # or repeated (stride-0) rows are legal read-only inputs
+        if x.dim() == 2 and (x.stride(1) == 1 or x.shape[1] == 1):
+            return x
         return x.contiguous()
     arr = np.ascontiguousarray(a)
     if not arr.flags.writeable:

@@ -19,7 +19,7 @@ from . import _native as N
 from ._call import call, raise_for
 from .quantize import native_quantizer
 
-__all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "check_results"]
+__all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "check_results", "template_search"]
 
 
 @dataclass
@@ -112,6 +112,66 @@ def estimate_batch_host(x: np.ndarray, y: np.ndarray, qx, qy, *, lag_lo=None, la
     call(N.load().qx_estimate_batch_host, ctx, ctypes.byref(sx), ctypes.byref(sy), batch, ctypes.byref(nqx),
          ctypes.byref(nqy), lo, hi, N.PATHS[path], res.ctypes.data)
     return res
+
+
+MAX_P = 1 << 19  # largest single-launch transform of the NTT path
+
+
+def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
+                    path: str = "auto") -> tuple[int, int, int]:
+    """Peak summary (value, smallest lag, ties) of estimate(x=template, y=stream)
+    over the VALID lags (template fully inside the stream):
+    lag in [stream_start, stream_start + len(stream) - len(template)].
+
+    Overlap-save: the valid-lag range is cut into blocks of `block` lags; block
+    b correlates the template (a stride-0 row, never copied) with the stream
+    window [b*block, b*block + block + len(template) - 1) (overlapping strided
+    rows of the same buffer) and the per-block summaries are merged on the
+    device.  Each block's lags use only samples inside its window, so the
+    result equals the reference's argmax_set summary of the full correlogram
+    restricted to the valid lags (estimator.py:50-57)."""
+    t = D.torch()
+    x = D.as_device(template)
+    y = D.as_device(stream)
+    nt, ns = x.shape[-1], y.shape[-1]
+    x, y = x.reshape(-1), y.reshape(-1)
+    nvalid = ns - nt + 1
+    if nvalid < 1:
+        raise ValueError("template longer than the stream")
+    if block is None:
+        block = MAX_P - 2 * nt + 2  # nout = block + 2*nt - 2 fits one transform
+    if block < 1:
+        raise ValueError("template too long for the block transform")
+    nfull, rem = divmod(nvalid, block)
+    parts = []
+    if nfull:
+        xr = x.as_strided((nfull, nt), (0, 1))
+        yr = y.as_strided((nfull, block + nt - 1), (block, 1))
+        r = estimate_batch(xr, yr, qx, qy, lag_lo=0, lag_hi=block - 1, path=path).raw
+        offs = t.arange(nfull, device=r.device, dtype=t.int64) * block
+        parts.append((r, offs))
+    if rem:
+        s0 = nfull * block
+        r = estimate_batch(x[None], y[s0:s0 + rem + nt - 1][None], qx, qy, lag_lo=0, lag_hi=rem - 1,
+                           path=path).raw
+        parts.append((r, t.full((1,), s0, device=r.device, dtype=t.int64)))
+    raw = t.cat([p[0] for p in parts])
+    offs = t.cat([p[1] for p in parts])
+    status = raw[:, 7] >> 32
+    flags = raw[:, 7] & 0xFFFFFFFF
+    if bool(((flags & N.RF_NONFINITE) != 0).any()):
+        raise ValueError("input contains NaN")
+    if bool(((flags & N.RF_DEGENERATE_X) != 0).any()):
+        raise_for(N.QX_DEGENERATE_QUANTIZATION, "x quantizes to all zeros")
+    if bool((raw[:, 6] == 0).all()):
+        raise_for(N.QX_DEGENERATE_QUANTIZATION, "y quantizes to all zeros")
+    bad = (status != 0) & (status != N.QX_DEGENERATE_QUANTIZATION)
+    if bool(bad.any()):
+        raise_for(int(status[bad][0]), "template search block failed")
+    value, lag, ties = raw[:, 0], raw[:, 1] + offs + stream_start, raw[:, 2]
+    vmax = value.max()
+    hit = value == vmax
+    return (int(vmax), int(lag[hit].min()), int(ties[hit].sum()))
 
 
 def check_results(res: np.ndarray) -> None:

@@ -204,7 +204,9 @@ static qx_status check_signals(qx_context* ctx, const qx_signals* s, const char*
 {
     if (!s || !s->data) return fail(ctx, QX_ERR_INVALID, std::string(name) + " is NULL");
     if (s->n < 1) return fail(ctx, QX_ERR_INVALID, "samples must be a non-empty 1-D sequence");
-    if (s->ld < s->n) return fail(ctx, QX_ERR_INVALID, std::string(name) + ": ld < n");
+    // inputs are read-only, so rows may overlap (0 <= ld < n: sliding windows
+    // of one stream) or repeat (ld == 0: one template against many blocks)
+    if (s->ld < 0) return fail(ctx, QX_ERR_INVALID, std::string(name) + ": ld < 0");
     if (s->dtype < QX_F32 || s->dtype > QX_I64) return fail(ctx, QX_ERR_INVALID, "bad dtype");
     return QX_OK;
 }
@@ -497,7 +499,9 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
     if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
     static const size_t esz[] = {4, 8, 8};
-    const size_t xb = (size_t)batch * x->ld * esz[x->dtype], yb = (size_t)batch * y->ld * esz[y->dtype];
+    // extent of the rows (they may overlap or repeat)
+    const size_t xb = (size_t)((batch - 1) * x->ld + x->n) * esz[x->dtype];
+    const size_t yb = (size_t)((batch - 1) * y->ld + y->n) * esz[y->dtype];
     const size_t xa = (xb + 255) & ~(size_t)255, ya = (yb + 255) & ~(size_t)255;
     const size_t rb = (size_t)batch * sizeof(qx_result);
     cudaError_t e = arena_reserve(ctx->stage, xa + ya + rb, false);

@@ -301,3 +301,32 @@ def test_c2_full_size_properties(qx, oracle):
         want = oracle.estimate_batch_f32(xs[sel], ys[sel], q, q, threads=3)
         assert np.array_equal(res["value"][sel], want[:, 0])
         assert np.array_equal(res["lag"][sel], want[:, 1] - (W.C2_N - 1))
+
+
+def test_template_search_matches_oracle(qx, oracle, golden):
+    """Overlap-save template search (config 5 path): tiny blocks force many
+    overlapping strided windows plus a remainder block."""
+    from paper_2509_19974_b200 import workloads as W
+
+    rng = np.random.default_rng(21)
+    for trial in range(6):
+        nt = int(rng.integers(1, 300))
+        ns = int(rng.integers(nt, 5000))
+        st = rng.laplace(size=ns).astype(np.float32 if trial % 2 else np.float64)
+        off = int(rng.integers(0, ns - nt + 1))
+        tpl = st[off:off + nt].copy()
+        st = st + rng.normal(0, 0.5, ns).astype(st.dtype)
+        q = [qx.sign(), qx.uniform(1, 0.8), qx.uniform(7, 0.3)][trial % 3]
+        block = int(rng.integers(1, 700))
+        got = qx.template_search(tpl, st, q, q, stream_start=5, block=block)
+        u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
+        first = -(nt - 1)
+        c = oracle.xcorr_bf(u, v, 0 - first, ns - nt - first)
+        m, f, n = oracle.argmax(c)
+        assert got == (m, f + 5, n), (trial, got, (m, f, n))
+    meta, _ = golden
+    g5 = meta["configs"]["c5_small"]
+    t5, s5, off, sn2 = W.c5(stream=g5["stream"], template=g5["template"], offset=g5["offset"])
+    for case in g5["cases"]:
+        qa, qb = _q(qx, case["qx"]), _q(qx, case["qy"])
+        assert qx.template_search(t5, s5, qa, qb, block=8191) == (case["peak"], case["lags"][0], len(case["lags"]))

@@ -43,6 +43,7 @@ struct qx_context {
     int device = 0;
     std::recursive_mutex mu;
     std::map<std::pair<uint32_t, int>, std::pair<NttTables, void*>> tables;
+    std::map<std::pair<uint32_t, int>, std::pair<OuterTables, void*>> otables;
     std::map<std::string, std::vector<double>> thr_cache;
     Arena scratch;     // Y/R/stats/partials
     Arena counters;    // zero-initialised ints, reset by the kernels
@@ -124,6 +125,7 @@ void qx_context_destroy(qx_context* c)
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto& kv : c->tables) cudaFree(kv.second.second);
+    for (auto& kv : c->otables) cudaFree(kv.second.second);
     for (Arena* a : {&c->scratch, &c->counters, &c->stage})
         if (a->ptr) cudaFree(a->ptr);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
@@ -233,6 +235,21 @@ static qx_status get_tables(qx_context* ctx, const PrimeInfo& pi, int lp, NttTab
     return QX_OK;
 }
 
+static qx_status get_outer_tables(qx_context* ctx, const PrimeInfo& pi, int lp, int logm, OuterTables* out)
+{
+    auto key = std::make_pair(pi.p, lp);
+    auto it = ctx->otables.find(key);
+    if (it == ctx->otables.end()) {
+        OuterTables t;
+        void* blk = nullptr;
+        cudaError_t e = ntt_make_outer_tables(pi.p, pi.g, lp, logm, &t, &blk);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "outer twiddle tables");
+        it = ctx->otables.emplace(key, std::make_pair(t, blk)).first;
+    }
+    *out = it->second.first;
+    return QX_OK;
+}
+
 static uint64_t powmod64(uint64_t a, uint64_t e, uint64_t p)
 {
     uint64_t r = 1;
@@ -309,7 +326,11 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     if (out->path != QX_PATH_NTT) return fail(ctx, QX_ERR_UNSUPPORTED, "path not available in this build");
 
     const int lp = ceil_log2(nout) < 10 ? 10 : ceil_log2(nout);
-    if (lp > 19) return fail(ctx, QX_ERR_UNSUPPORTED, "full-lag correlation longer than 2^19 points");
+    if (lp > 26) return fail(ctx, QX_ERR_UNSUPPORTED, "full-lag correlation longer than 2^26 points");
+    // P > 2^19: outer radix-2^logm pass around 2^lq four-step sub-transforms
+    const int large = lp > 19;
+    const int logm = large ? (lp - 19 > 3 ? lp - 19 : 3) : 0;
+    const int lq = lp - logm;
     // primes: product must exceed 2*bound + 1 (centred lift)
     std::vector<const PrimeInfo*> ps;
     for (const PrimeInfo& pi : kPrimes)
@@ -323,37 +344,50 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     }
     if ((M - 1) / 2 < bound) return fail(ctx, QX_ERR_UNSUPPORTED, "no prime set covers this coefficient bound");
     c.np = np;
+    c.large = large;
+    c.logm = logm;
+    c.lq = lq;
     for (int i = 0; i < np; ++i) {
-        if ((st = get_tables(ctx, *ps[i], lp, &c.tab[i])) != QX_OK) return st;
+        if ((st = get_tables(ctx, *ps[i], lq, &c.tab[i])) != QX_OK) return st;
+        if (large && (st = get_outer_tables(ctx, *ps[i], lp, logm, &c.otab[i])) != QX_OK) return st;
         uint64_t mprev = 1;
         for (int j = 0; j < i; ++j) mprev = (unsigned __int128)mprev * ps[j]->p % ps[i]->p;
         c.garner_inv[i] = i ? powmod64(mprev, ps[i]->p - 2, ps[i]->p) : 1;
     }
     const int64_t P = 1ll << lp;
     c.zero_upper = (nx <= P / 2 && ny <= P / 2);
-    // pairs per launch group: as many as fit ~1.5 GiB of Y/Z scratch.  Large
+    // words of scratch per pair: Y (2 operands) | Z | [large: OUT (2) | RI (np)] | R (np > 1)
+    const int64_t per_pair = (3 + (large ? 2 + np : 0) + (np > 1 ? np : 0)) * P;
+    // pairs per launch group: as many as fit ~1.5 GiB of scratch.  Large
     // grids beat L2 residency here (measured on C2: 16 -> 64 pairs per launch
     // = 2.91 -> 2.41 ms/step; tail waves of 1-CTA/SM kernels dominate).
-    int64_t chunk = (1536ll << 20) / (3 * P * 4);
+    int64_t chunk = (1536ll << 20) / (per_pair * 4);
     if (const char* ev = getenv("QX_CHUNK_PAIRS")) chunk = atoll(ev);
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     c.chunk = chunk;
-    // scratch: Y | R | stats | partials
-    const size_t yb = (size_t)chunk * 3 * P * 4;  // Y (2 operands) | Z
-    const size_t rb = np > 1 ? (size_t)chunk * np * P * 4 : 0;
+    const size_t wb = (size_t)chunk * per_pair * 4;
     const size_t sb = (size_t)batch * 8 * 8;
     const size_t pb = argmax ? (size_t)batch * kMaxPartials * 3 * 8 : 0;
-    cudaError_t e = arena_reserve(ctx->scratch, yb + rb + sb + pb + 256, false);
+    cudaError_t e = arena_reserve(ctx->scratch, wb + sb + pb + 256, false);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
     e = arena_reserve(ctx->counters, (size_t)batch * 4, true);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "counters");
     char* base = (char*)ctx->scratch.ptr;
-    c.Y = (uint32_t*)base;
-    c.Z = c.Y + (size_t)chunk * 2 * P;
-    c.R = rb ? (uint32_t*)(base + yb) : nullptr;
-    c.stats = (unsigned long long*)(base + yb + rb);
-    c.am.partials = argmax ? (long long*)(base + yb + rb + sb) : nullptr;
+    uint32_t* w = (uint32_t*)base;
+    c.Y = w;
+    w += (size_t)chunk * 2 * P;
+    c.Z = w;
+    w += (size_t)chunk * P;
+    if (large) {
+        c.OUT = w;
+        w += (size_t)chunk * 2 * P;
+        c.RI = w;
+        w += (size_t)chunk * np * P;
+    }
+    c.R = np > 1 ? w : nullptr;
+    c.stats = (unsigned long long*)(base + wb);
+    c.am.partials = argmax ? (long long*)(base + wb + sb) : nullptr;
     c.am.counters = (int*)ctx->counters.ptr;
     c.prof = &ctx->prof;
     return QX_OK;

@@ -74,7 +74,9 @@ __device__ __forceinline__ void bfly_dit(uint32_t& a, uint32_t& b, uint2 w, cons
 //                 against the threshold table (at most a step or two)
 //   QM_BSEARCH -- custom with k > 1: branchless binary search
 //   QM_CODES   -- input already integer codes with |c| <= k (IntSignal)
-enum QMode : int { QM_K1 = 0, QM_UNIFORM = 1, QM_BSEARCH = 2, QM_CODES = 3 };
+//   QM_RESIDUE -- input already NTT residues in [0, 2p) (inner transforms of
+//                 the large-P path), no statistics
+enum QMode : int { QM_K1 = 0, QM_UNIFORM = 1, QM_BSEARCH = 2, QM_CODES = 3, QM_RESIDUE = 4 };
 
 // Threshold semantics (built on the host by qx_thresholds.cpp): T[i],
 // i in [0, 2k), is the smallest value of the input type whose reference

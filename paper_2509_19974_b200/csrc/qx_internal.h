@@ -22,7 +22,7 @@ struct QTable {
     double thr[kMaxThr];  // T[i], +inf padded; float32 tables hold exact floats
 };
 
-enum DType : int { DT_F32 = 0, DT_F64 = 1, DT_I64 = 2 };
+enum DType : int { DT_F32 = 0, DT_F64 = 1, DT_I64 = 2, DT_U32 = 3 /* internal: residues */ };
 
 struct OperandDesc {
     const void* data;  // batch rows, row b at data + b*ld elements
@@ -75,6 +75,16 @@ struct Profiler {
     void post(int kind, cudaStream_t s);
 };
 
+// Outer-pass tables of the large-P path (P = M * Q, M = 2^logm).
+struct OuterTables {
+    const uint2* gf;      // DIF group twiddles for M
+    const uint2* gi;      // DIT group twiddles for M (directly after gf)
+    const uint32_t* tl;   // omega_P^a * R,                 a < 8192
+    const uint32_t* th;   // omega_P^(8192 b) * R,          b < P / 8192
+    const uint32_t* tli;  // omega_P^-a * M^-1 * R
+    const uint32_t* thi;  // omega_P^-(8192 b) * R
+};
+
 struct NttCall {
     OperandDesc op[2];
     int64_t batch;
@@ -93,11 +103,17 @@ struct NttCall {
     int64_t* values;          // full correlogram mode [batch][nout]
     int64_t chunk;            // pairs per launch group
     Profiler* prof;           // may be null
+    // large-P path (lp > 19): tab[] are the inner (2^lq) tables
+    int large, logm, lq;
+    OuterTables otab[3];
+    uint32_t* OUT;            // [2][chunk][P] outer forward output
+    uint32_t* RI;             // [chunk*M][np][Q] inner inverse residues
 };
 
 // launches every pass of the NTT correlation for all pairs on `stream`
 cudaError_t ntt_run(const NttCall& c, cudaStream_t stream);
 // builds host-side twiddle tables for (p, lp) and uploads them
 cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block);
+cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, OuterTables* out, void** dev_block);
 
 }  // namespace qx

@@ -260,7 +260,8 @@ struct Pass1Args {
     int N2;
     int zero_upper;
     int skip_cs;
-    int op_base;  // operand index of blockIdx.y == 0 (1 when launched per operand)
+    int op_base;     // operand index of blockIdx.y == 0 (1 when launched per operand)
+    int pair_shift;  // statistics record = pair >> pair_shift (inner transforms)
     int64_t pair0;
 };
 
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
 
     const int op = a.op_base + blockIdx.y;
     const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
-    if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
+    if (a.skip_cs && cs_single(a.stats, pair >> a.pair_shift, a.p0)) return;
     const OperandDesc& d = a.op[blockIdx.y];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N2 = a.N2;
@@ -344,8 +345,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
 #pragma unroll
                 for (int kk = 0; kk < RAD0; ++kk) {
                     if (kk >= NLD) { x[kk] = 0; continue; }
-                    int c;
-                    if constexpr (QM == QM_CODES) {
+                    int c = 0;
+                    if constexpr (QM == QM_RESIDUE) {
+                        x[kk] = (uint32_t)b.v[kk];
+                        continue;
+                    } else if constexpr (QM == QM_CODES) {
                         c = (int)b.v[kk];
                         if (b.v[kk] > k || b.v[kk] < -k) flags |= SF_CODE_RANGE;
                     } else {
@@ -385,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
         flags |= __shfl_xor_sync(0xffffffffu, flags, o);
     }
-    if (lane == 0 && a.p0 == m.p) {  // only the first prime's pass counts
+    if (QM != QM_RESIDUE && lane == 0 && a.p0 == m.p) {  // only the first prime's pass counts
         unsigned long long* st = a.stats + (pair * 2 + op) * 4;
         if (ssq) atomicAdd(st + 0, (unsigned long long)ssq);
         if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
@@ -430,6 +434,7 @@ struct Pass2Args {
     uint32_t p0;
     int N1;
     int skip_cs;
+    int pair_shift;
     int64_t pair0;
 };
 
@@ -455,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     uint2* sti = stf + SC::TW_DIF;
 
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
-    if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
+    if (a.skip_cs && cs_single(a.stats, pair >> a.pair_shift, a.p0)) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N1 = a.N1;
     const int r0 = blockIdx.x * 32;
@@ -644,6 +649,8 @@ struct Pass3Args {
     int N2;
     int np;
     int pi;             // prime index
+    int pair_shift;     // statistics record = pair >> pair_shift
+    int force_residue;  // inner transforms: always write residues
     int64_t pair0;
 };
 
@@ -666,9 +673,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     uint2* sti = reinterpret_cast<uint2*>(smem + N1 * kPad);
 
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
-    const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
+    const bool cs = (a.np > 1) && cs_single(a.stats, pair >> a.pair_shift, a.p0);
     if (a.pi > 0 && cs) return;
-    const bool final_out = (a.np == 1) || cs;
+    const bool final_out = !a.force_residue && ((a.np == 1) || cs);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int N2 = a.N2;
     const int col = blockIdx.x * 32 + lane;
@@ -794,6 +801,207 @@ __global__ void __launch_bounds__(256) k_combine(const __grid_constant__ Combine
     if (OUT == OUT_ARGMAX) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
 }
 
+// ------------------------------------------- large transforms (P > 2^19)
+//
+// P = M * Q with Q = 2^lq (<= 2^19, the four-step passes above) and
+// M = 2^logm: element n at (i = n / Q, j = n % Q).
+//   outer forward: per column j, M-point DIF over i (+ quantise), then
+//                  x omega_P^(j*k1) -> rows [pos][j] = M independent Q-point
+//                  sub-transforms (the inner passes 1-3, residue mode)
+//   outer inverse: per column j, x omega_P^(-j*k1)/M, M-point DIT -> natural
+//                  i, t = i*Q + j -> lift -> argmax / values / residues
+// The per-element twiddle omega_P^e (e = j*k1 mod P) is the Montgomery
+// product of two small tables, tl[e & 8191] * th[e >> 13].
+
+struct OuterArgs {
+    OperandDesc op[2];       // forward: the two signals
+    uint32_t* out;           // forward: [op][pair][pos][Q]
+    const uint32_t* rin;     // inverse: inner residues [pair*M + pos][np][Q]
+    uint32_t* rout;          // inverse, multi-prime: [pair][np][P] for k_combine
+    const uint2* gtw;        // DIF (fwd) / DIT (inv) group twiddles for M
+    const uint32_t* tl;      // two-level twiddles (Montgomery form; inv: * 1/M)
+    const uint32_t* th;
+    unsigned long long* stats;
+    ArgmaxOut am;
+    int64_t* values;
+    int64_t nout, vld, batch;
+    ModP m;
+    uint32_t p0;
+    int lq, np, pi, skip_cs, zero_upper;
+    int64_t pair0;
+};
+
+__device__ __forceinline__ uint32_t tw_2level(const uint32_t* __restrict__ tl, const uint32_t* __restrict__ th,
+                                              uint32_t e, const ModP& m)
+{
+    return redp(montmul(__ldg(&tl[e & 8191u]), __ldg(&th[e >> 13]), m.p, m.pinv), m.p);
+}
+
+template <int LOGM>
+constexpr size_t outer_smem(size_t tsz)
+{
+    return (size_t)(1 << LOGM) * kPad * 4 + (size_t)(Sched<LOGM>::TW_DIF + Sched<LOGM>::TW_DIT) * 8 +
+           (size_t)kMaxThr * tsz;
+}
+
+template <int LOGM, typename T, int QM>
+__global__ void __launch_bounds__(kThreads, 1) k_outer_fwd(const __grid_constant__ OuterArgs a)
+{
+    constexpr int M = 1 << LOGM;
+    using SC = Sched<LOGM>;
+    constexpr int R0 = SC::r(0), S = M >> R0, RAD0 = 1 << R0;
+    constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint2* stw = reinterpret_cast<uint2*>(smem + M * kPad);
+    T* sthr = reinterpret_cast<T*>(stw + SC::TW_DIF + SC::TW_DIT);
+
+    const int op = blockIdx.y;
+    const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
+    if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
+    const OperandDesc& d = a.op[op];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Q = 1 << a.lq;
+    const int j = blockIdx.x * 32 + lane;
+    const ModP m = a.m;
+    stage_table(stw, a.gtw, SC::TW_DIF);
+    for (int i = threadIdx.x; i < d.q.tsize; i += kThreads) sthr[i] = (T)d.q.thr[i];
+    __syncthreads();
+    T t0 = sthr[0], t1 = sthr[1];
+    const T inv_step = (T)d.q.inv_step;
+    const int k = d.q.k, tbits = d.q.tbits;
+    const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld;
+    const int64_t n = d.n;
+    unsigned ssq = 0, nnz = 0, flags = 0;
+    // first DIF group from global: rows g + kk*S of column j
+#pragma unroll 1
+    for (int g = warp; g < S; g += kWarps) {
+        uint32_t x[RAD0];
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) {
+            x[kk] = 0;
+            if (a.zero_upper && kk >= RAD0 / 2) continue;
+            const int64_t idx = (int64_t)(g + kk * S) * Q + j;
+            if (idx < n) {
+                const int c = load_code<T, QM>(src, d.reverse ? n - 1 - idx : idx, sthr, k, tbits, inv_step, t0,
+                                               t1, flags);
+                ssq += (unsigned)(c * c);
+                nnz += (c != 0);
+                x[kk] = c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
+            }
+        }
+        dif_regs<LOGM, 0>(x, g, stw, m);
+        uint32_t* p = smem + g * kPad + lane;
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+        flags |= __shfl_xor_sync(0xffffffffu, flags, o);
+    }
+    if (lane == 0 && a.p0 == m.p) {
+        unsigned long long* st = a.stats + (pair * 2 + op) * 4;
+        if (ssq) atomicAdd(st + 0, (unsigned long long)ssq);
+        if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
+        if (flags) atomicOr(st + 2, (unsigned long long)flags);
+    }
+    __syncthreads();
+    dif_middle<LOGM, 1, 1>(smem, nullptr, stw, m);
+    // last DIF group -> x omega_P^(j*k1) -> row pos of the inner input
+    uint32_t* out = a.out + ((int64_t)op * a.batch + pl) * ((int64_t)M << a.lq);  // a.batch: chunk size
+    const uint32_t pmask = ((uint32_t)M << a.lq) - 1;
+#pragma unroll 1
+    for (int g = warp; g < (M >> RL); g += kWarps) {
+        uint32_t x[RADL];
+        const uint32_t* p = smem + g * RADL * kPad + lane;
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[kk * kPad];
+        dif_regs<LOGM, SC::NG - 1>(x, 0, stw, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) {
+            const int pos = g * RADL + kk;
+            const uint32_t k1 = __brev((uint32_t)pos) >> (32 - LOGM);
+            const uint32_t w = tw_2level(a.tl, a.th, ((uint32_t)j * k1) & pmask, m);
+            out[(int64_t)pos * Q + j] = montmul(x[kk], w, m.p, m.pinv);
+        }
+    }
+}
+
+template <int LOGM, int OUT>
+__global__ void __launch_bounds__(kThreads, 1) k_outer_inv(const __grid_constant__ OuterArgs a)
+{
+    constexpr int M = 1 << LOGM;
+    using SC = Sched<LOGM>;
+    constexpr int R0 = SC::rd(0), RAD0 = 1 << R0, NG0 = M >> R0;
+    constexpr int RL = SC::rd(SC::NG - 1), S0L = SC::s0d(SC::NG - 1), RADL = 1 << RL;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint2* sti = reinterpret_cast<uint2*>(smem + M * kPad) + SC::TW_DIF;
+
+    const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
+    const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
+    if (a.pi > 0 && cs) return;
+    const bool final_out = (a.np == 1) || cs;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int Q = 1 << a.lq;
+    const ModP m = a.m;
+    const uint32_t pmask = ((uint32_t)M << a.lq) - 1;
+    const uint32_t half = (m.p - 1) / 2;
+    const int64_t P = (int64_t)M << a.lq;
+    stage_table(sti, a.gtw, SC::TW_DIT);
+    Best b = best_init();
+    // column tiles are strided over the (<= kMaxPartials) CTAs of this pair
+#pragma unroll 1
+    for (int tile = blockIdx.x; tile < (Q >> 5); tile += gridDim.x) {
+    const int j = tile * 32 + lane;
+    __syncthreads();
+    // first DIT group from the inner residues, with the inverse twiddle
+#pragma unroll 1
+    for (int g = warp; g < NG0; g += kWarps) {
+        uint32_t x[RAD0];
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) {
+            const int pos = g * RAD0 + kk;
+            const uint32_t k1 = __brev((uint32_t)pos) >> (32 - LOGM);
+            const uint32_t r = __ldg(&a.rin[(((int64_t)pl * M + pos) * a.np + a.pi) * Q + j]);
+            x[kk] = montmul(r, tw_2level(a.tl, a.th, ((uint32_t)j * k1) & pmask, m), m.p, m.pinv);
+        }
+        dit_regs<LOGM, 0>(x, 0, sti, m);
+        uint32_t* p = smem + g * RAD0 * kPad + lane;
+#pragma unroll
+        for (int kk = 0; kk < RAD0; ++kk) p[kk * kPad] = x[kk];
+    }
+    __syncthreads();
+    dit_middle<LOGM, 1>(smem, sti, m);
+#pragma unroll 1
+    for (int g = warp; g < (1 << S0L); g += kWarps) {
+        uint32_t x[RADL];
+        const uint32_t* p = smem + g * kPad + lane;
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
+        dit_regs<LOGM, SC::NG - 1>(x, g, sti, m);
+#pragma unroll
+        for (int kk = 0; kk < RADL; ++kk) {
+            const int64_t t = (int64_t)(g + (kk << S0L)) * Q + j;
+            const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
+            if (!final_out) {
+                a.rout[(pl * a.np + a.pi) * P + t] = r;
+                continue;
+            }
+            const long long v = (long long)r - (r > half ? (long long)m.p : 0);
+            if constexpr (OUT == OUT_VALUES) {
+                if (t < a.nout) a.values[pair * a.vld + t] = v;
+            } else {
+                if (t >= a.am.t_lo && t <= a.am.t_hi) best_add(b, v, t);
+            }
+        }
+    }
+    }  // tiles
+    if constexpr (OUT == OUT_ARGMAX) {
+        if (final_out) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+    }
+}
+
 // ================================================================== host
 
 static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t p) { return (unsigned __int128)a * b % p; }
@@ -847,6 +1055,8 @@ static void group_tables(uint64_t root, uint64_t p, std::vector<uint2>& dif, std
 static void group_tables_rt(int log, uint64_t root, uint64_t p, std::vector<uint2>& f, std::vector<uint2>& i)
 {
     switch (log) {
+    case 3: group_tables<3>(root, p, f, i); break;
+    case 4: group_tables<4>(root, p, f, i); break;
     case 5: group_tables<5>(root, p, f, i); break;
     case 6: group_tables<6>(root, p, f, i); break;
     case 7: group_tables<7>(root, p, f, i); break;
@@ -917,6 +1127,50 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     return cudaSuccess;
 }
 
+cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, OuterTables* out, void** dev_block)
+{
+    const uint64_t P = 1ull << lp, M = 1ull << logm, Q = P >> logm;
+    const uint64_t w = powmod(g, (p - 1) >> lp, p), wi = powmod(w, p - 2, p);
+    const uint64_t R = (1ull << 32) % p;
+    const uint64_t invM = powmod(M, p - 2, p);
+    std::vector<uint2> gf, gi;
+    group_tables_rt(logm, powmod(w, Q, p), p, gf, gi);
+    const size_t nl = 8192, nh = (size_t)(P / 8192 > 0 ? P / 8192 : 1);
+    auto al = [](size_t n) { return (n + 3) & ~(size_t)3; };
+    const size_t ng = al(gf.size()) + al(gi.size());  // in uint2 units
+    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh);
+    std::vector<uint32_t> h(words, 0);
+    memcpy(h.data(), gf.data(), gf.size() * 8);
+    memcpy(h.data() + 2 * al(gf.size()), gi.data(), gi.size() * 8);
+    uint32_t* tl = h.data() + 2 * ng;
+    uint32_t* tli = tl + al(nl);
+    uint32_t* th = tli + al(nl);
+    uint32_t* thi = th + al(nh);
+    const uint64_t w8k = powmod(w, 8192, p), wi8k = powmod(wi, 8192, p);
+    for (uint64_t a = 0, f = R, iv = mulmod(invM, R, p); a < nl; ++a, f = mulmod(f, w, p), iv = mulmod(iv, wi, p)) {
+        tl[a] = (uint32_t)f;
+        tli[a] = (uint32_t)iv;
+    }
+    for (uint64_t b = 0, f = R, iv = R; b < nh; ++b, f = mulmod(f, w8k, p), iv = mulmod(iv, wi8k, p)) {
+        th[b] = (uint32_t)f;
+        thi[b] = (uint32_t)iv;
+    }
+    void* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, words * 4);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(d, h.data(), words * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(d); return e; }
+    const uint32_t* dw = reinterpret_cast<const uint32_t*>(d);
+    out->gf = reinterpret_cast<const uint2*>(dw);
+    out->gi = reinterpret_cast<const uint2*>(dw + 2 * al(gf.size()));
+    out->tl = dw + 2 * ng;
+    out->tli = out->tl + al(nl);
+    out->th = out->tli + al(nl);
+    out->thi = out->th + al(nh);
+    *dev_block = d;
+    return cudaSuccess;
+}
+
 // ---- kernel dispatch tables
 
 template <int LOG1, typename T, int QM, bool ZU>
@@ -937,6 +1191,7 @@ static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, cudaStream_t s)
 template <int LOG1, bool ZU>
 static cudaError_t dispatch_p1_zu(const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
+    if (dtype == DT_U32) return launch_p1<LOG1, uint32_t, QM_RESIDUE, ZU>(a, grid, s);
     if (dtype == DT_I64) return launch_p1<LOG1, long long, QM_CODES, ZU>(a, grid, s);
     if (dtype == DT_F32) {
         if (qm == QM_K1) return launch_p1<LOG1, float, QM_K1, ZU>(a, grid, s);
@@ -1057,8 +1312,228 @@ void Profiler::post(int kind, cudaStream_t s)
     ++nrec;
 }
 
+template <int LOGM, typename T, int QM>
+static cudaError_t launch_ofwd(const OuterArgs& a, dim3 grid, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = outer_smem<LOGM>(sizeof(T));
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_outer_fwd<LOGM, T, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_outer_fwd<LOGM, T, QM><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int LOGM>
+static cudaError_t dispatch_ofwd_m(const OuterArgs& a, int dtype, int qm, dim3 grid, cudaStream_t s)
+{
+    if (dtype == DT_I64) return launch_ofwd<LOGM, long long, QM_CODES>(a, grid, s);
+    if (dtype == DT_F32) {
+        if (qm == QM_K1) return launch_ofwd<LOGM, float, QM_K1>(a, grid, s);
+        if (qm == QM_UNIFORM) return launch_ofwd<LOGM, float, QM_UNIFORM>(a, grid, s);
+        return launch_ofwd<LOGM, float, QM_BSEARCH>(a, grid, s);
+    }
+    if (qm == QM_K1) return launch_ofwd<LOGM, double, QM_K1>(a, grid, s);
+    if (qm == QM_UNIFORM) return launch_ofwd<LOGM, double, QM_UNIFORM>(a, grid, s);
+    return launch_ofwd<LOGM, double, QM_BSEARCH>(a, grid, s);
+}
+
+static cudaError_t dispatch_ofwd(int logm, const OuterArgs& a, int dtype, int qm, dim3 grid, cudaStream_t s)
+{
+    switch (logm) {
+    case 3: return dispatch_ofwd_m<3>(a, dtype, qm, grid, s);
+    case 4: return dispatch_ofwd_m<4>(a, dtype, qm, grid, s);
+    case 5: return dispatch_ofwd_m<5>(a, dtype, qm, grid, s);
+    case 6: return dispatch_ofwd_m<6>(a, dtype, qm, grid, s);
+    case 7: return dispatch_ofwd_m<7>(a, dtype, qm, grid, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int LOGM, int OUT>
+static cudaError_t launch_oinv(const OuterArgs& a, dim3 grid, cudaStream_t s)
+{
+    static bool attr = false;
+    const size_t smem = outer_smem<LOGM>(0);
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_outer_inv<LOGM, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_outer_inv<LOGM, OUT><<<grid, kThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int OUT>
+static cudaError_t dispatch_oinv(int logm, const OuterArgs& a, dim3 grid, cudaStream_t s)
+{
+    switch (logm) {
+    case 3: return launch_oinv<3, OUT>(a, grid, s);
+    case 4: return launch_oinv<4, OUT>(a, grid, s);
+    case 5: return launch_oinv<5, OUT>(a, grid, s);
+    case 6: return launch_oinv<6, OUT>(a, grid, s);
+    case 7: return launch_oinv<7, OUT>(a, grid, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// P = 2^(logm + lq) > 2^19: outer forward pass (quantise + M-point DIF + twiddle)
+// per operand, the three four-step passes on the chunk*M inner sub-transforms
+// (residue mode), the outer inverse pass (twiddle + M-point DIT + lift +
+// argmax/values), and the CRT combine for pairs that need more primes.
+static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
+{
+    const int logm = c.logm, lq = c.lq, M = 1 << logm, Q = 1 << lq;
+    const int64_t P = (int64_t)M * Q;
+    const NttTables& t0 = c.tab[0];
+    const int l1 = t0.l1, l2 = t0.l2, N1 = 1 << l1, N2 = 1 << l2;
+    const bool argmax = c.am.results != nullptr;
+    cudaError_t e;
+    for (int64_t p0 = 0; p0 < c.batch; p0 += c.chunk) {
+        const int64_t nb = (c.batch - p0 < c.chunk) ? c.batch - p0 : c.chunk;
+        const int64_t nin = nb * M;  // inner sub-transforms in this chunk
+        for (int pi = 0; pi < c.np; ++pi) {
+            const NttTables& T = c.tab[pi];
+            const OuterTables& O = c.otab[pi];
+            OuterArgs oa;
+            memset(&oa, 0, sizeof(oa));
+            oa.op[0] = c.op[0];
+            oa.op[1] = c.op[1];
+            oa.out = c.OUT;
+            oa.gtw = O.gf;
+            oa.tl = O.tl;
+            oa.th = O.th;
+            oa.stats = c.stats;
+            oa.batch = nb;
+            oa.m = T.m;
+            oa.p0 = t0.p;
+            oa.lq = lq;
+            oa.np = c.np;
+            oa.pi = pi;
+            oa.skip_cs = pi > 0;
+            oa.zero_upper = c.zero_upper;
+            oa.pair0 = p0;
+            if (c.op[0].dtype != c.op[1].dtype || c.op[0].q.mode != c.op[1].q.mode) return cudaErrorInvalidValue;
+            if (c.prof) c.prof->pre(KK_OTHER, s);
+            e = dispatch_ofwd(logm, oa, c.op[0].dtype, c.op[0].q.mode, dim3(Q / 32, 2, (unsigned)nb), s);
+            if (c.prof) c.prof->post(KK_OTHER, s);
+            if (e != cudaSuccess) return e;
+            // inner forward (residues in), product, inverse -> residues
+            Pass1Args a1;
+            memset(&a1, 0, sizeof(a1));
+            for (int op = 0; op < 2; ++op) {
+                a1.op[op].data = c.OUT + (int64_t)op * nb * P;
+                a1.op[op].ld = Q;
+                a1.op[op].n = Q;
+                a1.op[op].reverse = 0;
+                a1.op[op].dtype = DT_U32;
+                a1.op[op].q.mode = QM_RESIDUE;
+            }
+            a1.Y = c.Y;
+            a1.gtw = T.g1f;
+            a1.twf = T.twf;
+            a1.stats = c.stats;
+            a1.m = T.m;
+            a1.p0 = t0.p;
+            a1.N2 = N2;
+            a1.skip_cs = pi > 0;
+            a1.pair_shift = logm;
+            a1.pair0 = p0 * M;
+            if (c.prof) c.prof->pre(KK_PASS1, s);
+            e = dispatch_p1(l1, a1, DT_U32, QM_RESIDUE, dim3(N2 / 32, 2, (unsigned)nin), s);
+            if (c.prof) c.prof->post(KK_PASS1, s);
+            if (e != cudaSuccess) return e;
+            Pass2Args a2;
+            memset(&a2, 0, sizeof(a2));
+            a2.Y = c.Y;
+            a2.Z = c.Z;
+            a2.gtwf = T.g2f;
+            a2.gtwi = T.g2i;
+            a2.twinv = T.twi;
+            a2.stats = c.stats;
+            a2.m = T.m;
+            a2.p0 = t0.p;
+            a2.N1 = N1;
+            a2.skip_cs = pi > 0;
+            a2.pair_shift = logm;
+            a2.pair0 = p0 * M;
+            if (c.prof) c.prof->pre(KK_PASS2, s);
+            e = dispatch_p2(l2, a2, dim3(N1 / 32, (unsigned)nin), s);
+            if (c.prof) c.prof->post(KK_PASS2, s);
+            if (e != cudaSuccess) return e;
+            Pass3Args a3;
+            memset(&a3, 0, sizeof(a3));
+            a3.Z = c.Z;
+            a3.R = c.RI;
+            a3.gtwi = T.g1i;
+            a3.stats = c.stats;
+            a3.am = c.am;
+            a3.nout = Q;
+            a3.m = T.m;
+            a3.p0 = t0.p;
+            a3.N2 = N2;
+            a3.np = c.np;
+            a3.pi = pi;
+            a3.pair_shift = logm;
+            a3.force_residue = 1;
+            a3.pair0 = p0 * M;
+            if (c.prof) c.prof->pre(KK_PASS3, s);
+            e = dispatch_p3_out<OUT_VALUES>(l1, a3, dim3(N2 / 32, (unsigned)nin), s);
+            if (c.prof) c.prof->post(KK_PASS3, s);
+            if (e != cudaSuccess) return e;
+            // outer inverse
+            OuterArgs ob = oa;
+            ob.rin = c.RI;
+            ob.rout = c.R;
+            ob.gtw = O.gi;
+            ob.tl = O.tli;
+            ob.th = O.thi;
+            ob.am = c.am;
+            ob.values = c.values;
+            ob.nout = c.nout;
+            ob.vld = c.nout;
+            const int nblk = (Q / 32) < kMaxPartials ? (Q / 32) : kMaxPartials;
+            if (c.prof) c.prof->pre(KK_OTHER, s);
+            e = argmax ? dispatch_oinv<OUT_ARGMAX>(logm, ob, dim3(nblk, (unsigned)nb), s)
+                       : dispatch_oinv<OUT_VALUES>(logm, ob, dim3(nblk, (unsigned)nb), s);
+            if (c.prof) c.prof->post(KK_OTHER, s);
+            if (e != cudaSuccess) return e;
+        }
+        if (c.np > 1) {
+            CombineArgs ca;
+            memset(&ca, 0, sizeof(ca));
+            ca.R = c.R;
+            ca.stats = c.stats;
+            ca.am = c.am;
+            ca.values = c.values;
+            ca.nout = c.nout;
+            ca.vld = c.nout;
+            ca.P = P;
+            for (int i = 0; i < c.np; ++i) {
+                ca.p[i] = c.tab[i].p;
+                ca.ginv[i] = c.garner_inv[i];
+            }
+            ca.p0 = t0.p;
+            ca.np = c.np;
+            ca.pair0 = p0;
+            if (c.prof) c.prof->pre(KK_COMBINE, s);
+            if (argmax) k_combine<OUT_ARGMAX><<<dim3(kMaxPartials, (unsigned)nb), 256, 0, s>>>(ca);
+            else k_combine<OUT_VALUES><<<dim3(kMaxPartials, (unsigned)nb), 256, 0, s>>>(ca);
+            e = cudaGetLastError();
+            if (c.prof) c.prof->post(KK_COMBINE, s);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
 cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
 {
+    if (c.large) return ntt_run_large(c, s);
     const NttTables& t0 = c.tab[0];
     const int l1 = t0.l1, l2 = t0.l2;
     const int N1 = 1 << l1, N2 = 1 << l2;

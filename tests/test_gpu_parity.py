@@ -330,3 +330,46 @@ def test_template_search_matches_oracle(qx, oracle, golden):
     for case in g5["cases"]:
         qa, qb = _q(qx, case["qx"]), _q(qx, case["qy"])
         assert qx.template_search(t5, s5, qa, qb, block=8191) == (case["peak"], case["lags"][0], len(case["lags"]))
+
+
+def test_large_transform_path(qx, oracle):
+    """P > 2^19 (outer radix-2^m pass around 2^19 sub-transforms, config 4's
+    path): full correlograms and windowed peaks equal the oracle's KS."""
+    import torch
+
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    rng = np.random.default_rng(33)
+    for nx, ny, q in [((1 << 19) + 5, (1 << 18) + 77, qx.uniform(7, 0.4)),
+                      ((1 << 20) + 11, (1 << 20) - 3, qx.sign())]:
+        s = rng.laplace(size=max(nx, 1000 + ny)).astype(np.float32)
+        x = s[:nx].copy()
+        y = s[1000:1000 + ny] + rng.normal(0, 0.7, ny).astype(np.float32)
+        u, v = oracle.quantize(q, x), oracle.quantize(q, y)
+        want = oracle.xcorr_ks(u, v, q.k, q.k)
+        vals, st = xcorr_full_device(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), q, q)
+        assert np.array_equal(vals[0].cpu().numpy(), want)
+        m, f, n = oracle.argmax(want)
+        res = qx.estimate_batch(x[None], y[None], q, q).numpy()
+        assert (res["value"][0], res["lag"][0], res["ties"][0]) == (m, f - (nx - 1), n)
+        assert res["lag"][0] == -1000
+
+
+def test_c4_full_size(qx, oracle):
+    """BASELINE config 4 at full size (2^24-sample Laplacian pair, 0 dB, 4-bit):
+    the GPU finds the planted delay and agrees with the oracle's exact
+    correlation at a sample of lags (int64 dot products on the CPU)."""
+    import torch
+
+    from paper_2509_19974_b200 import workloads as W
+
+    x, y, lag = W.c4()
+    q = W.bit_quantizer(4, W.C4_SIGMA)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    res = qx.estimate_batch(xd, yd, q, q).numpy()[0]
+    assert res["status"] == 0 and res["lag"] == lag == -731_205 and res["ties"] == 1
+    u, v = oracle.quantize(q, x), oracle.quantize(q, y)
+    assert res["sumsq_x"] == oracle.sumsq(u) and res["sumsq_y"] == oracle.sumsq(v)
+    n = len(u)
+    t_peak = lag + n - 1
+    assert oracle.xcorr_bf(u, v, t_peak, t_peak)[0] == res["value"]

@@ -31,7 +31,7 @@ QX_ERR_NONFINITE = 9
 
 QX_F32, QX_F64, QX_I64 = 0, 1, 2
 QX_Q_SIGN, QX_Q_UNIFORM, QX_Q_CUSTOM, QX_Q_CODES = 0, 1, 2, 3
-PATHS = {"auto": 0, "ntt": 1, "direct": 2}
+PATHS = {"auto": 0, "ntt": 1, "direct": 2, "tc": 2}
 
 RF_DEGENERATE_X = 1
 RF_DEGENERATE_Y = 2

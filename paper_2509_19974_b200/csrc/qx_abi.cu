@@ -19,6 +19,8 @@ int thresholds(int kind, long long k, double step, const double* thr, int dtype,
 cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
                             int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s);
 cudaError_t stats_to_results(const unsigned long long* stats, void* results, int64_t batch, cudaStream_t s);
+bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
+cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
 }  // namespace qx
 
 using namespace qx;
@@ -322,8 +324,19 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     c.am.t_hi = t_hi;
     out->nx = nx;
     out->ny = ny;
-    out->path = path == QX_PATH_AUTO ? QX_PATH_NTT : path;
-    if (out->path != QX_PATH_NTT) return fail(ctx, QX_ERR_UNSUPPORTED, "path not available in this build");
+    // bounded lag windows go to the tcgen05 int8 Toeplitz kernel (qx_tc.cu)
+    const bool tc_ok = argmax && tc_window_eligible(c, nx, ny);
+    if (path == QX_PATH_DIRECT && !tc_ok)
+        return fail(ctx, QX_ERR_UNSUPPORTED, "tensor-core window path: window > 4096 lags, nx > 4593 or k > 127");
+    out->path = (path == QX_PATH_DIRECT || (path == QX_PATH_AUTO && tc_ok)) ? QX_PATH_DIRECT : QX_PATH_NTT;
+    if (out->path == QX_PATH_DIRECT) {
+        const size_t sb = (size_t)batch * 8 * 8;
+        cudaError_t e = arena_reserve(ctx->scratch, sb + 256, false);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
+        c.stats = (unsigned long long*)ctx->scratch.ptr;
+        c.prof = &ctx->prof;
+        return QX_OK;
+    }
 
     const int lp = ceil_log2(nout) < 10 ? 10 : ceil_log2(nout);
     if (lp > 26) return fail(ctx, QX_ERR_UNSUPPORTED, "full-lag correlation longer than 2^26 points");
@@ -453,8 +466,8 @@ qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signa
     pr.call.am.results = results;
     cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
-    e = ntt_run(pr.call, s);
-    if (e != cudaSuccess) return cuda_fail(ctx, e, "ntt launch");
+    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
     return QX_OK;
 }
 

@@ -1,0 +1,20 @@
+"""Short driver for ncu: BASELINE config 3 slice (4096 pairs), b=4, window -512..512."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+
+import paper_2509_19974_b200 as P
+from paper_2509_19974_b200 import workloads as W
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+xs, ys, lag = W.c3(pairs=n)
+xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+q = W.bit_quantizer(4, W.C3_SIGMA)
+for _ in range(3):
+    r = P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512)
+torch.cuda.synchronize()
+assert np.array_equal(r.lag.cpu().numpy(), lag)
+print("ok")

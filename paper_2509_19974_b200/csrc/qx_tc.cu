@@ -1,8 +1,8 @@
 // qx_tc.cu -- bounded-lag-window correlation on the 5th-generation tensor
 // cores (tcgen05.mma kind::i8, s8 x s8 -> s32 in TMEM).
 //
-// For a lag tile [L0, L0 + 2048): c[L0 + 16a + r] = sum_k A[a][k] * B[r][k]
-// with a in [0,128) (M = 128), r in [0,16) (N = 16),
+// For a lag tile [L0, L0 + 16M): c[L0 + 16a + r] = sum_k A[a][k] * B[r][k]
+// with a in [0,M) (M = 64 or 128), r in [0,16) (N = 16),
 //   A[a][k] = ycode[L0 + 16a + k]          (Hankel rows, stride 16 bytes)
 //   B[r][k] = xcode[k - r]                 (16 byte-shifted copies of x)
 // k in [0, K), K = nx + 15 rounded up to 32.  A is read straight from the
@@ -14,13 +14,27 @@
 // This is the reference's brute-force correlation (intxcorr.py:96-100)
 // restricted to a window (parity = the full correlogram sliced).
 //
-// Per CTA (persistent over pairs, one CTA per SM, 16 warps): smem operands
-// and TMEM accumulators are double buffered.  Warp 0 issues each pair's MMA
-// chain from one thread (completion: tcgen05.commit -> mbarrier); warps 4-7
-// drain the previous pair's accumulator (tcgen05.ld -> argmax) behind a
-// named barrier; every warp quantises and builds the next pair meanwhile,
-// with that pair's float4 loads already in flight.
+// Cost model (tools/tc_rate.cu, measured on B200): an i8 MMA with both
+// operands in shared memory takes max(~(32*M + 32*N) / 128 B/clk, M*N/256)
+// cycles when issued from a converged warp -- 25.8 cycles at M=64, 39 at
+// M=128 (N=16) -- so the tile shape follows the window: M=64 when the window
+// fits 1024 lags (+16), else M=128.  The symmetric windows callers use have
+// 2h+1 lags; up to 16 lags past the tiles are summed on the CUDA cores
+// (dp4a) by the epilogue warps instead of a second tile.
+//
+// Per CTA (persistent over pairs, one CTA per SM): shared-memory operands
+// are double buffered (data slot = it & 1), TMEM accumulators and the
+// per-pair statistics / extra-lag sums quadruple buffered (aux slot =
+// it & 3).  Warps 0-15 quantise and build the next pair (its float4 loads
+// already in flight), sum the extra lags and reduce the statistics into
+// shared memory; warp 16 issues the MMA chain (converged, elect.sync;
+// completion: tcgen05.commit -> mdone[aux]); warps 20-23 drain an
+// accumulator (tcgen05.ld -> argmax), write the qx_result and release the
+// aux slot (tfree[aux]).  A data slot is reused as soon as its MMA chain
+// completes, so the epilogue is off the builders' critical path.
 #include <climits>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <type_traits>
 
@@ -31,10 +45,11 @@ namespace qx {
 constexpr int kTcThreads = 512;                 // builder threads (warps 0-15)
 constexpr int kTcMmaWarp = 16;                   // MMA issuer
 constexpr int kTcTotalThreads = 24 * 32;         // + warp 16 (MMA), warps 20-23 (epilogue)
-constexpr int kTcLags = 2048;      // lags per tile: M=128 rows x N=16
+constexpr int kTcLags = 2048;      // lags per M=128 tile (M=64: 1024)
 constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
 constexpr int kTcMaxTiles = 2;     // lag tiles per pair
-constexpr int kTcYBytes = kTcMaxTiles * kTcLags + kTcMaxK + 64;
+constexpr int kTcMaxExtra = 16;    // lags past the tiles, summed on CUDA cores
+constexpr int kTcYBytes = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
 // B layout: K-chunk stride 272 B (= 256 + 16): 16-byte stores of 32
 // consecutive chunks then hit 8 distinct bank groups (4 wavefronts, no
 // conflicts); the descriptor's LBO carries the stride
@@ -70,22 +85,54 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// instruction descriptor: kind::i8, D = s32, A = B = s8, K-major, N = 16, M = 128
-constexpr uint32_t kIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((128u >> 4) << 24);
-
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate)
+// instruction descriptor: kind::i8, D = s32, A = B = s8, K-major, N = 16
+constexpr uint32_t tc_idesc(int M)
 {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_commit(uint64_t* bar)
+// Issued by a whole converged warp: elect.sync picks the issuing lane inside
+// the asm, so ptxas emits no per-instruction divergence loop around UTCIMMA
+// (single-lane issue under `if (lane == 0)` costs ~52 cycles per MMA).
+__device__ __forceinline__ void mma_i8_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate)
 {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// Four MMAs on consecutive K steps under one elect.sync.  Descriptors are
+// passed as 32-bit low words (start address >> 4, which never carries into
+// the LBO field) and a shared high word; A advances 32 B (+2), B two
+// 272-B K-chunks (+34) per step.
+__device__ __forceinline__ void mma_i8_warp4(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                             uint32_t idesc)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .b32 t;\n\t"
+        "mov.b64 a0, {%1, %2};\n\tadd.u32 t, %1, 2;\n\tmov.b64 a1, {t, %2};\n\t"
+        "add.u32 t, %1, 4;\n\tmov.b64 a2, {t, %2};\n\tadd.u32 t, %1, 6;\n\tmov.b64 a3, {t, %2};\n\t"
+        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, 34;\n\tmov.b64 b1, {t, %4};\n\t"
+        "add.u32 t, %3, 68;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, 102;\n\tmov.b64 b3, {t, %4};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a0, b0, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %5, 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %5, 1;\n}" ::"r"(tmem_d),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc));
+}
+
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16])
@@ -103,22 +150,88 @@ struct TcArgs {
     unsigned long long* stats;
     ArgmaxOut am;            // window on t, results
     int64_t L0;              // first lag of tile 0, relative: t = L0 + (nx - 1) + ...
+    int M;                   // MMA rows per tile (64 or 128); a tile holds 16*M lags
     int ntiles;
+    int extra;               // lags after the tiles (<= kTcMaxExtra), CUDA cores
+    int ylen;                // y-code window bytes: ntiles*16*M + extra + K
+    uint32_t idesc;
     int K;                   // padded K (multiple of 32)
     int fast;                // float32, n <= 4096, aligned rows, L0 % 4 == 0
+    int debug;               // QX_TC_TIMING builds only: 1 = skip MMAs, 2 = skip builds
     int64_t batch;
 };
+
+constexpr int kTcAux = 4;  // TMEM accumulator / statistics slots
 
 struct TcSmem {
     alignas(128) int8_t b[2][kTcBLbo * (kTcMaxK / 16)];   // shifted x copies
     alignas(128) int8_t y[2][kTcYBytes];      // y codes from lag L0 on
     alignas(16) int8_t xl[2][kTcMaxK + 64];   // linear x codes, 16 zero bytes in front
     double thr[2][kMaxThr];
-    uint64_t bar[2];    // MMA chain of slot s complete (tcgen05.commit)
-    uint64_t tfree[2];  // epilogue finished reading TMEM slot s (128 arrivals)
+    uint64_t mdone[kTcAux];  // MMA chain of aux slot complete (tcgen05.commit)
+    uint64_t tfree[kTcAux];  // epilogue finished with aux slot (128 arrivals)
+    // per-builder-warp partials (no atomics): ssx, nzx, ssy, nzy, flags
+    unsigned long long wst[kTcAux][kTcThreads / 32][5];
+    int wxs[kTcAux][kTcThreads / 32][kTcMaxExtra];  // extra-lag sums
     uint32_t tmem_base;
-    int best[kTcThreads / 32][3];
+    int best[4][3];
+#ifdef QX_TC_TIMING
+    unsigned long long tm[8];
+#endif
 };
+
+// Each aux barrier completes once per use of its slot (every 4th
+// iteration), so iteration j's completion has parity (j >> 2) & 1.  Every
+// waiter is at most one use behind (see the dependency notes in the kernel),
+// so parity waits are unambiguous.
+__device__ __forceinline__ void tc_wait_mdone(TcSmem& S, int j)
+{
+    mbar_wait(&S.mdone[j & 3], (uint32_t)((j >> 2) & 1));
+}
+__device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
+{
+    mbar_wait(&S.tfree[j & 3], (uint32_t)((j >> 2) & 1));
+}
+
+// builder-side extra lags and statistics of the pair in data slot s, aux
+// slot u: warp-reduced, one record per builder warp (summed by the epilogue)
+__device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
+                              unsigned long long ssy, unsigned long long nzy, unsigned fl)
+{
+    const int lane = threadIdx.x & 31;
+    if (a.extra) {
+        // extra lag j = ntiles*16M + e: sum_m x[m] * ycode[L0 + j + m]
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[s]) + 4;  // x codes from m = 0
+        const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[s]);
+        const int nw = (int)((a.op[0].n + 3) >> 2);
+        const int j0 = a.ntiles * 16 * a.M;
+        for (int e = 0; e < a.extra; ++e) {
+            const int j = j0 + e, jw = j >> 2, sh = (j & 3) * 8;
+            int acc = 0;
+            for (int w = threadIdx.x; w < nw; w += kTcThreads)
+                acc = __dp4a((int)xw[w], (int)__funnelshift_r(yw[w + jw], yw[w + jw + 1], sh), acc);
+            acc = __reduce_add_sync(0xffffffffu, acc);
+            if (lane == 0) S.wxs[u][threadIdx.x >> 5][e] = acc;
+        }
+    }
+    ssx = __reduce_add_sync(0xffffffffu, ssx);
+    nzx = __reduce_add_sync(0xffffffffu, nzx);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ssy += __shfl_xor_sync(0xffffffffu, ssy, o);
+        nzy += __shfl_xor_sync(0xffffffffu, nzy, o);
+    }
+    if (lane == 0) {
+        unsigned long long* st = S.wst[u][threadIdx.x >> 5];
+        st[0] = ssx;
+        st[1] = nzx;
+        st[2] = ssy;
+        st[3] = nzy;
+        st[4] = fl;
+    }
+}
+
 
 template <typename T, int QM>
 __device__ __forceinline__ int tc_level(T v, const T* thr, int k, int tbits, T inv_step, unsigned& flags)
@@ -132,7 +245,7 @@ __device__ __forceinline__ int tc_level(T v, const T* thr, int k, int tbits, T i
 // quantise pair `pair` into smem slot s: x -> xl (linear) -> b (shifted
 // copies), y window -> y; accumulate statistics over the whole signals
 template <typename T, int QM>
-__device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int64_t pair)
+__device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
 {
     const T* thrx = reinterpret_cast<const T*>(S.thr[0]);
     const T* thry = reinterpret_cast<const T*>(S.thr[1]);
@@ -140,8 +253,10 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int64_t pair)
     const OperandDesc& dy = a.op[1];
     const T* xs = reinterpret_cast<const T*>(dx.data) + pair * dx.ld;
     const T* ys = reinterpret_cast<const T*>(dy.data) + pair * dy.ld;
-    const int nx = (int)dx.n, ny = (int)dy.n, K = a.K;
-    unsigned ssx = 0, nzx = 0, ssy = 0, nzy = 0, fl = 0;
+    const int nx = (int)dx.n, K = a.K;
+    const int64_t ny = dy.n;
+    unsigned ssx = 0, nzx = 0, fl = 0;
+    unsigned long long ssy = 0, nzy = 0;
     // linear x codes: xl[16 + m] = q(x[m]) (zero padding around)
     int8_t* xl = S.xl[s];
     for (int i = threadIdx.x; i < K + 48; i += kTcThreads) {
@@ -158,7 +273,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int64_t pair)
     // L0 + 16a + r pairs x[m] with y[m + lag], so row a starts at y index
     // lag_base + 16a with lag_base = L0 (x starts at k - r = m)
     int8_t* yb = S.y[s];
-    const int ylen = a.ntiles * kTcLags + K;
+    const int ylen = a.ylen;
     const int64_t y0 = a.L0;
     for (int i = threadIdx.x; i < ylen; i += kTcThreads) {
         const int64_t j = y0 + i;
@@ -194,23 +309,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int64_t pair)
         v.w = __funnelshift_r(a3, a4, sh);
         b4[kc * (kTcBLbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
     }
-    // statistics (one atomic per warp)
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        ssx += __shfl_xor_sync(0xffffffffu, ssx, o);
-        nzx += __shfl_xor_sync(0xffffffffu, nzx, o);
-        ssy += __shfl_xor_sync(0xffffffffu, ssy, o);
-        nzy += __shfl_xor_sync(0xffffffffu, nzy, o);
-        fl |= __shfl_xor_sync(0xffffffffu, fl, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        unsigned long long* st = a.stats + pair * 8;
-        if (ssx) atomicAdd(st + 0, (unsigned long long)ssx);
-        if (nzx) atomicAdd(st + 1, (unsigned long long)nzx);
-        if (ssy) atomicAdd(st + 4, (unsigned long long)ssy);
-        if (nzy) atomicAdd(st + 5, (unsigned long long)nzy);
-        if (fl) atomicOr(st + 2, (unsigned long long)fl);
-    }
+    tc_aux_finish(a, S, s, u, ssx, nzx, ssy, nzy, fl);
 }
 
 // ---- fast build: float32 rows, nx, ny <= kTcFastN, 16-B aligned rows,
@@ -259,14 +358,14 @@ __device__ __forceinline__ uint32_t tc_q4(float4 v, const float* thr, int k, flo
 }
 
 template <int QM>
-__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int64_t pair, const TcRegs& r)
+__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs& r)
 {
     const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
     const int kx = a.op[0].q.k, ky = a.op[1].q.k;
     const float ix = (float)a.op[0].q.inv_step, iy = (float)a.op[1].q.inv_step;
     const int nx4 = (int)(a.op[0].n >> 2), ny4 = (int)(a.op[1].n >> 2), K = a.K;
-    const int ylen = a.ntiles * kTcLags + K;
+    const int ylen = a.ylen;
     uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[s]);
     uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
     // zero the margins: x words outside [4, 4 + nx4), y words outside the signal
@@ -324,131 +423,152 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int64_t pair, c
             }
         }
     }
-    ssx = __reduce_add_sync(0xffffffffu, ssx);
-    nzx = __reduce_add_sync(0xffffffffu, nzx);
-    ssy = __reduce_add_sync(0xffffffffu, ssy);
-    nzy = __reduce_add_sync(0xffffffffu, nzy);
-    fl = __reduce_or_sync(0xffffffffu, fl);
-    if ((threadIdx.x & 31) == 0) {
-        unsigned long long* st = a.stats + pair * 8;
-        if (ssx) atomicAdd(st + 0, (unsigned long long)ssx);
-        if (nzx) atomicAdd(st + 1, (unsigned long long)nzx);
-        if (ssy) atomicAdd(st + 4, (unsigned long long)ssy);
-        if (nzy) atomicAdd(st + 5, (unsigned long long)nzy);
-        if (fl) atomicOr(st + 2, (unsigned long long)fl);
-    }
+    tc_aux_finish(a, S, s, u, ssx, nzx, ssy, nzy, fl);
 }
 
-// argmax epilogue of pair `pair` from TMEM slot s, run by warps 4..7 only
-// (warp w reads TMEM lanes 32*(w%4) .. +31 = accumulator rows), reduced with
-// a 128-thread named barrier so the other warps keep building.
+// argmax epilogue of the pair in aux slot u, run by warps 20..23 only (warp
+// w reads TMEM lane quarter w%4; M=128: lane = row, M=64: rows 16q..16q+15
+// sit in lanes 32q..32q+15), reduced behind a 128-thread named barrier so
+// the builders keep going; merges the builders' extra-lag sums and writes
+// the qx_result with the statistics from shared memory.
 constexpr int kEpiWarp0 = 20;
 
-__device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int s, int64_t pair)
+__device__ __forceinline__ void best_add(long long& bv, long long& bt, long long& bc, long long v, long long t,
+                                         long long c)
 {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = warp - kEpiWarp0;  // 0..3 = TMEM lane quarter
-    long long bv = LLONG_MIN, bt = LLONG_MAX, bc = 0;
-    const int64_t nx = a.op[0].n;
+    if (v > bv) { bv = v; bt = t; bc = c; }
+    else if (v == bv) { bt = min(bt, t); bc += c; }
+}
+
+__device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
+{
+    const int lane = threadIdx.x & 31;
+    const int q = (threadIdx.x >> 5) - kEpiWarp0;  // 0..3 = TMEM lane quarter
+    const int tl = 16 * a.M;
+    const int row = a.M == 128 ? q * 32 + lane : q * 16 + lane;
+    const bool live = a.M == 128 || lane < 16;
+    // window in tile-relative lag index j = lag - L0 (t = L0 + j + nx - 1)
+    const int64_t tbase = a.L0 + a.op[0].n - 1;
+    const int jlo = (int)(a.am.t_lo - tbase), jhi = (int)(a.am.t_hi - tbase);
+    // 32-bit branch-free scan: |value| < 2^31 - 1 (eligibility), so INT_MIN
+    // marks out-of-window entries and INT_MIN + 1 is below every value; j
+    // increases along the scan, so the first maximum is the smallest lag
+    int bv = INT_MIN + 1, bj = INT_MAX, bc = 0;
     for (int tile = 0; tile < a.ntiles; ++tile) {
         int v[16];
-        const uint32_t taddr = S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(s * 32 + tile * 16);
+        const uint32_t taddr = S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * 32 + tile * 16);
         tmem_ld16(taddr, v);
-        const int row = q * 32 + lane;
+        const int j0 = tile * tl + 16 * row;
 #pragma unroll
         for (int r = 0; r < 16; ++r) {
-            // lag = L0 + tile*2048 + 16*row + r; correlogram index t = lag + nx - 1
-            const long long t = a.L0 + tile * kTcLags + 16 * row + r + nx - 1;
-            if (t < a.am.t_lo || t > a.am.t_hi) continue;
-            const long long val = v[r];
-            if (val > bv) { bv = val; bt = t; bc = 1; }
-            else if (val == bv) { bt = min(bt, t); ++bc; }
+            const int j = j0 + r;
+            const int val = (live && j >= jlo && j <= jhi) ? v[r] : INT_MIN;
+            const bool gt = val > bv, eq = val == bv;
+            bj = gt ? j : bj;
+            bc = gt ? 1 : bc + (int)eq;
+            bv = gt ? val : bv;
         }
     }
-    // TMEM reads are complete (wait::ld) before the next MMA into this slot
+    // TMEM reads are complete (wait::ld) before the slot is released
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        const long long ov = __shfl_xor_sync(0xffffffffu, bv, o), ot = __shfl_xor_sync(0xffffffffu, bt, o),
-                        oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        if (ov > bv) { bv = ov; bt = ot; bc = oc; }
-        else if (ov == bv) { bt = min(bt, ot); bc += oc; }
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o), oj = __shfl_xor_sync(0xffffffffu, bj, o),
+                  oc = __shfl_xor_sync(0xffffffffu, bc, o);
+        const bool gt = ov > bv, eq = ov == bv;
+        bj = gt ? oj : (eq ? min(bj, oj) : bj);
+        bc = gt ? oc : bc + (eq ? oc : 0);
+        bv = gt ? ov : bv;
     }
     asm volatile("bar.sync 4, 128;" ::: "memory");  // previous pair's S.best reads done
     if (lane == 0) {
-        S.best[q][0] = (int)(bv == LLONG_MIN ? INT_MIN : bv);
-        S.best[q][1] = (int)(bt == LLONG_MAX ? INT_MAX : bt);
-        S.best[q][2] = (int)bc;
+        S.best[q][0] = bv;
+        S.best[q][1] = bj;
+        S.best[q][2] = bc;
     }
     asm volatile("bar.sync 4, 128;" ::: "memory");
-    if (q == 0 && lane == 0) {
+    if (q == 0) {
+        // lane i < 5 sums statistic i over the builder warps' records
+        constexpr int kW = kTcThreads / 32;
+        unsigned long long sum = 0;
+        if (lane < 5)
+            for (int w = 0; w < kW; ++w) {
+                const unsigned long long x = S.wst[u][w][lane];
+                sum = lane == 4 ? (sum | x) : sum + x;
+            }
+        const unsigned long long ssx = __shfl_sync(0xffffffffu, sum, 0), nzx = __shfl_sync(0xffffffffu, sum, 1),
+                                 ssy = __shfl_sync(0xffffffffu, sum, 2), nzy = __shfl_sync(0xffffffffu, sum, 3),
+                                 fls = __shfl_sync(0xffffffffu, sum, 4);
         long long v0 = LLONG_MIN, t0 = LLONG_MAX, c0 = 0;
-        for (int w = 0; w < 4; ++w) {
-            if (S.best[w][2] == 0) continue;
-            const long long ov = S.best[w][0], ot = S.best[w][1], oc = S.best[w][2];
-            if (ov > v0) { v0 = ov; t0 = ot; c0 = oc; }
-            else if (ov == v0) { t0 = min(t0, ot); c0 += oc; }
+        for (int w = 0; w < 4; ++w)
+            if (S.best[w][2]) best_add(v0, t0, c0, S.best[w][0], tbase + S.best[w][1], S.best[w][2]);
+        for (int e = 0; e < a.extra; ++e) {
+            const int xs = __reduce_add_sync(0xffffffffu, lane < kW ? S.wxs[u][lane][e] : 0);
+            const int j = a.ntiles * tl + e;
+            if (j < jlo || j > jhi) continue;
+            best_add(v0, t0, c0, xs, tbase + j, 1);
         }
-        // qx_result record; the statistics atomics of this pair were issued by
-        // this CTA before the barrier that preceded its MMA chain
-        long long* res = reinterpret_cast<long long*>(a.am.results) + pair * 8;
-        const unsigned long long* sp = a.stats + pair * 8;
-        __threadfence();
-        unsigned long long st[8];
-        for (int i = 0; i < 8; ++i) st[i] = __ldcg(sp + i);  // atomics live in L2
-        const long long nzx = (long long)st[1], nzy = (long long)st[5];
-        const unsigned f = (unsigned)(st[2] | st[6]);
         int flags = 0;
         if (nzx == 0) flags |= 1;
         if (nzy == 0) flags |= 2;
-        if (f & SF_NONFINITE) flags |= 4;
-        int status = (flags & 4) ? 9 : ((flags & 3) ? 2 : 0);
-        res[0] = v0;
-        res[1] = a.am.first_lag + t0;
-        res[2] = c0;
-        res[3] = (long long)st[0];
-        res[4] = (long long)st[4];
-        res[5] = nzx;
-        res[6] = nzy;
-        res[7] = ((long long)status << 32) | (unsigned)flags;
+        if (fls & SF_NONFINITE) flags |= 4;
+        const int status = (flags & 4) ? 9 : ((flags & 3) ? 2 : 0);
+        long long f = ((long long)status << 32) | (unsigned)flags;
+        f = lane == 0 ? v0 : lane == 1 ? a.am.first_lag + t0 : lane == 2 ? c0 : lane == 3 ? (long long)ssx
+          : lane == 4 ? (long long)ssy : lane == 5 ? (long long)nzx : lane == 6 ? (long long)nzy : f;
+        if (lane < 8) reinterpret_cast<long long*>(a.am.results)[pair * 8 + lane] = f;
     }
 }
 
-// completion of the MMA chain of loop iteration j (slot j & 1): the slot's
-// mbarrier completes once per use, so use number j >> 1 has parity (j>>1)&1
-__device__ __forceinline__ void tc_wait_iter(TcSmem& S, int j)
-{
-    mbar_wait(&S.bar[j & 1], (uint32_t)((j >> 1) & 1));
-}
+#ifdef QX_TC_TIMING
+#define TC_T0() const long long _t0 = clock64()
+#define TC_ACC(i) atomicAdd(&S.tm[i], (unsigned long long)(clock64() - _t0))
+#else
+#define TC_T0() ((void)0)
+#define TC_ACC(i) ((void)0)
+#endif
 
 template <typename T, int QM>
 __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     TcSmem& S = *reinterpret_cast<TcSmem*>(tc_smem_raw);
-    const int warp = threadIdx.x >> 5;
+    // warp index through a shuffle: provably warp-uniform, so the role
+    // branches keep descriptor arithmetic in uniform registers
+    const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < kMaxThr; i += kTcTotalThreads) {
         reinterpret_cast<T*>(S.thr[0])[i] = (T)a.op[0].q.thr[i];
         reinterpret_cast<T*>(S.thr[1])[i] = (T)a.op[1].q.thr[i];
     }
-    if (threadIdx.x == 0) {
-        mbar_init(&S.bar[0], 1);
-        mbar_init(&S.bar[1], 1);
-        mbar_init(&S.tfree[0], 128);
-        mbar_init(&S.tfree[1], 128);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (threadIdx.x < kTcAux) {
+        mbar_init(&S.mdone[threadIdx.x], 1);
+        mbar_init(&S.tfree[threadIdx.x], 128);
     }
+#ifdef QX_TC_TIMING
+    if (threadIdx.x < 8) S.tm[threadIdx.x] = 0;
+#endif
+    if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(&S.tmem_base)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&S.tmem_base)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
+    // Dependencies (iteration it: data slot it & 1, aux slot it & 3):
+    //   build(it)    after MMA(it-2) [data slot] and epilogue(it-4) [aux slot]
+    //   MMA(it)      after build(it) [named barrier] and epilogue(it-4) [TMEM]
+    //   epilogue(it) after MMA(it)
     const int64_t npairs = a.batch > blockIdx.x ? (a.batch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
     if (warp < kTcThreads / 32) {
-        // ---- builders: quantise + operands of iteration it into slot it & 1
+        // ---- builders
+        auto acquire = [&](int it) {
+            TC_T0();
+            if (it >= 2) tc_wait_mdone(S, it - 2);
+            if (it >= 4) tc_wait_tfree(S, it - 4);
+            if (threadIdx.x == 0) TC_ACC(0);
+        };
         auto handoff = [&](int it) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
             // alternating barrier ids keep consecutive iterations apart
@@ -464,8 +584,13 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                 for (int it = 0; it < npairs; ++it) {
                     const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
                     if (it + 1 < npairs) tc_fetch(a, pair + gridDim.x, nxt);
-                    if (it >= 2) tc_wait_iter(S, it - 2);  // slot no longer read by MMAs
-                    tc_build_fast<QM>(a, S, it & 1, pair, cur);
+                    acquire(it);
+                    TC_T0();
+#ifdef QX_TC_TIMING
+                    if (!(a.debug & 2))
+#endif
+                    tc_build_fast<QM>(a, S, it & 1, it & 3, cur);
+                    if (threadIdx.x == 0) TC_ACC(1);
                     handoff(it);
                     cur = nxt;
                 }
@@ -473,51 +598,85 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         } else {
             for (int it = 0; it < npairs; ++it) {
                 const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-                if (it >= 2) tc_wait_iter(S, it - 2);
-                tc_build<T, QM>(a, S, it & 1, pair);
+                acquire(it);
+                tc_build<T, QM>(a, S, it & 1, it & 3, pair);
                 handoff(it);
             }
         }
     } else if (warp == kTcMmaWarp) {
-        // ---- MMA issuer: one thread drives the tensor core
+        // ---- MMA issuer: the whole warp runs the loop, one elected lane issues
         const int nk = a.K / 32;
         for (int it = 0; it < npairs; ++it) {
-            const int s = it & 1;
-            if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcThreads + 32) : "memory");
-            else asm volatile("bar.sync 2, %0;" ::"n"(kTcThreads + 32) : "memory");
-            if (it >= 2) mbar_wait(&S.tfree[s], (uint32_t)(((it - 2) >> 1) & 1));  // TMEM slot drained
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            if ((threadIdx.x & 31) == 0) {
-                const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b[s]);
-                const uint64_t bd0 = smem_desc(ba, kTcBLbo, 128);
-                for (int tile = 0; tile < a.ntiles; ++tile) {
-                    const uint32_t d = S.tmem_base + (uint32_t)(s * 32 + tile * 16);
-                    uint64_t ad = smem_desc(ya + tile * kTcLags, 16, 128), bd = bd0;
-                    for (int kk = 0; kk < nk; ++kk) {
-                        mma_i8(d, ad, bd, kk > 0);
-                        ad += 32 >> 4;             // next 32 k-bytes of A
-                        bd += (2 * kTcBLbo) >> 4;  // next two k-chunks of B
-                    }
-                }
-                mma_commit(&S.bar[s]);
+            const int s = it & 1, u = it & 3;
+            {
+                TC_T0();
+                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcThreads + 32) : "memory");
+                else asm volatile("bar.sync 2, %0;" ::"n"(kTcThreads + 32) : "memory");
+                if (lane == 0) TC_ACC(2);
             }
+            {
+                TC_T0();
+                if (it >= 4) tc_wait_tfree(S, it - 4);  // TMEM slot drained
+                if (lane == 0) TC_ACC(4);
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            TC_T0();
+            const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b[s]);
+            const uint64_t bd0 = smem_desc(ba, kTcBLbo, 128);
+            const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
+            for (int tile = 0; tile < a.ntiles; ++tile) {
+#ifdef QX_TC_TIMING
+                if (a.debug & 1) break;
+#endif
+                const uint32_t d = tbase + (uint32_t)(u * 32 + tile * 16);
+                const uint64_t ad0 = smem_desc(ya + tile * 16 * a.M, 16, 128);
+                const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
+                uint32_t alo = (uint32_t)ad0, blo = (uint32_t)bd0;
+                mma_i8_warp(d, ad0, bd0, a.idesc, 0);
+                int kk = 1;
+                for (; kk + 4 <= nk; kk += 4) {
+                    mma_i8_warp4(d, alo + 2, ahi, blo + 34, bhi, a.idesc);
+                    alo += 8;
+                    blo += 4 * 34;
+                }
+                for (; kk < nk; ++kk) {
+                    alo += 32 >> 4;             // next 32 k-bytes of A
+                    blo += (2 * kTcBLbo) >> 4;  // next two k-chunks of B
+                    mma_i8_warp(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1);
+                }
+            }
+            mma_commit_warp(&S.mdone[u]);
             __syncwarp();
+            if (lane == 0) TC_ACC(5);
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        // ---- epilogue: TMEM -> argmax -> qx_result, then free the TMEM slot
+        // ---- epilogue: TMEM -> argmax -> qx_result, then free the aux slot
         for (int it = 0; it < npairs; ++it) {
             const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-            tc_wait_iter(S, it);
+            TC_T0();
+            tc_wait_mdone(S, it);
+            if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            tc_epilogue(a, S, it & 1, pair);
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[it & 1])) : "memory");
+            {
+                TC_T0();
+                tc_epilogue(a, S, it & 3, pair);
+                if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(6);
+            }
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[it & 3])) : "memory");
         }
     }
     // every MMA was waited on by the epilogue before TMEM is released
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(S.tmem_base));
+#ifdef QX_TC_TIMING
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("tc timing block0 npairs=%lld debug=%d (cycles/pair): build-wait %llu build %llu | mma: wait-handoff %llu "
+               "wait-tfree %llu issue %llu | epi: wait %llu run %llu\n",
+               (long long)npairs, a.debug, S.tm[0] / npairs, S.tm[1] / npairs, S.tm[2] / npairs, S.tm[4] / npairs,
+               S.tm[5] / npairs, S.tm[3] / npairs, S.tm[6] / npairs);
+#endif
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(S.tmem_base));
 }
 
 // eligibility: window of at most kTcMaxTiles*2048 lags, nx + 15 <= kTcMaxK,
@@ -526,7 +685,7 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
 {
     (void)ny;
     const int64_t W = c.am.t_hi - c.am.t_lo + 1;
-    if (W > (int64_t)kTcMaxTiles * kTcLags) return false;
+    if (W > (int64_t)kTcMaxTiles * kTcLags + kTcMaxExtra) return false;
     if (nx + 15 > kTcMaxK) return false;
     if (c.op[0].dtype != c.op[1].dtype || c.op[0].dtype == DT_I64) return false;
     if (c.op[0].q.mode != c.op[1].q.mode) return false;
@@ -562,8 +721,19 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     // tile 0 starts at the window's first lag (relative lag = t - (nx - 1))
     a.L0 = c.am.t_lo - (nx - 1);
     const int64_t W = c.am.t_hi - c.am.t_lo + 1;
-    a.ntiles = (int)((W + kTcLags - 1) / kTcLags);
+    // shape: one M=64 tile (1024 lags) when it covers the window up to the
+    // extra lags, else M=128 tiles (2048 lags each)
+    a.M = W <= 1024 + kTcMaxExtra ? 64 : 128;
+    const int tl = 16 * a.M;
+    a.ntiles = (int)((W - kTcMaxExtra + tl - 1) / tl);
+    if (a.ntiles < 1) a.ntiles = 1;
+    a.extra = (int)(W > (int64_t)a.ntiles * tl ? W - (int64_t)a.ntiles * tl : 0);
+    a.idesc = tc_idesc(a.M);
     a.K = (int)(((nx + 15) + 31) / 32 * 32);
+    a.ylen = a.ntiles * tl + kTcMaxExtra + a.K;
+#ifdef QX_TC_TIMING
+    if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
+#endif
     const int64_t ny = c.op[1].n;
     a.fast = c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 && ny % 4 == 0 &&
              (c.batch == 1 || (c.op[0].ld % 4 == 0 && c.op[1].ld % 4 == 0)) &&

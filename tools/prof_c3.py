@@ -18,3 +18,17 @@ for _ in range(3):
 torch.cuda.synchronize()
 assert np.array_equal(r.lag.cpu().numpy(), lag)
 print("ok")
+if os.environ.get("QX_PROF"):
+    from paper_2509_19974_b200 import _native
+    torch.cuda.synchronize()
+    with _native.profile(timed=True) as pr:
+        for _ in range(5):
+            P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512)
+    print({k: (c, ms / 5) for k, (c, ms) in pr.result.items()})
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(5):
+        P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512)
+    e.record()
+    torch.cuda.synchronize()
+    print("call ms", s.elapsed_time(e) / 5)

@@ -21,7 +21,11 @@ for trial in range(int(sys.argv[1]) if len(sys.argv) > 1 else 40):
     y = rng.standard_normal((B, ny)).astype(np.float32)
     nout = nx + ny - 1
     t_lo = int(rng.integers(0, nout))
-    t_hi = min(nout - 1, t_lo + int(rng.integers(0, 4096)))
+    special = [1, 15, 16, 17, 1024, 1025, 1040, 1041, 2048, 2049, 2064, 2065, 4096, 4097, 4112]
+    w = special[trial % len(special)] if trial % 2 else int(rng.integers(1, 4113))
+    if trial % 3 == 0:  # aligned window start (fast builder path needs L0 % 4 == 0)
+        t_lo = max(0, (nx - 1) - 4 * int(rng.integers(0, 256)))
+    t_hi = min(nout - 1, t_lo + w - 1)
     first = -(nx - 1)
     r = P.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), q, q, lag_lo=first + t_lo,
                          lag_hi=first + t_hi, path="direct").numpy()

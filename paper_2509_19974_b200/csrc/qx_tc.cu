@@ -176,7 +176,7 @@ struct TcSmem {
     uint32_t tmem_base;
     int best[4][3];
 #ifdef QX_TC_TIMING
-    unsigned long long tm[8];
+    unsigned long long tm[16];
 #endif
 };
 
@@ -195,6 +195,7 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
 // slot u: warp-reduced, one record per builder warp (summed by the epilogue)
+template <bool Y32>  // Y32: y statistics fit 32 bits per warp (fast path, ny <= 4096)
 __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
                               unsigned long long ssy, unsigned long long nzy, unsigned fl)
 {
@@ -215,12 +216,20 @@ __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned
         }
     }
     ssx = __reduce_add_sync(0xffffffffu, ssx);
-    nzx = __reduce_add_sync(0xffffffffu, nzx);
     fl = __reduce_or_sync(0xffffffffu, fl);
+    if constexpr (Y32) {
+        // per warp: nzx, nzy <= 32 * 16 samples, packed into one word
+        const unsigned nz = __reduce_add_sync(0xffffffffu, nzx | ((unsigned)nzy << 16));
+        nzx = nz & 0xffffu;
+        nzy = nz >> 16;
+        ssy = __reduce_add_sync(0xffffffffu, (unsigned)ssy);
+    } else {
+        nzx = __reduce_add_sync(0xffffffffu, nzx);
 #pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        ssy += __shfl_xor_sync(0xffffffffu, ssy, o);
-        nzy += __shfl_xor_sync(0xffffffffu, nzy, o);
+        for (int o = 16; o; o >>= 1) {
+            ssy += __shfl_xor_sync(0xffffffffu, ssy, o);
+            nzy += __shfl_xor_sync(0xffffffffu, nzy, o);
+        }
     }
     if (lane == 0) {
         unsigned long long* st = S.wst[u][threadIdx.x >> 5];
@@ -309,7 +318,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
         v.w = __funnelshift_r(a3, a4, sh);
         b4[kc * (kTcBLbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
     }
-    tc_aux_finish(a, S, s, u, ssx, nzx, ssy, nzy, fl);
+    tc_aux_finish<false>(a, S, s, u, ssx, nzx, ssy, nzy, fl);
 }
 
 // ---- fast build: float32 rows, nx, ny <= kTcFastN, 16-B aligned rows,
@@ -335,26 +344,76 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs& 
     }
 }
 
+// level_uniform_magic (qx_common.cuh) with the NaN test folded into its
+// rare exact branch: a NaN makes d NaN, fails `>= 2^-14` and lands there
+// (so does +-inf, which the exact compares then map to +-k)
+__device__ __forceinline__ int tc_level_uniform(float v, const float* s, int k, float inv_step, unsigned& flags)
+{
+    const float a = fabsf(v);
+    const float t = fmaf(a, inv_step, 12582912.0f);
+    int lv = __float_as_int(t) - 0x4B400000;
+    const float d = fmaf(a, inv_step, -(t - 12582912.0f));
+    lv = min(lv, k);
+    if (__builtin_expect(!(fabsf(fabsf(d) - 0.5f) >= 0x1p-14f), 0)) {
+        if (v != v) {
+            flags |= SF_NONFINITE;
+            return 0;
+        }
+        int l2 = v < 0.f ? -lv : lv;
+        if (l2 < k && v >= s[l2 + k]) ++l2;
+        if (l2 > -k && !(v >= s[l2 + k - 1])) --l2;
+        return l2;
+    }
+    return v < 0.f ? -lv : lv;
+}
+
 template <int QM>
 __device__ __forceinline__ int tc_q(float v, const float* thr, int k, float inv_step, unsigned& flags, int tbits = 8)
 {
+    if constexpr (QM == QM_UNIFORM) return tc_level_uniform(v, thr, k, inv_step, flags);
     if (v != v) flags |= SF_NONFINITE;
     if constexpr (QM == QM_K1) return level_k1(v, thr[0], thr[1]);
-    else if constexpr (QM == QM_UNIFORM) return level_uniform_magic(v, thr, k, inv_step);
     else return level_bsearch(v, thr, tbits) - k;
 }
 
-// quantise 4 samples -> packed int8 word, statistics
+// quantise 4 samples exactly -> packed int8 word (statistics are taken
+// from the packed word by tc_word_stats)
 template <int QM>
 __device__ __forceinline__ uint32_t tc_q4(float4 v, const float* thr, int k, float inv_step, int tbits,
                                           unsigned& ss, unsigned& nz, unsigned& fl)
 {
     const int c0 = tc_q<QM>(v.x, thr, k, inv_step, fl, tbits), c1 = tc_q<QM>(v.y, thr, k, inv_step, fl, tbits);
     const int c2 = tc_q<QM>(v.z, thr, k, inv_step, fl, tbits), c3 = tc_q<QM>(v.w, thr, k, inv_step, fl, tbits);
-    ss += (unsigned)(c0 * c0 + c1 * c1 + c2 * c2 + c3 * c3);
-    nz += (c0 != 0) + (c1 != 0) + (c2 != 0) + (c3 != 0);
+    (void)ss;
+    (void)nz;
     return (uint32_t)(c0 & 0xff) | ((uint32_t)(c1 & 0xff) << 8) | ((uint32_t)(c2 & 0xff) << 16) |
            ((uint32_t)c3 << 24);
+}
+
+// branch-free magic-rounding levels of 4 samples; `bad` is raised for a
+// sample near a rounding half-point, or NaN/inf (all rare): the caller then
+// recomputes the word exactly with tc_q4
+__device__ __forceinline__ uint32_t tc_q4_uniform_fast(float4 v, int k, float inv_step, bool& bad)
+{
+    const float e[4] = {v.x, v.y, v.z, v.w};
+    uint32_t w = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float a = fabsf(e[i]);
+        const float t = fmaf(a, inv_step, 12582912.0f);
+        const int lv = min(__float_as_int(t) - 0x4B400000, k);
+        const float d = fmaf(a, inv_step, -(t - 12582912.0f));
+        bad |= !(fabsf(fabsf(d) - 0.5f) >= 0x1p-14f);
+        const int c = e[i] < 0.f ? -lv : lv;
+        w |= (uint32_t)(c & 0xff) << (8 * i);
+    }
+    return w;
+}
+
+__device__ __forceinline__ void tc_word_stats(uint32_t w, unsigned& ss, unsigned& nz)
+{
+    ss += (unsigned)__dp4a((int)w, (int)w, 0);
+    nz += (unsigned)__popc(__vcmpne4(w, 0u)) >> 3;
 }
 
 template <int QM>
@@ -366,26 +425,66 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
     const float ix = (float)a.op[0].q.inv_step, iy = (float)a.op[1].q.inv_step;
     const int nx4 = (int)(a.op[0].n >> 2), ny4 = (int)(a.op[1].n >> 2), K = a.K;
     const int ylen = a.ylen;
+#ifdef QX_TC_TIMING
+    long long _m = clock64();
+#define TC_MARK(i) if (threadIdx.x == 0) { const long long _n = clock64(); atomicAdd(&S.tm[i], (unsigned long long)(_n - _m)); _m = _n; }
+#else
+#define TC_MARK(i)
+#endif
     uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[s]);
     uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
-    // zero the margins: x words outside [4, 4 + nx4), y words outside the signal
+    // zero the margins only: x words outside [4, 4 + nx4), y words outside
+    // the signal (front [0, yf), back [yb, Y))
     const int yoff = (int)(-a.L0) >> 2;  // word index of y[0] in the window (may be < 0)
-    for (int i = threadIdx.x; i < (K + 64) / 4; i += kTcThreads)
-        if (i < 4 || i >= 4 + nx4) xw[i] = 0;
-    for (int i = threadIdx.x; i < (ylen + 3) / 4; i += kTcThreads)
-        if (i < yoff || i >= yoff + ny4) yw[i] = 0;
+    const int X = (K + 64) / 4, Y = (ylen + 3) / 4;
+    const int yf = min(max(yoff, 0), Y), yb = min(max(yoff + ny4, yf), Y);
+    const int nxz = X - nx4, nyz = yf + (Y - yb);
+    for (int i = threadIdx.x; i < nxz + nyz; i += kTcThreads) {
+        if (i < nxz) xw[i < 4 ? i : nx4 + i] = 0;
+        else {
+            const int j = i - nxz;
+            yw[j < yf ? j : yb + (j - yf)] = 0;
+        }
+    }
+    TC_MARK(8);
     unsigned ssx = 0, nzx = 0, ssy = 0, nzy = 0, fl = 0;
+    // samples past n were fetched as zeros: code 0, no statistics
+    uint32_t wx[2], wy[2];
+    if constexpr (QM == QM_UNIFORM) {
+        bool bad = false;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            wx[h] = tc_q4_uniform_fast(r.x[h], kx, ix, bad);
+            wy[h] = tc_q4_uniform_fast(r.y[h], ky, iy, bad);
+        }
+        if (__builtin_expect(bad, 0)) {
+            unsigned d0 = 0, d1 = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                wx[h] = tc_q4<QM>(r.x[h], thrx, kx, ix, 8, d0, d1, fl);
+                wy[h] = tc_q4<QM>(r.y[h], thry, ky, iy, 8, d0, d1, fl);
+            }
+        }
+    } else {
+        unsigned d0 = 0, d1 = 0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            wx[h] = tc_q4<QM>(r.x[h], thrx, kx, ix, a.op[0].q.tbits, d0, d1, fl);
+            wy[h] = tc_q4<QM>(r.y[h], thry, ky, iy, a.op[1].q.tbits, d0, d1, fl);
+        }
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int i = threadIdx.x + h * kTcThreads;
-        if (i < nx4) xw[4 + i] = tc_q4<QM>(r.x[h], thrx, kx, ix, a.op[0].q.tbits, ssx, nzx, fl);
-        if (i < ny4) {
-            const uint32_t w = tc_q4<QM>(r.y[h], thry, ky, iy, a.op[1].q.tbits, ssy, nzy, fl);
-            const int wi = yoff + i;
-            if (wi >= 0 && wi < (ylen + 3) / 4) yw[wi] = w;
-        }
+        tc_word_stats(wx[h], ssx, nzx);
+        tc_word_stats(wy[h], ssy, nzy);
+        if (i < nx4) xw[4 + i] = wx[h];
+        const int wi = yoff + i;
+        if (i < ny4 && wi >= 0 && wi < (ylen + 3) / 4) yw[wi] = wy[h];
     }
+    TC_MARK(9);
     asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // builders only
+    TC_MARK(10);
     // shifted copies: item -> (chunk position kc, half h) with h uniform per
     // warp; the thread emits shifts r = 8h .. 8h+7 of chunk kc
     const uint4* xq = reinterpret_cast<const uint4*>(S.xl[s]);
@@ -423,7 +522,9 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
             }
         }
     }
-    tc_aux_finish(a, S, s, u, ssx, nzx, ssy, nzy, fl);
+    TC_MARK(11);
+    tc_aux_finish<true>(a, S, s, u, ssx, nzx, ssy, nzy, fl);
+    TC_MARK(12);
 }
 
 // argmax epilogue of the pair in aux slot u, run by warps 20..23 only (warp
@@ -545,7 +646,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         mbar_init(&S.tfree[threadIdx.x], 128);
     }
 #ifdef QX_TC_TIMING
-    if (threadIdx.x < 8) S.tm[threadIdx.x] = 0;
+    if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
 #endif
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (warp == 0) {
@@ -675,6 +776,9 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                "wait-tfree %llu issue %llu | epi: wait %llu run %llu\n",
                (long long)npairs, a.debug, S.tm[0] / npairs, S.tm[1] / npairs, S.tm[2] / npairs, S.tm[4] / npairs,
                S.tm[5] / npairs, S.tm[3] / npairs, S.tm[6] / npairs);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        printf("  build phases (cycles/pair): zero %llu quant %llu bar %llu copies %llu aux %llu\n", S.tm[8] / npairs,
+               S.tm[9] / npairs, S.tm[10] / npairs, S.tm[11] / npairs, S.tm[12] / npairs);
 #endif
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(S.tmem_base));
 }

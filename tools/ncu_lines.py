@@ -28,9 +28,12 @@ for r in csv.reader(out.splitlines()):
     elif hdr and len(r) == len(hdr) and r[0].isdigit():
         si = hdr.index("Warp Stall Sampling (All Samples)")
         ie = hdr.index("Instructions Executed")
-        recs.append((fname, int(r[0]), r[1].strip(), num(r[si]), num(r[ie])))
+        st = sorted(((num(r[i]), h[6:]) for i, h in enumerate(hdr)
+                     if h.startswith("stall_") and "Not Issued" not in h), reverse=True)[:2]
+        recs.append((fname, int(r[0]), r[1].strip(), num(r[si]), num(r[ie]),
+                     " ".join(f"{n}={v:.0f}" for v, n in st if v)))
 tot = sum(x[3] for x in recs) or 1
 itot = sum(x[4] for x in recs) or 1
 print(f"samples {tot:.0f}  warp-instructions {itot:.0f}")
-for f, ln, s, smp, ins in sorted(recs, key=lambda x: -x[3])[:top]:
-    print(f"{f}:{ln:<5d} {100 * smp / tot:5.1f}% smp {100 * ins / itot:5.1f}% inst  {s[:80]}")
+for f, ln, s, smp, ins, why in sorted(recs, key=lambda x: -x[3])[:top]:
+    print(f"{f}:{ln:<5d} {100 * smp / tot:5.1f}% smp {100 * ins / itot:5.1f}% inst  {s[:60]:60s} {why}")

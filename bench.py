@@ -121,24 +121,29 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU (oracle)
-def cpu_arm(pairs_sample, threads, xs, ys):
+def cpu_arm(pairs_sample, threads, xs, ys, min_seconds=0.0):
     """Reference algorithm on the host: the C oracle (quantise in float64,
     Kronecker substitution + GMP multiply, argmax) for every bit depth on
-    `pairs_sample` pairs, threaded over pairs.  Returns (estimates/s, seconds)."""
+    `pairs_sample` pairs, threaded over pairs, repeated until `min_seconds`
+    of work.  Returns (estimates/s, seconds, passes)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
 
     from paper_2509_19974_b200 import workloads as W
 
     O.build()
+    qs = [W.bit_quantizer(b, W.C2_SIGMA) for b in BITS]
     t0 = time.perf_counter()
-    n_est = 0
-    for b in BITS:
-        q = W.bit_quantizer(b, W.C2_SIGMA)
-        rec = O.estimate_batch_f32(xs[:pairs_sample], ys[:pairs_sample], q, q, threads=threads)
-        n_est += len(rec)
+    n_est = passes = 0
+    while True:
+        for q in qs:
+            rec = O.estimate_batch_f32(xs[:pairs_sample], ys[:pairs_sample], q, q, threads=threads)
+            n_est += len(rec)
+        passes += 1
+        if time.perf_counter() - t0 >= min_seconds:
+            break
     dt = time.perf_counter() - t0
-    return n_est / dt, dt
+    return n_est / dt, dt, passes
 
 
 def reference_arm(args):
@@ -152,7 +157,7 @@ def reference_arm(args):
     xs, ys, lag = W.c2(pairs=sample)
     times = []
     for i in range(args.warmup + args.steps):
-        rate, dt = cpu_arm(sample, threads, xs, ys)
+        rate, dt, _ = cpu_arm(sample, threads, xs, ys)
         if i >= args.warmup:
             times.append(dt)
     per_step = sum(times) / len(times)
@@ -283,32 +288,33 @@ def main():
         hy = torch.from_numpy(ys).pin_memory()
         hxn, hyn = hx.numpy(), hy.numpy()
         n_e2e = max(3, args.steps // 3)
-        for q in qs:
-            P.estimate_batch_host(hxn, hyn, q, q, device=local)
+        sweep = [(q, q) for q in qs]
+        P.estimate_sweep_host(hxn, hyn, sweep, device=local)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(n_e2e):
-            for q in qs:
-                res = P.estimate_batch_host(hxn, hyn, q, q, device=local)
+            res = P.estimate_sweep_host(hxn, hyn, sweep, device=local)
         t1 = time.perf_counter()
         e2e_s = torch.tensor([t1 - t0], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
-        assert np.array_equal(res["lag"], lag)
+        for r in res:
+            assert np.array_equal(r["lag"], lag)
         e2e = {"value": est_per_step * n_e2e / float(e2e_s.item()), "unit": UNIT,
-               "h2d_bytes_per_step": int(len(BITS) * (xs.nbytes + ys.nbytes)),
+               "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes),
                "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e,
-               "path": "qx_estimate_batch_host (C ABI, host buffers)"}
+               "path": "qx_estimate_sweep_host (C ABI, pinned host buffers; inputs staged once per step "
+                       "in 8 pair chunks overlapped with compute, 4 bit depths)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sample = min(pairs, max(8, threads))
-        rate, dt = cpu_arm(sample, threads, xs, ys)
+        rate, dt, passes = cpu_arm(sample, threads, xs, ys, min_seconds=10.0)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": f"{sample} pairs x {len(BITS)} bit depths of config 2 ({dt:.1f} s): "
+               "sample": f"{passes} passes over {sample} pairs x {len(BITS)} bit depths of config 2 ({dt:.1f} s): "
                          "C oracle = reference algorithm (float64 quantise, KS + GMP mpn_mul, argmax)"}
 
     if rank == 0:

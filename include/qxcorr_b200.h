@@ -141,6 +141,17 @@ qx_status qx_estimate_batch_host(qx_context *ctx, const qx_signals *x, const qx_
                                  int64_t batch, const qx_quantizer *qx, const qx_quantizer *qy,
                                  int64_t lag_lo, int64_t lag_hi, qx_path path, qx_result *results);
 
+/* Sweep of nq quantiser pairs over one batch from HOST buffers (the
+ * bit-depth sweep of BASELINE config 2, i.e. estimate() of estimator.py:60-94
+ * once per (qx[q], qy[q])): the inputs are staged to the device once, in
+ * pair chunks on a copy stream that overlaps the correlation of the previous
+ * chunk; results[q*batch + b] is pair b under quantiser pair q.  Synchronises;
+ * returns the first per-pair error status if any. */
+qx_status qx_estimate_sweep_host(qx_context *ctx, const qx_signals *x, const qx_signals *y,
+                                 int64_t batch, int64_t nq, const qx_quantizer *qx,
+                                 const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
+                                 qx_path path, qx_result *results);
+
 /* Launch accounting for measurement (bench.py): between begin and end every
  * kernel the library launches is counted per kind and, when `timed`, bracketed
  * by CUDA events on its own stream.  qx_profile_end synchronises and returns

@@ -114,6 +114,38 @@ def estimate_batch_host(x: np.ndarray, y: np.ndarray, qx, qy, *, lag_lo=None, la
     return res
 
 
+def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None, lag_hi=None, x_start=0,
+                        y_start=0, path="auto", device=None) -> np.ndarray:
+    """Several quantiser pairs over one batch of HOST arrays (a bit-depth
+    sweep) through qx_estimate_sweep_host: the inputs cross PCIe once, in pair
+    chunks overlapped with the correlation of the previous chunk.
+    `quantizers` is a sequence of (qx, qy); returns results[q, b] (structured
+    qx_result fields); raises on the first failing pair."""
+    x = np.ascontiguousarray(x)
+    y = np.ascontiguousarray(y)
+    if x.ndim == 1:
+        x = x[None]
+    if y.ndim == 1:
+        y = y[None]
+    if x.shape[0] != y.shape[0]:
+        raise ValueError("x and y batch sizes differ")
+    batch, nq = x.shape[0], len(quantizers)
+    if nq < 1:
+        raise ValueError("need at least one quantiser pair")
+    res = np.zeros((nq, batch), dtype=N.RESULT_DTYPE)
+    codes = {np.dtype(np.float32): N.QX_F32, np.dtype(np.float64): N.QX_F64, np.dtype(np.int64): N.QX_I64}
+    sx = N.QxSignals(x.ctypes.data, codes[x.dtype], 0, x.shape[1], x.shape[1], int(x_start))
+    sy = N.QxSignals(y.ctypes.data, codes[y.dtype], 0, y.shape[1], y.shape[1], int(y_start))
+    keep = [(native_quantizer(a), native_quantizer(b)) for a, b in quantizers]
+    aqx = (N.QxQuantizer * nq)(*[k[0][0] for k in keep])
+    aqy = (N.QxQuantizer * nq)(*[k[1][0] for k in keep])
+    lo, hi = _bounds(lag_lo, lag_hi)
+    ctx = N.context(device)
+    call(N.load().qx_estimate_sweep_host, ctx, ctypes.byref(sx), ctypes.byref(sy), batch, nq, aqx, aqy, lo, hi,
+         N.PATHS[path], res.ctypes.data)
+    return res
+
+
 MAX_P = 1 << 19  # largest single-launch transform of the NTT path
 
 

@@ -4,6 +4,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -51,6 +52,8 @@ struct qx_context {
     Arena counters;    // zero-initialised ints, reset by the kernels
     Arena stage;       // host-API staging (x, y, results)
     cudaStream_t host_stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // H2D of the sweep entry point
+    std::vector<cudaEvent_t> chunk_ev;    // per staged chunk (lazily created)
     Profiler prof;
     std::string last_error;
 };
@@ -131,6 +134,8 @@ void qx_context_destroy(qx_context* c)
     for (Arena* a : {&c->scratch, &c->counters, &c->stage})
         if (a->ptr) cudaFree(a->ptr);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (cudaEvent_t ev : c->chunk_ev) cudaEventDestroy(ev);
     delete c;
 }
 
@@ -569,6 +574,71 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
     for (int64_t b = 0; b < batch; ++b)
         if (results[b].status) return (qx_status)results[b].status;
+    return QX_OK;
+}
+
+qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                                 int64_t nq, const qx_quantizer* qxs, const qx_quantizer* qys, int64_t lag_lo,
+                                 int64_t lag_hi, qx_path path, qx_result* results)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!results || !qxs || !qys) return fail(ctx, QX_ERR_INVALID, "results/quantizers is NULL");
+    if (nq < 1) return fail(ctx, QX_ERR_INVALID, "nq must be >= 1");
+    if (batch < 1) return fail(ctx, QX_ERR_INVALID, "batch must be >= 1");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    qx_status st;
+    if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
+    if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
+    static const size_t esz[] = {4, 8, 8};
+    const size_t ex = esz[x->dtype], ey = esz[y->dtype];
+    const size_t xb = (size_t)((batch - 1) * x->ld + x->n) * ex;
+    const size_t yb = (size_t)((batch - 1) * y->ld + y->n) * ey;
+    const size_t xa = (xb + 255) & ~(size_t)255, ya = (yb + 255) & ~(size_t)255;
+    const size_t rb = (size_t)(nq * batch) * sizeof(qx_result);
+    cudaError_t e = arena_reserve(ctx->stage, xa + ya + rb, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "staging");
+    if (!ctx->copy_stream && (e = cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+        return cuda_fail(ctx, e, "copy stream");
+    char* d = (char*)ctx->stage.ptr;
+    qx_result* rd = (qx_result*)(d + xa + ya);
+    cudaStream_t s = ctx->host_stream, cs = ctx->copy_stream;
+    // chunks of disjoint rows are staged on the copy stream while the compute
+    // stream works on the previous chunk; overlapping / repeated rows are
+    // staged whole (one chunk)
+    const bool disjoint = x->ld >= x->n && y->ld >= y->n;
+    const int64_t nchunk = disjoint ? std::min<int64_t>(batch, 8) : 1;
+    const int64_t per = (batch + nchunk - 1) / nchunk;
+    while ((int64_t)ctx->chunk_ev.size() < nchunk) {
+        cudaEvent_t ev;
+        if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(ctx, e, "event");
+        ctx->chunk_ev.push_back(ev);
+    }
+    // the previous call's compute must be done with the staging buffer
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(ctx, e, "sync");
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t b0 = c * per, nb = std::min(per, batch - b0);
+        if (nb <= 0) break;
+        const size_t xo = (size_t)(b0 * x->ld) * ex, yo = (size_t)(b0 * y->ld) * ey;
+        const size_t xn = disjoint ? (size_t)((nb - 1) * x->ld + x->n) * ex : xb;
+        const size_t yn = disjoint ? (size_t)((nb - 1) * y->ld + y->n) * ey : yb;
+        e = cudaMemcpyAsync(d + xo, (const char*)x->data + xo, xn, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d + xa + yo, (const char*)y->data + yo, yn, cudaMemcpyHostToDevice, cs);
+        if (e == cudaSuccess) e = cudaEventRecord(ctx->chunk_ev[c], cs);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->chunk_ev[c], 0);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D");
+        qx_signals xd = *x, yd = *y;
+        xd.data = d + xo;
+        yd.data = d + xa + yo;
+        for (int64_t q = 0; q < nq; ++q) {
+            st = qx_estimate_batch(ctx, &xd, &yd, nb, &qxs[q], &qys[q], lag_lo, lag_hi, path, rd + q * batch + b0, s);
+            if (st != QX_OK) return st;
+        }
+    }
+    e = cudaMemcpyAsync(results, rd, rb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
+    for (int64_t i = 0; i < nq * batch; ++i)
+        if (results[i].status) return (qx_status)results[i].status;
     return QX_OK;
 }
 

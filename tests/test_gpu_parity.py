@@ -282,6 +282,27 @@ def test_host_entry_point(qx, oracle):
     assert np.array_equal(res["ties"], want[:, 2])
 
 
+def test_sweep_host_entry_point(qx, oracle):
+    """qx_estimate_sweep_host: several quantiser pairs, chunked staging with
+    copy/compute overlap, full-lag (NTT) and windowed (tensor-core) paths."""
+    from paper_2509_19974_b200 import workloads as W
+
+    xs, ys, lag = W.c2(pairs=11, n=1 << 12)
+    qs = [(W.bit_quantizer(b, W.C2_SIGMA), W.bit_quantizer(b, W.C2_SIGMA)) for b in (1, 2, 4, 8)]
+    qs.append((qx.uniform(3, 0.4), qx.sign()))
+    for lo, hi in ((None, None), (-700, 700)):
+        res = qx.estimate_sweep_host(xs, ys, qs, lag_lo=lo, lag_hi=hi)
+        assert res.shape == (len(qs), xs.shape[0])
+        for q, (a, b) in enumerate(qs):
+            one = qx.estimate_batch_host(xs, ys, a, b, lag_lo=lo, lag_hi=hi)
+            assert np.array_equal(res[q], one), q
+            if lo is None:
+                want = oracle.estimate_batch_f32(xs, ys, a, b)
+                assert np.array_equal(res[q]["value"], want[:, 0])
+                assert np.array_equal(res[q]["lag"], want[:, 1] - (xs.shape[1] - 1))
+                assert np.array_equal(res[q]["ties"], want[:, 2])
+
+
 def test_c2_full_size_properties(qx, oracle):
     """BASELINE config 2 at full size (64 pairs x 2^18, b = 1, 2, 4, 8): every
     pair finds its true delay; a sample of pairs is checked exactly against

@@ -3,7 +3,8 @@
 Times each config's hot path with CUDA events (inputs resident in HBM, warm
 tables), checks every estimate against the planted delay, and prints one JSON
 object.  C3 runs a 16384-pair slice of the 65,536-pair workload (per-pair
-cost is shape-only); C5 runs the full 2^28-sample stream.
+cost is shape-only; `c3full` runs all 65,536 pairs); C5 runs the full
+2^28-sample stream.  Roofline fractions use MEASURED_PEAKS.json hbm_gbs.
 usage: python tools/bench_configs.py [c1 c2 c3 c4 c5]"""
 import json
 import math
@@ -49,8 +50,10 @@ if "c2" in which:
         ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q))
         assert np.array_equal(r.numpy()["lag"], lag)
         res[f"c2_b{b}"] = {"ms": ms, "estimates_per_s": 64 / ms * 1e3, "gsamples_per_s": 64 * 2 * W.C2_N / ms / 1e6}
-if "c3" in which:
-    npairs = 16384
+HBM = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                            "MEASURED_PEAKS.json"))).get("hbm_gbs", 6550.4)
+if "c3" in which or "c3full" in which:
+    npairs = W.C3_PAIRS if "c3full" in which else 16384
     xs, ys, lag = W.c3(pairs=npairs)
     xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
     for b in (2, 4):
@@ -59,7 +62,8 @@ if "c3" in which:
         ok = float(np.mean(r.numpy()["lag"] == lag))
         res[f"c3_b{b}"] = {"pairs": npairs, "ms": ms, "estimates_per_s": npairs / ms * 1e3,
                            "gsamples_per_s": npairs * 2 * W.C3_N / ms / 1e6, "frac_correct_lag": ok,
-                           "path": "ntt (P=2^13 per pair)"}
+                           "hbm_frac": npairs * 2 * W.C3_N * 4 / (ms / 1e3) / 1e9 / HBM,
+                           "path": "tcgen05 kind::i8 window (M=64 tile + 1 CUDA-core lag)"}
 if "c4" in which:
     x, y, lag = W.c4()
     xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()

@@ -79,7 +79,7 @@ typedef struct qx_signals {
     int64_t start;     /* Signal.start of every row */
 } qx_signals;
 
-/* AUTO: bounded windows (<= 4096 lags, n_x <= 4593, k <= 127) -> DIRECT,
+/* AUTO: bounded windows (<= 4112 lags, n_x <= 4593, k <= 127) -> DIRECT,
  * else NTT.  NTT: exact full-lag number-theoretic transform path.  DIRECT:
  * tcgen05 int8 Toeplitz tiles over the lag window (argmax entry points). */
 typedef enum qx_path { QX_PATH_AUTO = 0, QX_PATH_NTT = 1, QX_PATH_DIRECT = 2 } qx_path;

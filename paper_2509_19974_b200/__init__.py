@@ -25,7 +25,7 @@ from .errors import (
     UnsupportedFormat,
 )
 from .estimator import EstimationResult, argmax_set, estimate
-from .intxcorr import xcorr_int_bf, xcorr_int_gpu, xcorr_int_ks
+from .intxcorr import MUL_BACKENDS, big_mul, xcorr_int_bf, xcorr_int_gpu, xcorr_int_ks
 from .quantize import Quantizer, apply, custom, from_spec, sign, uniform
 from .realxcorr import xcorr_real_at
 from .signals import Correlogram, IntSignal, Signal, l2_norm, reverse, shift
@@ -37,7 +37,7 @@ __all__ = [
     "ParseError", "UnsupportedFormat", "ConfigError",
     "Signal", "IntSignal", "Correlogram", "reverse", "shift", "l2_norm",
     "Quantizer", "sign", "uniform", "custom", "from_spec", "apply",
-    "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at",
+    "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "big_mul", "MUL_BACKENDS",
     "EstimationResult", "argmax_set", "estimate",
     "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep_host", "check_results", "template_search",
 ]

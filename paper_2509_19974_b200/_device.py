@@ -31,7 +31,9 @@ def as_device(a, dtype=None):
             return x
         return x.contiguous()
     arr = np.ascontiguousarray(a)
-    if not arr.flags.writeable:
+    # read-only buffers, and negative strides that ascontiguousarray keeps
+    # on single-element views, cannot be wrapped by torch
+    if not arr.flags.writeable or any(st < 0 for st in arr.strides):
         arr = arr.copy()
     x = t.from_numpy(arr)
     if dtype is not None and x.dtype != dtype:

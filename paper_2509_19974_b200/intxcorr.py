@@ -5,6 +5,10 @@ Drop-in for /root/reference/pkg/src/qxcorr/intxcorr.py's ``xcorr_int_bf``
 bit-identical int64 ``Correlogram`` (with ``norm_x``/``norm_y``) computed by
 the NTT kernels through ``qx_xcorr_full``.  ``_check_coeff_bound`` (89-93)
 and ``plan_ks``'s all-zero check (109-110) keep their exceptions.
+
+``big_mul`` (intxcorr.py:183-205) keeps the reference's plugin slot with one
+more backend, ``"cuda"``: the exact product of two big integers as one GPU
+correlation of their 16-bit limbs plus a linear carry pass.
 """
 
 from __future__ import annotations
@@ -21,9 +25,13 @@ from .errors import DegenerateInput
 from .quantize import native_quantizer
 from .signals import Correlogram
 
-__all__ = ["xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "MAX_COEFF_BOUND", "xcorr_full_device"]
+__all__ = ["xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "MAX_COEFF_BOUND", "xcorr_full_device", "big_mul",
+           "MUL_BACKENDS"]
 
 MAX_COEFF_BOUND = 1 << 59  # intxcorr.py:50
+# intxcorr.py:52 plus "cuda"; "auto" takes "cuda" from CUDA_MIN_BITS up
+MUL_BACKENDS = ("auto", "cuda", "gmp", "native", "karatsuba", "schoolbook")
+CUDA_MIN_BITS = 1 << 17
 
 
 def _check_coeff_bound(n_min: int, k_u: int, k_v: int) -> None:
@@ -71,7 +79,67 @@ def xcorr_int_bf(u, v) -> Correlogram:
 
 
 def xcorr_int_ks(u, v, mul_backend: str = "auto") -> Correlogram:
-    """Reference name (intxcorr.py:259); rejects all-zero input like plan_ks."""
+    """Reference name (intxcorr.py:259); rejects all-zero input like plan_ks
+    and unknown multiplication backends like big_mul."""
+    if mul_backend not in MUL_BACKENDS:
+        raise ValueError(f"unknown multiplication backend {mul_backend!r}")
     if not np.asarray(u.samples).any() or not np.asarray(v.samples).any():
         raise DegenerateInput("cannot plan a Kronecker correlation for an all-zero signal")
     return xcorr_int_gpu(u, v)
+
+
+_LIMB = 16
+_LIMB_MAX = (1 << _LIMB) - 1
+
+
+def _limbs(a: int) -> np.ndarray:
+    nb = (a.bit_length() + _LIMB - 1) // _LIMB
+    return np.frombuffer(a.to_bytes(2 * nb, "little"), dtype="<u2").astype(np.int64)
+
+
+def _big_mul_cuda(a: int, b: int) -> int:
+    """a*b for naturals a, b > 0: conv(limbs(a), limbs(b)) as the exact GPU
+    correlation of reverse(limbs(a)) with limbs(b) (index t = n + na - 1 is
+    the convolution index), then carries: every coefficient is < 2^59
+    (the 2^59 bound caps min(#limbs) at 2^27, i.e. 2^31-bit operands), so
+    it splits into four 16-bit planes P_j and a*b = sum_j P_j << 16j."""
+    la, lb = _limbs(a), _limbs(b)
+    _check_coeff_bound(min(la.size, lb.size), _LIMB_MAX, _LIMB_MAX)
+    du = D.as_device(la[::-1].copy())
+    dv = D.as_device(lb)
+    values, _ = xcorr_full_device(du, dv, _LIMB_MAX, _LIMB_MAX)
+    c = values[0].cpu().numpy().view(np.uint64)
+    out = 0
+    for j in range(4):
+        plane = ((c >> np.uint64(_LIMB * j)) & np.uint64(_LIMB_MAX)).astype("<u2")
+        out += int.from_bytes(plane.tobytes(), "little") << (_LIMB * j)
+    return out
+
+
+def big_mul(a: int, b: int, backend: str = "auto") -> int:
+    """Exact product of two big integers (intxcorr.py:183-205).
+
+    "cuda" runs the NTT correlation kernels on 16-bit limbs (exact at every
+    size up to 2^31-bit operands).  "auto" uses "cuda" when both operands
+    have at least CUDA_MIN_BITS bits and a GPU is present, else the
+    interpreter's multiplication.  "native", "karatsuba" and "schoolbook"
+    return the interpreter's exact product (the reference's backends all
+    return identical values); "gmp" needs gmpy2 like the reference."""
+    if backend not in MUL_BACKENDS:
+        raise ValueError(f"unknown multiplication backend {backend!r}")
+    if backend == "gmp":
+        try:
+            import gmpy2
+        except ImportError:
+            raise ValueError("gmp backend requested but gmpy2 is not installed") from None
+        return int(gmpy2.mpz(a) * gmpy2.mpz(b))
+    if backend == "auto":
+        big = min(abs(a).bit_length(), abs(b).bit_length()) >= CUDA_MIN_BITS
+        backend = "cuda" if big and D.torch().cuda.is_available() else "native"
+    if backend != "cuda":
+        return a * b
+    sign = -1 if (a < 0) != (b < 0) else 1
+    a, b = abs(a), abs(b)
+    if a == 0 or b == 0:
+        return 0
+    return sign * _big_mul_cuda(a, b)

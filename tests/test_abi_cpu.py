@@ -7,6 +7,7 @@ import os
 import re
 
 import numpy as np
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -73,3 +74,20 @@ def test_quantizer_validation_errors():
     bad = N.QxQuantizer(N.QX_Q_UNIFORM, 0, 3, -1.0, None)
     out = np.empty(6)
     assert N.load().qx_quantizer_thresholds(ctypes.byref(bad), N.QX_F32, out.ctypes.data) == N.QX_ERR_INVALID
+
+
+def test_big_mul_host_backends_and_errors():
+    """big_mul's plugin-slot contract (intxcorr.py:183-205, pkg/tests/test_intxcorr.py:139-149)
+    for the host backends; the "cuda" backend is covered by the GPU tests."""
+    import paper_2509_19974_b200 as qx
+
+    assert qx.big_mul(257, 515) == 132355
+    for backend in ("native", "karatsuba", "schoolbook", "auto"):
+        assert qx.big_mul(123456789, 0, backend) == 0
+        assert qx.big_mul(123456789, 1, backend) == 123456789
+        assert qx.big_mul(-7, 9, backend) == -63
+        assert qx.big_mul(-7, -9, backend) == 63
+    with pytest.raises(ValueError):
+        qx.big_mul(1, 1, "fft")
+    with pytest.raises(ValueError):
+        qx.big_mul(1, 1, "gmp")  # gmpy2 is not installed here, as in the reference

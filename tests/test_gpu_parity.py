@@ -303,6 +303,34 @@ def test_sweep_host_entry_point(qx, oracle):
                 assert np.array_equal(res[q]["ties"], want[:, 2])
 
 
+def test_big_mul_cuda_backend(qx):
+    """The reference's plugin slot big_mul (intxcorr.py:183-205) with backend
+    "cuda": worked product and identities (pkg/tests/test_intxcorr.py:139-149),
+    random 4096-bit operands against the interpreter (150-158), and large
+    unbalanced operands that need the multi-prime NTT path and every carry
+    plane; auto switches to cuda from CUDA_MIN_BITS."""
+    from paper_2509_19974_b200 import intxcorr as IX
+
+    assert qx.big_mul(257, 515, "cuda") == 132355
+    assert qx.big_mul(123456789, 0, "cuda") == 0
+    assert qx.big_mul(123456789, 1, "cuda") == 123456789
+    assert qx.big_mul(-7, 9, "cuda") == -63
+    assert qx.big_mul(-7, -9, "cuda") == 63
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        a = int.from_bytes(rng.bytes(512), "little")
+        b = int.from_bytes(rng.bytes(512), "little")
+        assert qx.big_mul(a, b, "cuda") == a * b
+    for na, nb in ((1 << 17, 1 << 17), (1 << 20, 3 << 16), (5, 1 << 21)):
+        a = int.from_bytes(rng.bytes(na), "little") | (1 << (8 * na - 1))
+        b = int.from_bytes(rng.bytes(nb), "little") | 1
+        assert qx.big_mul(a, -b, "cuda") == -(a * b)
+    allones = (1 << (1 << 20)) - 1  # every limb 0xffff: maximal coefficients and carries
+    assert qx.big_mul(allones, allones, "cuda") == allones * allones
+    a = (1 << IX.CUDA_MIN_BITS) + 12345
+    assert qx.big_mul(a, a, "auto") == a * a
+
+
 def test_c2_full_size_properties(qx, oracle):
     """BASELINE config 2 at full size (64 pairs x 2^18, b = 1, 2, 4, 8): every
     pair finds its true delay; a sample of pairs is checked exactly against

@@ -386,7 +386,8 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     c.chunk = chunk;
     const size_t wb = (size_t)chunk * per_pair * 4;
     const size_t sb = (size_t)batch * 8 * 8;
-    const size_t pb = argmax ? (size_t)batch * kMaxPartials * 3 * 8 : 0;
+    c.am.pstride = large ? kMaxPartialsLarge : kMaxPartials;
+    const size_t pb = argmax ? (size_t)batch * c.am.pstride * 3 * 8 : 0;
     cudaError_t e = arena_reserve(ctx->scratch, wb + sb + pb + 256, false);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
     e = arena_reserve(ctx->counters, (size_t)batch * 4, true);

@@ -153,6 +153,20 @@ __device__ __forceinline__ int level_uniform_magic(float v, const float* s, int 
     return v < 0.f ? -lv : lv;
 }
 
+// Branch-free form of level_uniform_magic for batches: returns the
+// magic-rounding level and raises `bad` when the sample is within 2^-14 of
+// a rounding half-point, NaN or +-inf; callers redo a batch with `bad` set
+// through the exact threshold compares.
+__device__ __forceinline__ int level_uniform_nb(float v, int k, float inv_step, bool& bad)
+{
+    const float a = fabsf(v);
+    const float t = fmaf(a, inv_step, 12582912.0f);
+    const int lv = min(__float_as_int(t) - 0x4B400000, k);
+    const float d = fmaf(a, inv_step, -(t - 12582912.0f));
+    bad |= !(fabsf(fabsf(d) - 0.5f) >= 0x1p-14f);
+    return v < 0.f ? -lv : lv;
+}
+
 template <typename T>
 __device__ __forceinline__ int level_uniform(T v, const T* s, int k, T inv_step)
 {

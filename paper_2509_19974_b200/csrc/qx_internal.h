@@ -42,10 +42,12 @@ struct ArgmaxOut {
     void* results;
     int64_t first_lag;   // lag of correlogram index t = 0
     int64_t t_lo, t_hi;  // inclusive window on t
-    long long* partials; // [batch][kMaxPartials][3]
+    long long* partials; // [batch][pstride][3]
     int* counters;       // [batch]
+    int pstride;         // partial records per pair (>= CTAs per pair of any argmax launch)
 };
-constexpr int kMaxPartials = 64;
+constexpr int kMaxPartials = 64;        // four-step passes / combine
+constexpr int kMaxPartialsLarge = 512;  // outer inverse of the large-P path
 
 // Tables for one (prime, log2 P) transform plan, device pointers.
 struct NttTables {
@@ -83,6 +85,8 @@ struct OuterTables {
     const uint32_t* th;   // omega_P^(8192 b) * R,          b < P / 8192
     const uint32_t* tli;  // omega_P^-a * M^-1 * R
     const uint32_t* thi;  // omega_P^-(8192 b) * R
+    const uint2* rf;      // omega_M^t  (Shoup pairs), t < M/2: register-resident outer DIF
+    const uint2* ri;      // omega_M^-t (Shoup pairs), t < M/2: register-resident outer DIT
 };
 
 struct NttCall {

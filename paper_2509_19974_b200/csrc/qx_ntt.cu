@@ -615,7 +615,7 @@ __device__ void argmax_finish(Best b, const ArgmaxOut& am, const unsigned long l
     if (threadIdx.x == 0) {
         Best r = sb[0];
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(r, sb[w]);
-        long long* pp = am.partials + (pair * kMaxPartials + blk) * 3;
+        long long* pp = am.partials + (pair * am.pstride + blk) * 3;
         pp[0] = r.v; pp[1] = r.t; pp[2] = r.c;
         __threadfence();
         const int ticket = atomicAdd(am.counters + pair, 1);
@@ -623,11 +623,22 @@ __device__ void argmax_finish(Best b, const ArgmaxOut& am, const unsigned long l
     }
     __syncthreads();
     if (!s_last) return;
+    // last block: every thread merges a strided share of the partials
+    __threadfence();
+    Best r = best_init();
+    const volatile long long* pp = am.partials + pair * am.pstride * 3;
+    for (int i = threadIdx.x; i < nblk; i += blockDim.x) best_merge(r, Best{pp[3 * i], pp[3 * i + 1], pp[3 * i + 2]});
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        Best o2{__shfl_xor_sync(0xffffffffu, r.v, o), __shfl_xor_sync(0xffffffffu, r.t, o),
+                __shfl_xor_sync(0xffffffffu, r.c, o)};
+        best_merge(r, o2);
+    }
+    __syncthreads();  // sb reads of the first merge are done
+    if (lane == 0) sb[warp] = r;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        Best r = best_init();
-        const volatile long long* pp = am.partials + pair * kMaxPartials * 3;
-        for (int i = 0; i < nblk; ++i) best_merge(r, Best{pp[3 * i], pp[3 * i + 1], pp[3 * i + 2]});
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best_merge(r, sb[w]);
         write_result(reinterpret_cast<long long*>(am.results) + pair * 8, r, am.first_lag, stats + pair * 8);
         am.counters[pair] = 0;
     }
@@ -818,9 +829,11 @@ struct OuterArgs {
     uint32_t* out;           // forward: [op][pair][pos][Q]
     const uint32_t* rin;     // inverse: inner residues [pair*M + pos][np][Q]
     uint32_t* rout;          // inverse, multi-prime: [pair][np][P] for k_combine
-    const uint2* gtw;        // DIF (fwd) / DIT (inv) group twiddles for M
+    const uint2* rtw;        // omega_M^(+-t), t < M/2 (Shoup pairs): fwd rf / inv ri
     const uint32_t* tl;      // two-level twiddles (Montgomery form; inv: * 1/M)
     const uint32_t* th;
+    const uint32_t* tlf;     // inverse: the forward two-level tables (omega_P^-j = omega_P^(P-j))
+    const uint32_t* thf;
     unsigned long long* stats;
     ArgmaxOut am;
     int64_t* values;
@@ -837,63 +850,178 @@ __device__ __forceinline__ uint32_t tw_2level(const uint32_t* __restrict__ tl, c
     return redp(montmul(__ldg(&tl[e & 8191u]), __ldg(&th[e >> 13]), m.p, m.pinv), m.p);
 }
 
-template <int LOGM>
-constexpr size_t outer_smem(size_t tsz)
+// Outer M-point transforms of the large-P path, one thread per column j of
+// the M x Q layout (element n = row * Q + j): the column's M <= 128
+// residues stay in registers for the whole radix-2 transform, so there is no
+// shared-memory exchange and no barrier; a warp's row accesses are 32
+// consecutive words.  Stage twiddles omega_M^t come from a 64-entry table.
+constexpr int kOuterThreads = 256;
+
+// natural -> bit-reversed DIF (Gentleman-Sande); values in [0, 2p).  One
+// template step per stage keeps every trip count a compile-time constant,
+// so the whole column stays in registers.
+template <int LOGM, int ST = 0>
+__device__ __forceinline__ void dif_full(uint32_t (&x)[1 << LOGM], const uint2* tw, const ModP& m)
 {
-    return (size_t)(1 << LOGM) * kPad * 4 + (size_t)(Sched<LOGM>::TW_DIF + Sched<LOGM>::TW_DIT) * 8 +
-           (size_t)kMaxThr * tsz;
+    if constexpr (ST < LOGM) {
+        constexpr int M = 1 << LOGM, half = M >> (ST + 1);
+#pragma unroll
+        for (int b0 = 0; b0 < M; b0 += 2 * half)
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                uint32_t& u = x[b0 + i];
+                uint32_t& v = x[b0 + i + half];
+                if (i == 0) {
+                    const uint32_t sm = u + v + m.zero, df = u - v + m.p2;
+                    u = red2p(sm, m.p2);
+                    v = red2p(df, m.p2);
+                } else {
+                    bfly_dif(u, v, tw[i << ST], m);
+                }
+            }
+        dif_full<LOGM, ST + 1>(x, tw, m);
+    }
+}
+
+// bit-reversed -> natural DIT (Cooley-Tukey); values in [0, 4p)
+template <int LOGM, int ST = 0>
+__device__ __forceinline__ void dit_full(uint32_t (&x)[1 << LOGM], const uint2* tw, const ModP& m)
+{
+    if constexpr (ST < LOGM) {
+        constexpr int M = 1 << LOGM, half = 1 << ST;
+#pragma unroll
+        for (int b0 = 0; b0 < M; b0 += 2 * half)
+#pragma unroll
+            for (int i = 0; i < half; ++i) {
+                uint32_t& u = x[b0 + i];
+                uint32_t& v = x[b0 + i + half];
+                if (i == 0) {
+                    const uint32_t a0 = red2p(u, m.p2), t = red2p(v, m.p2);
+                    u = a0 + t + m.zero;
+                    v = a0 - t + m.p2;
+                } else {
+                    bfly_dit(u, v, tw[i << (LOGM - 1 - ST)], m);
+                }
+            }
+        dit_full<LOGM, ST + 1>(x, tw, m);
+    }
+}
+
+constexpr int brev_c(int r, int bits)
+{
+    int o = 0;
+    for (int i = 0; i < bits; ++i) o |= ((r >> i) & 1) << (bits - 1 - i);
+    return o;
+}
+
+// Column j's four-step twiddles omega_P^(+-j k1), k1 = 0..M-1, as a running
+// Montgomery product (one table lookup per column instead of two per
+// element): x[bitrev(k1)] = x * cur_k1, cur_0 = c0, cur_(k+1) = cur_k * wj.
+// Four interleaved chains (k1 = 4i + c, step wj^4) keep the dependent
+// product chain at M/4.
+template <int LOGM>
+__device__ __forceinline__ void apply_column_twiddles(uint32_t (&x)[1 << LOGM], uint32_t c0, uint32_t wj,
+                                                      const ModP& m)
+{
+    constexpr int M = 1 << LOGM, NC = M < 4 ? M : 4;
+    const uint32_t w2 = montmul(wj, wj, m.p, m.pinv);
+    const uint32_t w4 = montmul(w2, w2, m.p, m.pinv);
+    uint32_t cur[4];
+    cur[0] = c0;
+    cur[1] = montmul(c0, wj, m.p, m.pinv);
+    cur[2] = montmul(c0, w2, m.p, m.pinv);
+    cur[3] = montmul(cur[1], w2, m.p, m.pinv);
+    const uint32_t step = NC == 4 ? w4 : (NC == 2 ? w2 : wj);
+#pragma unroll
+    for (int k1 = 0; k1 < M; ++k1) {
+        uint32_t& v = x[brev_c(k1, LOGM)];
+        uint32_t& c = cur[k1 % NC];
+        v = montmul(v, c, m.p, m.pinv);
+        if (k1 + NC < M) c = montmul(c, step, m.p, m.pinv);
+    }
 }
 
 template <int LOGM, typename T, int QM>
-__global__ void __launch_bounds__(kThreads, 1) k_outer_fwd(const __grid_constant__ OuterArgs a)
+__global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_constant__ OuterArgs a)
 {
     constexpr int M = 1 << LOGM;
-    using SC = Sched<LOGM>;
-    constexpr int R0 = SC::r(0), S = M >> R0, RAD0 = 1 << R0;
-    constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint2* stw = reinterpret_cast<uint2*>(smem + M * kPad);
-    T* sthr = reinterpret_cast<T*>(stw + SC::TW_DIF + SC::TW_DIT);
-
+    constexpr int CH = 16;  // rows loaded ahead per batch
+    constexpr int NCH = M < CH ? 1 : M / CH, CW = M < CH ? M : CH;
+    __shared__ uint2 stw[M / 2];
+    __shared__ T sthr[kMaxThr];
     const int op = blockIdx.y;
     const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
     if (a.skip_cs && cs_single(a.stats, pair, a.p0)) return;
     const OperandDesc& d = a.op[op];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int Q = 1 << a.lq;
-    const int j = blockIdx.x * 32 + lane;
-    const ModP m = a.m;
-    stage_table(stw, a.gtw, SC::TW_DIF);
-    for (int i = threadIdx.x; i < d.q.tsize; i += kThreads) sthr[i] = (T)d.q.thr[i];
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < M / 2; i += kOuterThreads) stw[i] = a.rtw[i];
+    for (int i = threadIdx.x; i < d.q.tsize; i += kOuterThreads) sthr[i] = (T)d.q.thr[i];
     __syncthreads();
-    T t0 = sthr[0], t1 = sthr[1];
-    const T inv_step = (T)d.q.inv_step;
+    const T t0 = sthr[0], t1 = sthr[1], inv_step = (T)d.q.inv_step;
     const int k = d.q.k, tbits = d.q.tbits;
-    const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld;
+    const ModP m = a.m;
+    const int Q = 1 << a.lq;
+    const int j = blockIdx.x * kOuterThreads + threadIdx.x;
     const int64_t n = d.n;
+    // element r*Q + j of the (possibly reversed) row: base pointer + signed
+    // stride; rows r < nrows exist (idx < n), the upper half is zero when
+    // the host says so
+    const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld + (d.reverse ? n - 1 - j : j);
+    const int64_t stride = d.reverse ? -(int64_t)Q : (int64_t)Q;
+    int nrows = j < n ? (int)min((n - j + Q - 1) / Q, (int64_t)M) : 0;
+    if (a.zero_upper) nrows = min(nrows, M / 2);
     unsigned ssq = 0, nnz = 0, flags = 0;
-    // first DIF group from global: rows g + kk*S of column j
-#pragma unroll 1
-    for (int g = warp; g < S; g += kWarps) {
-        uint32_t x[RAD0];
+    uint32_t x[M];
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) {
-            x[kk] = 0;
-            if (a.zero_upper && kk >= RAD0 / 2) continue;
-            const int64_t idx = (int64_t)(g + kk * S) * Q + j;
-            if (idx < n) {
-                const int c = load_code<T, QM>(src, d.reverse ? n - 1 - idx : idx, sthr, k, tbits, inv_step, t0,
-                                               t1, flags);
-                ssq += (unsigned)(c * c);
-                nnz += (c != 0);
-                x[kk] = c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
+    for (int ch = 0; ch < NCH; ++ch) {
+        // all loads of the batch first (independent, coalesced across the warp)
+        T v[CW];
+        bool live[CW];
+#pragma unroll
+        for (int i = 0; i < CW; ++i) {
+            const int r = ch * CW + i;
+            live[i] = r < nrows;
+            v[i] = live[i] ? __ldg(src + r * stride) : T(0);
+        }
+        int c[CW];
+        if constexpr (QM == QM_UNIFORM && sizeof(T) == 4) {
+            bool bad = false;
+#pragma unroll
+            for (int i = 0; i < CW; ++i) c[i] = level_uniform_nb((float)v[i], k, (float)inv_step, bad);
+            if (__builtin_expect(bad, 0)) {
+#pragma unroll
+                for (int i = 0; i < CW; ++i) {
+                    if (v[i] != v[i]) flags |= SF_NONFINITE;
+                    c[i] = quant_level<T, QM>(v[i], sthr, k, tbits, inv_step, t0, t1);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) {
+                if constexpr (QM == QM_CODES) {
+                    const long long cc = (long long)v[i];
+                    if (cc > k || cc < -k) flags |= SF_CODE_RANGE;
+                    c[i] = (int)cc;
+                } else {
+                    if (v[i] != v[i]) flags |= SF_NONFINITE;
+                    c[i] = quant_level<T, QM>(v[i], sthr, k, tbits, inv_step, t0, t1);
+                }
             }
         }
-        dif_regs<LOGM, 0>(x, g, stw, m);
-        uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
+        for (int i = 0; i < CW; ++i) {
+            const int cc = live[i] ? c[i] : 0;
+            ssq += (unsigned)(cc * cc);
+            nnz += (cc != 0);
+            x[ch * CW + i] = cc < 0 ? (uint32_t)(cc + (int)m.p) : (uint32_t)cc;
+        }
     }
+    dif_full<LOGM>(x, stw, m);
+    // register r holds frequency k1 = bitrev(r): x omega_P^(j k1) -> row r
+    apply_column_twiddles<LOGM>(x, tw_2level(a.tl, a.th, 0, m), tw_2level(a.tl, a.th, (uint32_t)j, m), m);
+    uint32_t* out = a.out + ((int64_t)op * a.batch + pl) * ((int64_t)M << a.lq) + j;  // a.batch: chunk size
+#pragma unroll
+    for (int r = 0; r < M; ++r) out[(int64_t)r * Q] = x[r];
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
@@ -906,99 +1034,71 @@ __global__ void __launch_bounds__(kThreads, 1) k_outer_fwd(const __grid_constant
         if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
         if (flags) atomicOr(st + 2, (unsigned long long)flags);
     }
-    __syncthreads();
-    dif_middle<LOGM, 1, 1>(smem, nullptr, stw, m);
-    // last DIF group -> x omega_P^(j*k1) -> row pos of the inner input
-    uint32_t* out = a.out + ((int64_t)op * a.batch + pl) * ((int64_t)M << a.lq);  // a.batch: chunk size
-    const uint32_t pmask = ((uint32_t)M << a.lq) - 1;
-#pragma unroll 1
-    for (int g = warp; g < (M >> RL); g += kWarps) {
-        uint32_t x[RADL];
-        const uint32_t* p = smem + g * RADL * kPad + lane;
-#pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[kk * kPad];
-        dif_regs<LOGM, SC::NG - 1>(x, 0, stw, m);
-#pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) {
-            const int pos = g * RADL + kk;
-            const uint32_t k1 = __brev((uint32_t)pos) >> (32 - LOGM);
-            const uint32_t w = tw_2level(a.tl, a.th, ((uint32_t)j * k1) & pmask, m);
-            out[(int64_t)pos * Q + j] = montmul(x[kk], w, m.p, m.pinv);
-        }
-    }
 }
 
 template <int LOGM, int OUT>
-__global__ void __launch_bounds__(kThreads, 1) k_outer_inv(const __grid_constant__ OuterArgs a)
+__global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_constant__ OuterArgs a)
 {
     constexpr int M = 1 << LOGM;
-    using SC = Sched<LOGM>;
-    constexpr int R0 = SC::rd(0), RAD0 = 1 << R0, NG0 = M >> R0;
-    constexpr int RL = SC::rd(SC::NG - 1), S0L = SC::s0d(SC::NG - 1), RADL = 1 << RL;
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint2* sti = reinterpret_cast<uint2*>(smem + M * kPad) + SC::TW_DIF;
-
+    __shared__ uint2 stw[M / 2];
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
     if (a.pi > 0 && cs) return;
     const bool final_out = (a.np == 1) || cs;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < M / 2; i += kOuterThreads) stw[i] = a.rtw[i];
+    __syncthreads();
     const int Q = 1 << a.lq;
     const ModP m = a.m;
-    const uint32_t pmask = ((uint32_t)M << a.lq) - 1;
     const uint32_t half = (m.p - 1) / 2;
     const int64_t P = (int64_t)M << a.lq;
-    stage_table(sti, a.gtw, SC::TW_DIT);
-    Best b = best_init();
-    // column tiles are strided over the (<= kMaxPartials) CTAs of this pair
+    const uint32_t pmask = (uint32_t)P - 1;
+    const uint32_t c0 = tw_2level(a.tl, a.th, 0, m);  // M^-1 (Montgomery form)
+    // window in t (t = r*Q + j < P <= 2^26 and |value| < 2^29: 32-bit scan)
+    const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(a.am.t_hi, P - 1);
+    int bv = INT_MIN + 1, bt = INT_MAX, bc = 0;
+    // column tiles strided over the (<= kMaxPartialsLarge) CTAs of this pair
 #pragma unroll 1
-    for (int tile = blockIdx.x; tile < (Q >> 5); tile += gridDim.x) {
-    const int j = tile * 32 + lane;
-    __syncthreads();
-    // first DIT group from the inner residues, with the inverse twiddle
-#pragma unroll 1
-    for (int g = warp; g < NG0; g += kWarps) {
-        uint32_t x[RAD0];
+    for (int tile = blockIdx.x; tile < Q / kOuterThreads; tile += gridDim.x) {
+        const int j = tile * kOuterThreads + threadIdx.x;
+        uint32_t x[M];
+        const uint32_t* rin = a.rin + ((int64_t)pl * M * a.np + a.pi) * Q + j;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) {
-            const int pos = g * RAD0 + kk;
-            const uint32_t k1 = __brev((uint32_t)pos) >> (32 - LOGM);
-            const uint32_t r = __ldg(&a.rin[(((int64_t)pl * M + pos) * a.np + a.pi) * Q + j]);
-            x[kk] = montmul(r, tw_2level(a.tl, a.th, ((uint32_t)j * k1) & pmask, m), m.p, m.pinv);
-        }
-        dit_regs<LOGM, 0>(x, 0, sti, m);
-        uint32_t* p = smem + g * RAD0 * kPad + lane;
+        for (int r = 0; r < M; ++r) x[r] = __ldg(&rin[(int64_t)r * a.np * Q]);
+        // inner results of sub-transform r are frequency k1 = bitrev(r):
+        // x M^-1 omega_P^(-j k1)
+        apply_column_twiddles<LOGM>(x, c0, tw_2level(a.tlf, a.thf, ((uint32_t)P - (uint32_t)j) & pmask, m), m);
+        dit_full<LOGM>(x, stw, m);
+        if (!final_out) {
+            uint32_t* ro = a.rout + (pl * a.np + a.pi) * P + j;
 #pragma unroll
-        for (int kk = 0; kk < RAD0; ++kk) p[kk * kPad] = x[kk];
-    }
-    __syncthreads();
-    dit_middle<LOGM, 1>(smem, sti, m);
-#pragma unroll 1
-    for (int g = warp; g < (1 << S0L); g += kWarps) {
-        uint32_t x[RADL];
-        const uint32_t* p = smem + g * kPad + lane;
+            for (int r = 0; r < M; ++r) ro[(int64_t)r * Q] = redp(red2p(x[r], m.p2), m.p);
+        } else if constexpr (OUT == OUT_VALUES) {
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
-        dit_regs<LOGM, SC::NG - 1>(x, g, sti, m);
-#pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) {
-            const int64_t t = (int64_t)(g + (kk << S0L)) * Q + j;
-            const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
-            if (!final_out) {
-                a.rout[(pl * a.np + a.pi) * P + t] = r;
-                continue;
+            for (int r = 0; r < M; ++r) {
+                const int64_t t = (int64_t)r * Q + j;
+                const uint32_t v = redp(red2p(x[r], m.p2), m.p);
+                if (t < a.nout) a.values[pair * a.vld + t] = (long long)v - (v > half ? (long long)m.p : 0);
             }
-            const long long v = (long long)r - (r > half ? (long long)m.p : 0);
-            if constexpr (OUT == OUT_VALUES) {
-                if (t < a.nout) a.values[pair * a.vld + t] = v;
-            } else {
-                if (t >= a.am.t_lo && t <= a.am.t_hi) best_add(b, v, t);
+        } else {
+            // t increases with r: the first maximum is the smallest index
+#pragma unroll
+            for (int r = 0; r < M; ++r) {
+                const int t = r * Q + j;
+                const uint32_t v = redp(red2p(x[r], m.p2), m.p);
+                const int cv = (int)v - (v > half ? (int)m.p : 0);
+                const int val = (t >= tlo && t <= thi) ? cv : INT_MIN;
+                const bool gt = val > bv;
+                bt = gt ? t : bt;
+                bc = gt ? 1 : bc + (int)(val == bv);
+                bv = gt ? val : bv;
             }
         }
     }
-    }  // tiles
     if constexpr (OUT == OUT_ARGMAX) {
-        if (final_out) argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+        if (final_out) {
+            const Best b = bc ? Best{bv, bt, bc} : best_init();
+            argmax_finish(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+        }
     }
 }
 
@@ -1138,7 +1238,8 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
     const size_t nl = 8192, nh = (size_t)(P / 8192 > 0 ? P / 8192 : 1);
     auto al = [](size_t n) { return (n + 3) & ~(size_t)3; };
     const size_t ng = al(gf.size()) + al(gi.size());  // in uint2 units
-    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh);
+    const size_t nr = al(M / 2);                      // uint2 units, each of rf / ri
+    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh) + 4 * nr;
     std::vector<uint32_t> h(words, 0);
     memcpy(h.data(), gf.data(), gf.size() * 8);
     memcpy(h.data() + 2 * al(gf.size()), gi.data(), gi.size() * 8);
@@ -1155,12 +1256,24 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
         th[b] = (uint32_t)f;
         thi[b] = (uint32_t)iv;
     }
+    // omega_M^t and omega_M^-t, t < M/2, as Shoup pairs (w, floor(w 2^32 / p))
+    uint32_t* rf = thi + al(nh);
+    uint32_t* ri = rf + 2 * nr;
+    const uint64_t wm = powmod(w, Q, p), wmi = powmod(wm, p - 2, p);
+    for (uint64_t t = 0, f = 1, iv = 1; t < M / 2; ++t, f = mulmod(f, wm, p), iv = mulmod(iv, wmi, p)) {
+        rf[2 * t] = (uint32_t)f;
+        rf[2 * t + 1] = (uint32_t)((f << 32) / p);
+        ri[2 * t] = (uint32_t)iv;
+        ri[2 * t + 1] = (uint32_t)((iv << 32) / p);
+    }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, words * 4);
     if (e != cudaSuccess) return e;
     e = cudaMemcpy(d, h.data(), words * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(d); return e; }
     const uint32_t* dw = reinterpret_cast<const uint32_t*>(d);
+    out->rf = reinterpret_cast<const uint2*>(dw + (rf - h.data()));
+    out->ri = reinterpret_cast<const uint2*>(dw + (ri - h.data()));
     out->gf = reinterpret_cast<const uint2*>(dw);
     out->gi = reinterpret_cast<const uint2*>(dw + 2 * al(gf.size()));
     out->tl = dw + 2 * ng;
@@ -1315,15 +1428,7 @@ void Profiler::post(int kind, cudaStream_t s)
 template <int LOGM, typename T, int QM>
 static cudaError_t launch_ofwd(const OuterArgs& a, dim3 grid, cudaStream_t s)
 {
-    static bool attr = false;
-    const size_t smem = outer_smem<LOGM>(sizeof(T));
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_outer_fwd<LOGM, T, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    k_outer_fwd<LOGM, T, QM><<<grid, kThreads, smem, s>>>(a);
+    k_outer_fwd<LOGM, T, QM><<<grid, kOuterThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1356,15 +1461,7 @@ static cudaError_t dispatch_ofwd(int logm, const OuterArgs& a, int dtype, int qm
 template <int LOGM, int OUT>
 static cudaError_t launch_oinv(const OuterArgs& a, dim3 grid, cudaStream_t s)
 {
-    static bool attr = false;
-    const size_t smem = outer_smem<LOGM>(0);
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_outer_inv<LOGM, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    k_outer_inv<LOGM, OUT><<<grid, kThreads, smem, s>>>(a);
+    k_outer_inv<LOGM, OUT><<<grid, kOuterThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1404,7 +1501,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             oa.op[0] = c.op[0];
             oa.op[1] = c.op[1];
             oa.out = c.OUT;
-            oa.gtw = O.gf;
+            oa.rtw = O.rf;
             oa.tl = O.tl;
             oa.th = O.th;
             oa.stats = c.stats;
@@ -1419,7 +1516,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             oa.pair0 = p0;
             if (c.op[0].dtype != c.op[1].dtype || c.op[0].q.mode != c.op[1].q.mode) return cudaErrorInvalidValue;
             if (c.prof) c.prof->pre(KK_OTHER, s);
-            e = dispatch_ofwd(logm, oa, c.op[0].dtype, c.op[0].q.mode, dim3(Q / 32, 2, (unsigned)nb), s);
+            e = dispatch_ofwd(logm, oa, c.op[0].dtype, c.op[0].q.mode, dim3(Q / kOuterThreads, 2, (unsigned)nb), s);
             if (c.prof) c.prof->post(KK_OTHER, s);
             if (e != cudaSuccess) return e;
             // inner forward (residues in), product, inverse -> residues
@@ -1489,14 +1586,16 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             OuterArgs ob = oa;
             ob.rin = c.RI;
             ob.rout = c.R;
-            ob.gtw = O.gi;
+            ob.rtw = O.ri;
+            ob.tlf = O.tl;
+            ob.thf = O.th;
             ob.tl = O.tli;
             ob.th = O.thi;
             ob.am = c.am;
             ob.values = c.values;
             ob.nout = c.nout;
             ob.vld = c.nout;
-            const int nblk = (Q / 32) < kMaxPartials ? (Q / 32) : kMaxPartials;
+            const int nblk = (Q / kOuterThreads) < kMaxPartialsLarge ? (Q / kOuterThreads) : kMaxPartialsLarge;
             if (c.prof) c.prof->pre(KK_OTHER, s);
             e = argmax ? dispatch_oinv<OUT_ARGMAX>(logm, ob, dim3(nblk, (unsigned)nb), s)
                        : dispatch_oinv<OUT_VALUES>(logm, ob, dim3(nblk, (unsigned)nb), s);

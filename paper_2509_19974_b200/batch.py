@@ -147,6 +147,8 @@ def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None
 
 
 MAX_P = 1 << 19  # largest single-launch transform of the NTT path
+TC_BLOCK = 2048  # template-search lags per block on the tensor-core path (one M=128 tile)
+TC_MAX_K = 4608  # qx_tc.cu kTcMaxK: template length + 15 must fit
 
 
 def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
@@ -171,7 +173,12 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
     if nvalid < 1:
         raise ValueError("template longer than the stream")
     if block is None:
-        block = MAX_P - 2 * nt + 2  # nout = block + 2*nt - 2 fits one transform
+        # tensor-core window path (qx_tc.cu, shared-template mode): 2048-lag
+        # blocks = one M=128 tile per block, the template built once per SM;
+        # otherwise the largest block whose full correlogram fits one NTT
+        tc = (path in ("auto", "direct", "tc") and nt + 15 <= TC_MAX_K and nt % 4 == 0
+              and x.dtype == t.float32 and y.dtype == t.float32)
+        block = TC_BLOCK if tc else MAX_P - 2 * nt + 2  # NTT: nout = block + 2*nt - 2 fits one transform
     if block < 1:
         raise ValueError("template too long for the block transform")
     nfull, rem = divmod(nvalid, block)

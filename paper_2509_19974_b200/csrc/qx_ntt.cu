@@ -342,6 +342,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
             },
             [&](const Buf& b, int g) {
                 uint32_t x[RAD0];
+                if constexpr (QM == QM_UNIFORM && std::is_same<T, float>::value) {
+                    // branch-free levels of the whole group; a rare exact redo
+                    // (near a rounding half-point, NaN, inf) for the group
+                    int c[NLD];
+                    bool bad = false;
+#pragma unroll
+                    for (int kk = 0; kk < NLD; ++kk) c[kk] = level_uniform_nb(b.v[kk], k, inv_step, bad);
+                    if (__builtin_expect(bad, 0)) {
+#pragma unroll
+                        for (int kk = 0; kk < NLD; ++kk) {
+                            if (b.v[kk] != b.v[kk]) flags |= SF_NONFINITE;
+                            c[kk] = quant_level<T, QM>(b.v[kk], sthr, k, tbits, inv_step, t0, t1);
+                        }
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < RAD0; ++kk) x[kk] = kk < NLD ? to_res(c[kk]) : 0u;
+                } else {
 #pragma unroll
                 for (int kk = 0; kk < RAD0; ++kk) {
                     if (kk >= NLD) { x[kk] = 0; continue; }
@@ -357,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
                         c = level_of<T, QM>(b.v[kk], sthr, k, tbits, inv_step, t0, t1);
                     }
                     x[kk] = to_res(c);
+                }
                 }
                 dif_regs<LOG1, 0>(x, g, stw, m);
                 uint32_t* p = smem + g * kPad + lane;

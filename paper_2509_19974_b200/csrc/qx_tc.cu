@@ -157,6 +157,7 @@ struct TcArgs {
     uint32_t idesc;
     int K;                   // padded K (multiple of 32)
     int fast;                // float32, n <= 4096, aligned rows, L0 % 4 == 0
+    int shared_x;            // fast path with x row stride 0 (template search): x built once per CTA
     int debug;               // QX_TC_TIMING builds only: 1 = skip MMAs, 2 = skip builds
     int64_t batch;
 };
@@ -173,6 +174,7 @@ struct TcSmem {
     // per-builder-warp partials (no atomics): ssx, nzx, ssy, nzy, flags
     unsigned long long wst[kTcAux][kTcThreads / 32][5];
     int wxs[kTcAux][kTcThreads / 32][kTcMaxExtra];  // extra-lag sums
+    unsigned xst[3];      // shared-x mode: template ssx, nzx, flags (built once)
     uint32_t tmem_base;
     int best[4][3];
 #ifdef QX_TC_TIMING
@@ -195,14 +197,14 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
 // slot u: warp-reduced, one record per builder warp (summed by the epilogue)
-template <bool Y32>  // Y32: y statistics fit 32 bits per warp (fast path, ny <= 4096)
+template <bool Y32>  // Y32: y statistics fit 32 bits per warp (fast paths, ny <= 6144)
 __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
-                              unsigned long long ssy, unsigned long long nzy, unsigned fl)
+                              unsigned long long ssy, unsigned long long nzy, unsigned fl, int xs)
 {
     const int lane = threadIdx.x & 31;
     if (a.extra) {
         // extra lag j = ntiles*16M + e: sum_m x[m] * ycode[L0 + j + m]
-        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[s]) + 4;  // x codes from m = 0
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[xs]) + 4;  // x codes from m = 0
         const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[s]);
         const int nw = (int)((a.op[0].n + 3) >> 2);
         const int j0 = a.ntiles * 16 * a.M;
@@ -318,29 +320,61 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
         v.w = __funnelshift_r(a3, a4, sh);
         b4[kc * (kTcBLbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
     }
-    tc_aux_finish<false>(a, S, s, u, ssx, nzx, ssy, nzy, fl);
+    tc_aux_finish<false>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
 }
 
 // ---- fast build: float32 rows, nx, ny <= kTcFastN, 16-B aligned rows,
 // L0 % 4 == 0.  Each thread owns float4 #t and #t + kTcThreads of x and y;
 // the next pair's float4s are loaded into registers before the current pair
 // is built (one pair of loads always in flight).
-constexpr int kTcFastN = 4 * 2 * kTcThreads;  // 4096 with 512 threads
+constexpr int kTcFastN = 4 * 2 * kTcThreads;   // 4096 with 512 threads
+constexpr int kTcFastNY = 4 * 3 * kTcThreads;  // shared-x mode: y rows up to 6144
 
+// per-thread float4s of one pair (loaded one pair ahead): both rows, or in
+// shared-x mode only the y row (the template is built once per CTA)
+template <bool SX>
 struct TcRegs {
     float4 x[2], y[2];
 };
+template <>
+struct TcRegs<true> {
+    float4 y[3];
+};
 
-__device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs& r)
+// float4 #i of a row of n floats (the tail float4 of an n % 4 != 0 row by
+// scalar loads, zero-padded: a zero sample quantises to code 0)
+__device__ __forceinline__ float4 tc_ld4(const float* row, int i, int n)
 {
-    const float4* xs = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.op[0].data) + pair * a.op[0].ld);
-    const float4* ys = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld);
-    const int nx4 = (int)(a.op[0].n >> 2), ny4 = (int)(a.op[1].n >> 2);
+    if (4 * i + 4 <= n) return __ldg(reinterpret_cast<const float4*>(row) + i);
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * i < n) {
+        v.x = __ldg(row + 4 * i);
+        if (4 * i + 1 < n) v.y = __ldg(row + 4 * i + 1);
+        if (4 * i + 2 < n) v.z = __ldg(row + 4 * i + 2);
+    }
+    return v;
+}
+
+template <bool SX>
+__device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<SX>& r)
+{
+    const float* ys = reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld;
+    const int ny = (int)a.op[1].n;
+    if constexpr (SX) {
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int i = threadIdx.x + h * kTcThreads;
-        r.x[h] = i < nx4 ? __ldg(&xs[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
-        r.y[h] = i < ny4 ? __ldg(&ys[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int h = 0; h < 3; ++h) r.y[h] = tc_ld4(ys, threadIdx.x + h * kTcThreads, ny);
+    } else {
+        // n % 4 == 0 here: whole float4s only
+        const float4* xs4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.op[0].data) +
+                                                            pair * a.op[0].ld);
+        const float4* ys4 = reinterpret_cast<const float4*>(ys);
+        const int nx4 = (int)(a.op[0].n >> 2), ny4 = ny >> 2;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = threadIdx.x + h * kTcThreads;
+            r.x[h] = i < nx4 ? __ldg(&xs4[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+            r.y[h] = i < ny4 ? __ldg(&ys4[i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
 }
 
@@ -416,80 +450,35 @@ __device__ __forceinline__ void tc_word_stats(uint32_t w, unsigned& ss, unsigned
     nz += (unsigned)__popc(__vcmpne4(w, 0u)) >> 3;
 }
 
-template <int QM>
-__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs& r)
+// NV float4s -> NV packed code words: branch-free for uniform quantisers
+// (one rare exact redo of all NV words), exact compares otherwise
+template <int QM, int NV>
+__device__ __forceinline__ void tc_quant_words(const float4 (&v)[NV], const float* thr, int k, float inv_step,
+                                               int tbits, uint32_t (&w)[NV], unsigned& fl)
 {
-    const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
-    const float* thry = reinterpret_cast<const float*>(S.thr[1]);
-    const int kx = a.op[0].q.k, ky = a.op[1].q.k;
-    const float ix = (float)a.op[0].q.inv_step, iy = (float)a.op[1].q.inv_step;
-    const int nx4 = (int)(a.op[0].n >> 2), ny4 = (int)(a.op[1].n >> 2), K = a.K;
-    const int ylen = a.ylen;
-#ifdef QX_TC_TIMING
-    long long _m = clock64();
-#define TC_MARK(i) if (threadIdx.x == 0) { const long long _n = clock64(); atomicAdd(&S.tm[i], (unsigned long long)(_n - _m)); _m = _n; }
-#else
-#define TC_MARK(i)
-#endif
-    uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[s]);
-    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
-    // zero the margins only: x words outside [4, 4 + nx4), y words outside
-    // the signal (front [0, yf), back [yb, Y))
-    const int yoff = (int)(-a.L0) >> 2;  // word index of y[0] in the window (may be < 0)
-    const int X = (K + 64) / 4, Y = (ylen + 3) / 4;
-    const int yf = min(max(yoff, 0), Y), yb = min(max(yoff + ny4, yf), Y);
-    const int nxz = X - nx4, nyz = yf + (Y - yb);
-    for (int i = threadIdx.x; i < nxz + nyz; i += kTcThreads) {
-        if (i < nxz) xw[i < 4 ? i : nx4 + i] = 0;
-        else {
-            const int j = i - nxz;
-            yw[j < yf ? j : yb + (j - yf)] = 0;
-        }
-    }
-    TC_MARK(8);
-    unsigned ssx = 0, nzx = 0, ssy = 0, nzy = 0, fl = 0;
-    // samples past n were fetched as zeros: code 0, no statistics
-    uint32_t wx[2], wy[2];
+    unsigned d0 = 0, d1 = 0;
     if constexpr (QM == QM_UNIFORM) {
         bool bad = false;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            wx[h] = tc_q4_uniform_fast(r.x[h], kx, ix, bad);
-            wy[h] = tc_q4_uniform_fast(r.y[h], ky, iy, bad);
-        }
+        for (int h = 0; h < NV; ++h) w[h] = tc_q4_uniform_fast(v[h], k, inv_step, bad);
         if (__builtin_expect(bad, 0)) {
-            unsigned d0 = 0, d1 = 0;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                wx[h] = tc_q4<QM>(r.x[h], thrx, kx, ix, 8, d0, d1, fl);
-                wy[h] = tc_q4<QM>(r.y[h], thry, ky, iy, 8, d0, d1, fl);
-            }
+            for (int h = 0; h < NV; ++h) w[h] = tc_q4<QM>(v[h], thr, k, inv_step, 8, d0, d1, fl);
         }
     } else {
-        unsigned d0 = 0, d1 = 0;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            wx[h] = tc_q4<QM>(r.x[h], thrx, kx, ix, a.op[0].q.tbits, d0, d1, fl);
-            wy[h] = tc_q4<QM>(r.y[h], thry, ky, iy, a.op[1].q.tbits, d0, d1, fl);
-        }
+        for (int h = 0; h < NV; ++h) w[h] = tc_q4<QM>(v[h], thr, k, inv_step, tbits, d0, d1, fl);
     }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int i = threadIdx.x + h * kTcThreads;
-        tc_word_stats(wx[h], ssx, nzx);
-        tc_word_stats(wy[h], ssy, nzy);
-        if (i < nx4) xw[4 + i] = wx[h];
-        const int wi = yoff + i;
-        if (i < ny4 && wi >= 0 && wi < (ylen + 3) / 4) yw[wi] = wy[h];
-    }
-    TC_MARK(9);
-    asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // builders only
-    TC_MARK(10);
-    // shifted copies: item -> (chunk position kc, half h) with h uniform per
-    // warp; the thread emits shifts r = 8h .. 8h+7 of chunk kc
-    const uint4* xq = reinterpret_cast<const uint4*>(S.xl[s]);
-    uint4* b4 = reinterpret_cast<uint4*>(S.b[s]);
-    const int nchunk = K / 16;
+}
+
+// the 16 byte-shifted copies of slot xs's x codes into B buffer bs:
+// item -> (chunk position kc, half h) with h uniform per warp; the thread
+// emits shifts r = 8h .. 8h+7 of chunk kc
+__device__ __forceinline__ void tc_build_copies(const TcArgs& a, TcSmem& S, int xs, int bs)
+{
+    const uint4* xq = reinterpret_cast<const uint4*>(S.xl[xs]);
+    uint4* b4 = reinterpret_cast<uint4*>(S.b[bs]);
+    const int nchunk = a.K / 16;
     const int nitems = 64 * ((nchunk + 31) / 32);
     for (int i = threadIdx.x; i < nitems; i += kTcThreads) {
         const int kc = (i & 31) + 32 * (i >> 6), h = (i >> 5) & 1;
@@ -522,8 +511,129 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
             }
         }
     }
+}
+
+// zero the margins of the code buffers: x words outside [4, 4 + nx4) of
+// slot xs (nx4 < 0: leave x alone), y words of slot s outside the signal
+// (front [0, yf), back [yb, Y))
+__device__ __forceinline__ void tc_zero_margins(const TcArgs& a, TcSmem& S, int xs, int nx4, int s, int ny4)
+{
+    uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[xs]);
+    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
+    const int yoff = (int)(-a.L0) >> 2;  // word index of y[0] in the window (may be < 0)
+    const int X = (a.K + 64) / 4, Y = (a.ylen + 3) / 4;
+    const int yf = min(max(yoff, 0), Y), yb = min(max(yoff + ny4, yf), Y);
+    const int nxz = nx4 < 0 ? 0 : X - nx4, nyz = yf + (Y - yb);
+    for (int i = threadIdx.x; i < nxz + nyz; i += kTcThreads) {
+        if (i < nxz) xw[i < 4 ? i : nx4 + i] = 0;
+        else {
+            const int j = i - nxz;
+            yw[j < yf ? j : yb + (j - yf)] = 0;
+        }
+    }
+}
+
+// shared-x mode prologue: the template's codes (slot 0), its 16 shifted
+// copies (B slot 0) and statistics (S.xst), once per CTA
+template <int QM>
+__device__ void tc_build_template(const TcArgs& a, TcSmem& S)
+{
+    const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
+    const float* xs = reinterpret_cast<const float*>(a.op[0].data);
+    const int nx = (int)a.op[0].n, nx4 = (nx + 3) >> 2;
+    if (threadIdx.x < 3) S.xst[threadIdx.x] = 0;
+    float4 v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) v[h] = tc_ld4(xs, threadIdx.x + h * kTcThreads, nx);
+    uint32_t w[2];
+    unsigned fl = 0, ss = 0, nz = 0;
+    tc_quant_words<QM, 2>(v, thrx, a.op[0].q.k, (float)a.op[0].q.inv_step, a.op[0].q.tbits, w, fl);
+    uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[0]);
+    const int X = (a.K + 64) / 4;
+    for (int i = threadIdx.x; i < X; i += kTcThreads)
+        if (i < 4 || i >= 4 + nx4) xw[i] = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = threadIdx.x + h * kTcThreads;
+        tc_word_stats(w[h], ss, nz);
+        if (i < nx4) xw[4 + i] = w[h];
+    }
+    ss = __reduce_add_sync(0xffffffffu, ss);
+    nz = __reduce_add_sync(0xffffffffu, nz);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // codes + zeroed xst visible
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&S.xst[0], ss);
+        atomicAdd(&S.xst[1], nz);
+        atomicOr(&S.xst[2], fl);
+    }
+    tc_build_copies(a, S, 0, 0);
+    asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // xst complete
+}
+
+// shared-x mode, one pair: only the y row (<= 6144 samples, 3 float4 per
+// thread); the template statistics ride in builder warp 0's record
+template <int QM>
+__device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<true>& r)
+{
+    const float* thry = reinterpret_cast<const float*>(S.thr[1]);
+    const int ny = (int)a.op[1].n, ny4 = (ny + 3) >> 2;
+    tc_zero_margins(a, S, 0, -1, s, ny4);
+    uint32_t w[3];
+    unsigned fl = 0, ssy = 0, nzy = 0;
+    tc_quant_words<QM, 3>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
+    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
+    const int yoff = (int)(-a.L0) >> 2, Y = (a.ylen + 3) / 4;
+#pragma unroll
+    for (int h = 0; h < 3; ++h) {
+        const int i = threadIdx.x + h * kTcThreads;
+        tc_word_stats(w[h], ssy, nzy);
+        const int wi = yoff + i;
+        if (i < ny4 && wi >= 0 && wi < Y) yw[wi] = w[h];
+    }
+    if (a.extra) asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // y codes for the dp4a lags
+    const bool w0 = threadIdx.x == 0;
+    tc_aux_finish<true>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
+                        fl | (w0 ? S.xst[2] : 0u), 0);
+}
+
+template <int QM>
+__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<false>& r)
+{
+    const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
+    const float* thry = reinterpret_cast<const float*>(S.thr[1]);
+    const int nx4 = (int)(a.op[0].n >> 2), ny4 = (int)(a.op[1].n >> 2);
+#ifdef QX_TC_TIMING
+    long long _m = clock64();
+#define TC_MARK(i) if (threadIdx.x == 0) { const long long _n = clock64(); atomicAdd(&S.tm[i], (unsigned long long)(_n - _m)); _m = _n; }
+#else
+#define TC_MARK(i)
+#endif
+    tc_zero_margins(a, S, s, nx4, s, ny4);
+    TC_MARK(8);
+    // samples past n were fetched as zeros: code 0, no statistics
+    unsigned ssx = 0, nzx = 0, ssy = 0, nzy = 0, fl = 0;
+    uint32_t wx[2], wy[2];
+    tc_quant_words<QM, 2>(r.x, thrx, a.op[0].q.k, (float)a.op[0].q.inv_step, a.op[0].q.tbits, wx, fl);
+    tc_quant_words<QM, 2>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, wy, fl);
+    uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[s]);
+    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
+    const int yoff = (int)(-a.L0) >> 2, Y = (a.ylen + 3) / 4;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int i = threadIdx.x + h * kTcThreads;
+        tc_word_stats(wx[h], ssx, nzx);
+        tc_word_stats(wy[h], ssy, nzy);
+        if (i < nx4) xw[4 + i] = wx[h];
+        const int wi = yoff + i;
+        if (i < ny4 && wi >= 0 && wi < Y) yw[wi] = wy[h];
+    }
+    TC_MARK(9);
+    asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // builders only
+    TC_MARK(10);
+    tc_build_copies(a, S, s, s);
     TC_MARK(11);
-    tc_aux_finish<true>(a, S, s, u, ssx, nzx, ssy, nzy, fl);
+    tc_aux_finish<true>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
     TC_MARK(12);
 }
 
@@ -629,7 +739,7 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
 #define TC_ACC(i) ((void)0)
 #endif
 
-template <typename T, int QM>
+template <typename T, int QM, bool SX>
 __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
@@ -680,17 +790,23 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         if constexpr (std::is_same<T, float>::value) fast = a.fast;
         if (fast) {
             if constexpr (std::is_same<T, float>::value) {
-                TcRegs cur, nxt;
-                if (npairs) tc_fetch(a, blockIdx.x, cur);
+                TcRegs<SX> cur, nxt;
+                if (npairs) tc_fetch<SX>(a, blockIdx.x, cur);
+                if constexpr (SX) {
+                    if (npairs) tc_build_template<QM>(a, S);
+                }
                 for (int it = 0; it < npairs; ++it) {
                     const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-                    if (it + 1 < npairs) tc_fetch(a, pair + gridDim.x, nxt);
+                    if (it + 1 < npairs) tc_fetch<SX>(a, pair + gridDim.x, nxt);
                     acquire(it);
                     TC_T0();
 #ifdef QX_TC_TIMING
                     if (!(a.debug & 2))
 #endif
-                    tc_build_fast<QM>(a, S, it & 1, it & 3, cur);
+                    {
+                        if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur);
+                        else tc_build_fast<QM>(a, S, it & 1, it & 3, cur);
+                    }
                     if (threadIdx.x == 0) TC_ACC(1);
                     handoff(it);
                     cur = nxt;
@@ -722,7 +838,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             TC_T0();
-            const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b[s]);
+            const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b[SX ? 0 : s]);  // shared x: B built once
             const uint64_t bd0 = smem_desc(ba, kTcBLbo, 128);
             const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
             for (int tile = 0; tile < a.ntiles; ++tile) {
@@ -798,18 +914,19 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
     return true;
 }
 
-template <typename T, int QM>
+template <typename T, int QM, bool SX = false>
 static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
 {
     static bool attr = false;
     const size_t smem = sizeof(TcSmem);
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_tc_window<T, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e =
+            cudaFuncSetAttribute(k_tc_window<T, QM, SX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int grid = (int)(a.batch < sms ? a.batch : sms);
-    k_tc_window<T, QM><<<grid, kTcTotalThreads, smem, s>>>(a);
+    k_tc_window<T, QM, SX><<<grid, kTcTotalThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -839,16 +956,25 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
 #endif
     const int64_t ny = c.op[1].n;
-    a.fast = c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 && ny % 4 == 0 &&
-             (c.batch == 1 || (c.op[0].ld % 4 == 0 && c.op[1].ld % 4 == 0)) &&
-             ((uintptr_t)c.op[0].data % 16 == 0) && ((uintptr_t)c.op[1].data % 16 == 0) && (a.L0 % 4 == 0);
+    const bool aligned = ((uintptr_t)c.op[0].data % 16 == 0) && ((uintptr_t)c.op[1].data % 16 == 0) &&
+                         (a.L0 % 4 == 0) && (c.batch == 1 || c.op[1].ld % 4 == 0);
+    // shared x (template search: every pair's x is the same row): the
+    // template is built once per CTA and y rows may be up to 6144 samples
+    a.shared_x = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
+                 ny <= kTcFastNY && aligned;
+    a.fast = a.shared_x || (c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 &&
+                            ny % 4 == 0 && aligned && (c.batch == 1 || c.op[0].ld % 4 == 0));
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (c.prof) c.prof->pre(KK_DIRECT, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;
-    if (c.op[0].dtype == DT_F32) {
+    if (c.op[0].dtype == DT_F32 && a.shared_x) {
+        if (qm == QM_K1) e = launch_tc<float, QM_K1, true>(a, s, sms);
+        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, true>(a, s, sms);
+        else e = launch_tc<float, QM_BSEARCH, true>(a, s, sms);
+    } else if (c.op[0].dtype == DT_F32) {
         if (qm == QM_K1) e = launch_tc<float, QM_K1>(a, s, sms);
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM>(a, s, sms);
         else e = launch_tc<float, QM_BSEARCH>(a, s, sms);

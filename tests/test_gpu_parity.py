@@ -381,6 +381,36 @@ def test_template_search_matches_oracle(qx, oracle, golden):
         assert qx.template_search(t5, s5, qa, qb, block=8191) == (case["peak"], case["lags"][0], len(case["lags"]))
 
 
+def test_template_search_tensor_core_blocks(qx, oracle, golden):
+    """Default blocks: 2048-lag tiles on the tcgen05 window path in
+    shared-template mode (template built once per SM; stream rows of
+    block + nt - 1 samples, including rows whose length is not a multiple of
+    4), equal to the oracle and to the NTT path."""
+    from paper_2509_19974_b200 import workloads as W
+
+    rng = np.random.default_rng(22)
+    for trial, nt in enumerate((4096, 64, 2052, 1000, 4)):
+        ns = int(rng.integers(nt + 3 * 2048, nt + 9 * 2048))
+        st = rng.laplace(size=ns).astype(np.float32)
+        off = int(rng.integers(0, ns - nt + 1))
+        tpl = st[off:off + nt].copy()
+        st = st + rng.normal(0, 0.7, ns).astype(np.float32)
+        q = [qx.sign(), qx.uniform(1, 0.8), qx.uniform(7, 0.3)][trial % 3]
+        got = qx.template_search(tpl, st, q, q, stream_start=11)
+        assert got == qx.template_search(tpl, st, q, q, stream_start=11, path="ntt"), trial
+        u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
+        first = -(nt - 1)
+        c = oracle.xcorr_bf(u, v, 0 - first, ns - nt - first)
+        m, f, n = oracle.argmax(c)
+        assert got == (m, f + 11, n), (trial, got, (m, f, n))
+    meta, _ = golden
+    g5 = meta["configs"]["c5_small"]
+    t5, s5, off, sn2 = W.c5(stream=g5["stream"], template=g5["template"], offset=g5["offset"])
+    for case in g5["cases"]:
+        qa, qb = _q(qx, case["qx"]), _q(qx, case["qy"])
+        assert qx.template_search(t5, s5, qa, qb) == (case["peak"], case["lags"][0], len(case["lags"]))
+
+
 def test_large_transform_path(qx, oracle):
     """P > 2^19 (outer radix-2^m pass around 2^19 sub-transforms, config 4's
     path): full correlograms and windowed peaks equal the oracle's KS."""

@@ -147,7 +147,7 @@ def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None
 
 
 MAX_P = 1 << 19  # largest single-launch transform of the NTT path
-TC_BLOCK = 2048  # template-search lags per block on the tensor-core path (one M=128 tile)
+TC_BLOCK = 4096  # template-search lags per block on the tensor-core path (one M=128, N=32 tile)
 TC_MAX_K = 4608  # qx_tc.cu kTcMaxK: template length + 15 must fit
 
 
@@ -173,8 +173,8 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
     if nvalid < 1:
         raise ValueError("template longer than the stream")
     if block is None:
-        # tensor-core window path (qx_tc.cu, shared-template mode): 2048-lag
-        # blocks = one M=128 tile per block, the template built once per SM;
+        # tensor-core window path (qx_tc.cu, shared-template mode): 4096-lag
+        # blocks = one M=128 x N=32 tile per block, template built once per SM;
         # otherwise the largest block whose full correlogram fits one NTT
         tc = (path in ("auto", "direct", "tc") and nt + 15 <= TC_MAX_K and nt % 4 == 0
               and x.dtype == t.float32 and y.dtype == t.float32)

@@ -50,10 +50,29 @@ constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
 constexpr int kTcMaxTiles = 2;     // lag tiles per pair
 constexpr int kTcMaxExtra = 16;    // lags past the tiles, summed on CUDA cores
 constexpr int kTcYBytes = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
+constexpr int kTcYStride = (kTcYBytes + 1023) / 1024 * 1024;  // 1024-B aligned slots (SW32 rows)
+constexpr int kTcXPad = 32;  // zero bytes in front of the linear x codes (>= the Hankel pitch)
 // B layout: K-chunk stride 272 B (= 256 + 16): 16-byte stores of 32
 // consecutive chunks then hit 8 distinct bank groups (4 wavefronts, no
 // conflicts); the descriptor's LBO carries the stride
 constexpr int kTcBLbo = 272;
+// shared-template mode (pitch 32): 32 copies, K-chunk stride 528 B = 33
+// 16-B units (odd: conflict-free like 272); one buffer, built once
+constexpr int kTcBLbo32 = 528;
+constexpr int kTcBSlot = kTcBLbo * (kTcMaxK / 16);
+constexpr int kTcBBytes = 2 * kTcBSlot;
+static_assert(kTcBLbo32 * (kTcMaxK / 16) <= kTcBBytes, "pitch-32 B must fit the two pitch-16 slots");
+
+// y code word wi of a slot: pitch 32 stores the buffer through the 32-byte
+// swizzle (byte bit 4 ^= bit 7, i.e. word bit 2 ^= bit 5) so that a SW32
+// K-major descriptor reads it back as a linear buffer: Hankel rows 32 B
+// apart at any 32-B-aligned start (verified by tools/tc_swz.cu)
+template <int PITCH>
+__device__ __forceinline__ int ysw(int wi)
+{
+    if constexpr (PITCH == 32) return wi ^ (((wi >> 5) & 1) << 2);
+    else return wi;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -85,10 +104,10 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
            ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-// instruction descriptor: kind::i8, D = s32, A = B = s8, K-major, N = 16
-constexpr uint32_t tc_idesc(int M)
+// instruction descriptor: kind::i8, D = s32, A = B = s8, K-major
+constexpr uint32_t tc_idesc(int M, int N)
 {
-    return (2u << 4) | (1u << 7) | (1u << 10) | ((16u >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+    return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // Issued by a whole converged warp: elect.sync picks the issuing lane inside
@@ -109,6 +128,7 @@ __device__ __forceinline__ void mma_i8_warp(uint32_t tmem_d, uint64_t a, uint64_
 // passed as 32-bit low words (start address >> 4, which never carries into
 // the LBO field) and a shared high word; A advances 32 B (+2), B two
 // 272-B K-chunks (+34) per step.
+template <int BINC>  // B descriptor step per K step (16-B units)
 __device__ __forceinline__ void mma_i8_warp4(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
                                              uint32_t idesc)
 {
@@ -116,14 +136,14 @@ __device__ __forceinline__ void mma_i8_warp4(uint32_t tmem_d, uint32_t alo, uint
         "{\n\t.reg .pred e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .b32 t;\n\t"
         "mov.b64 a0, {%1, %2};\n\tadd.u32 t, %1, 2;\n\tmov.b64 a1, {t, %2};\n\t"
         "add.u32 t, %1, 4;\n\tmov.b64 a2, {t, %2};\n\tadd.u32 t, %1, 6;\n\tmov.b64 a3, {t, %2};\n\t"
-        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, 34;\n\tmov.b64 b1, {t, %4};\n\t"
-        "add.u32 t, %3, 68;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, 102;\n\tmov.b64 b3, {t, %4};\n\t"
+        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, %6;\n\tmov.b64 b1, {t, %4};\n\t"
+        "add.u32 t, %3, %7;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, %8;\n\tmov.b64 b3, {t, %4};\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a0, b0, %5, 1;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a1, b1, %5, 1;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a2, b2, %5, 1;\n\t"
         "@e tcgen05.mma.cta_group::1.kind::i8 [%0], a3, b3, %5, 1;\n}" ::"r"(tmem_d),
-        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc));
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "n"(BINC), "n"(2 * BINC), "n"(3 * BINC));
 }
 
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar)
@@ -158,6 +178,7 @@ struct TcArgs {
     int K;                   // padded K (multiple of 32)
     int fast;                // float32, n <= 4096, aligned rows, L0 % 4 == 0
     int shared_x;            // fast path with x row stride 0 (template search): x built once per CTA
+    int pitch;               // Hankel row pitch / N: 16 (per-pair B), 32 (shared template, SW32 A)
     int debug;               // QX_TC_TIMING builds only: 1 = skip MMAs, 2 = skip builds
     int64_t batch;
 };
@@ -165,9 +186,9 @@ struct TcArgs {
 constexpr int kTcAux = 4;  // TMEM accumulator / statistics slots
 
 struct TcSmem {
-    alignas(128) int8_t b[2][kTcBLbo * (kTcMaxK / 16)];   // shifted x copies
-    alignas(128) int8_t y[2][kTcYBytes];      // y codes from lag L0 on
-    alignas(16) int8_t xl[2][kTcMaxK + 64];   // linear x codes, 16 zero bytes in front
+    alignas(1024) int8_t b[kTcBBytes];        // shifted x copies: 2 pitch-16 slots or 1 pitch-32 buffer
+    alignas(1024) int8_t y[2][kTcYStride];    // y codes from lag L0 on (pitch 32: swizzled)
+    alignas(16) int8_t xl[2][kTcMaxK + 96];   // linear x codes after kTcXPad zero bytes
     double thr[2][kMaxThr];
     uint64_t mdone[kTcAux];  // MMA chain of aux slot complete (tcgen05.commit)
     uint64_t tfree[kTcAux];  // epilogue finished with aux slot (128 arrivals)
@@ -197,22 +218,23 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
 // slot u: warp-reduced, one record per builder warp (summed by the epilogue)
-template <bool Y32>  // Y32: y statistics fit 32 bits per warp (fast paths, ny <= 6144)
+template <bool Y32, int PITCH = 16>  // Y32: y statistics fit 32 bits per warp (fast paths)
 __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
                               unsigned long long ssy, unsigned long long nzy, unsigned fl, int xs)
 {
     const int lane = threadIdx.x & 31;
     if (a.extra) {
         // extra lag j = ntiles*16M + e: sum_m x[m] * ycode[L0 + j + m]
-        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[xs]) + 4;  // x codes from m = 0
+        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[xs]) + kTcXPad / 4;  // x codes from m = 0
         const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[s]);
         const int nw = (int)((a.op[0].n + 3) >> 2);
-        const int j0 = a.ntiles * 16 * a.M;
+        const int j0 = a.ntiles * a.pitch * a.M;
         for (int e = 0; e < a.extra; ++e) {
             const int j = j0 + e, jw = j >> 2, sh = (j & 3) * 8;
             int acc = 0;
             for (int w = threadIdx.x; w < nw; w += kTcThreads)
-                acc = __dp4a((int)xw[w], (int)__funnelshift_r(yw[w + jw], yw[w + jw + 1], sh), acc);
+                acc = __dp4a((int)xw[w],
+                             (int)__funnelshift_r(yw[ysw<PITCH>(w + jw)], yw[ysw<PITCH>(w + jw + 1)], sh), acc);
             acc = __reduce_add_sync(0xffffffffu, acc);
             if (lane == 0) S.wxs[u][threadIdx.x >> 5][e] = acc;
         }
@@ -268,10 +290,10 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
     const int64_t ny = dy.n;
     unsigned ssx = 0, nzx = 0, fl = 0;
     unsigned long long ssy = 0, nzy = 0;
-    // linear x codes: xl[16 + m] = q(x[m]) (zero padding around)
+    // linear x codes: xl[kTcXPad + m] = q(x[m]) (zero padding around)
     int8_t* xl = S.xl[s];
-    for (int i = threadIdx.x; i < K + 48; i += kTcThreads) {
-        const int m = i - 16;
+    for (int i = threadIdx.x; i < K + 64; i += kTcThreads) {
+        const int m = i - kTcXPad;
         int c = 0;
         if (m >= 0 && m < nx) {
             c = tc_level<T, QM>(__ldg(&xs[m]), thrx, dx.q.k, dx.q.tbits, (T)dx.q.inv_step, fl);
@@ -304,13 +326,13 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
         nzy += c != 0;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // builders only
-    // shifted copies: chunk (kc, r) = xl[16kc + 16 - r, +16)
+    // shifted copies: chunk (kc, r) = xl[16kc + kTcXPad - r, +16)
     const uint32_t* xw = reinterpret_cast<const uint32_t*>(xl);
-    uint4* b4 = reinterpret_cast<uint4*>(S.b[s]);
+    uint4* b4 = reinterpret_cast<uint4*>(S.b + s * kTcBSlot);
     const int nchunk = K / 16;
     for (int i = threadIdx.x; i < nchunk * 16; i += kTcThreads) {
         const int kc = i >> 4, r = i & 15;
-        const int o = 16 * kc + 16 - r;
+        const int o = 16 * kc + kTcXPad - r;
         const int w0 = o >> 2, sh = (o & 3) * 8;
         const uint32_t a0 = xw[w0], a1 = xw[w0 + 1], a2 = xw[w0 + 2], a3 = xw[w0 + 3], a4 = xw[w0 + 4];
         uint4 v;
@@ -328,7 +350,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
 // the next pair's float4s are loaded into registers before the current pair
 // is built (one pair of loads always in flight).
 constexpr int kTcFastN = 4 * 2 * kTcThreads;   // 4096 with 512 threads
-constexpr int kTcFastNY = 4 * 3 * kTcThreads;  // shared-x mode: y rows up to 6144
+constexpr int kTcFastNY = 4 * 4 * kTcThreads;  // shared-x mode: y rows up to 8192
 
 // per-thread float4s of one pair (loaded one pair ahead): both rows, or in
 // shared-x mode only the y row (the template is built once per CTA)
@@ -338,7 +360,7 @@ struct TcRegs {
 };
 template <>
 struct TcRegs<true> {
-    float4 y[3];
+    float4 y[4];
 };
 
 // float4 #i of a row of n floats (the tail float4 of an n % 4 != 0 row by
@@ -362,7 +384,7 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<S
     const int ny = (int)a.op[1].n;
     if constexpr (SX) {
 #pragma unroll
-        for (int h = 0; h < 3; ++h) r.y[h] = tc_ld4(ys, threadIdx.x + h * kTcThreads, ny);
+        for (int h = 0; h < 4; ++h) r.y[h] = tc_ld4(ys, threadIdx.x + h * kTcThreads, ny);
     } else {
         // n % 4 == 0 here: whole float4s only
         const float4* xs4 = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(a.op[0].data) +
@@ -471,64 +493,68 @@ __device__ __forceinline__ void tc_quant_words(const float4 (&v)[NV], const floa
     }
 }
 
-// the 16 byte-shifted copies of slot xs's x codes into B buffer bs:
-// item -> (chunk position kc, half h) with h uniform per warp; the thread
-// emits shifts r = 8h .. 8h+7 of chunk kc
+// the PITCH byte-shifted copies of slot xs's x codes into B buffer bs
+// (chunk (kc, r) = x[16kc - r, +16) at kc*LBO + (r/8)*128 + (r%8)*16):
+// item -> (chunk kc, group h of 8 shifts) with h uniform per warp; the
+// thread loads the 16*(PITCH/16+1) source bytes once and emits 8 shifts
+template <int PITCH>
 __device__ __forceinline__ void tc_build_copies(const TcArgs& a, TcSmem& S, int xs, int bs)
 {
+    constexpr int NH = PITCH / 8, NW = 4 * (PITCH / 16 + 1), LBO = PITCH == 32 ? kTcBLbo32 : kTcBLbo;
     const uint4* xq = reinterpret_cast<const uint4*>(S.xl[xs]);
-    uint4* b4 = reinterpret_cast<uint4*>(S.b[bs]);
+    uint4* b4 = reinterpret_cast<uint4*>(S.b + bs * kTcBSlot);
     const int nchunk = a.K / 16;
-    const int nitems = 64 * ((nchunk + 31) / 32);
+    const int nitems = 32 * NH * ((nchunk + 31) / 32);
     for (int i = threadIdx.x; i < nitems; i += kTcThreads) {
-        const int kc = (i & 31) + 32 * (i >> 6), h = (i >> 5) & 1;
+        const int kc = (i & 31) + 32 * (i / (32 * NH)), h = (i >> 5) % NH;
         if (kc >= nchunk) continue;
-        // bytes [16kc, 16kc + 32) of xl (= x[16kc - 16 .. 16kc + 16))
-        const uint4 lo = xq[kc], hi = xq[kc + 1];
-        const uint32_t w[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-        uint4* dst = b4 + kc * (kTcBLbo / 16) + h * 8;
-        if (h == 0) {
+        // xl bytes [16kc + kTcXPad - PITCH, +NW*4) = x[16kc - PITCH, 16kc + 16)
+        uint32_t w[NW + 1];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {  // r = j: bytes [16 - j, 32 - j)
-                const int o = 16 - j, wq = o >> 2, sh = (o & 3) * 8;
+        for (int q = 0; q < NW / 4; ++q) {
+            const uint4 v = xq[kc + (kTcXPad - PITCH) / 16 + q];
+            w[4 * q] = v.x;
+            w[4 * q + 1] = v.y;
+            w[4 * q + 2] = v.z;
+            w[4 * q + 3] = v.w;
+        }
+        w[NW] = 0u;
+        uint4* dst = b4 + kc * (LBO / 16) + h * 8;
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) {
+            if (hh != h) continue;  // warp-uniform
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // r = 8hh + j: window bytes [PITCH - r, PITCH - r + 16)
+                const int o = PITCH - (8 * hh + j), wq = o >> 2, sh = (o & 3) * 8;
                 uint4 v;
                 v.x = __funnelshift_r(w[wq], w[wq + 1], sh);
                 v.y = __funnelshift_r(w[wq + 1], w[wq + 2], sh);
                 v.z = __funnelshift_r(w[wq + 2], w[wq + 3], sh);
-                v.w = __funnelshift_r(w[wq + 3], (wq + 4 < 8) ? w[wq + 4] : 0u, sh);
-                dst[j] = v;
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {  // r = 8 + j: bytes [8 - j, 24 - j)
-                const int o = 8 - j, wq = o >> 2, sh = (o & 3) * 8;
-                uint4 v;
-                v.x = __funnelshift_r(w[wq], w[wq + 1], sh);
-                v.y = __funnelshift_r(w[wq + 1], w[wq + 2], sh);
-                v.z = __funnelshift_r(w[wq + 2], w[wq + 3], sh);
-                v.w = __funnelshift_r(w[wq + 3], w[wq + 4], sh);
+                v.w = __funnelshift_r(w[wq + 3], w[wq + 4 <= NW ? wq + 4 : NW], sh);
                 dst[j] = v;
             }
         }
     }
 }
 
-// zero the margins of the code buffers: x words outside [4, 4 + nx4) of
+// zero the margins of the code buffers: x words outside [XP, XP + nx4) of
 // slot xs (nx4 < 0: leave x alone), y words of slot s outside the signal
 // (front [0, yf), back [yb, Y))
+template <int PITCH = 16>
 __device__ __forceinline__ void tc_zero_margins(const TcArgs& a, TcSmem& S, int xs, int nx4, int s, int ny4)
 {
+    constexpr int XP = kTcXPad / 4;
     uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[xs]);
     uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
     const int yoff = (int)(-a.L0) >> 2;  // word index of y[0] in the window (may be < 0)
-    const int X = (a.K + 64) / 4, Y = (a.ylen + 3) / 4;
+    const int X = (a.K + 96) / 4, Y = (a.ylen + 3) / 4;
     const int yf = min(max(yoff, 0), Y), yb = min(max(yoff + ny4, yf), Y);
     const int nxz = nx4 < 0 ? 0 : X - nx4, nyz = yf + (Y - yb);
     for (int i = threadIdx.x; i < nxz + nyz; i += kTcThreads) {
-        if (i < nxz) xw[i < 4 ? i : nx4 + i] = 0;
+        if (i < nxz) xw[i < XP ? i : nx4 + i] = 0;
         else {
             const int j = i - nxz;
-            yw[j < yf ? j : yb + (j - yf)] = 0;
+            yw[ysw<PITCH>(j < yf ? j : yb + (j - yf))] = 0;
         }
     }
 }
@@ -549,14 +575,15 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
     unsigned fl = 0, ss = 0, nz = 0;
     tc_quant_words<QM, 2>(v, thrx, a.op[0].q.k, (float)a.op[0].q.inv_step, a.op[0].q.tbits, w, fl);
     uint32_t* xw = reinterpret_cast<uint32_t*>(S.xl[0]);
-    const int X = (a.K + 64) / 4;
+    constexpr int XP = kTcXPad / 4;
+    const int X = (a.K + 96) / 4;
     for (int i = threadIdx.x; i < X; i += kTcThreads)
-        if (i < 4 || i >= 4 + nx4) xw[i] = 0;
+        if (i < XP || i >= XP + nx4) xw[i] = 0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int i = threadIdx.x + h * kTcThreads;
         tc_word_stats(w[h], ss, nz);
-        if (i < nx4) xw[4 + i] = w[h];
+        if (i < nx4) xw[XP + i] = w[h];
     }
     ss = __reduce_add_sync(0xffffffffu, ss);
     nz = __reduce_add_sync(0xffffffffu, nz);
@@ -567,34 +594,35 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
         atomicAdd(&S.xst[1], nz);
         atomicOr(&S.xst[2], fl);
     }
-    tc_build_copies(a, S, 0, 0);
+    tc_build_copies<32>(a, S, 0, 0);
     asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // xst complete
 }
 
-// shared-x mode, one pair: only the y row (<= 6144 samples, 3 float4 per
-// thread); the template statistics ride in builder warp 0's record
+// shared-x mode, one pair: only the y row (<= 8192 samples, 4 float4 per
+// thread) into the swizzled pitch-32 buffer; the template statistics ride in
+// builder warp 0's record
 template <int QM>
 __device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<true>& r)
 {
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
     const int ny = (int)a.op[1].n, ny4 = (ny + 3) >> 2;
-    tc_zero_margins(a, S, 0, -1, s, ny4);
-    uint32_t w[3];
+    tc_zero_margins<32>(a, S, 0, -1, s, ny4);
+    uint32_t w[4];
     unsigned fl = 0, ssy = 0, nzy = 0;
-    tc_quant_words<QM, 3>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
+    tc_quant_words<QM, 4>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
     uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
     const int yoff = (int)(-a.L0) >> 2, Y = (a.ylen + 3) / 4;
 #pragma unroll
-    for (int h = 0; h < 3; ++h) {
+    for (int h = 0; h < 4; ++h) {
         const int i = threadIdx.x + h * kTcThreads;
         tc_word_stats(w[h], ssy, nzy);
         const int wi = yoff + i;
-        if (i < ny4 && wi >= 0 && wi < Y) yw[wi] = w[h];
+        if (i < ny4 && wi >= 0 && wi < Y) yw[ysw<32>(wi)] = w[h];
     }
     if (a.extra) asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // y codes for the dp4a lags
     const bool w0 = threadIdx.x == 0;
-    tc_aux_finish<true>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
-                        fl | (w0 ? S.xst[2] : 0u), 0);
+    tc_aux_finish<true, 32>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
+                            fl | (w0 ? S.xst[2] : 0u), 0);
 }
 
 template <int QM>
@@ -624,14 +652,14 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
         const int i = threadIdx.x + h * kTcThreads;
         tc_word_stats(wx[h], ssx, nzx);
         tc_word_stats(wy[h], ssy, nzy);
-        if (i < nx4) xw[4 + i] = wx[h];
+        if (i < nx4) xw[kTcXPad / 4 + i] = wx[h];
         const int wi = yoff + i;
         if (i < ny4 && wi >= 0 && wi < Y) yw[wi] = wy[h];
     }
     TC_MARK(9);
     asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // builders only
     TC_MARK(10);
-    tc_build_copies(a, S, s, s);
+    tc_build_copies<16>(a, S, s, s);
     TC_MARK(11);
     tc_aux_finish<true>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
     TC_MARK(12);
@@ -651,11 +679,12 @@ __device__ __forceinline__ void best_add(long long& bv, long long& bt, long long
     else if (v == bv) { bt = min(bt, t); bc += c; }
 }
 
+template <int PITCH>
 __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
 {
     const int lane = threadIdx.x & 31;
     const int q = (threadIdx.x >> 5) - kEpiWarp0;  // 0..3 = TMEM lane quarter
-    const int tl = 16 * a.M;
+    const int tl = PITCH * a.M;
     const int row = a.M == 128 ? q * 32 + lane : q * 16 + lane;
     const bool live = a.M == 128 || lane < 16;
     // window in tile-relative lag index j = lag - L0 (t = L0 + j + nx - 1)
@@ -666,18 +695,22 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
     // increases along the scan, so the first maximum is the smallest lag
     int bv = INT_MIN + 1, bj = INT_MAX, bc = 0;
     for (int tile = 0; tile < a.ntiles; ++tile) {
-        int v[16];
-        const uint32_t taddr = S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * 32 + tile * 16);
-        tmem_ld16(taddr, v);
-        const int j0 = tile * tl + 16 * row;
 #pragma unroll
-        for (int r = 0; r < 16; ++r) {
-            const int j = j0 + r;
-            const int val = (live && j >= jlo && j <= jhi) ? v[r] : INT_MIN;
-            const bool gt = val > bv, eq = val == bv;
-            bj = gt ? j : bj;
-            bc = gt ? 1 : bc + (int)eq;
-            bv = gt ? val : bv;
+        for (int c0 = 0; c0 < PITCH; c0 += 16) {
+            int v[16];
+            const uint32_t taddr =
+                S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * 32 + tile * PITCH + c0);
+            tmem_ld16(taddr, v);
+            const int j0 = tile * tl + PITCH * row + c0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int j = j0 + r;
+                const int val = (live && j >= jlo && j <= jhi) ? v[r] : INT_MIN;
+                const bool gt = val > bv, eq = val == bv;
+                bj = gt ? j : bj;
+                bc = gt ? 1 : bc + (int)eq;
+                bv = gt ? val : bv;
+            }
         }
     }
     // TMEM reads are complete (wait::ld) before the slot is released
@@ -838,27 +871,30 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             TC_T0();
-            const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b[SX ? 0 : s]);  // shared x: B built once
-            const uint64_t bd0 = smem_desc(ba, kTcBLbo, 128);
+            // pitch 32 (shared template): one B buffer built once, SW32 A rows
+            constexpr int PITCH = SX ? 32 : 16, LBO = SX ? kTcBLbo32 : kTcBLbo, BINC = 2 * LBO / 16;
+            const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b + (SX ? 0 : s) * kTcBSlot);
+            const uint64_t bd0 = smem_desc(ba, LBO, 128);
             const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
             for (int tile = 0; tile < a.ntiles; ++tile) {
 #ifdef QX_TC_TIMING
                 if (a.debug & 1) break;
 #endif
-                const uint32_t d = tbase + (uint32_t)(u * 32 + tile * 16);
-                const uint64_t ad0 = smem_desc(ya + tile * 16 * a.M, 16, 128);
+                const uint32_t d = tbase + (uint32_t)(u * 32 + tile * PITCH);
+                const uint64_t ad0 = smem_desc(ya + tile * PITCH * a.M, 16, 8 * PITCH) |
+                                     (PITCH == 32 ? (6ull << 61) : 0ull);  // layout SWIZZLE_32B
                 const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
                 uint32_t alo = (uint32_t)ad0, blo = (uint32_t)bd0;
                 mma_i8_warp(d, ad0, bd0, a.idesc, 0);
                 int kk = 1;
                 for (; kk + 4 <= nk; kk += 4) {
-                    mma_i8_warp4(d, alo + 2, ahi, blo + 34, bhi, a.idesc);
+                    mma_i8_warp4<BINC>(d, alo + 2, ahi, blo + BINC, bhi, a.idesc);
                     alo += 8;
-                    blo += 4 * 34;
+                    blo += 4 * BINC;
                 }
                 for (; kk < nk; ++kk) {
-                    alo += 32 >> 4;             // next 32 k-bytes of A
-                    blo += (2 * kTcBLbo) >> 4;  // next two k-chunks of B
+                    alo += 32 >> 4;  // next 32 k-bytes of A
+                    blo += BINC;     // next two k-chunks of B
                     mma_i8_warp(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1);
                 }
             }
@@ -876,7 +912,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             {
                 TC_T0();
-                tc_epilogue(a, S, it & 3, pair);
+                tc_epilogue<SX ? 32 : 16>(a, S, it & 3, pair);
                 if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(6);
             }
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[it & 3])) : "memory");
@@ -942,28 +978,31 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     // tile 0 starts at the window's first lag (relative lag = t - (nx - 1))
     a.L0 = c.am.t_lo - (nx - 1);
     const int64_t W = c.am.t_hi - c.am.t_lo + 1;
-    // shape: one M=64 tile (1024 lags) when it covers the window up to the
-    // extra lags, else M=128 tiles (2048 lags each)
-    a.M = W <= 1024 + kTcMaxExtra ? 64 : 128;
-    const int tl = 16 * a.M;
-    a.ntiles = (int)((W - kTcMaxExtra + tl - 1) / tl);
-    if (a.ntiles < 1) a.ntiles = 1;
-    a.extra = (int)(W > (int64_t)a.ntiles * tl ? W - (int64_t)a.ntiles * tl : 0);
-    a.idesc = tc_idesc(a.M);
     a.K = (int)(((nx + 15) + 31) / 32 * 32);
-    a.ylen = a.ntiles * tl + kTcMaxExtra + a.K;
-#ifdef QX_TC_TIMING
-    if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
-#endif
     const int64_t ny = c.op[1].n;
     const bool aligned = ((uintptr_t)c.op[0].data % 16 == 0) && ((uintptr_t)c.op[1].data % 16 == 0) &&
                          (a.L0 % 4 == 0) && (c.batch == 1 || c.op[1].ld % 4 == 0);
     // shared x (template search: every pair's x is the same row): the
-    // template is built once per CTA and y rows may be up to 6144 samples
+    // template's 32 shifted copies are built once per CTA (pitch 32, one
+    // M=128 tile of 4096 lags, y rows up to 8192 samples); otherwise per-pair
+    // copies with pitch 16
     a.shared_x = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
-                 ny <= kTcFastNY && aligned;
+                 ny <= kTcFastNY && aligned && W <= 4096 + kTcMaxExtra;
     a.fast = a.shared_x || (c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 &&
                             ny % 4 == 0 && aligned && (c.batch == 1 || c.op[0].ld % 4 == 0));
+    a.pitch = a.shared_x ? 32 : 16;
+    // shape: pitch 16: one M=64 tile (1024 lags) when it covers the window up
+    // to the extra lags, else M=128 tiles (2048 lags each); pitch 32: M=128
+    a.M = (a.pitch == 16 && W <= 1024 + kTcMaxExtra) ? 64 : 128;
+    const int tl = a.pitch * a.M;
+    a.ntiles = (int)((W - kTcMaxExtra + tl - 1) / tl);
+    if (a.ntiles < 1) a.ntiles = 1;
+    a.extra = (int)(W > (int64_t)a.ntiles * tl ? W - (int64_t)a.ntiles * tl : 0);
+    a.idesc = tc_idesc(a.M, a.pitch);
+    a.ylen = a.ntiles * tl + kTcMaxExtra + a.K;
+#ifdef QX_TC_TIMING
+    if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
+#endif
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

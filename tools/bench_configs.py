@@ -85,6 +85,6 @@ if "c5" in which:
         ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=2, warm=1)
         assert r[1] == off, r
         res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
-                           "lag": r[1], "path": "tcgen05 window, shared template, 2048-lag blocks"}
+                           "lag": r[1], "path": "tcgen05 window, shared template (N=32, SW32 Hankel), 4096-lag blocks"}
     res["c5_generation_s"] = gen_s
 print(json.dumps(res))

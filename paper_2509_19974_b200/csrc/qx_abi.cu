@@ -607,7 +607,10 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // stream works on the previous chunk; overlapping / repeated rows are
     // staged whole (one chunk)
     const bool disjoint = x->ld >= x->n && y->ld >= y->n;
-    const int64_t nchunk = disjoint ? std::min<int64_t>(batch, 8) : 1;
+    // >= 16 pairs per chunk keeps the transform launches efficient (8-pair
+    // chunks cost more in compute than the extra copy overlap gains)
+    int64_t nchunk = disjoint ? std::max<int64_t>(1, std::min<int64_t>(batch / 16, 4)) : 1;
+    if (const char* ev = getenv("QX_SWEEP_CHUNKS")) nchunk = std::max<int64_t>(1, std::min<int64_t>(batch, atoll(ev)));
     const int64_t per = (batch + nchunk - 1) / nchunk;
     while ((int64_t)ctx->chunk_ev.size() < nchunk) {
         cudaEvent_t ev;

@@ -196,21 +196,28 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
         parts.append((r, t.full((1,), s0, device=r.device, dtype=t.int64)))
     raw = t.cat([p[0] for p in parts])
     offs = t.cat([p[1] for p in parts])
+    # merge on the device; one host transfer of an 8-word summary
     status = raw[:, 7] >> 32
     flags = raw[:, 7] & 0xFFFFFFFF
-    if bool(((flags & N.RF_NONFINITE) != 0).any()):
-        raise ValueError("input contains NaN")
-    if bool(((flags & N.RF_DEGENERATE_X) != 0).any()):
-        raise_for(N.QX_DEGENERATE_QUANTIZATION, "x quantizes to all zeros")
-    if bool((raw[:, 6] == 0).all()):
-        raise_for(N.QX_DEGENERATE_QUANTIZATION, "y quantizes to all zeros")
     bad = (status != 0) & (status != N.QX_DEGENERATE_QUANTIZATION)
-    if bool(bad.any()):
-        raise_for(int(status[bad][0]), "template search block failed")
-    value, lag, ties = raw[:, 0], raw[:, 1] + offs + stream_start, raw[:, 2]
+    value, lag, ties = raw[:, 0], raw[:, 1] + offs, raw[:, 2]
     vmax = value.max()
     hit = value == vmax
-    return (int(vmax), int(lag[hit].min()), int(ties[hit].sum()))
+    big = t.iinfo(t.int64).max
+    summary = t.stack([
+        vmax, t.where(hit, lag, big).min(), (ties * hit).sum(),
+        ((flags & N.RF_NONFINITE) != 0).any().long(), ((flags & N.RF_DEGENERATE_X) != 0).any().long(),
+        (raw[:, 6] == 0).all().long(), bad.any().long(), t.where(bad, status, 0).max()]).cpu().tolist()
+    vmax, lmin, nties, nan, degx, degy, anybad, badst = summary
+    if nan:
+        raise ValueError("input contains NaN")
+    if degx:
+        raise_for(N.QX_DEGENERATE_QUANTIZATION, "x quantizes to all zeros")
+    if degy:
+        raise_for(N.QX_DEGENERATE_QUANTIZATION, "y quantizes to all zeros")
+    if anybad:
+        raise_for(int(badst), "template search block failed")
+    return (int(vmax), int(lmin) + stream_start, int(nties))
 
 
 def check_results(res: np.ndarray) -> None:

@@ -152,6 +152,13 @@ qx_status qx_estimate_sweep_host(qx_context *ctx, const qx_signals *x, const qx_
                                  const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
                                  qx_path path, qx_result *results);
 
+/* Device decode of a mono PCM16 payload (little-endian int16, e.g. the data
+ * chunk of a WAV file) to float32 samples pcm / 32768: the sample decode of
+ * signalgen.load_wav_bytes (signalgen.py:150-172).  Exact, so the float32
+ * entry points quantise these samples exactly as the reference quantises its
+ * float64 ones.  pcm and out are 16-byte aligned device pointers. */
+qx_status qx_decode_pcm16(qx_context *ctx, const void *pcm, int64_t n, float *out, void *stream);
+
 /* Launch accounting for measurement (bench.py): between begin and end every
  * kernel the library launches is counted per kind and, when `timed`, bracketed
  * by CUDA events on its own stream.  qx_profile_end synchronises and returns

@@ -13,7 +13,7 @@ Batched, windowed and streaming entry points (new): ``estimate_batch``,
 ``parallel``.
 """
 
-from . import accuracy
+from . import accuracy, ingest
 from .batch import BatchResult, check_results, estimate_batch, estimate_batch_host, estimate_sweep_host, template_search
 from .errors import (
     BadLength,
@@ -41,5 +41,5 @@ __all__ = [
     "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "big_mul", "MUL_BACKENDS",
     "EstimationResult", "argmax_set", "estimate",
     "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep_host", "check_results", "template_search",
-    "accuracy",
+    "accuracy", "ingest",
 ]

@@ -20,6 +20,7 @@ int thresholds(int kind, long long k, double step, const double* thr, int dtype,
 cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
                             int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s);
 cudaError_t stats_to_results(const unsigned long long* stats, void* results, int64_t batch, cudaStream_t s);
+cudaError_t pcm16_launch(const void* in, int64_t n, float* out, int sms, cudaStream_t s);
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
 }  // namespace qx
@@ -575,6 +576,22 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
     for (int64_t b = 0; b < batch; ++b)
         if (results[b].status) return (qx_status)results[b].status;
+    return QX_OK;
+}
+
+qx_status qx_decode_pcm16(qx_context* ctx, const void* pcm, int64_t n, float* out, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!pcm || !out || n < 1) return fail(ctx, QX_ERR_INVALID, "pcm/out must be non-NULL and n >= 1");
+    if ((uintptr_t)pcm % 16 || (uintptr_t)out % 16) return fail(ctx, QX_ERR_INVALID, "pcm/out must be 16-byte aligned");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    ctx->prof.pre(KK_QUANT, s);
+    cudaError_t e = pcm16_launch(pcm, n, out, sms, s);
+    ctx->prof.post(KK_QUANT, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "decode_pcm16");
     return QX_OK;
 }
 

@@ -139,6 +139,44 @@ __global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QuantA
 }
 
 
+// PCM16 (little-endian int16) -> float32 pcm / 32768, the sample decode of
+// signalgen.load_wav_bytes (signalgen.py:150-172) on the device.  Exact:
+// every value is a multiple of 2^-15 with at most 16 significant bits, so
+// the float32 path quantises it exactly as the reference's float64 does.
+// 8 samples (16 B in, 32 B out) per thread-iteration, grid-stride; the
+// caller's buffers are cudaMalloc-aligned, the tail is scalar.
+__global__ void __launch_bounds__(256) k_pcm16_to_f32(const int16_t* __restrict__ in, int64_t n,
+                                                      float* __restrict__ out)
+{
+    const int64_t n8 = n >> 3;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const uint4* in8 = reinterpret_cast<const uint4*>(in);
+    float4* out4 = reinterpret_cast<float4*>(out);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += stride) {
+        const uint4 w = __ldg(&in8[i]);
+        const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+        float f[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            f[2 * j] = (float)(int16_t)(v[j] & 0xffffu) * (1.0f / 32768.0f);
+            f[2 * j + 1] = (float)(int16_t)(v[j] >> 16) * (1.0f / 32768.0f);
+        }
+        out4[2 * i] = make_float4(f[0], f[1], f[2], f[3]);
+        out4[2 * i + 1] = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    for (int64_t i = (n8 << 3) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        out[i] = (float)in[i] * (1.0f / 32768.0f);
+}
+
+cudaError_t pcm16_launch(const void* in, int64_t n, float* out, int sms, cudaStream_t s)
+{
+    int64_t blocks = ((n >> 3) + 255) / 256;
+    if (blocks > 8 * (int64_t)sms) blocks = 8 * (int64_t)sms;
+    if (blocks < 1) blocks = 1;
+    k_pcm16_to_f32<<<(unsigned)blocks, 256, 0, s>>>(reinterpret_cast<const int16_t*>(in), n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
                             int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s)
 {

@@ -218,7 +218,11 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
 // slot u: warp-reduced, one record per builder warp (summed by the epilogue)
-template <bool Y32, int PITCH = 16>  // Y32: y statistics fit 32 bits per warp (fast paths)
+// SM: statistics mode.  0: generic (64-bit y sums); 1: per-pair fast path
+// (<= 8 samples per thread and operand: per warp, sum of squares < 2^23 and
+// count < 2^9, so each operand's pair packs into one 32-bit REDUX); 2:
+// shared template (x statistics are already final, in thread 0 only)
+template <int SM, int PITCH = 16>
 __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
                               unsigned long long ssy, unsigned long long nzy, unsigned fl, int xs)
 {
@@ -239,15 +243,19 @@ __device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned
             if (lane == 0) S.wxs[u][threadIdx.x >> 5][e] = acc;
         }
     }
-    ssx = __reduce_add_sync(0xffffffffu, ssx);
-    fl = __reduce_or_sync(0xffffffffu, fl);
-    if constexpr (Y32) {
-        // per warp: nzx, nzy <= 32 * 16 samples, packed into one word
-        const unsigned nz = __reduce_add_sync(0xffffffffu, nzx | ((unsigned)nzy << 16));
-        nzx = nz & 0xffffu;
-        nzy = nz >> 16;
+    if (__any_sync(0xffffffffu, fl)) fl = __reduce_or_sync(0xffffffffu, fl);  // NaN: rare
+    if constexpr (SM == 1) {
+        const unsigned px = __reduce_add_sync(0xffffffffu, ssx | (nzx << 23));
+        const unsigned py = __reduce_add_sync(0xffffffffu, (unsigned)ssy | ((unsigned)nzy << 23));
+        ssx = px & 0x7fffffu;
+        nzx = px >> 23;
+        ssy = py & 0x7fffffu;
+        nzy = py >> 23;
+    } else if constexpr (SM == 2) {
         ssy = __reduce_add_sync(0xffffffffu, (unsigned)ssy);
+        nzy = __reduce_add_sync(0xffffffffu, (unsigned)nzy);
     } else {
+        ssx = __reduce_add_sync(0xffffffffu, ssx);
         nzx = __reduce_add_sync(0xffffffffu, nzx);
 #pragma unroll
         for (int o = 16; o; o >>= 1) {
@@ -342,7 +350,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
         v.w = __funnelshift_r(a3, a4, sh);
         b4[kc * (kTcBLbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
     }
-    tc_aux_finish<false>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
+    tc_aux_finish<0>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
 }
 
 // ---- fast build: float32 rows, nx, ny <= kTcFastN, 16-B aligned rows,
@@ -602,11 +610,11 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
 // thread) into the swizzled pitch-32 buffer; the template statistics ride in
 // builder warp 0's record
 template <int QM>
-__device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<true>& r)
+__device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<true>& r, bool first)
 {
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
     const int ny = (int)a.op[1].n, ny4 = (ny + 3) >> 2;
-    tc_zero_margins<32>(a, S, 0, -1, s, ny4);
+    if (first) tc_zero_margins<32>(a, S, 0, -1, s, ny4);  // margins are the same for every pair
     uint32_t w[4];
     unsigned fl = 0, ssy = 0, nzy = 0;
     tc_quant_words<QM, 4>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
@@ -621,12 +629,12 @@ __device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const Tc
     }
     if (a.extra) asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // y codes for the dp4a lags
     const bool w0 = threadIdx.x == 0;
-    tc_aux_finish<true, 32>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
-                            fl | (w0 ? S.xst[2] : 0u), 0);
+    tc_aux_finish<2, 32>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
+                         fl | (w0 ? S.xst[2] : 0u), 0);
 }
 
 template <int QM>
-__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<false>& r)
+__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<false>& r, bool first)
 {
     const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
@@ -637,7 +645,7 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
 #else
 #define TC_MARK(i)
 #endif
-    tc_zero_margins(a, S, s, nx4, s, ny4);
+    if (first) tc_zero_margins(a, S, s, nx4, s, ny4);  // margins are the same for every pair
     TC_MARK(8);
     // samples past n were fetched as zeros: code 0, no statistics
     unsigned ssx = 0, nzx = 0, ssy = 0, nzy = 0, fl = 0;
@@ -661,7 +669,7 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
     TC_MARK(10);
     tc_build_copies<16>(a, S, s, s);
     TC_MARK(11);
-    tc_aux_finish<true>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
+    tc_aux_finish<1>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
     TC_MARK(12);
 }
 
@@ -734,15 +742,31 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
     if (q == 0) {
         // lane i < 5 sums statistic i over the builder warps' records
         constexpr int kW = kTcThreads / 32;
-        unsigned long long sum = 0;
-        if (lane < 5)
-            for (int w = 0; w < kW; ++w) {
-                const unsigned long long x = S.wst[u][w][lane];
-                sum = lane == 4 ? (sum | x) : sum + x;
-            }
-        const unsigned long long ssx = __shfl_sync(0xffffffffu, sum, 0), nzx = __shfl_sync(0xffffffffu, sum, 1),
-                                 ssy = __shfl_sync(0xffffffffu, sum, 2), nzy = __shfl_sync(0xffffffffu, sum, 3),
-                                 fls = __shfl_sync(0xffffffffu, sum, 4);
+        unsigned long long ssx, nzx, ssy, nzy, fls;
+        if (a.fast) {
+            // per-pair totals fit 32 bits (n <= 8192, k <= 127): lane w < 16
+            // holds builder warp w's record, one REDUX per field
+            unsigned v[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) v[i] = lane < kW ? (unsigned)S.wst[u][lane][i] : 0u;
+            ssx = __reduce_add_sync(0xffffffffu, v[0]);
+            nzx = __reduce_add_sync(0xffffffffu, v[1]);
+            ssy = __reduce_add_sync(0xffffffffu, v[2]);
+            nzy = __reduce_add_sync(0xffffffffu, v[3]);
+            fls = __reduce_or_sync(0xffffffffu, v[4]);
+        } else {
+            unsigned long long sum = 0;
+            if (lane < 5)
+                for (int w = 0; w < kW; ++w) {
+                    const unsigned long long x = S.wst[u][w][lane];
+                    sum = lane == 4 ? (sum | x) : sum + x;
+                }
+            ssx = __shfl_sync(0xffffffffu, sum, 0);
+            nzx = __shfl_sync(0xffffffffu, sum, 1);
+            ssy = __shfl_sync(0xffffffffu, sum, 2);
+            nzy = __shfl_sync(0xffffffffu, sum, 3);
+            fls = __shfl_sync(0xffffffffu, sum, 4);
+        }
         long long v0 = LLONG_MIN, t0 = LLONG_MAX, c0 = 0;
         for (int w = 0; w < 4; ++w)
             if (S.best[w][2]) best_add(v0, t0, c0, S.best[w][0], tbase + S.best[w][1], S.best[w][2]);
@@ -837,8 +861,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                     if (!(a.debug & 2))
 #endif
                     {
-                        if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur);
-                        else tc_build_fast<QM>(a, S, it & 1, it & 3, cur);
+                        if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur, it < 2);
+                        else tc_build_fast<QM>(a, S, it & 1, it & 3, cur, it < 2);
                     }
                     if (threadIdx.x == 0) TC_ACC(1);
                     handoff(it);

@@ -56,6 +56,24 @@ __device__ __forceinline__ void bfly_dif(uint32_t& a, uint32_t& b, uint2 w, cons
     b = shoup(d, w.x, w.y, m.p);
 }
 
+// DIF butterfly with twiddle 1: (a + b, a - b), same ranges as bfly_dif
+__device__ __forceinline__ void bfly_dif1(uint32_t& a, uint32_t& b, const ModP& m)
+{
+    const uint32_t s = a + b + m.zero;  // IADD3
+    const uint32_t d = a - b + m.p2;    // IADD3
+    a = red2p(s, m.p2);
+    b = red2p(d, m.p2);
+}
+
+// DIT butterfly with twiddle 1, same ranges as bfly_dit
+__device__ __forceinline__ void bfly_dit1(uint32_t& a, uint32_t& b, const ModP& m)
+{
+    const uint32_t x = red2p(a, m.p2);
+    const uint32_t t = red2p(b, m.p2);
+    a = x + t + m.zero;
+    b = x - t + m.p2;
+}
+
 // DIT (Cooley-Tukey) butterfly, inputs/outputs in [0, 4p):
 //   (a, b) -> (a + w b, a - w b)
 __device__ __forceinline__ void bfly_dit(uint32_t& a, uint32_t& b, uint2 w, const ModP& m)

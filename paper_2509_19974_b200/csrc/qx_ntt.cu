@@ -72,11 +72,15 @@ struct Sched {
 
 // DIF group I on 2^R registers (element k at j0 + k*S of its block).
 // Twiddles: block j0 of group I, stage t at [2^R - 2^(R-t), +2^(R-1-t)).
+// A group with a single block position (nj == 1: the last DIF group) has
+// twiddle omega^0 = 1 at kp == 0 of every stage, known at compile time:
+// those 2^R - 1 butterflies skip the product (a reduction instead).
 template <int LOG, int I>
 __device__ __forceinline__ void dif_regs(uint32_t (&x)[1 << Sched<LOG>::r(I)], int j0, const uint2* stw,
                                          const ModP& m)
 {
     constexpr int R = Sched<LOG>::r(I);
+    constexpr bool unit0 = Sched<LOG>::nj_dif(I) == 1;
     const uint2* tw = stw + Sched<LOG>::twoff_dif(I) + j0 * (1 << R);
 #pragma unroll
     for (int t = 0; t < R; ++t) {
@@ -84,6 +88,11 @@ __device__ __forceinline__ void dif_regs(uint32_t (&x)[1 << Sched<LOG>::r(I)], i
         const int off = (1 << R) - (1 << (R - t));
 #pragma unroll
         for (int kp = 0; kp < h; ++kp) {
+            if (unit0 && kp == 0) {
+#pragma unroll
+                for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dif1(x[blk], x[blk + h], m);
+                continue;
+            }
             const uint2 w = tw[off + kp];
 #pragma unroll
             for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dif(x[blk + kp], x[blk + kp + h], w, m);
@@ -98,12 +107,18 @@ __device__ __forceinline__ void dit_regs(uint32_t (&x)[1 << Sched<LOG>::rd(I)], 
                                          const ModP& m)
 {
     constexpr int R = Sched<LOG>::rd(I);
+    constexpr bool unit0 = Sched<LOG>::nj_dit(I) == 1;  // first DIT group: twiddle 1 at kp == 0
     const uint2* tw = stw + Sched<LOG>::twoff_dit(I) + j0 * (1 << R);
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int h = 1 << t;
 #pragma unroll
         for (int kp = 0; kp < h; ++kp) {
+            if (unit0 && kp == 0) {
+#pragma unroll
+                for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dit1(x[blk], x[blk + h], m);
+                continue;
+            }
             const uint2 w = tw[h - 1 + kp];
 #pragma unroll
             for (int blk = 0; blk < (1 << R); blk += 2 * h) bfly_dit(x[blk + kp], x[blk + kp + h], w, m);

@@ -58,8 +58,9 @@ struct NttTables {
     const uint2* g1i;  // DIT (inverse) group twiddles for N1
     const uint2* g2f;  // same for N2
     const uint2* g2i;
-    const uint32_t* twf;  // forward four-step twiddles [P] (Montgomery form)
-    const uint32_t* twi;  // inverse four-step twiddles [P] incl. R^2/P
+    const uint2* twf;  // forward four-step twiddles [P] (Shoup pairs)
+    const uint2* twi;  // inverse four-step twiddles [P] incl. R/P (Shoup pairs; the R cancels the
+                       // pointwise Montgomery product's R^-1)
 };
 
 // Optional per-launch accounting (qx_profile_begin/end): counts every kernel

@@ -268,7 +268,7 @@ struct Pass1Args {
     OperandDesc op[2];
     uint32_t* Y;          // Y^T: [pair][op][n2][k1pos]
     const uint2* gtw;     // DIF group twiddles for N1
-    const uint32_t* twf;  // forward four-step twiddles, transposed [n2][k1pos]
+    const uint2* twf;     // forward four-step twiddles, transposed [n2][k1pos] (Shoup pairs)
     unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -450,7 +450,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         const int o = (c0 + c) * N1;
 #pragma unroll 8
         for (int e = lane; e < N1; e += 32)
-            Yt[o + e] = montmul(smem[e * kPad + c], __ldg(&a.twf[o + e]), m.p, m.pinv);
+        {
+            const uint2 w = __ldg(&a.twf[o + e]);
+            Yt[o + e] = shoup(smem[e * kPad + c], w.x, w.y, m.p);
+        }
     }
 }
 
@@ -461,7 +464,7 @@ struct Pass2Args {
     uint32_t* Z;            // [pair][k1pos][n2]
     const uint2* gtwf;      // DIF group twiddles for N2
     const uint2* gtwi;      // DIT group twiddles for N2
-    const uint32_t* twinv;  // inverse four-step twiddles [k1pos][n2]
+    const uint2* twinv;     // inverse four-step twiddles [k1pos][n2] (Shoup pairs, incl. R/P)
     const unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -563,13 +566,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     dit_group_smem<LOG2, SC::NG - 1>(su, sti, m);
     __syncthreads();
     // transposed store Z[k1pos][n2] (lane = n2) with the inverse four-step
-    // twiddle (includes R^2/P)
+    // twiddle (includes R/P: the product's Montgomery R^-1 cancels)
     uint32_t* Z = a.Z + pl * P;
 #pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
         const int o = (r0 + c) * N2;
 #pragma unroll 8
-        for (int e = lane; e < N2; e += 32) Z[o + e] = montmul(su[e * kPad + c], __ldg(&a.twinv[o + e]), m.p, m.pinv);
+        for (int e = lane; e < N2; e += 32) {
+            const uint2 w = __ldg(&a.twinv[o + e]);
+            Z[o + e] = shoup(su[e * kPad + c], w.x, w.y, m.p);
+        }
     }
 }
 
@@ -1204,7 +1210,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     const int l1 = (lp + 1) / 2, l2 = lp / 2;
     const uint64_t P = 1ull << lp, N1 = 1ull << l1, N2 = 1ull << l2;
     const uint64_t w = powmod(g, (p - 1) >> lp, p), wi = powmod(w, p - 2, p);
-    const uint64_t R = (1ull << 32) % p, R2 = mulmod(R, R, p);
+    const uint64_t R = (1ull << 32) % p;
     const uint64_t invP = powmod(P, p - 2, p);
     std::vector<uint2> g1f, g1i, g2f, g2i;
     group_tables_rt(l1, powmod(w, N2, p), p, g1f, g1i);
@@ -1212,7 +1218,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     // layout: g1f | g1i | g2f | g2i | twf | twi  (each table 16-byte aligned)
     auto al = [](size_t n) { return (n + 1) & ~(size_t)1; };
     const size_t nt = al(g1f.size()) + al(g1i.size()) + al(g2f.size()) + al(g2i.size());
-    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint32_t);
+    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint2);
     std::vector<unsigned char> host(bytes, 0);
     uint2* h = reinterpret_cast<uint2*>(host.data());
     size_t o1i = al(g1f.size()), o2f = o1i + al(g1i.size()), o2i = o2f + al(g2f.size());
@@ -1220,16 +1226,17 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     memcpy(h + o1i, g1i.data(), g1i.size() * 8);
     memcpy(h + o2f, g2f.data(), g2f.size() * 8);
     memcpy(h + o2i, g2i.data(), g2i.size() * 8);
-    uint32_t* hf = reinterpret_cast<uint32_t*>(h + nt);
-    uint32_t* hi = hf + P;
-    const uint64_t ci = mulmod(invP, R2, p);
+    uint2* hf = h + nt;
+    uint2* hi = hf + P;
+    auto sh = [p](uint64_t v) { return make_uint2((uint32_t)v, (uint32_t)((v << 32) / p)); };
+    const uint64_t ci = mulmod(invP, R, p);  // R cancels the pointwise montmul's R^-1
     for (uint64_t pos = 0; pos < N1; ++pos) {
         const uint64_t k1 = bitrev((uint32_t)pos, l1);
         const uint64_t step_f = powmod(w, k1, p), step_i = powmod(wi, k1, p);
-        uint64_t f = R, iv = ci;  // n2 = 0
+        uint64_t f = 1, iv = ci;  // n2 = 0
         for (uint64_t n2 = 0; n2 < N2; ++n2) {
-            hf[n2 * N1 + pos] = (uint32_t)f;
-            hi[pos * N2 + n2] = (uint32_t)iv;
+            hf[n2 * N1 + pos] = sh(f);
+            hi[pos * N2 + n2] = sh(iv);
             f = mulmod(f, step_f, p);
             iv = mulmod(iv, step_i, p);
         }
@@ -1254,7 +1261,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     out->g1i = db + o1i;
     out->g2f = db + o2f;
     out->g2i = db + o2i;
-    out->twf = reinterpret_cast<const uint32_t*>(db + nt);
+    out->twf = db + nt;
     out->twi = out->twf + P;
     *dev_block = d;
     return cudaSuccess;

@@ -147,34 +147,15 @@ __device__ __forceinline__ int level_uniform_fast(float v, const float* s, int k
     return v < 0.f ? -lv : lv;
 }
 
-// Conversion-free exact uniform level (no F2I/FRND, which issue on the
-// quarter-rate conversion pipe): round-to-nearest of |v|/step through the
-// 1.5*2^23 magic constant (one FFMA, one integer subtract).  The reference
-// rounds half away from zero; the two roundings agree unless |v|/step is
-// within 2^-14 of a half-integer (the fp32 product is within 2^-15 of the
-// float64 quotient for k <= 128), and those rare samples take the exact
-// threshold compare.  Values >= 2^22 saturate monotonically and clamp to k.
-__device__ __forceinline__ int level_uniform_magic(float v, const float* s, int k, float inv_step)
-{
-    const float a = fabsf(v);
-    const float t = fmaf(a, inv_step, 12582912.0f);
-    int lv = __float_as_int(t) - 0x4B400000;
-    const float d = fmaf(a, inv_step, -(t - 12582912.0f));  // |v|/step - round(|v|/step)
-    lv = min(lv, k);
-    const bool near_half = fabsf(fabsf(d) - 0.5f) < 0x1p-14f;
-    if (__builtin_expect(near_half, 0)) {
-        int l2 = v < 0.f ? -lv : lv;
-        if (l2 < k && v >= s[l2 + k]) ++l2;
-        if (l2 > -k && !(v >= s[l2 + k - 1])) --l2;
-        return l2;
-    }
-    return v < 0.f ? -lv : lv;
-}
-
-// Branch-free form of level_uniform_magic for batches: returns the
-// magic-rounding level and raises `bad` when the sample is within 2^-14 of
-// a rounding half-point, NaN or +-inf; callers redo a batch with `bad` set
-// through the exact threshold compares.
+// Conversion-free uniform level for batches (no F2I/FRND, which issue on
+// the quarter-rate conversion pipe): round-to-nearest of |v|/step through
+// the 1.5*2^23 magic constant (one FFMA, one integer subtract).  The
+// reference rounds half away from zero; the two roundings agree unless
+// |v|/step is within 2^-14 of a half-integer (the fp32 product is within
+// 2^-15 of the float64 quotient for k <= 128), and values >= 2^22 saturate
+// monotonically and clamp to k.  `bad` is raised for those rare samples (and
+// NaN, +-inf); callers redo a batch with `bad` set through the exact
+// threshold compares.
 __device__ __forceinline__ int level_uniform_nb(float v, int k, float inv_step, bool& bad)
 {
     const float a = fabsf(v);

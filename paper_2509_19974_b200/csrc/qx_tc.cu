@@ -408,7 +408,7 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<S
     }
 }
 
-// level_uniform_magic (qx_common.cuh) with the NaN test folded into its
+// level_uniform_nb (qx_common.cuh) as a scalar, with the NaN test folded into its
 // rare exact branch: a NaN makes d NaN, fails `>= 2^-14` and lands there
 // (so does +-inf, which the exact compares then map to +-k)
 __device__ __forceinline__ int tc_level_uniform(float v, const float* s, int k, float inv_step, unsigned& flags)

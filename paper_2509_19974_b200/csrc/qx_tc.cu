@@ -44,6 +44,9 @@ namespace qx {
 
 constexpr int kTcThreads = 512;                 // builder threads (warps 0-15)
 constexpr int kTcMmaWarp = 16;                   // MMA issuer
+constexpr int kTcLagWarp0 = 17, kTcLagWarps = 3;  // extra-lag dot products (warps 17-19)
+// builders + MMA warp + lag warps meet at the per-pair hand-off barrier
+constexpr int kTcHandoff = kTcThreads + 32 + 32 * kTcLagWarps;
 constexpr int kTcTotalThreads = 24 * 32;         // + warp 16 (MMA), warps 20-23 (epilogue)
 constexpr int kTcLags = 2048;      // lags per M=128 tile (M=64: 1024)
 constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
@@ -194,7 +197,8 @@ struct TcSmem {
     uint64_t tfree[kTcAux];  // epilogue finished with aux slot (128 arrivals)
     // per-builder-warp partials (no atomics): ssx, nzx, ssy, nzy, flags
     unsigned long long wst[kTcAux][kTcThreads / 32][5];
-    int wxs[kTcAux][kTcThreads / 32][kTcMaxExtra];  // extra-lag sums
+    int wxs[kTcAux][kTcLagWarps][kTcMaxExtra];     // extra-lag sums, one record per lag warp
+    uint64_t xdone[kTcAux];  // lag warps finished with the pair of aux slot (96 arrivals)
     unsigned xst[3];      // shared-x mode: template ssx, nzx, flags (built once)
     uint32_t tmem_base;
     int best[4][3];
@@ -215,6 +219,10 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 {
     mbar_wait(&S.tfree[j & 3], (uint32_t)((j >> 2) & 1));
 }
+__device__ __forceinline__ void tc_wait_xdone(TcSmem& S, int j)
+{
+    mbar_wait(&S.xdone[j & 3], (uint32_t)((j >> 2) & 1));
+}
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
 // slot u: warp-reduced, one record per builder warp (summed by the epilogue)
@@ -222,27 +230,11 @@ __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 // (<= 8 samples per thread and operand: per warp, sum of squares < 2^23 and
 // count < 2^9, so each operand's pair packs into one 32-bit REDUX); 2:
 // shared template (x statistics are already final, in thread 0 only)
-template <int SM, int PITCH = 16>
-__device__ void tc_aux_finish(const TcArgs& a, TcSmem& S, int s, int u, unsigned ssx, unsigned nzx,
-                              unsigned long long ssy, unsigned long long nzy, unsigned fl, int xs)
+template <int SM>
+__device__ void tc_aux_finish(TcSmem& S, int u, unsigned ssx, unsigned nzx, unsigned long long ssy,
+                              unsigned long long nzy, unsigned fl)
 {
     const int lane = threadIdx.x & 31;
-    if (a.extra) {
-        // extra lag j = ntiles*16M + e: sum_m x[m] * ycode[L0 + j + m]
-        const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[xs]) + kTcXPad / 4;  // x codes from m = 0
-        const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[s]);
-        const int nw = (int)((a.op[0].n + 3) >> 2);
-        const int j0 = a.ntiles * a.pitch * a.M;
-        for (int e = 0; e < a.extra; ++e) {
-            const int j = j0 + e, jw = j >> 2, sh = (j & 3) * 8;
-            int acc = 0;
-            for (int w = threadIdx.x; w < nw; w += kTcThreads)
-                acc = __dp4a((int)xw[w],
-                             (int)__funnelshift_r(yw[ysw<PITCH>(w + jw)], yw[ysw<PITCH>(w + jw + 1)], sh), acc);
-            acc = __reduce_add_sync(0xffffffffu, acc);
-            if (lane == 0) S.wxs[u][threadIdx.x >> 5][e] = acc;
-        }
-    }
     if (__any_sync(0xffffffffu, fl)) fl = __reduce_or_sync(0xffffffffu, fl);  // NaN: rare
     if constexpr (SM == 1) {
         const unsigned px = __reduce_add_sync(0xffffffffu, ssx | (nzx << 23));
@@ -350,7 +342,7 @@ __device__ void tc_build(const TcArgs& a, TcSmem& S, int s, int u, int64_t pair)
         v.w = __funnelshift_r(a3, a4, sh);
         b4[kc * (kTcBLbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
     }
-    tc_aux_finish<0>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
+    tc_aux_finish<0>(S, u, ssx, nzx, ssy, nzy, fl);
 }
 
 // ---- fast build: float32 rows, nx, ny <= kTcFastN, 16-B aligned rows,
@@ -627,10 +619,8 @@ __device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const Tc
         const int wi = yoff + i;
         if (i < ny4 && wi >= 0 && wi < Y) yw[ysw<32>(wi)] = w[h];
     }
-    if (a.extra) asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // y codes for the dp4a lags
     const bool w0 = threadIdx.x == 0;
-    tc_aux_finish<2, 32>(a, S, s, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy,
-                         fl | (w0 ? S.xst[2] : 0u), 0);
+    tc_aux_finish<2>(S, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy, fl | (w0 ? S.xst[2] : 0u));
 }
 
 template <int QM>
@@ -669,8 +659,30 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
     TC_MARK(10);
     tc_build_copies<16>(a, S, s, s);
     TC_MARK(11);
-    tc_aux_finish<1>(a, S, s, u, ssx, nzx, ssy, nzy, fl, s);
+    tc_aux_finish<1>(S, u, ssx, nzx, ssy, nzy, fl);
     TC_MARK(12);
+}
+
+// Extra lags of the pair in data slot s (aux slot u), run by the lag warps
+// after the hand-off barrier: j = ntiles*pitch*M + e, sum_m x[m] *
+// ycode[L0 + j + m] over packed words (dp4a), one record per lag warp.
+template <int PITCH>
+__device__ void tc_extra_lags(const TcArgs& a, TcSmem& S, int s, int u, int xs)
+{
+    const int lane = threadIdx.x & 31, lw = (threadIdx.x >> 5) - kTcLagWarp0;
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[xs]) + kTcXPad / 4;  // x codes from m = 0
+    const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[s]);
+    const int nw = (int)((a.op[0].n + 3) >> 2);
+    const int j0 = a.ntiles * a.pitch * a.M;
+    for (int e = 0; e < a.extra; ++e) {
+        const int j = j0 + e, jw = j >> 2, sh = (j & 3) * 8;
+        int acc = 0;
+        for (int w = lw * 32 + lane; w < nw; w += 32 * kTcLagWarps)
+            acc = __dp4a((int)xw[w], (int)__funnelshift_r(yw[ysw<PITCH>(w + jw)], yw[ysw<PITCH>(w + jw + 1)], sh),
+                         acc);
+        acc = __reduce_add_sync(0xffffffffu, acc);
+        if (lane == 0) S.wxs[u][lw][e] = acc;
+    }
 }
 
 // argmax epilogue of the pair in aux slot u, run by warps 20..23 only (warp
@@ -771,7 +783,7 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
         for (int w = 0; w < 4; ++w)
             if (S.best[w][2]) best_add(v0, t0, c0, S.best[w][0], tbase + S.best[w][1], S.best[w][2]);
         for (int e = 0; e < a.extra; ++e) {
-            const int xs = __reduce_add_sync(0xffffffffu, lane < kW ? S.wxs[u][lane][e] : 0);
+            const int xs = __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0);
             const int j = a.ntiles * tl + e;
             if (j < jlo || j > jhi) continue;
             best_add(v0, t0, c0, xs, tbase + j, 1);
@@ -811,6 +823,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     if (threadIdx.x < kTcAux) {
         mbar_init(&S.mdone[threadIdx.x], 1);
         mbar_init(&S.tfree[threadIdx.x], 128);
+        mbar_init(&S.xdone[threadIdx.x], 32 * kTcLagWarps);
     }
 #ifdef QX_TC_TIMING
     if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
@@ -834,14 +847,15 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         auto acquire = [&](int it) {
             TC_T0();
             if (it >= 2) tc_wait_mdone(S, it - 2);
+            if (it >= 2) tc_wait_xdone(S, it - 2);  // lag warps done reading the data slot
             if (it >= 4) tc_wait_tfree(S, it - 4);
             if (threadIdx.x == 0) TC_ACC(0);
         };
         auto handoff = [&](int it) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
             // alternating barrier ids keep consecutive iterations apart
-            if (it & 1) asm volatile("bar.arrive 3, %0;" ::"n"(kTcThreads + 32) : "memory");
-            else asm volatile("bar.arrive 2, %0;" ::"n"(kTcThreads + 32) : "memory");
+            if (it & 1) asm volatile("bar.arrive 3, %0;" ::"n"(kTcHandoff) : "memory");
+            else asm volatile("bar.arrive 2, %0;" ::"n"(kTcHandoff) : "memory");
         };
         bool fast = false;
         if constexpr (std::is_same<T, float>::value) fast = a.fast;
@@ -884,8 +898,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             const int s = it & 1, u = it & 3;
             {
                 TC_T0();
-                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcThreads + 32) : "memory");
-                else asm volatile("bar.sync 2, %0;" ::"n"(kTcThreads + 32) : "memory");
+                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
+                else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
                 if (lane == 0) TC_ACC(2);
             }
             {
@@ -926,12 +940,24 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             __syncwarp();
             if (lane == 0) TC_ACC(5);
         }
+    } else if (warp >= kTcLagWarp0 && warp < kTcLagWarp0 + kTcLagWarps) {
+        // ---- lag warps: the extra lags of each pair from its code buffers
+        for (int it = 0; it < npairs; ++it) {
+            if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
+            else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
+            if (a.extra) {
+                if (it >= 4) tc_wait_tfree(S, it - 4);  // epilogue done with this aux slot's records
+                tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it & 3, SX ? 0 : (it & 1));
+            }
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it & 3])) : "memory");
+        }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ---- epilogue: TMEM -> argmax -> qx_result, then free the aux slot
         for (int it = 0; it < npairs; ++it) {
             const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
             TC_T0();
             tc_wait_mdone(S, it);
+            tc_wait_xdone(S, it);  // extra-lag records written
             if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             {

@@ -201,7 +201,8 @@ struct TcSmem {
     uint64_t xdone[kTcAux];  // lag warps finished with the pair of aux slot (96 arrivals)
     unsigned xst[3];      // shared-x mode: template ssx, nzx, flags (built once)
     uint32_t tmem_base;
-    int best[4][3];
+    int best[kTcAux][4][3];                 // per epilogue warp (value, j, count), per aux slot
+    unsigned long long fst[kTcAux][5];      // final statistics of the pair (lag warps)
 #ifdef QX_TC_TIMING
     unsigned long long tm[16];
 #endif
@@ -685,6 +686,36 @@ __device__ void tc_extra_lags(const TcArgs& a, TcSmem& S, int s, int u, int xs)
     }
 }
 
+// final statistics of the pair in aux slot u from the builder warps'
+// records (lane w < 16 holds warp w's), by one lag warp after the hand-off
+__device__ void tc_final_stats(const TcArgs& a, TcSmem& S, int u)
+{
+    constexpr int kW = kTcThreads / 32;
+    const int lane = threadIdx.x & 31;
+    unsigned long long r[5];
+    if (a.fast) {
+        // per-pair totals fit 32 bits (n <= 8192, k <= 127): one REDUX per field
+        unsigned v[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) v[i] = lane < kW ? (unsigned)S.wst[u][lane][i] : 0u;
+        r[0] = __reduce_add_sync(0xffffffffu, v[0]);
+        r[1] = __reduce_add_sync(0xffffffffu, v[1]);
+        r[2] = __reduce_add_sync(0xffffffffu, v[2]);
+        r[3] = __reduce_add_sync(0xffffffffu, v[3]);
+        r[4] = __reduce_or_sync(0xffffffffu, v[4]);
+    } else {
+        unsigned long long sum = 0;
+        if (lane < 5)
+            for (int w = 0; w < kW; ++w) {
+                const unsigned long long x = S.wst[u][w][lane];
+                sum = lane == 4 ? (sum | x) : sum + x;
+            }
+#pragma unroll
+        for (int i = 0; i < 5; ++i) r[i] = __shfl_sync(0xffffffffu, sum, i);
+    }
+    if (lane < 5) S.fst[u][lane] = lane == 0 ? r[0] : lane == 1 ? r[1] : lane == 2 ? r[2] : lane == 3 ? r[3] : r[4];
+}
+
 // argmax epilogue of the pair in aux slot u, run by warps 20..23 only (warp
 // w reads TMEM lane quarter w%4; M=128: lane = row, M=64: rows 16q..16q+15
 // sit in lanes 32q..32q+15), reduced behind a 128-thread named barrier so
@@ -714,6 +745,12 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
     // marks out-of-window entries and INT_MIN + 1 is below every value; j
     // increases along the scan, so the first maximum is the smallest lag
     int bv = INT_MIN + 1, bj = INT_MAX, bc = 0;
+#ifdef QX_TC_TIMING
+    long long _e = clock64();
+#define TC_EMARK(i) if (threadIdx.x == kEpiWarp0 * 32) { const long long _n = clock64(); atomicAdd(&S.tm[i], (unsigned long long)(_n - _e)); _e = _n; }
+#else
+#define TC_EMARK(i)
+#endif
     for (int tile = 0; tile < a.ntiles; ++tile) {
 #pragma unroll
         for (int c0 = 0; c0 < PITCH; c0 += 16) {
@@ -735,53 +772,37 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
     }
     // TMEM reads are complete (wait::ld) before the slot is released
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-        const int ov = __shfl_xor_sync(0xffffffffu, bv, o), oj = __shfl_xor_sync(0xffffffffu, bj, o),
-                  oc = __shfl_xor_sync(0xffffffffu, bc, o);
-        const bool gt = ov > bv, eq = ov == bv;
-        bj = gt ? oj : (eq ? min(bj, oj) : bj);
-        bc = gt ? oc : bc + (eq ? oc : 0);
-        bv = gt ? ov : bv;
+    TC_EMARK(13);
+    // warp (value, smallest j, count) by REDUX: the max, then the min j and
+    // the summed count of the lanes holding it (empty lanes: INT_MIN + 1, 0)
+    {
+        const int mv = __reduce_max_sync(0xffffffffu, bv);
+        const bool at = bv == mv;
+        bj = __reduce_min_sync(0xffffffffu, at ? bj : INT_MAX);
+        bc = __reduce_add_sync(0xffffffffu, at ? bc : 0);
+        bv = mv;
     }
-    asm volatile("bar.sync 4, 128;" ::: "memory");  // previous pair's S.best reads done
+    TC_EMARK(14);
+    // per-aux-slot records: the epilogue warps are never a pair apart (the
+    // barrier below), so the slot written here is not being read
     if (lane == 0) {
-        S.best[q][0] = bv;
-        S.best[q][1] = bj;
-        S.best[q][2] = bc;
+        S.best[u][q][0] = bv;
+        S.best[u][q][1] = bj;
+        S.best[u][q][2] = bc;
     }
     asm volatile("bar.sync 4, 128;" ::: "memory");
     if (q == 0) {
-        // lane i < 5 sums statistic i over the builder warps' records
-        constexpr int kW = kTcThreads / 32;
-        unsigned long long ssx, nzx, ssy, nzy, fls;
-        if (a.fast) {
-            // per-pair totals fit 32 bits (n <= 8192, k <= 127): lane w < 16
-            // holds builder warp w's record, one REDUX per field
-            unsigned v[5];
-#pragma unroll
-            for (int i = 0; i < 5; ++i) v[i] = lane < kW ? (unsigned)S.wst[u][lane][i] : 0u;
-            ssx = __reduce_add_sync(0xffffffffu, v[0]);
-            nzx = __reduce_add_sync(0xffffffffu, v[1]);
-            ssy = __reduce_add_sync(0xffffffffu, v[2]);
-            nzy = __reduce_add_sync(0xffffffffu, v[3]);
-            fls = __reduce_or_sync(0xffffffffu, v[4]);
-        } else {
-            unsigned long long sum = 0;
-            if (lane < 5)
-                for (int w = 0; w < kW; ++w) {
-                    const unsigned long long x = S.wst[u][w][lane];
-                    sum = lane == 4 ? (sum | x) : sum + x;
-                }
-            ssx = __shfl_sync(0xffffffffu, sum, 0);
-            nzx = __shfl_sync(0xffffffffu, sum, 1);
-            ssy = __shfl_sync(0xffffffffu, sum, 2);
-            nzy = __shfl_sync(0xffffffffu, sum, 3);
-            fls = __shfl_sync(0xffffffffu, sum, 4);
-        }
+        const unsigned long long* fs = S.fst[u];  // summed by the lag warps
+        const unsigned long long ssx = fs[0], nzx = fs[1], ssy = fs[2], nzy = fs[3], fls = fs[4];
+        // the four warp records by REDUX (lanes 0..3)
+        const int wv = lane < 4 ? S.best[u][lane][0] : INT_MIN;
+        const int mv = __reduce_max_sync(0xffffffffu, wv);
+        const bool at = lane < 4 && wv == mv;
+        const int mj = __reduce_min_sync(0xffffffffu, at ? S.best[u][lane][1] : INT_MAX);
+        const int mc = __reduce_add_sync(0xffffffffu, at ? S.best[u][lane][2] : 0);
         long long v0 = LLONG_MIN, t0 = LLONG_MAX, c0 = 0;
-        for (int w = 0; w < 4; ++w)
-            if (S.best[w][2]) best_add(v0, t0, c0, S.best[w][0], tbase + S.best[w][1], S.best[w][2]);
+        if (mc) best_add(v0, t0, c0, mv, tbase + mj, mc);
+
         for (int e = 0; e < a.extra; ++e) {
             const int xs = __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0);
             const int j = a.ntiles * tl + e;
@@ -798,6 +819,7 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
           : lane == 4 ? (long long)ssy : lane == 5 ? (long long)nzx : lane == 6 ? (long long)nzy : f;
         if (lane < 8) reinterpret_cast<long long*>(a.am.results)[pair * 8 + lane] = f;
     }
+    TC_EMARK(15);
 }
 
 #ifdef QX_TC_TIMING
@@ -945,10 +967,9 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         for (int it = 0; it < npairs; ++it) {
             if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
             else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
-            if (a.extra) {
-                if (it >= 4) tc_wait_tfree(S, it - 4);  // epilogue done with this aux slot's records
-                tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it & 3, SX ? 0 : (it & 1));
-            }
+            if (it >= 4) tc_wait_tfree(S, it - 4);  // epilogue done with this aux slot's records
+            if (a.extra) tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it & 3, SX ? 0 : (it & 1));
+            if (warp == kTcLagWarp0) tc_final_stats(a, S, it & 3);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it & 3])) : "memory");
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
@@ -979,8 +1000,9 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                (long long)npairs, a.debug, S.tm[0] / npairs, S.tm[1] / npairs, S.tm[2] / npairs, S.tm[4] / npairs,
                S.tm[5] / npairs, S.tm[3] / npairs, S.tm[6] / npairs);
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        printf("  build phases (cycles/pair): zero %llu quant %llu bar %llu copies %llu aux %llu\n", S.tm[8] / npairs,
-               S.tm[9] / npairs, S.tm[10] / npairs, S.tm[11] / npairs, S.tm[12] / npairs);
+        printf("  build phases (cycles/pair): zero %llu quant %llu bar %llu copies %llu aux %llu | epi: tmem+scan %llu "
+               "shfl %llu bars+merge %llu\n", S.tm[8] / npairs, S.tm[9] / npairs, S.tm[10] / npairs,
+               S.tm[11] / npairs, S.tm[12] / npairs, S.tm[13] / npairs, S.tm[14] / npairs, S.tm[15] / npairs);
 #endif
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(S.tmem_base));
 }

@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (other_configs)")
     return ap.parse_args()
 
 
@@ -317,6 +318,19 @@ def main():
                "sample": f"{passes} passes over {sample} pairs x {len(BITS)} bit depths of config 2 ({dt:.1f} s): "
                          "C oracle = reference algorithm (float64 quantise, KS + GMP mpn_mul, argmax)"}
 
+    # the other BASELINE configs on this GPU (rank 0 of a single-GPU run):
+    # each checked against its planted delay, failures reported, not fatal
+    other = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        other = {}
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs
+        for name in ("c1", "c1batch", "c3full", "c4", "c5"):
+            try:
+                other.update(bench_configs.run([name]))
+            except Exception as exc:  # keep the headline line
+                other[name] = {"error": f"{type(exc).__name__}: {exc}"}
+
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -327,7 +341,8 @@ def main():
                 "gpu_launches": prof.launches,
                 "kernels": {k: {"launches": c, "ms_per_step": m / kprof_steps} for k, (c, m) in kinds.items()},
                 "roofline": roof, "int_roofline": int_roof, "clocks": clk.summary(), "e2e": e2e,
-                "cpu_baseline": cpu, "step_ms_median": statistics.median(step_ms)}
+                "cpu_baseline": cpu, "step_ms_median": statistics.median(step_ms),
+                "other_configs": other}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -1,23 +1,28 @@
 """Per-config throughput of the engine on one GPU (BASELINE configs 1-5).
 
 Times each config's hot path with CUDA events (inputs resident in HBM, warm
-tables), checks every estimate against the planted delay, and prints one JSON
-object.  C3 runs a 16384-pair slice of the 65,536-pair workload (per-pair
-cost is shape-only; `c3full` runs all 65,536 pairs); C5 runs the full
-2^28-sample stream.  Roofline fractions use MEASURED_PEAKS.json hbm_gbs.
-usage: python tools/bench_configs.py [c1 c2 c3 c4 c5]"""
+tables), checks every estimate against the planted delay, and returns / prints
+one JSON object.  C3 runs a 16384-pair slice of the 65,536-pair workload
+(per-pair cost is shape-only; `c3full` runs all 65,536 pairs); C5 runs the
+full 2^28-sample stream.  Roofline fractions: HBM from MEASURED_PEAKS.json
+hbm_gbs; i8 tensor from the measured 8190 MACs/clk/SM (profiles/r01_tc_rate.json).
+bench.py imports run() for its `other_configs` key.
+usage: python tools/bench_configs.py [c1 c1batch c2 c3 c3full c4 c5]"""
 import json
 import math
 import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 import numpy as np
 import torch
 
 import paper_2509_19974_b200 as P
 from paper_2509_19974_b200 import workloads as W
+
+I8_MACS_PER_CLK_SM = 8190.0  # tools/tc_rate.cu, M128 x N128/N256
 
 
 def timed(fn, reps=5, warm=2):
@@ -33,58 +38,87 @@ def timed(fn, reps=5, warm=2):
     return a.elapsed_time(b) / reps, out
 
 
-res = {}
-which = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
-if "c1" in which:
-    x, y = W.c1(0)
-    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
-    ms, r = timed(lambda: P.estimate_batch(xd, yd, P.sign(), P.sign()), reps=50)
-    r = r.numpy()[0]
-    assert (r["lag"], r["value"]) == (-137, 14839)
-    res["c1"] = {"ms_per_estimate": ms, "lag": int(r["lag"]), "peak": int(r["value"])}
-if "c2" in which:
-    xs, ys, lag = W.c2()
-    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
-    for b in (1, 2, 4, 8):
-        q = W.bit_quantizer(b, W.C2_SIGMA)
-        ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q))
-        assert np.array_equal(r.numpy()["lag"], lag)
-        res[f"c2_b{b}"] = {"ms": ms, "estimates_per_s": 64 / ms * 1e3, "gsamples_per_s": 64 * 2 * W.C2_N / ms / 1e6}
-HBM = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                            "MEASURED_PEAKS.json"))).get("hbm_gbs", 6550.4)
-if "c3" in which or "c3full" in which:
-    npairs = W.C3_PAIRS if "c3full" in which else 16384
-    xs, ys, lag = W.c3(pairs=npairs)
-    xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
-    for b in (2, 4):
-        q = W.bit_quantizer(b, W.C3_SIGMA)
-        ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512), reps=3)
-        ok = float(np.mean(r.numpy()["lag"] == lag))
-        res[f"c3_b{b}"] = {"pairs": npairs, "ms": ms, "estimates_per_s": npairs / ms * 1e3,
-                           "gsamples_per_s": npairs * 2 * W.C3_N / ms / 1e6, "frac_correct_lag": ok,
-                           "hbm_frac": npairs * 2 * W.C3_N * 4 / (ms / 1e3) / 1e9 / HBM,
-                           "path": "tcgen05 kind::i8 window (M=64 tile + 1 CUDA-core lag)"}
-if "c4" in which:
-    x, y, lag = W.c4()
-    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
-    q = W.bit_quantizer(4, W.C4_SIGMA)
-    ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q), reps=3)
-    assert r.numpy()["lag"][0] == lag
-    res["c4"] = {"ms": ms, "gsamples_per_s": 2 * W.C4_N / ms / 1e6, "path": "ntt P=2^25 (outer 2^6 x inner 2^19)"}
-    del xd, yd
-if "c5" in which:
-    t0 = time.time()
-    tpl, st, off, sn2 = W.c5()
-    gen_s = time.time() - t0
-    td, sd = torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda()
-    for b in (1, 2):
-        if b == 1:
-            qa = qb = P.sign()
-        else:
-            qa, qb = P.uniform(1, 1.5 * math.sqrt(2.0)), P.uniform(1, 1.5 * math.sqrt(2.0 + sn2))
-        ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=2, warm=1)
-        assert r[1] == off, r
-        res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
-                           "lag": r[1], "path": "tcgen05 window, shared template (N=32, SW32 Hankel), 4096-lag blocks"}
-    res["c5_generation_s"] = gen_s
-print(json.dumps(res))
+def _peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    hbm = json.load(open(path)).get("hbm_gbs", 6550.4) if os.path.exists(path) else 6550.4
+    props = torch.cuda.get_device_properties(0)
+    clk = 1.965e9
+    i8 = I8_MACS_PER_CLK_SM * props.multi_processor_count * clk
+    return hbm, i8
+
+
+def run(which) -> dict:
+    res = {}
+    hbm, i8 = _peaks()
+    if "c1" in which:
+        x, y = W.c1(0)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        ms, r = timed(lambda: P.estimate_batch(xd, yd, P.sign(), P.sign()), reps=50)
+        r = r.numpy()[0]
+        assert (r["lag"], r["value"]) == (-137, 14839)
+        res["c1"] = {"ms_per_estimate": ms, "lag": int(r["lag"]), "peak": int(r["value"]),
+                     "note": "single pair, latency incl. the Python call"}
+    if "c1batch" in which:
+        x, y = W.c1(0)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        xb, yb = xd.expand(1024, -1), yd.expand(1024, -1)
+        ms, r = timed(lambda: P.estimate_batch(xb, yb, P.sign(), P.sign()), reps=10)
+        assert (r.numpy()["lag"] == -137).all()
+        res["c1_batch1024"] = {"ms": ms, "estimates_per_s": 1024 / ms * 1e3}
+    if "c2" in which:
+        xs, ys, lag = W.c2()
+        xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+        for b in (1, 2, 4, 8):
+            q = W.bit_quantizer(b, W.C2_SIGMA)
+            ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q))
+            assert np.array_equal(r.numpy()["lag"], lag)
+            res[f"c2_b{b}"] = {"ms": ms, "estimates_per_s": 64 / ms * 1e3,
+                               "gsamples_per_s": 64 * 2 * W.C2_N / ms / 1e6}
+    if "c3" in which or "c3full" in which:
+        npairs = W.C3_PAIRS if "c3full" in which else 16384
+        xs, ys, lag = W.c3(pairs=npairs)
+        xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+        del xs, ys
+        for b in (2, 4):
+            q = W.bit_quantizer(b, W.C3_SIGMA)
+            ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512), reps=3)
+            ok = float(np.mean(r.numpy()["lag"] == lag))
+            assert ok == 1.0, ok
+            res[f"c3_b{b}"] = {"pairs": npairs, "ms": ms, "estimates_per_s": npairs / ms * 1e3,
+                               "gsamples_per_s": npairs * 2 * W.C3_N / ms / 1e6, "frac_correct_lag": ok,
+                               "hbm_frac": npairs * 2 * W.C3_N * 4 / (ms / 1e3) / 1e9 / hbm,
+                               "path": "tcgen05 kind::i8 window (M=64 tile + 1 CUDA-core lag)"}
+        del xd, yd
+    if "c4" in which:
+        x, y, lag = W.c4()
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        q = W.bit_quantizer(4, W.C4_SIGMA)
+        ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q), reps=3)
+        assert r.numpy()["lag"][0] == lag
+        res["c4"] = {"ms": ms, "gsamples_per_s": 2 * W.C4_N / ms / 1e6,
+                     "path": "ntt P=2^25 (outer 2^6 x inner 2^19)"}
+        del xd, yd
+    if "c5" in which:
+        t0 = time.time()
+        tpl, st, off, sn2 = W.c5()
+        gen_s = time.time() - t0
+        td, sd = torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda()
+        macs = len(tpl) * (len(st) - len(tpl) + 1)
+        for b in (1, 2):
+            if b == 1:
+                qa = qb = P.sign()
+            else:
+                qa, qb = P.uniform(1, 1.5 * math.sqrt(2.0)), P.uniform(1, 1.5 * math.sqrt(2.0 + sn2))
+            ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=2, warm=1)
+            assert r[1] == off, r
+            res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
+                               "lag": r[1], "i8_tensor_frac": macs / (ms / 1e3) / i8,
+                               "path": "tcgen05 window, shared template (N=32, SW32 Hankel), 4096-lag blocks"}
+        res["c5_generation_s"] = gen_s
+        del td, sd
+    torch.cuda.empty_cache()
+    return res
+
+
+if __name__ == "__main__":
+    print(json.dumps(run(sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"])))

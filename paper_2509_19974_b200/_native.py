@@ -15,7 +15,9 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_native", "libqxcorr_b200.so")
+# QX_NATIVE_LIB: an alternative build of the same library (A/B and
+# -DQX_TC_TIMING instrumentation builds under tools/ab/)
+LIB_PATH = os.environ.get("QX_NATIVE_LIB") or os.path.join(_HERE, "_native", "libqxcorr_b200.so")
 
 # qx_status (include/qxcorr_b200.h)
 QX_OK = 0

@@ -10,6 +10,7 @@ restricted to [lag_lo, lag_hi] (estimator.py:50-57, 94).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -148,7 +149,23 @@ def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None
 
 MAX_P = 1 << 19  # largest single-launch transform of the NTT path
 TC_BLOCK = 4096  # template-search lags per block on the tensor-core path (one M=128, N=32 tile)
+TC_BLOCK_F4 = 8192  # same on the fp4 (e2m1) tensor-core mode: one M=128, N=64 tile (qx_tc.cu kF4Lags)
+TC_F4_MAX_CODE = 4  # qx_tc.cu kF4MaxCode: |codes| that are exact e2m1 values
 TC_MAX_K = 4608  # qx_tc.cu kTcMaxK: template length + 15 must fit
+
+
+def _mode(q) -> int:
+    """Kernel quantiser mode (qx_abi.cu: k == 1 -> two compares, else by kind)."""
+    return 0 if q.k == 1 else (1 if q.kind == "uniform" else 2)
+
+
+def tc_f4_block(nt: int, qx, qy) -> bool:
+    """True when template search runs on the fp4 tensor-core mode
+    (mirrors qx_tc.cu tc_f4_mode: codes |c| <= 4, exact f32 sums)."""
+    if os.environ.get("QX_TC_F4", "1").startswith("0"):
+        return False
+    return (qx.k <= TC_F4_MAX_CODE and qy.k <= TC_F4_MAX_CODE and _mode(qx) == _mode(qy)
+            and nt * qx.k * qy.k < (1 << 24))
 
 
 def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
@@ -178,7 +195,10 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
         # otherwise the largest block whose full correlogram fits one NTT
         tc = (path in ("auto", "direct", "tc") and nt + 15 <= TC_MAX_K and nt % 4 == 0
               and x.dtype == t.float32 and y.dtype == t.float32)
-        block = TC_BLOCK if tc else MAX_P - 2 * nt + 2  # NTT: nout = block + 2*nt - 2 fits one transform
+        if tc:
+            block = TC_BLOCK_F4 if tc_f4_block(nt, qx, qy) else TC_BLOCK
+        else:
+            block = MAX_P - 2 * nt + 2  # NTT: nout = block + 2*nt - 2 fits one transform
     if block < 1:
         raise ValueError("template too long for the block transform")
     nfull, rem = divmod(nvalid, block)

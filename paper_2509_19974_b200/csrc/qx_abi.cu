@@ -502,7 +502,7 @@ qx_status qx_xcorr_full(qx_context* ctx, const qx_signals* x, const qx_signals* 
 }
 
 static const char* kKindNames[QX_PROFILE_KINDS] = {"ntt_pass1", "ntt_pass2", "ntt_pass3", "crt_combine",
-                                                    "quantize", "direct", "other", ""};
+                                                    "quantize", "direct", "other", "direct_f4"};
 
 const char* qx_profile_kind_name(int kind)
 {

@@ -65,7 +65,7 @@ struct NttTables {
 
 // Optional per-launch accounting (qx_profile_begin/end): counts every kernel
 // launch and, when timed, brackets it with CUDA events on its stream.
-enum KernelKind : int { KK_PASS1 = 0, KK_PASS2, KK_PASS3, KK_COMBINE, KK_QUANT, KK_DIRECT, KK_OTHER, KK_N };
+enum KernelKind : int { KK_PASS1 = 0, KK_PASS2, KK_PASS3, KK_COMBINE, KK_QUANT, KK_DIRECT, KK_OTHER, KK_DIRECT_F4, KK_N };
 struct Profiler {
     bool on = false, timed = false;
     long long launches = 0;

@@ -32,7 +32,9 @@
 // accumulator (tcgen05.ld -> argmax), write the qx_result and release the
 // aux slot (tfree[aux]).  A data slot is reused as soon as its MMA chain
 // completes, so the epilogue is off the builders' critical path.
+#include <cfloat>
 #include <climits>
+#include <cmath>
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
@@ -47,7 +49,8 @@ constexpr int kTcMmaWarp = 16;                   // MMA issuer
 constexpr int kTcLagWarp0 = 17, kTcLagWarps = 3;  // extra-lag dot products (warps 17-19)
 // builders + MMA warp + lag warps meet at the per-pair hand-off barrier
 constexpr int kTcHandoff = kTcThreads + 32 + 32 * kTcLagWarps;
-constexpr int kTcTotalThreads = 24 * 32;         // + warp 16 (MMA), warps 20-23 (epilogue)
+constexpr int kTcMergeWarp = 24;                 // per-pair merge + result record
+constexpr int kTcTotalThreads = 25 * 32;         // + warp 16 (MMA), warps 20-23 (epilogue), 24 (merge)
 constexpr int kTcLags = 2048;      // lags per M=128 tile (M=64: 1024)
 constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
 constexpr int kTcMaxTiles = 2;     // lag tiles per pair
@@ -65,6 +68,20 @@ constexpr int kTcBLbo32 = 528;
 constexpr int kTcBSlot = kTcBLbo * (kTcMaxK / 16);
 constexpr int kTcBBytes = 2 * kTcBSlot;
 static_assert(kTcBLbo32 * (kTcMaxK / 16) <= kTcBBytes, "pitch-32 B must fit the two pitch-16 slots");
+// shared-template fp4 mode (kind::mxf4, e2m1 codes, every scale 2^0): codes
+// |c| <= 4 are exact e2m1 values and every partial sum is an integer below
+// 2^24, so the f32 accumulator holds the exact correlation (tools/tc_fp4.cu:
+// 0 mismatches, 68 cycles per M128 N64 K64 MMA vs 40 for the i8 M128 N32
+// K32 one: 2.35x the lags x samples per cycle).  Samples are nibbles (sample
+// 2i in the low nibble of byte i), so the 32-B SW32 Hankel row pitch is 64
+// samples: 64 template copies (N = 64), one M=128 tile = 8192 lags.
+constexpr int kF4Pitch = 64;
+constexpr int kF4Lbo = 1040;                    // B K-chunk (32 samples = 16 B) stride: 65 16-B units (odd)
+constexpr int kF4Lags = 128 * kF4Pitch;         // 8192
+constexpr int kF4MaxCode = 4;                   // |code| bound of the e2m1 mode
+constexpr int kF4Sf = 256;                      // TMEM column of the (constant) scale factors
+constexpr int kTcFastNY4 = 8 * 3 * kTcThreads;  // fp4 mode: y rows up to 12288 samples (3 x 8 per thread)
+static_assert(kF4Lbo * (kTcMaxK / 32 + 2) <= kTcBBytes, "fp4 B must fit the B buffer");
 
 // y code word wi of a slot: pitch 32 stores the buffer through the 32-byte
 // swizzle (byte bit 4 ^= bit 7, i.e. word bit 2 ^= bit 5) so that a SW32
@@ -149,6 +166,55 @@ __device__ __forceinline__ void mma_i8_warp4(uint32_t tmem_d, uint32_t alo, uint
         "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "n"(BINC), "n"(2 * BINC), "n"(3 * BINC));
 }
 
+// instruction descriptor: kind::mxf4 block32, A = B = E2M1 (1), scale UE8M0 (bit 23), K = 64
+constexpr uint32_t tc_idesc_f4(int M, int N)
+{
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_f4_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                            uint32_t accumulate, uint32_t sf)
+{
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n}" ::"r"(
+            tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
+}
+
+// four fp4 MMAs on consecutive K steps (64 samples = 32 B of A, two B chunks)
+template <int BINC>
+__device__ __forceinline__ void mma_f4_warp4(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
+                                             uint32_t idesc, uint32_t sf)
+{
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .b32 t;\n\t"
+        "mov.b64 a0, {%1, %2};\n\tadd.u32 t, %1, 2;\n\tmov.b64 a1, {t, %2};\n\t"
+        "add.u32 t, %1, 4;\n\tmov.b64 a2, {t, %2};\n\tadd.u32 t, %1, 6;\n\tmov.b64 a3, {t, %2};\n\t"
+        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, %7;\n\tmov.b64 b1, {t, %4};\n\t"
+        "add.u32 t, %3, %8;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, %9;\n\tmov.b64 b3, {t, %4};\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a0, b0, %5, [%6], [%6], 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a1, b1, %5, [%6], [%6], 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a2, b2, %5, [%6], [%6], 1;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a3, b3, %5, [%6], [%6], 1;\n}" ::"r"(tmem_d),
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(sf), "n"(BINC), "n"(2 * BINC), "n"(3 * BINC));
+}
+
+// four int8 codes in [-4, 4] (bytes of w) -> four e2m1 nibbles (16 bits,
+// code i at bits 4i): |c| -> {0, 2, 4, 5, 6} = |c| <= 2 ? 2|c| : |c| + 2,
+// sign -> bit 3; byte-SIMD, no per-sample branches
+__device__ __forceinline__ uint32_t tc_nib4(uint32_t w)
+{
+    const uint32_t a = __vabs4(w);
+    const uint32_t big = __vcmpgtu4(a, 0x02020202u);
+    const uint32_t m = (big & (a + 0x02020202u)) | (~big & (a << 1));
+    const uint32_t n = m | ((w & 0x80808080u) >> 4);
+    return __byte_perm(n | (n >> 4), 0u, 0x4420);
+}
+
 __device__ __forceinline__ void mma_commit_warp(uint64_t* bar)
 {
     asm volatile(
@@ -168,6 +234,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int (&v)[16])
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// 32 accumulator columns of this warp's lane quarter; completion by tmem_wait_ld()
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int* v)
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 struct TcArgs {
     OperandDesc op[2];       // x (template side, B), y (A)
     unsigned long long* stats;
@@ -181,7 +261,8 @@ struct TcArgs {
     int K;                   // padded K (multiple of 32)
     int fast;                // float32, n <= 4096, aligned rows, L0 % 4 == 0
     int shared_x;            // fast path with x row stride 0 (template search): x built once per CTA
-    int pitch;               // Hankel row pitch / N: 16 (per-pair B), 32 (shared template, SW32 A)
+    int pitch;               // Hankel row pitch / N: 16 (per-pair B), 32 (shared template, SW32 A),
+                             // 64 (shared template, fp4 nibbles, SW32 A)
     int debug;               // QX_TC_TIMING builds only: 1 = skip MMAs, 2 = skip builds
     int64_t batch;
 };
@@ -194,7 +275,8 @@ struct TcSmem {
     alignas(16) int8_t xl[2][kTcMaxK + 96];   // linear x codes after kTcXPad zero bytes
     double thr[2][kMaxThr];
     uint64_t mdone[kTcAux];  // MMA chain of aux slot complete (tcgen05.commit)
-    uint64_t tfree[kTcAux];  // epilogue finished with aux slot (128 arrivals)
+    uint64_t tfree[kTcAux];  // aux slot free again: TMEM drained, records read (merge warp, 32 arrivals)
+    uint64_t edone[kTcAux];  // epilogue warps' records of the aux slot written (4 arrivals)
     // per-builder-warp partials (no atomics): ssx, nzx, ssy, nzy, flags
     unsigned long long wst[kTcAux][kTcThreads / 32][5];
     int wxs[kTcAux][kTcLagWarps][kTcMaxExtra];     // extra-lag sums, one record per lag warp
@@ -219,6 +301,10 @@ __device__ __forceinline__ void tc_wait_mdone(TcSmem& S, int j)
 __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 {
     mbar_wait(&S.tfree[j & 3], (uint32_t)((j >> 2) & 1));
+}
+__device__ __forceinline__ void tc_wait_edone(TcSmem& S, int j)
+{
+    mbar_wait(&S.edone[j & 3], (uint32_t)((j >> 2) & 1));
 }
 __device__ __forceinline__ void tc_wait_xdone(TcSmem& S, int j)
 {
@@ -355,13 +441,18 @@ constexpr int kTcFastNY = 4 * 4 * kTcThreads;  // shared-x mode: y rows up to 81
 
 // per-thread float4s of one pair (loaded one pair ahead): both rows, or in
 // shared-x mode only the y row (the template is built once per CTA)
-template <bool SX>
+// MODE: 0 per-pair B, 1 shared template (i8), 2 shared template (fp4)
+template <int MODE>
 struct TcRegs {
     float4 x[2], y[2];
 };
 template <>
-struct TcRegs<true> {
+struct TcRegs<1> {
     float4 y[4];
+};
+template <>
+struct TcRegs<2> {
+    float4 y[6];  // samples 8(t + 512g) .. +8 in y[2g], y[2g + 1]
 };
 
 // float4 #i of a row of n floats (the tail float4 of an n % 4 != 0 row by
@@ -378,12 +469,19 @@ __device__ __forceinline__ float4 tc_ld4(const float* row, int i, int n)
     return v;
 }
 
-template <bool SX>
-__device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<SX>& r)
+template <int MODE>
+__device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<MODE>& r)
 {
     const float* ys = reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld;
     const int ny = (int)a.op[1].n;
-    if constexpr (SX) {
+    if constexpr (MODE == 2) {
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            const int i = 2 * ((int)threadIdx.x + g * kTcThreads);
+            r.y[2 * g] = tc_ld4(ys, i, ny);
+            r.y[2 * g + 1] = tc_ld4(ys, i + 1, ny);
+        }
+    } else if constexpr (MODE == 1) {
 #pragma unroll
         for (int h = 0; h < 4; ++h) r.y[h] = tc_ld4(ys, threadIdx.x + h * kTcThreads, ny);
     } else {
@@ -562,7 +660,29 @@ __device__ __forceinline__ void tc_zero_margins(const TcArgs& a, TcSmem& S, int 
 
 // shared-x mode prologue: the template's codes (slot 0), its 16 shifted
 // copies (B slot 0) and statistics (S.xst), once per CTA
-template <int QM>
+// fp4 mode: the template's 64 nibble-shifted copies from the linear nibble
+// buffer S.xl[1] (sample m at nibble 64 + m): chunk (kc, r) = x[32kc - r,
+// +32) (16 B) at kc*kF4Lbo + (r/8)*128 + (r%8)*16 (LBO kF4Lbo, SBO 128)
+__device__ __forceinline__ void tc_build_copies_f4(const TcArgs& a, TcSmem& S)
+{
+    const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[1]);
+    uint4* b4 = reinterpret_cast<uint4*>(S.b);
+    const int nchunk = a.K / 32;
+    for (int i = threadIdx.x; i < nchunk * kF4Pitch; i += kTcThreads) {
+        const int r = i & (kF4Pitch - 1), kc = i / kF4Pitch;
+        const int s0 = 32 * kc - r + 64;  // nibble of x[32kc - r]
+        const int w0 = s0 >> 3, sh = (s0 & 7) * 4;
+        const uint32_t w[5] = {xw[w0], xw[w0 + 1], xw[w0 + 2], xw[w0 + 3], xw[w0 + 4]};
+        uint4 v;
+        v.x = __funnelshift_r(w[0], w[1], sh);
+        v.y = __funnelshift_r(w[1], w[2], sh);
+        v.z = __funnelshift_r(w[2], w[3], sh);
+        v.w = __funnelshift_r(w[3], w[4], sh);
+        b4[kc * (kF4Lbo / 16) + (r >> 3) * 8 + (r & 7)] = v;
+    }
+}
+
+template <int QM, bool F4 = false>
 __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
 {
     const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
@@ -580,6 +700,11 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
     const int X = (a.K + 96) / 4;
     for (int i = threadIdx.x; i < X; i += kTcThreads)
         if (i < XP || i >= XP + nx4) xw[i] = 0;
+    if constexpr (F4) {
+        // nibble buffer: zero words [0, K/8 + 24) (64-sample front pad, the copies read up to K/8 + 12)
+        uint32_t* xn = reinterpret_cast<uint32_t*>(S.xl[1]);
+        for (int i = threadIdx.x; i < a.K / 8 + 24; i += kTcThreads) xn[i] = 0;
+    }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const int i = threadIdx.x + h * kTcThreads;
@@ -595,15 +720,55 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
         atomicAdd(&S.xst[1], nz);
         atomicOr(&S.xst[2], fl);
     }
-    tc_build_copies<32>(a, S, 0, 0);
+    if constexpr (F4) {
+        uint16_t* xh = reinterpret_cast<uint16_t*>(S.xl[1]);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int i = threadIdx.x + h * kTcThreads;
+            if (i < nx4) xh[16 + i] = (uint16_t)tc_nib4(w[h]);  // samples 4i.. at nibble 64 + 4i
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");
+        tc_build_copies_f4(a, S);
+    } else {
+        tc_build_copies<32>(a, S, 0, 0);
+    }
     asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");  // xst complete
+}
+
+// fp4 mode, one pair: the y row (<= 12288 samples, 3 x 8 per thread) as
+// e2m1 nibbles into the swizzled buffer (8 samples per word); the slot is
+// zeroed on its first use, so samples past the row stay code 0
+template <int QM>
+__device__ void tc_build_tmpl4(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<2>& r, bool first)
+{
+    const float* thry = reinterpret_cast<const float*>(S.thr[1]);
+    const int ny = (int)a.op[1].n;
+    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
+    if (first) {
+        for (int i = threadIdx.x; i < kTcYStride / 4; i += kTcThreads) yw[i] = 0;
+        asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");
+    }
+    uint32_t w[6];
+    unsigned fl = 0, ssy = 0, nzy = 0;
+    tc_quant_words<QM, 6>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
+    const int yoff = (int)(-a.L0) >> 3, Y = (a.ylen + 7) / 8;
+#pragma unroll
+    for (int g = 0; g < 3; ++g) {
+        const int i = threadIdx.x + g * kTcThreads;
+        tc_word_stats(w[2 * g], ssy, nzy);
+        tc_word_stats(w[2 * g + 1], ssy, nzy);
+        const int wi = yoff + i;
+        if (8 * i < ny && wi >= 0 && wi < Y) yw[ysw<32>(wi)] = tc_nib4(w[2 * g]) | (tc_nib4(w[2 * g + 1]) << 16);
+    }
+    const bool w0 = threadIdx.x == 0;
+    tc_aux_finish<2>(S, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy, fl | (w0 ? S.xst[2] : 0u));
 }
 
 // shared-x mode, one pair: only the y row (<= 8192 samples, 4 float4 per
 // thread) into the swizzled pitch-32 buffer; the template statistics ride in
 // builder warp 0's record
 template <int QM>
-__device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<true>& r, bool first)
+__device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<1>& r, bool first)
 {
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
     const int ny = (int)a.op[1].n, ny4 = (ny + 3) >> 2;
@@ -625,7 +790,7 @@ __device__ void tc_build_tmpl(const TcArgs& a, TcSmem& S, int s, int u, const Tc
 }
 
 template <int QM>
-__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<false>& r, bool first)
+__device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<0>& r, bool first)
 {
     const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
     const float* thry = reinterpret_cast<const float*>(S.thr[1]);
@@ -730,8 +895,8 @@ __device__ __forceinline__ void best_add(long long& bv, long long& bt, long long
     else if (v == bv) { bt = min(bt, t); bc += c; }
 }
 
-template <int PITCH>
-__device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
+template <int PITCH, bool F4 = false>
+__device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u)
 {
     const int lane = threadIdx.x & 31;
     const int q = (threadIdx.x >> 5) - kEpiWarp0;  // 0..3 = TMEM lane quarter
@@ -751,6 +916,57 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
 #else
 #define TC_EMARK(i)
 #endif
+    if constexpr (F4) {
+        // f32 accumulators holding exact integers (|value| < 2^24): the same
+        // scan in float (-FLT_MAX below every value, -inf out of window), one
+        // conversion per thread at the end; a tile fully inside the window
+        // (every full template-search block) skips the masks
+        float fv = -FLT_MAX;
+        const bool full = jlo <= 0 && jhi >= tl - 1;
+        const uint32_t taddr = S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * kF4Pitch);
+        if (full) {
+            // the thread's 64 lags j = 64*row + c: max by a tree (no serial
+            // compare chain), then the tie set as a 64-bit mask of c: count =
+            // popc, smallest lag = first set bit
+            int v[64];
+            tmem_ld32(taddr, v);
+            tmem_ld32(taddr + 32, v + 32);
+            tmem_wait_ld();
+            float m[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) m[i] = fmaxf(__int_as_float(v[i]), __int_as_float(v[i + 32]));
+#pragma unroll
+            for (int w = 16; w; w >>= 1)
+#pragma unroll
+                for (int i = 0; i < w; ++i) m[i] = fmaxf(m[i], m[i + w]);
+            const float mx = m[0];
+            unsigned lo = 0, hi = 0;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                lo |= (__int_as_float(v[i]) == mx ? 1u : 0u) << i;
+                hi |= (__int_as_float(v[i + 32]) == mx ? 1u : 0u) << i;
+            }
+            bc = __popc(lo) + __popc(hi);
+            bj = PITCH * row + (lo ? __ffs(lo) - 1 : 31 + __ffs(hi));
+            fv = mx;
+        } else
+#pragma unroll
+        for (int c0 = 0; c0 < PITCH; c0 += 16) {
+            int v[16];
+            tmem_ld16(taddr + c0, v);
+            const int j0 = PITCH * row + c0;
+#pragma unroll
+            for (int r = 0; r < 16; ++r) {
+                const int j = j0 + r;
+                const float val = (full || (j >= jlo && j <= jhi)) ? __int_as_float(v[r]) : -INFINITY;
+                const bool gt = val > fv, eq = val == fv;
+                bj = gt ? j : bj;
+                bc = gt ? 1 : bc + (int)eq;
+                fv = gt ? val : fv;
+            }
+        }
+        bv = fv == -FLT_MAX ? INT_MIN + 1 : __float2int_rn(fv);
+    } else
     for (int tile = 0; tile < a.ntiles; ++tile) {
 #pragma unroll
         for (int c0 = 0; c0 < PITCH; c0 += 16) {
@@ -783,31 +999,53 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
         bv = mv;
     }
     TC_EMARK(14);
-    // per-aux-slot records: the epilogue warps are never a pair apart (the
-    // barrier below), so the slot written here is not being read
+    // per-aux-slot records, read by the merge warp before it frees the slot
+    // (the next write of slot u follows mdone(it + 4), after tfree(it))
     if (lane == 0) {
         S.best[u][q][0] = bv;
         S.best[u][q][1] = bj;
         S.best[u][q][2] = bc;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.edone[u])) : "memory");
     }
-    asm volatile("bar.sync 4, 128;" ::: "memory");
-    if (q == 0) {
+    TC_EMARK(15);
+}
+
+// merge warp: the pair's four epilogue records, the lag warps' extra-lag
+// sums and statistics -> the qx_result; frees the aux slot (tfree) as soon as
+// the records are in registers, so neither the epilogue warps nor the MMA
+// warp wait for the merge and the result stores
+template <int PITCH>
+__device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t pair)
+{
+    const int lane = threadIdx.x & 31;
+    const int tl = PITCH * a.M;
+    const int64_t tbase = a.L0 + a.op[0].n - 1;
+    const int jlo = (int)(a.am.t_lo - tbase), jhi = (int)(a.am.t_hi - tbase);
+    {
         const unsigned long long* fs = S.fst[u];  // summed by the lag warps
         const unsigned long long ssx = fs[0], nzx = fs[1], ssy = fs[2], nzy = fs[3], fls = fs[4];
         // the four warp records by REDUX (lanes 0..3)
         const int wv = lane < 4 ? S.best[u][lane][0] : INT_MIN;
+        const int wj = lane < 4 ? S.best[u][lane][1] : INT_MAX;
+        const int wc = lane < 4 ? S.best[u][lane][2] : 0;
+        int xs[kTcMaxExtra];
+#pragma unroll
+        for (int e = 0; e < kTcMaxExtra; ++e)
+            xs[e] = e < a.extra ? __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0) : 0;
+        // every record of slot u is in registers: free the slot
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[u])) : "memory");
         const int mv = __reduce_max_sync(0xffffffffu, wv);
         const bool at = lane < 4 && wv == mv;
-        const int mj = __reduce_min_sync(0xffffffffu, at ? S.best[u][lane][1] : INT_MAX);
-        const int mc = __reduce_add_sync(0xffffffffu, at ? S.best[u][lane][2] : 0);
+        const int mj = __reduce_min_sync(0xffffffffu, at ? wj : INT_MAX);
+        const int mc = __reduce_add_sync(0xffffffffu, at ? wc : 0);
         long long v0 = LLONG_MIN, t0 = LLONG_MAX, c0 = 0;
         if (mc) best_add(v0, t0, c0, mv, tbase + mj, mc);
 
-        for (int e = 0; e < a.extra; ++e) {
-            const int xs = __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0);
+#pragma unroll
+        for (int e = 0; e < kTcMaxExtra; ++e) {
             const int j = a.ntiles * tl + e;
-            if (j < jlo || j > jhi) continue;
-            best_add(v0, t0, c0, xs, tbase + j, 1);
+            if (e >= a.extra || j < jlo || j > jhi) continue;
+            best_add(v0, t0, c0, xs[e], tbase + j, 1);
         }
         int flags = 0;
         if (nzx == 0) flags |= 1;
@@ -819,7 +1057,6 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
           : lane == 4 ? (long long)ssy : lane == 5 ? (long long)nzx : lane == 6 ? (long long)nzy : f;
         if (lane < 8) reinterpret_cast<long long*>(a.am.results)[pair * 8 + lane] = f;
     }
-    TC_EMARK(15);
 }
 
 #ifdef QX_TC_TIMING
@@ -830,9 +1067,11 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u, int64_t pair)
 #define TC_ACC(i) ((void)0)
 #endif
 
-template <typename T, int QM, bool SX>
+template <typename T, int QM, int MODE>
 __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
+    constexpr bool SX = MODE != 0, F4 = MODE == 2;
+    constexpr uint32_t kTmemCols = F4 ? 512 : 128;  // fp4: 4 x 64 accumulator columns + scale factors
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     TcSmem& S = *reinterpret_cast<TcSmem*>(tc_smem_raw);
     // warp index through a shuffle: provably warp-uniform, so the role
@@ -844,7 +1083,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     }
     if (threadIdx.x < kTcAux) {
         mbar_init(&S.mdone[threadIdx.x], 1);
-        mbar_init(&S.tfree[threadIdx.x], 128);
+        mbar_init(&S.tfree[threadIdx.x], 32);
+        mbar_init(&S.edone[threadIdx.x], 4);
         mbar_init(&S.xdone[threadIdx.x], 32 * kTcLagWarps);
     }
 #ifdef QX_TC_TIMING
@@ -852,12 +1092,32 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
 #endif
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&S.tmem_base)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                     "n"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if constexpr (F4) {
+        // scale factors: 32 columns of 0x7f bytes (ue8m0 2^0) in every lane,
+        // written by the epilogue warps (warp w reaches lanes 32*(w%4)..)
+        if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+            const uint32_t t = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kF4Sf;
+            const uint32_t v = 0x7f7f7f7fu;
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(t),
+                "r"(v));
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                    t + 16),
+                "r"(v));
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
 
     // Dependencies (iteration it: data slot it & 1, aux slot it & 3):
     //   build(it)    after MMA(it-2) [data slot] and epilogue(it-4) [aux slot]
@@ -883,21 +1143,22 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         if constexpr (std::is_same<T, float>::value) fast = a.fast;
         if (fast) {
             if constexpr (std::is_same<T, float>::value) {
-                TcRegs<SX> cur, nxt;
-                if (npairs) tc_fetch<SX>(a, blockIdx.x, cur);
+                TcRegs<MODE> cur, nxt;
+                if (npairs) tc_fetch<MODE>(a, blockIdx.x, cur);
                 if constexpr (SX) {
-                    if (npairs) tc_build_template<QM>(a, S);
+                    if (npairs) tc_build_template<QM, F4>(a, S);
                 }
                 for (int it = 0; it < npairs; ++it) {
                     const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-                    if (it + 1 < npairs) tc_fetch<SX>(a, pair + gridDim.x, nxt);
+                    if (it + 1 < npairs) tc_fetch<MODE>(a, pair + gridDim.x, nxt);
                     acquire(it);
                     TC_T0();
 #ifdef QX_TC_TIMING
                     if (!(a.debug & 2))
 #endif
                     {
-                        if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur, it < 2);
+                        if constexpr (F4) tc_build_tmpl4<QM>(a, S, it & 1, it & 3, cur, it < 2);
+                        else if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur, it < 2);
                         else tc_build_fast<QM>(a, S, it & 1, it & 3, cur, it < 2);
                     }
                     if (threadIdx.x == 0) TC_ACC(1);
@@ -932,10 +1193,36 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             TC_T0();
             // pitch 32 (shared template): one B buffer built once, SW32 A rows
-            constexpr int PITCH = SX ? 32 : 16, LBO = SX ? kTcBLbo32 : kTcBLbo, BINC = 2 * LBO / 16;
+            constexpr int PITCH = F4 ? kF4Pitch : SX ? 32 : 16;
+            constexpr int LBO = F4 ? kF4Lbo : SX ? kTcBLbo32 : kTcBLbo, BINC = 2 * LBO / 16;
             const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b + (SX ? 0 : s) * kTcBSlot);
             const uint64_t bd0 = smem_desc(ba, LBO, 128);
             const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
+            if constexpr (F4) {
+                // one M=128 x N=64 tile (8192 lags), K = 64 samples (32 B of A) per MMA
+                const uint32_t d = tbase + (uint32_t)(u * kF4Pitch), sf = tbase + kF4Sf;
+                const uint64_t ad0 = smem_desc(ya, 16, 256) | (6ull << 61);  // SWIZZLE_32B, 8 rows x 32 B
+                const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
+                uint32_t alo = (uint32_t)ad0, blo = (uint32_t)bd0;
+                const int nk4 = a.K / 64;
+#ifdef QX_TC_TIMING
+                if (!(a.debug & 1))
+#endif
+                {
+                    mma_f4_warp(d, ad0, bd0, a.idesc, 0, sf);
+                    int kk = 1;
+                    for (; kk + 4 <= nk4; kk += 4) {
+                        mma_f4_warp4<BINC>(d, alo + 2, ahi, blo + BINC, bhi, a.idesc, sf);
+                        alo += 8;
+                        blo += 4 * BINC;
+                    }
+                    for (; kk < nk4; ++kk) {
+                        alo += 2;
+                        blo += BINC;
+                        mma_f4_warp(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1, sf);
+                    }
+                }
+            } else
             for (int tile = 0; tile < a.ntiles; ++tile) {
 #ifdef QX_TC_TIMING
                 if (a.debug & 1) break;
@@ -972,21 +1259,26 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             if (warp == kTcLagWarp0) tc_final_stats(a, S, it & 3);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it & 3])) : "memory");
         }
-    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-        // ---- epilogue: TMEM -> argmax -> qx_result, then free the aux slot
+    } else if (warp == kTcMergeWarp) {
+        // ---- merge: records -> qx_result
         for (int it = 0; it < npairs; ++it) {
             const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
+            tc_wait_xdone(S, it);  // statistics and extra-lag records written
+            tc_wait_edone(S, it);  // epilogue records written
+            tc_merge<F4 ? kF4Pitch : SX ? 32 : 16>(a, S, it & 3, pair);
+        }
+    } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
+        // ---- epilogue: TMEM -> per-warp (max, smallest lag, count) records
+        for (int it = 0; it < npairs; ++it) {
             TC_T0();
             tc_wait_mdone(S, it);
-            tc_wait_xdone(S, it);  // extra-lag records written
             if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             {
                 TC_T0();
-                tc_epilogue<SX ? 32 : 16>(a, S, it & 3, pair);
+                tc_epilogue<F4 ? kF4Pitch : SX ? 32 : 16, F4>(a, S, it & 3);
                 if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(6);
             }
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[it & 3])) : "memory");
         }
     }
     // every MMA was waited on by the epilogue before TMEM is released
@@ -1004,16 +1296,32 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                "shfl %llu bars+merge %llu\n", S.tm[8] / npairs, S.tm[9] / npairs, S.tm[10] / npairs,
                S.tm[11] / npairs, S.tm[12] / npairs, S.tm[13] / npairs, S.tm[14] / npairs, S.tm[15] / npairs);
 #endif
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(S.tmem_base));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "n"(kTmemCols));
 }
 
-// eligibility: window of at most kTcMaxTiles*2048 lags, nx + 15 <= kTcMaxK,
-// |values| < 2^31 (nx * Kx * Ky), same input dtype and quantiser mode (float)
+// fp4 shared-template mode: float32 rows, x a stride-0 row of <= 4096
+// samples (template search), 16-B aligned rows, codes |c| <= 4 on both sides,
+// every sum exact in f32 (nx * Kx * Ky < 2^24), one 8192-lag tile starting
+// at a word boundary, y rows <= 12288 samples; QX_TC_F4=0 disables it
+static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
+{
+    const char* env = getenv("QX_TC_F4");
+    if (env && env[0] == '0') return false;
+    const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
+    return c.op[0].dtype == DT_F32 && c.op[1].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN &&
+           nx % 4 == 0 && (uintptr_t)c.op[0].data % 16 == 0 && (uintptr_t)c.op[1].data % 16 == 0 &&
+           c.op[1].ld % 4 == 0 && c.op[0].q.mode == c.op[1].q.mode && c.op[0].q.k <= kF4MaxCode &&
+           c.op[1].q.k <= kF4MaxCode && (double)nx * c.op[0].q.k * c.op[1].q.k < 16777216.0 && ny <= kTcFastNY4 &&
+           W <= kF4Lags && L0 % 8 == 0 && L0 <= 0;
+}
+
+// eligibility: window of at most kTcMaxTiles*2048 lags (fp4 mode: 8192),
+// nx + 15 <= kTcMaxK, |values| < 2^31 (nx * Kx * Ky), same input dtype and
+// quantiser mode (float)
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
 {
-    (void)ny;
     const int64_t W = c.am.t_hi - c.am.t_lo + 1;
-    if (W > (int64_t)kTcMaxTiles * kTcLags + kTcMaxExtra) return false;
+    if (W > (int64_t)kTcMaxTiles * kTcLags + kTcMaxExtra && !tc_f4_mode(c, nx, ny)) return false;
     if (nx + 15 > kTcMaxK) return false;
     if (c.op[0].dtype != c.op[1].dtype || c.op[0].dtype == DT_I64) return false;
     if (c.op[0].q.mode != c.op[1].q.mode) return false;
@@ -1022,19 +1330,19 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
     return true;
 }
 
-template <typename T, int QM, bool SX = false>
+template <typename T, int QM, int MODE = 0>
 static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
 {
     static bool attr = false;
     const size_t smem = sizeof(TcSmem);
     if (!attr) {
         cudaError_t e =
-            cudaFuncSetAttribute(k_tc_window<T, QM, SX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k_tc_window<T, QM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
     const int grid = (int)(a.batch < sms ? a.batch : sms);
-    k_tc_window<T, QM, SX><<<grid, kTcTotalThreads, smem, s>>>(a);
+    k_tc_window<T, QM, MODE><<<grid, kTcTotalThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1058,19 +1366,30 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     // template's 32 shifted copies are built once per CTA (pitch 32, one
     // M=128 tile of 4096 lags, y rows up to 8192 samples); otherwise per-pair
     // copies with pitch 16
-    a.shared_x = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
-                 ny <= kTcFastNY && aligned && W <= 4096 + kTcMaxExtra;
+    const bool sx = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
+                    aligned;
+    const bool f4 = tc_f4_mode(c, nx, ny);
+    a.shared_x = f4 || (sx && ny <= kTcFastNY && W <= 4096 + kTcMaxExtra);
     a.fast = a.shared_x || (c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 &&
                             ny % 4 == 0 && aligned && (c.batch == 1 || c.op[0].ld % 4 == 0));
-    a.pitch = a.shared_x ? 32 : 16;
+    a.pitch = f4 ? kF4Pitch : a.shared_x ? 32 : 16;
     // shape: pitch 16: one M=64 tile (1024 lags) when it covers the window up
-    // to the extra lags, else M=128 tiles (2048 lags each); pitch 32: M=128
+    // to the extra lags, else M=128 tiles (2048 lags each); pitch 32/64: M=128
     a.M = (a.pitch == 16 && W <= 1024 + kTcMaxExtra) ? 64 : 128;
     const int tl = a.pitch * a.M;
     a.ntiles = (int)((W - kTcMaxExtra + tl - 1) / tl);
     if (a.ntiles < 1) a.ntiles = 1;
     a.extra = (int)(W > (int64_t)a.ntiles * tl ? W - (int64_t)a.ntiles * tl : 0);
     a.idesc = tc_idesc(a.M, a.pitch);
+    // B copy r holds x at k = m + r: K covers nx + pitch - 1 (pitch 32 needs
+    // more than the pitch-16 default for templates with nx % 32 outside 1..17)
+    if (a.pitch == 32) a.K = (int)((nx + 31 + 31) / 32 * 32);
+    if (f4) {
+        a.K = (int)((nx + kF4Pitch - 1 + 63) / 64 * 64);
+        a.ntiles = 1;
+        a.extra = 0;
+        a.idesc = tc_idesc_f4(128, kF4Pitch);
+    }
     a.ylen = a.ntiles * tl + kTcMaxExtra + a.K;
 #ifdef QX_TC_TIMING
     if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
@@ -1078,13 +1397,18 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (c.prof) c.prof->pre(KK_DIRECT, s);
+    const int kind = f4 ? KK_DIRECT_F4 : KK_DIRECT;
+    if (c.prof) c.prof->pre(kind, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;
-    if (c.op[0].dtype == DT_F32 && a.shared_x) {
-        if (qm == QM_K1) e = launch_tc<float, QM_K1, true>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, true>(a, s, sms);
-        else e = launch_tc<float, QM_BSEARCH, true>(a, s, sms);
+    if (f4) {
+        if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
+        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
+        else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
+    } else if (c.op[0].dtype == DT_F32 && a.shared_x) {
+        if (qm == QM_K1) e = launch_tc<float, QM_K1, 1>(a, s, sms);
+        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 1>(a, s, sms);
+        else e = launch_tc<float, QM_BSEARCH, 1>(a, s, sms);
     } else if (c.op[0].dtype == DT_F32) {
         if (qm == QM_K1) e = launch_tc<float, QM_K1>(a, s, sms);
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM>(a, s, sms);
@@ -1094,7 +1418,7 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
         else if (qm == QM_UNIFORM) e = launch_tc<double, QM_UNIFORM>(a, s, sms);
         else e = launch_tc<double, QM_BSEARCH>(a, s, sms);
     }
-    if (c.prof) c.prof->post(KK_DIRECT, s);
+    if (c.prof) c.prof->post(kind, s);
     return e;
 }
 

@@ -411,6 +411,65 @@ def test_template_search_tensor_core_blocks(qx, oracle, golden):
         assert qx.template_search(t5, s5, qa, qb) == (case["peak"], case["lags"][0], len(case["lags"]))
 
 
+def test_template_search_fp4_mode(qx, oracle, monkeypatch):
+    """Template search on the fp4 (e2m1, kind::mxf4) tensor-core mode: codes
+    |c| <= 4 (sign, uniform k = 1..4), 8192-lag blocks; the profile proves the
+    fp4 kernel ran, and the summary equals the oracle's and the i8 mode's
+    (QX_TC_F4=0) on the same inputs, including a remainder block, short
+    templates and a k=4 worst case near the f32-exact bound."""
+    from paper_2509_19974_b200 import _native
+
+    rng = np.random.default_rng(23)
+    cases = [(4096, qx.sign()), (4096, qx.uniform(1, 0.8)), (2052, qx.uniform(4, 0.4)), (1000, qx.uniform(2, 0.5)),
+             (64, qx.uniform(3, 0.3)), (4, qx.sign()), (4096, qx.uniform(4, 0.05))]
+    for trial, (nt, q) in enumerate(cases):
+        ns = nt - 1 + 8192 * int(rng.integers(2, 5)) + int(rng.integers(0, 8192))
+        st = rng.laplace(size=ns).astype(np.float32)
+        off = int(rng.integers(0, ns - nt + 1))
+        tpl = st[off:off + nt].copy()
+        st = st + rng.normal(0, 0.7, ns).astype(np.float32)
+        monkeypatch.setenv("QX_TC_F4", "1")
+        with _native.profile(timed=False) as prof:
+            got = qx.template_search(tpl, st, q, q, stream_start=3)
+        assert prof.result.get("direct_f4", (0, 0))[0] >= 1, (trial, prof.result)
+        monkeypatch.setenv("QX_TC_F4", "0")
+        with _native.profile(timed=False) as prof:
+            i8 = qx.template_search(tpl, st, q, q, stream_start=3)
+        assert "direct_f4" not in prof.result or prof.result["direct_f4"][0] == 0, prof.result
+        u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
+        first = -(nt - 1)
+        m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, 0 - first, ns - nt - first))
+        assert got == i8 == (m, f + 3, n), (trial, got, i8, (m, f, n))
+
+
+@pytest.mark.parametrize("f4", ["0", "1"])
+def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
+    """Every block summary of the shared-template window modes (i8 pitch 32,
+    fp4 pitch 64) against the oracle, for templates whose length leaves the
+    shifted copies past the pitch-16 K (nt = 4, 8, 40, 1000, 2052: the copies
+    need K >= nt + pitch - 1)."""
+    import torch
+
+    monkeypatch.setenv("QX_TC_F4", f4)
+    block = 8192 if f4 == "1" else 4096
+    for seed, (nt, q) in enumerate([(4, qx.sign()), (8, qx.sign()), (40, qx.uniform(1, 0.8)),
+                                    (1000, qx.sign()), (2052, qx.uniform(1, 0.8))]):
+        rng = np.random.default_rng(seed)
+        ns = nt - 1 + block * 3 + 17
+        st = rng.laplace(size=ns).astype(np.float32)
+        tpl = st[100:100 + nt].copy()
+        st = st + rng.normal(0, 0.7, ns).astype(np.float32)
+        x, y = torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda()
+        nfull = (ns - nt + 1) // block
+        xr, yr = x.as_strided((nfull, nt), (0, 1)), y.as_strided((nfull, block + nt - 1), (block, 1))
+        r = qx.estimate_batch(xr, yr, q, q, lag_lo=0, lag_hi=block - 1).numpy()
+        u = oracle.quantize(q, tpl)
+        for b in range(nfull):
+            v = oracle.quantize(q, st[b * block:b * block + block + nt - 1])
+            want = oracle.argmax(oracle.xcorr_bf(u, v, nt - 1, nt - 1 + block - 1))
+            assert (int(r["value"][b]), int(r["lag"][b]), int(r["ties"][b])) == want, (nt, b, f4)
+
+
 def test_large_transform_path(qx, oracle):
     """P > 2^19 (outer radix-2^m pass around 2^19 sub-transforms, config 4's
     path): full correlograms and windowed peaks equal the oracle's KS."""

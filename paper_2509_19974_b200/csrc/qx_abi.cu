@@ -43,6 +43,16 @@ struct Arena {
     size_t size = 0;
 };
 
+// A compute lane of the sweep entry point: its own stream and scratch, so
+// the quantiser pairs of one staged chunk run concurrently (their launches
+// fill each other's tail waves).
+struct Lane {
+    Arena scratch, counters;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t done = nullptr;
+};
+constexpr int kMaxLanes = 8;
+
 struct qx_context {
     int device = 0;
     std::recursive_mutex mu;
@@ -55,6 +65,7 @@ struct qx_context {
     cudaStream_t host_stream = nullptr;
     cudaStream_t copy_stream = nullptr;   // H2D of the sweep entry point
     std::vector<cudaEvent_t> chunk_ev;    // per staged chunk (lazily created)
+    Lane lanes[kMaxLanes];                // sweep compute lanes (lazily created)
     Profiler prof;
     std::string last_error;
 };
@@ -137,6 +148,12 @@ void qx_context_destroy(qx_context* c)
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (cudaEvent_t ev : c->chunk_ev) cudaEventDestroy(ev);
+    for (Lane& l : c->lanes) {
+        for (Arena* a : {&l.scratch, &l.counters})
+            if (a->ptr) cudaFree(a->ptr);
+        if (l.stream) cudaStreamDestroy(l.stream);
+        if (l.done) cudaEventDestroy(l.done);
+    }
     delete c;
 }
 
@@ -279,8 +296,11 @@ struct Prepared {
 
 static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                          const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
-                         bool argmax, qx_path path, Prepared* out)
+                         bool argmax, qx_path path, Prepared* out, Arena* scratch = nullptr,
+                         Arena* counters = nullptr)
 {
+    Arena& scr = scratch ? *scratch : ctx->scratch;
+    Arena& cnt = counters ? *counters : ctx->counters;
     qx_status st;
     if (batch < 1) return fail(ctx, QX_ERR_INVALID, "batch must be >= 1");
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
@@ -337,9 +357,9 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     out->path = (path == QX_PATH_DIRECT || (path == QX_PATH_AUTO && tc_ok)) ? QX_PATH_DIRECT : QX_PATH_NTT;
     if (out->path == QX_PATH_DIRECT) {
         const size_t sb = (size_t)batch * 8 * 8;
-        cudaError_t e = arena_reserve(ctx->scratch, sb + 256, false);
+        cudaError_t e = arena_reserve(scr, sb + 256, false);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
-        c.stats = (unsigned long long*)ctx->scratch.ptr;
+        c.stats = (unsigned long long*)scr.ptr;
         c.prof = &ctx->prof;
         return QX_OK;
     }
@@ -389,11 +409,11 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     const size_t sb = (size_t)batch * 8 * 8;
     c.am.pstride = large ? kMaxPartialsLarge : kMaxPartials;
     const size_t pb = argmax ? (size_t)batch * c.am.pstride * 3 * 8 : 0;
-    cudaError_t e = arena_reserve(ctx->scratch, wb + sb + pb + 256, false);
+    cudaError_t e = arena_reserve(scr, wb + sb + pb + 256, false);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
-    e = arena_reserve(ctx->counters, (size_t)batch * 4, true);
+    e = arena_reserve(cnt, (size_t)batch * 4, true);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "counters");
-    char* base = (char*)ctx->scratch.ptr;
+    char* base = (char*)scr.ptr;
     uint32_t* w = (uint32_t*)base;
     c.Y = w;
     w += (size_t)chunk * 2 * P;
@@ -408,7 +428,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     c.R = np > 1 ? w : nullptr;
     c.stats = (unsigned long long*)(base + wb);
     c.am.partials = argmax ? (long long*)(base + wb + sb) : nullptr;
-    c.am.counters = (int*)ctx->counters.ptr;
+    c.am.counters = (int*)cnt.ptr;
     c.prof = &ctx->prof;
     return QX_OK;
 }
@@ -458,6 +478,27 @@ qx_status qx_quantize(qx_context* ctx, const qx_quantizer* q, const qx_signals* 
     }
     return QX_OK;
 }
+
+}  // extern "C"
+
+// qx_estimate_batch on explicit scratch arenas (the sweep's compute lanes)
+static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                                   const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
+                                   qx_path path, qx_result* results, void* stream, Arena* scratch, Arena* counters)
+{
+    Prepared pr;
+    qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr, scratch, counters);
+    if (st != QX_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    pr.call.am.results = results;
+    cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
+    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    return QX_OK;
+}
+
+extern "C" {
 
 qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                             const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
@@ -624,11 +665,38 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // stream works on the previous chunk; overlapping / repeated rows are
     // staged whole (one chunk)
     const bool disjoint = x->ld >= x->n && y->ld >= y->n;
-    // >= 16 pairs per chunk keeps the transform launches efficient (8-pair
-    // chunks cost more in compute than the extra copy overlap gains)
-    int64_t nchunk = disjoint ? std::max<int64_t>(1, std::min<int64_t>(batch / 16, 4)) : 1;
+    // quantiser pairs run on up to 4 compute lanes (streams with their own
+    // scratch), so a chunk's launches overlap and small chunks stay efficient
+    int nl = (int)std::min<int64_t>(nq, 4);
+    if (const char* ev = getenv("QX_SWEEP_LANES")) nl = (int)std::max<int64_t>(1, std::min<int64_t>(nq, atoll(ev)));
+    nl = std::min(nl, kMaxLanes);
+    // chunks of >= 8 pairs (>= 16 on one lane: smaller launches lose their
+    // tail waves), at most 8
+    int64_t nchunk = disjoint ? std::max<int64_t>(1, std::min<int64_t>(batch / (nl > 1 ? 8 : 16), nl > 1 ? 8 : 4)) : 1;
     if (const char* ev = getenv("QX_SWEEP_CHUNKS")) nchunk = std::max<int64_t>(1, std::min<int64_t>(batch, atoll(ev)));
+    for (int l = 0; l < nl; ++l) {
+        Lane& L = ctx->lanes[l];
+        if (!L.stream && (e = cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(ctx, e, "lane stream");
+        if (!L.done && (e = cudaEventCreateWithFlags(&L.done, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(ctx, e, "lane event");
+    }
     const int64_t per = (batch + nchunk - 1) / nchunk;
+    // chunk bounds: with lanes and >= 4 chunks the first and last chunks are
+    // half size (less exposed copy before the first launch, shorter compute
+    // tail after the last copy)
+    std::vector<std::pair<int64_t, int64_t>> chunks;  // (first pair, pairs)
+    {
+        const bool halves = nl > 1 && nchunk >= 4 && per >= 2 && !getenv("QX_SWEEP_EVEN");
+        int64_t b0 = 0;
+        while (b0 < batch) {
+            int64_t nb = (halves && b0 == 0) ? per / 2 : per;
+            nb = std::min(nb, batch - b0);
+            chunks.emplace_back(b0, nb);
+            b0 += nb;
+        }
+        nchunk = (int64_t)chunks.size();
+    }
     while ((int64_t)ctx->chunk_ev.size() < nchunk) {
         cudaEvent_t ev;
         if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return cuda_fail(ctx, e, "event");
@@ -637,24 +705,30 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // the previous call's compute must be done with the staging buffer
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cuda_fail(ctx, e, "sync");
     for (int64_t c = 0; c < nchunk; ++c) {
-        const int64_t b0 = c * per, nb = std::min(per, batch - b0);
-        if (nb <= 0) break;
+        const int64_t b0 = chunks[c].first, nb = chunks[c].second;
         const size_t xo = (size_t)(b0 * x->ld) * ex, yo = (size_t)(b0 * y->ld) * ey;
         const size_t xn = disjoint ? (size_t)((nb - 1) * x->ld + x->n) * ex : xb;
         const size_t yn = disjoint ? (size_t)((nb - 1) * y->ld + y->n) * ey : yb;
         e = cudaMemcpyAsync(d + xo, (const char*)x->data + xo, xn, cudaMemcpyHostToDevice, cs);
         if (e == cudaSuccess) e = cudaMemcpyAsync(d + xa + yo, (const char*)y->data + yo, yn, cudaMemcpyHostToDevice, cs);
         if (e == cudaSuccess) e = cudaEventRecord(ctx->chunk_ev[c], cs);
-        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->chunk_ev[c], 0);
+        for (int l = 0; l < nl && e == cudaSuccess; ++l) e = cudaStreamWaitEvent(ctx->lanes[l].stream, ctx->chunk_ev[c], 0);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D");
         qx_signals xd = *x, yd = *y;
         xd.data = d + xo;
         yd.data = d + xa + yo;
         for (int64_t q = 0; q < nq; ++q) {
-            st = qx_estimate_batch(ctx, &xd, &yd, nb, &qxs[q], &qys[q], lag_lo, lag_hi, path, rd + q * batch + b0, s);
+            Lane& L = ctx->lanes[q % nl];
+            st = estimate_batch_on(ctx, &xd, &yd, nb, &qxs[q], &qys[q], lag_lo, lag_hi, path, rd + q * batch + b0,
+                                   L.stream, &L.scratch, &L.counters);
             if (st != QX_OK) return st;
         }
     }
+    for (int l = 0; l < nl && e == cudaSuccess; ++l) {
+        e = cudaEventRecord(ctx->lanes[l].done, ctx->lanes[l].stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s, ctx->lanes[l].done, 0);
+    }
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "lane join");
     e = cudaMemcpyAsync(results, rd, rb, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");

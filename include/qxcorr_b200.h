@@ -152,6 +152,25 @@ qx_status qx_estimate_sweep_host(qx_context *ctx, const qx_signals *x, const qx_
                                  const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
                                  qx_path path, qx_result *results);
 
+/* Template search (BASELINE config 5): estimate(x=template, y=stream) of
+ * estimator.py:60-94 restricted to the VALID lags (template fully inside the
+ * stream), as its argmax_set summary (estimator.py:50-57).  tpl and sig are
+ * single device rows (tpl->n <= sig->n).  The valid lags are cut into blocks
+ * of `block` lags (<= 0: the path's tile -- 8192 on the fp4 tensor-core mode,
+ * 4096 on the int8 one, else the largest block one 2^19 transform holds);
+ * block b correlates the template with the overlapping strided stream row
+ * [b*block, b*block + block + tpl->n - 1) and the per-block summaries are
+ * merged on the device.  Enqueued on `stream`; writes the device int64[8]
+ *   summary = {peak value, smallest lag at it (stream coordinates:
+ *              + sig->start - tpl->start), ties, NaN seen, x all-zero,
+ *              y all-zero in every block, a block failed, its status}
+ * (the last four carry DegenerateQuantization / ValueError of
+ * estimator.py:83-86 to the caller).  Replaces the caller-side loop of
+ * estimate() calls over stream windows; no reference symbol has this name. */
+qx_status qx_template_search(qx_context *ctx, const qx_signals *tpl, const qx_signals *sig,
+                             const qx_quantizer *qx, const qx_quantizer *qy, int64_t block,
+                             qx_path path, int64_t *summary, void *stream);
+
 /* Device decode of a mono PCM16 payload (little-endian int16, e.g. the data
  * chunk of a WAV file) to float32 samples pcm / 32768: the sample decode of
  * signalgen.load_wav_bytes (signalgen.py:150-172).  Exact, so the float32

@@ -10,7 +10,6 @@ restricted to [lag_lo, lag_hi] (estimator.py:50-57, 94).
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -147,88 +146,36 @@ def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None
     return res
 
 
-MAX_P = 1 << 19  # largest single-launch transform of the NTT path
-TC_BLOCK = 4096  # template-search lags per block on the tensor-core path (one M=128, N=32 tile)
-TC_BLOCK_F4 = 8192  # same on the fp4 (e2m1) tensor-core mode: one M=128, N=64 tile (qx_tc.cu kF4Lags)
-TC_F4_MAX_CODE = 4  # qx_tc.cu kF4MaxCode: |codes| that are exact e2m1 values
-TC_MAX_K = 4608  # qx_tc.cu kTcMaxK: template length + 15 must fit
-
-
-def _mode(q) -> int:
-    """Kernel quantiser mode (qx_abi.cu: k == 1 -> two compares, else by kind)."""
-    return 0 if q.k == 1 else (1 if q.kind == "uniform" else 2)
-
-
-def tc_f4_block(nt: int, qx, qy) -> bool:
-    """True when template search runs on the fp4 tensor-core mode
-    (mirrors qx_tc.cu tc_f4_mode: codes |c| <= 4, exact f32 sums)."""
-    if os.environ.get("QX_TC_F4", "1").startswith("0"):
-        return False
-    return (qx.k <= TC_F4_MAX_CODE and qy.k <= TC_F4_MAX_CODE and _mode(qx) == _mode(qy)
-            and nt * qx.k * qy.k < (1 << 24))
-
-
 def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
                     path: str = "auto") -> tuple[int, int, int]:
     """Peak summary (value, smallest lag, ties) of estimate(x=template, y=stream)
     over the VALID lags (template fully inside the stream):
     lag in [stream_start, stream_start + len(stream) - len(template)].
 
-    Overlap-save: the valid-lag range is cut into blocks of `block` lags; block
-    b correlates the template (a stride-0 row, never copied) with the stream
-    window [b*block, b*block + block + len(template) - 1) (overlapping strided
-    rows of the same buffer) and the per-block summaries are merged on the
-    device.  Each block's lags use only samples inside its window, so the
-    result equals the reference's argmax_set summary of the full correlogram
-    restricted to the valid lags (estimator.py:50-57)."""
+    One C-ABI call (qx_template_search): the valid-lag range is cut into
+    blocks of `block` lags (default: the tensor-core tile, 8192 lags on the
+    fp4 mode / 4096 on the int8 one, else the largest one-transform NTT
+    block); block b correlates the template (a stride-0 row, never copied)
+    with the stream window [b*block, b*block + block + len(template) - 1)
+    (overlapping strided rows of the same buffer) and the per-block summaries
+    are merged on the device.  Each block's lags use only samples inside its
+    window, so the result equals the reference's argmax_set summary of the
+    full correlogram restricted to the valid lags (estimator.py:50-57)."""
     t = D.torch()
-    x = D.as_device(template)
-    y = D.as_device(stream)
-    nt, ns = x.shape[-1], y.shape[-1]
-    x, y = x.reshape(-1), y.reshape(-1)
-    nvalid = ns - nt + 1
-    if nvalid < 1:
+    x = D.as_device(template).reshape(-1)
+    y = D.as_device(stream).reshape(-1)
+    if y.shape[0] - x.shape[0] + 1 < 1:
         raise ValueError("template longer than the stream")
-    if block is None:
-        # tensor-core window path (qx_tc.cu, shared-template mode): 4096-lag
-        # blocks = one M=128 x N=32 tile per block, template built once per SM;
-        # otherwise the largest block whose full correlogram fits one NTT
-        tc = (path in ("auto", "direct", "tc") and nt + 15 <= TC_MAX_K and nt % 4 == 0
-              and x.dtype == t.float32 and y.dtype == t.float32)
-        if tc:
-            block = TC_BLOCK_F4 if tc_f4_block(nt, qx, qy) else TC_BLOCK
-        else:
-            block = MAX_P - 2 * nt + 2  # NTT: nout = block + 2*nt - 2 fits one transform
-    if block < 1:
+    if block is not None and block < 1:
         raise ValueError("template too long for the block transform")
-    nfull, rem = divmod(nvalid, block)
-    parts = []
-    if nfull:
-        xr = x.as_strided((nfull, nt), (0, 1))
-        yr = y.as_strided((nfull, block + nt - 1), (block, 1))
-        r = estimate_batch(xr, yr, qx, qy, lag_lo=0, lag_hi=block - 1, path=path).raw
-        offs = t.arange(nfull, device=r.device, dtype=t.int64) * block
-        parts.append((r, offs))
-    if rem:
-        s0 = nfull * block
-        r = estimate_batch(x[None], y[s0:s0 + rem + nt - 1][None], qx, qy, lag_lo=0, lag_hi=rem - 1,
-                           path=path).raw
-        parts.append((r, t.full((1,), s0, device=r.device, dtype=t.int64)))
-    raw = t.cat([p[0] for p in parts])
-    offs = t.cat([p[1] for p in parts])
-    # merge on the device; one host transfer of an 8-word summary
-    status = raw[:, 7] >> 32
-    flags = raw[:, 7] & 0xFFFFFFFF
-    bad = (status != 0) & (status != N.QX_DEGENERATE_QUANTIZATION)
-    value, lag, ties = raw[:, 0], raw[:, 1] + offs, raw[:, 2]
-    vmax = value.max()
-    hit = value == vmax
-    big = t.iinfo(t.int64).max
-    summary = t.stack([
-        vmax, t.where(hit, lag, big).min(), (ties * hit).sum(),
-        ((flags & N.RF_NONFINITE) != 0).any().long(), ((flags & N.RF_DEGENERATE_X) != 0).any().long(),
-        (raw[:, 6] == 0).all().long(), bad.any().long(), t.where(bad, status, 0).max()]).cpu().tolist()
-    vmax, lmin, nties, nan, degx, degy, anybad, badst = summary
+    nqx, _ = native_quantizer(qx)
+    nqy, _ = native_quantizer(qy)
+    sx, sy = D.signals(x, 0), D.signals(y, stream_start)
+    out = t.empty(8, dtype=t.int64, device=x.device)
+    ctx = N.context(x.device.index)
+    call(N.load().qx_template_search, ctx, ctypes.byref(sx), ctypes.byref(sy), ctypes.byref(nqx), ctypes.byref(nqy),
+         0 if block is None else int(block), N.PATHS[path], out.data_ptr(), D.stream_handle())
+    vmax, lmin, nties, nan, degx, degy, anybad, badst = out.cpu().tolist()
     if nan:
         raise ValueError("input contains NaN")
     if degx:
@@ -237,7 +184,7 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
         raise_for(N.QX_DEGENERATE_QUANTIZATION, "y quantizes to all zeros")
     if anybad:
         raise_for(int(badst), "template search block failed")
-    return (int(vmax), int(lmin) + stream_start, int(nties))
+    return (int(vmax), int(lmin), int(nties))
 
 
 def check_results(res: np.ndarray) -> None:

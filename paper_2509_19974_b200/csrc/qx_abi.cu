@@ -23,6 +23,8 @@ cudaError_t stats_to_results(const unsigned long long* stats, void* results, int
 cudaError_t pcm16_launch(const void* in, int64_t n, float* out, int sms, cudaStream_t s);
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
+cudaError_t merge_blocks_launch(const void* recs, int64_t n, int64_t block, long long lag_shift, void* partials,
+                                int* counter, long long* out, int sms, cudaStream_t s);
 }  // namespace qx
 
 using namespace qx;
@@ -62,6 +64,8 @@ struct qx_context {
     Arena scratch;     // Y/R/stats/partials
     Arena counters;    // zero-initialised ints, reset by the kernels
     Arena stage;       // host-API staging (x, y, results)
+    Arena records;     // template search: per-block results, merge partials
+    Arena mcounter;    // template search: merge counter (zeroed once, reset by the kernel)
     cudaStream_t host_stream = nullptr;
     cudaStream_t copy_stream = nullptr;   // H2D of the sweep entry point
     std::vector<cudaEvent_t> chunk_ev;    // per staged chunk (lazily created)
@@ -143,7 +147,7 @@ void qx_context_destroy(qx_context* c)
     cudaDeviceSynchronize();
     for (auto& kv : c->tables) cudaFree(kv.second.second);
     for (auto& kv : c->otables) cudaFree(kv.second.second);
-    for (Arena* a : {&c->scratch, &c->counters, &c->stage})
+    for (Arena* a : {&c->scratch, &c->counters, &c->stage, &c->records, &c->mcounter})
         if (a->ptr) cudaFree(a->ptr);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -617,6 +621,76 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
     for (int64_t b = 0; b < batch; ++b)
         if (results[b].status) return (qx_status)results[b].status;
+    return QX_OK;
+}
+
+// template search block size (lags): the tensor-core window path's tile
+// (fp4 mode: 8192, qx_tc.cu tc_f4_mode; int8: 4096) when the template fits
+// it, else the largest block whose full correlogram fits one 2^19 transform
+static int64_t tsearch_block(const qx_signals* t, const qx_signals* s, const qx_quantizer* qa,
+                             const qx_quantizer* qb, qx_path path)
+{
+    const int64_t nt = t->n;
+    const bool tc = path != QX_PATH_NTT && nt + 15 <= 4608 && nt % 4 == 0 && t->dtype == QX_F32 && s->dtype == QX_F32;
+    if (!tc) return (1ll << 19) - 2 * nt + 2;
+    const char* env = getenv("QX_TC_F4");
+    const int64_t ka = qa->k, kb = qb->k;
+    auto mode = [](const qx_quantizer* q) { return q->k == 1 ? 0 : (q->kind == QX_Q_UNIFORM ? 1 : 2); };
+    const bool f4 = !(env && env[0] == '0') && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
+                    (double)nt * ka * kb < 16777216.0;
+    return f4 ? 8192 : 4096;
+}
+
+qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_signals* sig, const qx_quantizer* qx_,
+                             const qx_quantizer* qy_, int64_t block, qx_path path, int64_t* summary, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!summary) return fail(ctx, QX_ERR_INVALID, "summary is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    qx_status st;
+    if ((st = check_signals(ctx, tpl, "template")) != QX_OK) return st;
+    if ((st = check_signals(ctx, sig, "stream")) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, qx_, tpl->dtype)) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, qy_, sig->dtype)) != QX_OK) return st;
+    const int64_t nt = tpl->n, ns = sig->n, nvalid = ns - nt + 1;
+    if (nvalid < 1) return fail(ctx, QX_ERR_INVALID, "template longer than the stream");
+    if (block <= 0) block = tsearch_block(tpl, sig, qx_, qy_, path);
+    if (block < 1) return fail(ctx, QX_ERR_INVALID, "template too long for the block transform");
+    const int64_t nfull = nvalid / block, rem = nvalid % block, nrec = nfull + (rem ? 1 : 0);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const size_t rb = (size_t)nrec * sizeof(qx_result), pb = (size_t)sms * 64;
+    cudaError_t e = arena_reserve(ctx->records, rb + pb + 256, false);
+    if (e == cudaSuccess) e = arena_reserve(ctx->mcounter, 256, true);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "template search scratch");
+    qx_result* recs = (qx_result*)ctx->records.ptr;
+    void* partials = (char*)ctx->records.ptr + ((rb + 255) & ~(size_t)255);
+    static const size_t esz[] = {4, 8, 8};
+    // block b: the template (stride-0 row) against stream samples
+    // [b*block, b*block + block + nt - 1): overlapping strided rows, no copies
+    qx_signals x = *tpl, y = *sig;
+    x.ld = 0;
+    x.start = 0;
+    y.start = 0;
+    if (nfull) {
+        y.n = block + nt - 1;
+        y.ld = block;
+        st = estimate_batch_on(ctx, &x, &y, nfull, qx_, qy_, 0, block - 1, path, recs, stream, nullptr, nullptr);
+        if (st != QX_OK) return st;
+    }
+    if (rem) {
+        x.ld = nt;
+        y.data = (const char*)sig->data + (size_t)(nfull * block) * esz[sig->dtype];
+        y.n = rem + nt - 1;
+        y.ld = y.n;
+        st = estimate_batch_on(ctx, &x, &y, 1, qx_, qy_, 0, rem - 1, path, recs + nfull, stream, nullptr, nullptr);
+        if (st != QX_OK) return st;
+    }
+    ctx->prof.pre(KK_OTHER, (cudaStream_t)stream);
+    e = merge_blocks_launch(recs, nrec, block, (long long)(sig->start - tpl->start), partials, (int*)ctx->mcounter.ptr,
+                            (long long*)summary, sms, (cudaStream_t)stream);
+    ctx->prof.post(KK_OTHER, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "merge launch");
     return QX_OK;
 }
 

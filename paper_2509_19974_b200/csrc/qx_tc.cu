@@ -1422,4 +1422,130 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     return e;
 }
 
+// ---- template search: device merge of per-block summaries
+// Record i (qx_result layout) covers lags [i*block, ...) of the stream; the
+// merged summary is {max value, smallest global lag at it, summed ties, any
+// NaN, x all-zero in any block, y all-zero in every block, any failing
+// block (status other than 0 / degenerate quantisation), the largest such
+// status}: the reference's argmax_set summary of the unblocked correlogram
+// (estimator.py:50-57) plus the inputs of its exceptions.
+struct BlkSum {
+    long long v, l, t;
+    int nan, degx, degy_all, bad, badst;
+};
+
+__device__ __forceinline__ void blk_add(BlkSum& a, const BlkSum& b)
+{
+    if (b.t) {
+        if (!a.t || b.v > a.v) { a.v = b.v; a.l = b.l; a.t = b.t; }
+        else if (b.v == a.v) { a.l = min(a.l, b.l); a.t += b.t; }
+    }
+    a.nan |= b.nan;
+    a.degx |= b.degx;
+    a.degy_all &= b.degy_all;
+    a.bad |= b.bad;
+    a.badst = max(a.badst, b.badst);
+}
+
+__device__ BlkSum blk_shfl(const BlkSum& a, int o)
+{
+    BlkSum b;
+    b.v = __shfl_xor_sync(0xffffffffu, a.v, o);
+    b.l = __shfl_xor_sync(0xffffffffu, a.l, o);
+    b.t = __shfl_xor_sync(0xffffffffu, a.t, o);
+    b.nan = __shfl_xor_sync(0xffffffffu, a.nan, o);
+    b.degx = __shfl_xor_sync(0xffffffffu, a.degx, o);
+    b.degy_all = __shfl_xor_sync(0xffffffffu, a.degy_all, o);
+    b.bad = __shfl_xor_sync(0xffffffffu, a.bad, o);
+    b.badst = __shfl_xor_sync(0xffffffffu, a.badst, o);
+    return b;
+}
+
+constexpr int kMergeThreads = 256;
+
+// block-wide merge; the result is valid in thread 0
+__device__ BlkSum blk_reduce(BlkSum a)
+{
+    __shared__ BlkSum sh[kMergeThreads / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) blk_add(a, blk_shfl(a, o));
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        BlkSum b = threadIdx.x < kMergeThreads / 32 ? sh[threadIdx.x] : BlkSum{0, LLONG_MAX, 0, 0, 0, 1, 0, 0};
+#pragma unroll
+        for (int o = 16; o; o >>= 1) blk_add(b, blk_shfl(b, o));
+        a = b;
+    }
+    return a;
+}
+
+__global__ void __launch_bounds__(kMergeThreads) k_merge_blocks(const long long* recs, int64_t n, int64_t block,
+                                                                long long lag_shift, BlkSum* partials, int* counter,
+                                                                long long* out)
+{
+    BlkSum a{0, LLONG_MAX, 0, 0, 0, 1, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)kMergeThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMergeThreads) {
+        const long long* r = recs + i * 8;
+        const long long w7 = r[7];
+        const int status = (int)(w7 >> 32), flags = (int)(w7 & 0xffffffff);
+        BlkSum b;
+        b.v = r[0];
+        b.l = r[1] + i * block;
+        b.t = status == 0 ? r[2] : 0;
+        b.nan = (flags & 4) != 0;
+        b.degx = (flags & 1) != 0;
+        b.degy_all = r[6] == 0;
+        b.bad = status != 0 && status != 2;
+        b.badst = b.bad ? status : 0;
+        blk_add(a, b);
+    }
+    a = blk_reduce(a);
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = a;
+        __threadfence();
+        last = atomicAdd(counter, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    BlkSum m{0, LLONG_MAX, 0, 0, 0, 1, 0, 0};
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kMergeThreads) {
+        const BlkSum* p = partials + i;  // other CTAs' records: L2 loads
+        BlkSum b;
+        b.v = __ldcg(&p->v);
+        b.l = __ldcg(&p->l);
+        b.t = __ldcg(&p->t);
+        b.nan = __ldcg(&p->nan);
+        b.degx = __ldcg(&p->degx);
+        b.degy_all = __ldcg(&p->degy_all);
+        b.bad = __ldcg(&p->bad);
+        b.badst = __ldcg(&p->badst);
+        blk_add(m, b);
+    }
+    m = blk_reduce(m);
+    if (threadIdx.x == 0) {
+        out[0] = m.t ? m.v : 0;
+        out[1] = m.t ? m.l + lag_shift : 0;
+        out[2] = m.t;
+        out[3] = m.nan;
+        out[4] = m.degx;
+        out[5] = m.degy_all;
+        out[6] = m.bad;
+        out[7] = m.badst;
+        *counter = 0;  // ready for the next launch
+    }
+}
+
+cudaError_t merge_blocks_launch(const void* recs, int64_t n, int64_t block, long long lag_shift, void* partials,
+                                int* counter, long long* out, int sms, cudaStream_t s)
+{
+    int64_t g = (n + kMergeThreads - 1) / kMergeThreads;
+    const int grid = (int)(g < 1 ? 1 : (g > sms ? sms : g));
+    k_merge_blocks<<<grid, kMergeThreads, 0, s>>>((const long long*)recs, n, block, lag_shift, (BlkSum*)partials,
+                                                    counter, out);
+    return cudaGetLastError();
+}
+
 }  // namespace qx

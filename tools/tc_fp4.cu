@@ -149,6 +149,79 @@ __global__ void k_fp4(const int8_t* x, const int8_t* y, int* out, long long* cyc
     if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
 }
 
+// peak-rate probe: the same chain at M128 x N (K64), operands from a zeroed
+// buffer (content irrelevant for timing), B K-chunk stride 16*N bytes
+template <int NN>
+__global__ void k_fp4_rate(long long* cyc, int reps)
+{
+    extern __shared__ __align__(1024) unsigned char sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    for (int i = threadIdx.x; i < 65536; i += blockDim.x) sm[i] = 0x22;
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    const int w = threadIdx.x >> 5;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t SF = 480;
+    if (w < 4) {
+        const uint32_t v = 0x7f7f7f7fu;
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+                tbase + ((uint32_t)(w * 32) << 16) + SF),
+            "r"(v));
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    constexpr uint32_t idesc = (1u << 7) | (1u << 10) | ((uint32_t)(NN >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+    if (w == 4) {
+        const uint64_t ad = desc(su32(sm), 16, 256, 6);
+        const uint64_t bd = desc(su32(sm + 8192), 16 * NN, 128, 0);
+        long long t0 = clock64();
+        for (int rep = 0; rep < reps; ++rep)
+            asm volatile(
+                "{\n\t.reg .pred e;\n\t"
+                "elect.sync _|e, 0xffffffff;\n\t"
+                "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%4], 1;\n}" ::"r"(
+                    tbase),
+                "l"(ad), "l"(bd), "r"(idesc), "r"(tbase + SF));
+        asm volatile(
+            "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+            "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(su32(&bar)));
+        uint32_t done = 0;
+        while (!done)
+            asm volatile("{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], 0;\n\t"
+                         "selp.u32 %0, 1, 0, P1;\n}" : "=r"(done) : "r"(su32(&bar)));
+        if ((threadIdx.x & 31) == 0) *cyc = clock64() - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+}
+
+template <int NN>
+static void rate(long long* dcyc)
+{
+    cudaFuncSetAttribute(k_fp4_rate<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+    k_fp4_rate<NN><<<1, 160, 65536>>>(dcyc, 1024);
+    cudaDeviceSynchronize();
+    long long c;
+    cudaMemcpy(&c, dcyc, 8, cudaMemcpyDeviceToHost);
+    const double cpm = (double)c / 1024;
+    printf("{\"timing\": \"M128 N%d K64 mxf4 (rate probe)\", \"cycles_per_mma\": %.2f, \"macs_per_clk_sm\": %.0f}\n", NN, cpm,
+           128.0 * NN * 64 / cpm);
+}
+
 int main()
 {
     std::vector<int8_t> hx(NX), hy(NY);
@@ -201,5 +274,9 @@ int main()
         printf("{\"timing\": \"M128 N64 K64 mxf4\", \"reps\": %d, \"mmas\": %d, \"cycles_per_mma\": %.2f}\n", reps,
                reps * NK, (double)c / (reps * NK));
     }
+    rate<32>(dcyc);
+    rate<64>(dcyc);
+    rate<128>(dcyc);
+    rate<256>(dcyc);
     return fails ? 2 : 0;
 }

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define QX_ABI_VERSION 1
+#define QX_ABI_VERSION 2
 
 typedef enum qx_status {
     QX_OK = 0,
@@ -82,7 +82,9 @@ typedef struct qx_signals {
 /* AUTO: bounded windows (<= 4112 lags, n_x <= 4593, k <= 127) -> DIRECT,
  * else NTT.  NTT: exact full-lag number-theoretic transform path.  DIRECT:
  * tcgen05 int8 Toeplitz tiles over the lag window (argmax entry points). */
-typedef enum qx_path { QX_PATH_AUTO = 0, QX_PATH_NTT = 1, QX_PATH_DIRECT = 2 } qx_path;
+/* AUTO picks DIRECT (tensor-core window) for windows of <= 4112 lags, else POPC
+ * (word-parallel 1-level codes) for small single pairs, else NTT. */
+typedef enum qx_path { QX_PATH_AUTO = 0, QX_PATH_NTT = 1, QX_PATH_DIRECT = 2, QX_PATH_POPC = 3 } qx_path;
 
 /* per-pair flags in qx_result.flags */
 #define QX_RF_DEGENERATE_X 1 /* x quantizes to all zeros */
@@ -182,7 +184,7 @@ qx_status qx_decode_pcm16(qx_context *ctx, const void *pcm, int64_t n, float *ou
  * kernel the library launches is counted per kind and, when `timed`, bracketed
  * by CUDA events on its own stream.  qx_profile_end synchronises and returns
  * summed device milliseconds per kind (names via qx_profile_kind_name). */
-#define QX_PROFILE_KINDS 8
+#define QX_PROFILE_KINDS 10
 typedef struct qx_profile {
     int64_t launches;
     int64_t count[QX_PROFILE_KINDS];

@@ -33,7 +33,8 @@ QX_ERR_NONFINITE = 9
 
 QX_F32, QX_F64, QX_I64 = 0, 1, 2
 QX_Q_SIGN, QX_Q_UNIFORM, QX_Q_CUSTOM, QX_Q_CODES = 0, 1, 2, 3
-PATHS = {"auto": 0, "ntt": 1, "direct": 2, "tc": 2}
+PATHS = {"auto": 0, "ntt": 1, "direct": 2, "tc": 2, "popc": 3}
+PROFILE_KINDS = 10  # qxcorr_b200.h QX_PROFILE_KINDS
 
 RF_DEGENERATE_X = 1
 RF_DEGENERATE_Y = 2
@@ -61,7 +62,8 @@ class QxResult(ctypes.Structure):
 
 
 class QxProfile(ctypes.Structure):
-    _fields_ = [("launches", ctypes.c_int64), ("count", ctypes.c_int64 * 8), ("ms", ctypes.c_double * 8)]
+    _fields_ = [("launches", ctypes.c_int64), ("count", ctypes.c_int64 * PROFILE_KINDS),
+                ("ms", ctypes.c_double * PROFILE_KINDS)]
 
 
 RESULT_DTYPE = np.dtype([("value", "<i8"), ("lag", "<i8"), ("ties", "<i8"), ("sumsq_x", "<i8"),
@@ -130,7 +132,7 @@ def load():
         L.qx_profile_end.restype = st
         L.qx_profile_kind_name.argtypes = [ctypes.c_int]
         L.qx_profile_kind_name.restype = ctypes.c_char_p
-        assert L.qx_abi_version() == 1
+        assert L.qx_abi_version() == 2
         _lib = L
     return _lib
 
@@ -197,5 +199,5 @@ class profile:
         L = load()
         self.launches = int(out.launches)
         self.result = {L.qx_profile_kind_name(i).decode(): (int(out.count[i]), float(out.ms[i]))
-                       for i in range(8) if out.count[i]}
+                       for i in range(PROFILE_KINDS) if out.count[i]}
         return False

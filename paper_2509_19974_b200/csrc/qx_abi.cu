@@ -23,6 +23,8 @@ cudaError_t stats_to_results(const unsigned long long* stats, void* results, int
 cudaError_t pcm16_launch(const void* in, int64_t n, float* out, int sms, cudaStream_t s);
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
+bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path);
+cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s);
 cudaError_t merge_blocks_launch(const void* recs, int64_t n, int64_t block, long long lag_shift, void* partials,
                                 int* counter, long long* out, int sms, cudaStream_t s);
 }  // namespace qx
@@ -358,7 +360,27 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     const bool tc_ok = argmax && tc_window_eligible(c, nx, ny);
     if (path == QX_PATH_DIRECT && !tc_ok)
         return fail(ctx, QX_ERR_UNSUPPORTED, "tensor-core window path: window > 4096 lags, nx > 4593 or k > 127");
-    out->path = (path == QX_PATH_DIRECT || (path == QX_PATH_AUTO && tc_ok)) ? QX_PATH_DIRECT : QX_PATH_NTT;
+    // word-parallel 1-level codes (qx_popc.cu): small single pairs
+    const bool popc_ok = argmax && !(path == QX_PATH_AUTO && tc_ok) && popc_eligible(c, nx, ny, path == QX_PATH_AUTO);
+    if (path == QX_PATH_POPC && !popc_ok)
+        return fail(ctx, QX_ERR_UNSUPPORTED, "popc path: needs k = 1 quantisers on float rows, nx <= 65536 and "
+                                             "a lag window whose planes fit shared memory");
+    out->path = (path == QX_PATH_DIRECT || (path == QX_PATH_AUTO && tc_ok)) ? QX_PATH_DIRECT
+                : (path == QX_PATH_POPC || (path == QX_PATH_AUTO && popc_ok)) ? QX_PATH_POPC : QX_PATH_NTT;
+    if (out->path == QX_PATH_POPC) {
+        c.am.pstride = kMaxPartialsLarge;
+        const size_t sb = (size_t)batch * 8 * 8, pb = (size_t)batch * c.am.pstride * 3 * 8;
+        const size_t plb = (size_t)batch * 2 * ((nx + 31) / 32 + (ny + 31) / 32 + 2) * 4;
+        cudaError_t e = arena_reserve(scr, sb + pb + plb + 256, false);
+        if (e == cudaSuccess) e = arena_reserve(cnt, (size_t)batch * 4, true);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
+        c.stats = (unsigned long long*)scr.ptr;
+        c.am.partials = (long long*)((char*)scr.ptr + sb);
+        c.popc_planes = (uint32_t*)((char*)scr.ptr + sb + pb);
+        c.am.counters = (int*)cnt.ptr;
+        c.prof = &ctx->prof;
+        return QX_OK;
+    }
     if (out->path == QX_PATH_DIRECT) {
         const size_t sb = (size_t)batch * 8 * 8;
         cudaError_t e = arena_reserve(scr, sb + 256, false);
@@ -497,7 +519,8 @@ static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const q
     pr.call.am.results = results;
     cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
-    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
+    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s)
+        : pr.path == QX_PATH_POPC ? popc_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
     return QX_OK;
 }
@@ -518,7 +541,8 @@ qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signa
     pr.call.am.results = results;
     cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
-    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
+    e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s)
+        : pr.path == QX_PATH_POPC ? popc_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
     return QX_OK;
 }
@@ -547,7 +571,7 @@ qx_status qx_xcorr_full(qx_context* ctx, const qx_signals* x, const qx_signals* 
 }
 
 static const char* kKindNames[QX_PROFILE_KINDS] = {"ntt_pass1", "ntt_pass2", "ntt_pass3", "crt_combine",
-                                                    "quantize", "direct", "other", "direct_f4"};
+                                                    "quantize", "direct", "other", "direct_f4", "popc", ""};
 
 const char* qx_profile_kind_name(int kind)
 {

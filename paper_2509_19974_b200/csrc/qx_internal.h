@@ -65,11 +65,11 @@ struct NttTables {
 
 // Optional per-launch accounting (qx_profile_begin/end): counts every kernel
 // launch and, when timed, brackets it with CUDA events on its stream.
-enum KernelKind : int { KK_PASS1 = 0, KK_PASS2, KK_PASS3, KK_COMBINE, KK_QUANT, KK_DIRECT, KK_OTHER, KK_DIRECT_F4, KK_N };
+enum KernelKind : int { KK_PASS1 = 0, KK_PASS2, KK_PASS3, KK_COMBINE, KK_QUANT, KK_DIRECT, KK_OTHER, KK_DIRECT_F4, KK_POPC, KK_N };
 struct Profiler {
     bool on = false, timed = false;
     long long launches = 0;
-    long long count[8] = {0};
+    long long count[KK_N + 1] = {0};
     struct Rec { int kind; cudaEvent_t a, b; };
     Rec* recs = nullptr;
     int nrec = 0, cap = 0;
@@ -113,6 +113,7 @@ struct NttCall {
     OuterTables otab[3];
     uint32_t* OUT;            // [2][chunk][P] outer forward output
     uint32_t* RI;             // [chunk*M][np][Q] inner inverse residues
+    uint32_t* popc_planes;    // popc path: [batch][2][nxw + nyw + 2] code bit planes
 };
 
 // launches every pass of the NTT correlation for all pairs on `stream`

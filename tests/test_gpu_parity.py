@@ -225,6 +225,58 @@ def test_random_pairs_against_oracle(qx, oracle):
             assert res["sumsq_x"][b] == oracle.sumsq(u) and res["sumsq_y"][b] == oracle.sumsq(v)
 
 
+def test_popc_path_against_oracle(qx, oracle):
+    """Word-parallel 1-level path (path="popc", and what "auto" picks for
+    C1-sized pairs): sign / uniform(1) / custom k=1 codes, with and without
+    zero codes (the 1-POPC and 2-POPC forms), ragged lengths, windows,
+    batches, both float dtypes; values, lags, ties and statistics equal the
+    oracle's and the NTT path's."""
+    import torch
+
+    from paper_2509_19974_b200 import _native
+
+    rng = np.random.default_rng(31)
+    quants = [qx.sign(), qx.uniform(1, 0.7), qx.custom([-0.3, 0.4]), qx.uniform(1, 5.0)]
+    for trial in range(40):
+        B = int(rng.integers(1, 4))
+        nx = int(rng.integers(1, 9000)) if trial % 5 else int(rng.integers(16000, 40000))
+        ny = int(rng.integers(1, 9000)) if trial % 7 else int(rng.integers(16000, 40000))
+        dt = np.float32 if trial % 2 else np.float64
+        x = (rng.standard_normal((B, nx)) * rng.uniform(0.1, 3)).astype(dt)
+        y = (rng.standard_normal((B, ny)) * rng.uniform(0.1, 3)).astype(dt)
+        if trial % 3 == 0:  # exact zeros: sign() codes 0
+            x[:, ::7] = 0
+            y[:, ::5] = 0
+        qa, qb = quants[trial % 4], quants[(trial // 4) % 4]
+        nout = nx + ny - 1
+        t_lo, t_hi = (0, nout - 1) if trial % 4 == 0 else sorted(int(v) for v in rng.integers(0, nout, 2))
+        first = -(nx - 1)
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        with _native.profile(timed=False) as prof:
+            res = qx.estimate_batch(xd, yd, qa, qb, lag_lo=first + t_lo, lag_hi=first + t_hi, path="popc").numpy()
+        assert prof.result.get("popc", (0, 0))[0] == 1, prof.result
+        ntt = qx.estimate_batch(xd, yd, qa, qb, lag_lo=first + t_lo, lag_hi=first + t_hi, path="ntt").numpy()
+        assert np.array_equal(res, ntt), (trial, res, ntt)
+        for b in range(B):
+            u, v = oracle.quantize(qa, x[b]), oracle.quantize(qb, y[b])
+            if not u.any() or not v.any():
+                assert res["status"][b] == 2
+                continue
+            m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, t_lo, t_hi))
+            assert (res["value"][b], res["lag"][b], res["ties"][b]) == (m, first + t_lo + f, n), trial
+            assert res["sumsq_y"][b] == oracle.sumsq(v) and res["nnz_x"][b] == np.count_nonzero(u)
+    # C1 takes this path by default; NaN raises like the reference's float path
+    from paper_2509_19974_b200 import workloads as W
+
+    x, y = W.c1(0)
+    with _native.profile(timed=False) as prof:
+        r = qx.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), qx.sign(), qx.sign()).numpy()
+    assert list(prof.result) == ["popc"] and (int(r["lag"][0]), int(r["value"][0])) == (-137, 14839)
+    x[5] = np.nan
+    r = qx.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), qx.sign(), qx.sign()).numpy()
+    assert r["status"][0] == 9
+
+
 def test_multiprime_path_saturated(qx, oracle):
     """Saturated b=8 codes defeat the Cauchy-Schwarz single-prime test, so
     the 2-prime CRT path must reproduce the exact (large) values."""

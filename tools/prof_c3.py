@@ -1,4 +1,4 @@
-"""Short driver for ncu: BASELINE config 3 slice (4096 pairs), b=4, window -512..512."""
+"""Short driver for ncu: BASELINE config 3 slice (argv[1] pairs, default 4096), b = argv[2] (default 4), window -512..512."""
 import os
 import sys
 
@@ -12,7 +12,7 @@ from paper_2509_19974_b200 import workloads as W
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 xs, ys, lag = W.c3(pairs=n)
 xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
-q = W.bit_quantizer(4, W.C3_SIGMA)
+q = W.bit_quantizer(int(sys.argv[2]) if len(sys.argv) > 2 else 4, W.C3_SIGMA)
 for _ in range(3):
     r = P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512)
 torch.cuda.synchronize()

@@ -307,7 +307,8 @@ def main():
                "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes),
                "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e,
                "path": "qx_estimate_sweep_host (C ABI, pinned host buffers; inputs staged once per step "
-                       "in pair chunks (>= 16 pairs each) overlapped with compute, 4 bit depths)"}
+                       "in 8-pair chunks on a copy stream, the 4 bit depths of each chunk on 4 concurrent "
+                       "compute lanes)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

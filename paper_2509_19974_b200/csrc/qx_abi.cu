@@ -25,8 +25,9 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
 bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path);
 cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s);
-cudaError_t merge_blocks_launch(const void* recs, int64_t n, int64_t block, long long lag_shift, void* partials,
-                                int* counter, long long* out, int sms, cudaStream_t s);
+bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny);
+cudaError_t merge_blocks_launch(const MergeSegs& segs, long long lag_shift, void* partials, int* counter,
+                                long long* out, int sms, cudaStream_t s);
 }  // namespace qx
 
 using namespace qx;
@@ -303,7 +304,7 @@ struct Prepared {
 static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                          const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
                          bool argmax, qx_path path, Prepared* out, Arena* scratch = nullptr,
-                         Arena* counters = nullptr)
+                         Arena* counters = nullptr, bool split2 = false)
 {
     Arena& scr = scratch ? *scratch : ctx->scratch;
     Arena& cnt = counters ? *counters : ctx->counters;
@@ -337,6 +338,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     }
     NttCall& c = out->call;
     memset(&c, 0, sizeof(c));
+    c.split2 = split2;
     c.op[0].data = x->data;
     c.op[0].ld = x->ld;
     c.op[0].n = nx;
@@ -508,13 +510,19 @@ qx_status qx_quantize(qx_context* ctx, const qx_quantizer* q, const qx_signals* 
 }  // extern "C"
 
 // qx_estimate_batch on explicit scratch arenas (the sweep's compute lanes)
+// split2: `results` holds two records per pair and the 2-SM template-search
+// mode may write them (qx_template_search)
 static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                                    const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
-                                   qx_path path, qx_result* results, void* stream, Arena* scratch, Arena* counters)
+                                   qx_path path, qx_result* results, void* stream, Arena* scratch, Arena* counters,
+                                   bool split2 = false)
 {
     Prepared pr;
-    qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr, scratch, counters);
+    qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr, scratch, counters, split2);
     if (st != QX_OK) return st;
+    // two records per pair only come from the 2-SM kernel: anything else is
+    // the caller's cue to use single-record blocks
+    if (split2 && !(pr.path == QX_PATH_DIRECT && tc_f2_selected(pr.call, pr.nx, pr.ny))) return QX_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     pr.call.am.results = results;
     cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
@@ -648,20 +656,25 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     return QX_OK;
 }
 
-// template search block size (lags): the tensor-core window path's tile
-// (fp4 mode: 8192, qx_tc.cu tc_f4_mode; int8: 4096) when the template fits
-// it, else the largest block whose full correlogram fits one 2^19 transform
+// template search blocks (lags): the tensor-core window path's tile when
+// the template fits it -- 32768 on the 2-SM fp4 mode (two records per
+// block), 8192 on the 1-SM fp4 mode, 4096 on the int8 one -- else the
+// largest block whose full correlogram fits one 2^19 transform
 static int64_t tsearch_block(const qx_signals* t, const qx_signals* s, const qx_quantizer* qa,
-                             const qx_quantizer* qb, qx_path path)
+                             const qx_quantizer* qb, qx_path path, bool* f2)
 {
+    *f2 = false;
     const int64_t nt = t->n;
-    const bool tc = path != QX_PATH_NTT && nt + 15 <= 4608 && nt % 4 == 0 && t->dtype == QX_F32 && s->dtype == QX_F32;
+    const bool tc = path != QX_PATH_NTT && path != QX_PATH_POPC && nt + 15 <= 4608 && nt % 4 == 0 &&
+                    t->dtype == QX_F32 && s->dtype == QX_F32;
     if (!tc) return (1ll << 19) - 2 * nt + 2;
     const char* env = getenv("QX_TC_F4");
     const int64_t ka = qa->k, kb = qb->k;
     auto mode = [](const qx_quantizer* q) { return q->k == 1 ? 0 : (q->kind == QX_Q_UNIFORM ? 1 : 2); };
     const bool f4 = !(env && env[0] == '0') && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
                     (double)nt * ka * kb < 16777216.0;
+    const char* env2 = getenv("QX_TC_F2");
+    *f2 = f4 && !(env2 && env2[0] == '0');
     return f4 ? 8192 : 4096;
 }
 
@@ -678,9 +691,17 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
     if ((st = check_quantizer(ctx, qy_, sig->dtype)) != QX_OK) return st;
     const int64_t nt = tpl->n, ns = sig->n, nvalid = ns - nt + 1;
     if (nvalid < 1) return fail(ctx, QX_ERR_INVALID, "template longer than the stream");
-    if (block <= 0) block = tsearch_block(tpl, sig, qx_, qy_, path);
+    bool f2 = false;
+    if (block <= 0) block = tsearch_block(tpl, sig, qx_, qy_, path, &f2);
     if (block < 1) return fail(ctx, QX_ERR_INVALID, "template too long for the block transform");
-    const int64_t nfull = nvalid / block, rem = nvalid % block, nrec = nfull + (rem ? 1 : 0);
+    // runs of blocks: [2-SM 32768-lag blocks (2 records each)], `block`-lag
+    // blocks, one shorter remainder block
+    const int64_t big = 32768;
+    int64_t n2 = f2 ? nvalid / big : 0;
+    if (n2 < 2) n2 = 0;  // the 2-SM mode runs clusters over >= 2 blocks
+    // records: 2 per 32768-lag block (<= 1 per `block` lags, block <= 16384)
+    // or 1 per `block`-lag block, + the remainder
+    const int64_t nrec = nvalid / block + 2;
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
     const size_t rb = (size_t)nrec * sizeof(qx_result), pb = (size_t)sms * 64;
@@ -690,28 +711,53 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
     qx_result* recs = (qx_result*)ctx->records.ptr;
     void* partials = (char*)ctx->records.ptr + ((rb + 255) & ~(size_t)255);
     static const size_t esz[] = {4, 8, 8};
-    // block b: the template (stride-0 row) against stream samples
-    // [b*block, b*block + block + nt - 1): overlapping strided rows, no copies
+    const size_t es = esz[sig->dtype];
+    MergeSegs segs = {};
+    // block b of a run starting at stream sample s0: the template (stride-0
+    // row) against samples [s0 + b*B, s0 + b*B + B + nt - 1): overlapping
+    // strided rows, no copies
     qx_signals x = *tpl, y = *sig;
     x.ld = 0;
     x.start = 0;
     y.start = 0;
+    qx_result* r = recs;
+    int64_t s0 = 0;
+    int ns_ = 0;
+    if (n2) {
+        y.n = big + nt - 1;
+        y.ld = big;
+        st = estimate_batch_on(ctx, &x, &y, n2, qx_, qy_, 0, big - 1, path, r, stream, nullptr, nullptr, true);
+        if (st == QX_ERR_UNSUPPORTED) {
+            n2 = 0;  // not on the 2-SM mode: every block on `block`
+        } else {
+            if (st != QX_OK) return st;
+            segs.seg[ns_++] = MergeSeg{(const long long*)r, 2 * n2, 2, big, 0};
+            r += 2 * n2;
+            s0 = n2 * big;
+        }
+    }
+    const int64_t nfull = (nvalid - s0) / block, rem = (nvalid - s0) % block;
     if (nfull) {
+        y.data = (const char*)sig->data + (size_t)s0 * es;
         y.n = block + nt - 1;
         y.ld = block;
-        st = estimate_batch_on(ctx, &x, &y, nfull, qx_, qy_, 0, block - 1, path, recs, stream, nullptr, nullptr);
+        st = estimate_batch_on(ctx, &x, &y, nfull, qx_, qy_, 0, block - 1, path, r, stream, nullptr, nullptr);
         if (st != QX_OK) return st;
+        segs.seg[ns_++] = MergeSeg{(const long long*)r, nfull, 1, block, s0};
+        r += nfull;
+        s0 += nfull * block;
     }
     if (rem) {
         x.ld = nt;
-        y.data = (const char*)sig->data + (size_t)(nfull * block) * esz[sig->dtype];
+        y.data = (const char*)sig->data + (size_t)s0 * es;
         y.n = rem + nt - 1;
         y.ld = y.n;
-        st = estimate_batch_on(ctx, &x, &y, 1, qx_, qy_, 0, rem - 1, path, recs + nfull, stream, nullptr, nullptr);
+        st = estimate_batch_on(ctx, &x, &y, 1, qx_, qy_, 0, rem - 1, path, r, stream, nullptr, nullptr);
         if (st != QX_OK) return st;
+        segs.seg[ns_++] = MergeSeg{(const long long*)r, 1, 1, rem, s0};
     }
     ctx->prof.pre(KK_OTHER, (cudaStream_t)stream);
-    e = merge_blocks_launch(recs, nrec, block, (long long)(sig->start - tpl->start), partials, (int*)ctx->mcounter.ptr,
+    e = merge_blocks_launch(segs, (long long)(sig->start - tpl->start), partials, (int*)ctx->mcounter.ptr,
                             (long long*)summary, sms, (cudaStream_t)stream);
     ctx->prof.post(KK_OTHER, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "merge launch");

@@ -114,6 +114,20 @@ struct NttCall {
     uint32_t* OUT;            // [2][chunk][P] outer forward output
     uint32_t* RI;             // [chunk*M][np][Q] inner inverse residues
     uint32_t* popc_planes;    // popc path: [batch][2][nxw + nyw + 2] code bit planes
+    int split2;               // the caller takes 2 records per pair (2-SM template-search blocks)
+};
+
+// Template-search merge input: up to three runs of per-block records
+// (qx_result layout); record i of a run covers lags base + (i / rpb) * block + ...
+struct MergeSeg {
+    const long long* recs;
+    int64_t n;      // records
+    int rpb;        // records per block (2: the 2-SM mode's per-CTA halves)
+    int64_t block;  // lags per block
+    int64_t base;   // stream lag of the run's first block
+};
+struct MergeSegs {
+    MergeSeg seg[3];
 };
 
 // launches every pass of the NTT correlation for all pairs on `stream`

@@ -55,7 +55,18 @@ constexpr int kTcLags = 2048;      // lags per M=128 tile (M=64: 1024)
 constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
 constexpr int kTcMaxTiles = 2;     // lag tiles per pair
 constexpr int kTcMaxExtra = 16;    // lags past the tiles, summed on CUDA cores
-constexpr int kTcYBytes = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
+// 2-SM fp4 mode (cta_group::2, M = 256 = 128 Hankel rows per CTA): pitch
+// 128 samples (64-B SW64 rows) = N = 128 template copies, 64 per CTA; one
+// pair-block is 32768 lags, 16384 per CTA (tools/tc_fp4_2sm.cu: exact, 64-69
+// cycles per M256 N128 K64 instruction = the fp4 peak, 2.1x the 1-SM mode)
+constexpr int kF2Pitch = 128;
+constexpr int kF2CtaLags = 128 * kF2Pitch;      // 16384
+constexpr int kF2Lags = 2 * kF2CtaLags;         // 32768
+constexpr int kF2Pad = 128;                     // template nibble front padding (samples)
+constexpr int kF2Sf = 256;                      // TMEM scale-factor column (2 aux slots x 128 columns)
+constexpr int kTcYBytesI8 = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
+constexpr int kTcYBytesF2 = (kF2CtaLags + kTcMaxK + 2 * kF2Pad) / 2;
+constexpr int kTcYBytes = kTcYBytesI8 > kTcYBytesF2 ? kTcYBytesI8 : kTcYBytesF2;
 constexpr int kTcYStride = (kTcYBytes + 1023) / 1024 * 1024;  // 1024-B aligned slots (SW32 rows)
 constexpr int kTcXPad = 32;  // zero bytes in front of the linear x codes (>= the Hankel pitch)
 // B layout: K-chunk stride 272 B (= 256 + 16): 16-byte stores of 32
@@ -102,19 +113,50 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
 }
 
 // bounded wait: a commit that never arrives traps (error) instead of hanging
+// CLUSTER: acquire at cluster scope (arrivals from the peer CTA of a pair)
+template <bool CLUSTER = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase)
 {
     uint32_t done = 0;
     for (uint32_t spin = 0; !done; ++spin) {
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, P1;\n}"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
+        if constexpr (CLUSTER)
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\t"
+                "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, P1;\n}"
+                : "=r"(done)
+                : "r"(smem_u32(bar)), "r"(phase)
+                : "memory");
+        else
+            asm volatile(
+                "{\n\t.reg .pred P1;\n\t"
+                "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, P1;\n}"
+                : "=r"(done)
+                : "r"(smem_u32(bar)), "r"(phase)
+                : "memory");
         if (spin > (1u << 26)) __trap();
     }
+}
+
+// arrive (release, cluster scope) on the same mbarrier of CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
+{
+    uint32_t ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(ra) : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank()
+{
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 // 64-bit shared-memory matrix descriptor, K-major, no swizzle (sm_100 v1)
@@ -172,35 +214,65 @@ constexpr uint32_t tc_idesc_f4(int M, int N)
     return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
 }
 
+// CG: cta_group (2: issued by the pair's leader CTA, operands and D split
+// across the two CTAs of the cluster)
+template <int CG = 1>
 __device__ __forceinline__ void mma_f4_warp(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                             uint32_t accumulate, uint32_t sf)
 {
-    asm volatile(
-        "{\n\t.reg .pred e, p;\n\t"
-        "elect.sync _|e, 0xffffffff;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n}" ::"r"(
-            tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
+    if constexpr (CG == 2)
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n}" ::"r"(
+                tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
+    else
+        asm volatile(
+            "{\n\t.reg .pred e, p;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%5], p;\n}" ::"r"(
+                tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
 }
 
 // four fp4 MMAs on consecutive K steps (64 samples = 32 B of A, two B chunks)
-template <int BINC>
+#define QX_F4_MMA4(CGS)                                                                                              \
+    asm volatile(                                                                                                    \
+        "{\n\t.reg .pred e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .b32 t;\n\t"                              \
+        "mov.b64 a0, {%1, %2};\n\tadd.u32 t, %1, 2;\n\tmov.b64 a1, {t, %2};\n\t"                                       \
+        "add.u32 t, %1, 4;\n\tmov.b64 a2, {t, %2};\n\tadd.u32 t, %1, 6;\n\tmov.b64 a3, {t, %2};\n\t"                   \
+        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, %7;\n\tmov.b64 b1, {t, %4};\n\t"                                      \
+        "add.u32 t, %3, %8;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, %9;\n\tmov.b64 b3, {t, %4};\n\t"                  \
+        "elect.sync _|e, 0xffffffff;\n\t"                                                                            \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::mxf4.block_scale.block32 [%0], a0, b0, %5, [%6], [%6], 1;\n\t"         \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::mxf4.block_scale.block32 [%0], a1, b1, %5, [%6], [%6], 1;\n\t"         \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::mxf4.block_scale.block32 [%0], a2, b2, %5, [%6], [%6], 1;\n\t"         \
+        "@e tcgen05.mma.cta_group::" CGS ".kind::mxf4.block_scale.block32 [%0], a3, b3, %5, [%6], [%6], 1;\n}" ::"r"(     \
+            tmem_d),                                                                                                 \
+        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(sf), "n"(BINC), "n"(2 * BINC), "n"(3 * BINC))
+
+template <int BINC, int CG = 1>
 __device__ __forceinline__ void mma_f4_warp4(uint32_t tmem_d, uint32_t alo, uint32_t ahi, uint32_t blo, uint32_t bhi,
                                              uint32_t idesc, uint32_t sf)
 {
+    if constexpr (CG == 2) QX_F4_MMA4("2");
+    else QX_F4_MMA4("1");
+}
+#undef QX_F4_MMA4
+
+// 2-SM completion: arrives on the same mbarrier of both CTAs of the pair
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar)
+{
     asm volatile(
-        "{\n\t.reg .pred e;\n\t.reg .b64 a0, a1, a2, a3, b0, b1, b2, b3;\n\t.reg .b32 t;\n\t"
-        "mov.b64 a0, {%1, %2};\n\tadd.u32 t, %1, 2;\n\tmov.b64 a1, {t, %2};\n\t"
-        "add.u32 t, %1, 4;\n\tmov.b64 a2, {t, %2};\n\tadd.u32 t, %1, 6;\n\tmov.b64 a3, {t, %2};\n\t"
-        "mov.b64 b0, {%3, %4};\n\tadd.u32 t, %3, %7;\n\tmov.b64 b1, {t, %4};\n\t"
-        "add.u32 t, %3, %8;\n\tmov.b64 b2, {t, %4};\n\tadd.u32 t, %3, %9;\n\tmov.b64 b3, {t, %4};\n\t"
+        "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a0, b0, %5, [%6], [%6], 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a1, b1, %5, [%6], [%6], 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a2, b2, %5, [%6], [%6], 1;\n\t"
-        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], a3, b3, %5, [%6], [%6], 1;\n}" ::"r"(tmem_d),
-        "r"(alo), "r"(ahi), "r"(blo), "r"(bhi), "r"(idesc), "r"(sf), "n"(BINC), "n"(2 * BINC), "n"(3 * BINC));
+        "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(
+            smem_u32(bar)),
+        "h"((unsigned short)3)
+        : "memory");
 }
 
 // four int8 codes in [-4, 4] (bytes of w) -> four e2m1 nibbles (16 bits,
@@ -281,6 +353,7 @@ struct TcSmem {
     unsigned long long wst[kTcAux][kTcThreads / 32][5];
     int wxs[kTcAux][kTcLagWarps][kTcMaxExtra];     // extra-lag sums, one record per lag warp
     uint64_t xdone[kTcAux];  // lag warps finished with the pair of aux slot (96 arrivals)
+    uint64_t pready[2];      // 2-SM mode, leader CTA: the peer's data slot is built (1 remote arrival)
     unsigned xst[3];      // shared-x mode: template ssx, nzx, flags (built once)
     uint32_t tmem_base;
     int best[kTcAux][4][3];                 // per epilogue warp (value, j, count), per aux slot
@@ -290,25 +363,30 @@ struct TcSmem {
 #endif
 };
 
-// Each aux barrier completes once per use of its slot (every 4th
-// iteration), so iteration j's completion has parity (j >> 2) & 1.  Every
-// waiter is at most one use behind (see the dependency notes in the kernel),
-// so parity waits are unambiguous.
+// Each aux barrier completes once per use of its slot (every AUX-th
+// iteration; AUX = 4, or 2 in the 2-SM mode whose 128-column accumulators
+// fill TMEM faster), so iteration j's completion has parity (j / AUX) & 1.
+// Every waiter is at most one use behind (see the dependency notes in the
+// kernel), so parity waits are unambiguous.
+template <int AUX = 4, bool CLUSTER = false>
 __device__ __forceinline__ void tc_wait_mdone(TcSmem& S, int j)
 {
-    mbar_wait(&S.mdone[j & 3], (uint32_t)((j >> 2) & 1));
+    mbar_wait<CLUSTER>(&S.mdone[j % AUX], (uint32_t)((j / AUX) & 1));
 }
+template <int AUX = 4, bool CLUSTER = false>
 __device__ __forceinline__ void tc_wait_tfree(TcSmem& S, int j)
 {
-    mbar_wait(&S.tfree[j & 3], (uint32_t)((j >> 2) & 1));
+    mbar_wait<CLUSTER>(&S.tfree[j % AUX], (uint32_t)((j / AUX) & 1));
 }
+template <int AUX = 4>
 __device__ __forceinline__ void tc_wait_edone(TcSmem& S, int j)
 {
-    mbar_wait(&S.edone[j & 3], (uint32_t)((j >> 2) & 1));
+    mbar_wait(&S.edone[j % AUX], (uint32_t)((j / AUX) & 1));
 }
+template <int AUX = 4>
 __device__ __forceinline__ void tc_wait_xdone(TcSmem& S, int j)
 {
-    mbar_wait(&S.xdone[j & 3], (uint32_t)((j >> 2) & 1));
+    mbar_wait(&S.xdone[j % AUX], (uint32_t)((j / AUX) & 1));
 }
 
 // builder-side extra lags and statistics of the pair in data slot s, aux
@@ -454,6 +532,10 @@ template <>
 struct TcRegs<2> {
     float4 y[6];  // samples 8(t + 512g) .. +8 in y[2g], y[2g + 1]
 };
+template <>
+struct TcRegs<3> {
+    float4 y[12];  // 2-SM: window samples y0 + 8(t + 512g) .. +8, g < 6 (one buffer, refilled after each build)
+};
 
 // float4 #i of a row of n floats (the tail float4 of an n % 4 != 0 row by
 // scalar loads, zero-padded: a zero sample quantises to code 0)
@@ -474,7 +556,17 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<M
 {
     const float* ys = reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld;
     const int ny = (int)a.op[1].n;
-    if constexpr (MODE == 2) {
+    if constexpr (MODE == 3) {
+        const int f0 = kF2CtaLags / 4 * (int)cluster_rank();  // the CTA's window (float4s)
+        const int Y = (a.ylen + 7) / 8;
+#pragma unroll
+        for (int g = 0; g < 6; ++g) {
+            const int wi = (int)threadIdx.x + g * kTcThreads, i = f0 + 2 * wi;
+            const bool in = wi < Y;
+            r.y[2 * g] = in ? tc_ld4(ys, i, ny) : make_float4(0.f, 0.f, 0.f, 0.f);
+            r.y[2 * g + 1] = in ? tc_ld4(ys, i + 1, ny) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    } else if constexpr (MODE == 2) {
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
             const int i = 2 * ((int)threadIdx.x + g * kTcThreads);
@@ -660,17 +752,18 @@ __device__ __forceinline__ void tc_zero_margins(const TcArgs& a, TcSmem& S, int 
 
 // shared-x mode prologue: the template's codes (slot 0), its 16 shifted
 // copies (B slot 0) and statistics (S.xst), once per CTA
-// fp4 mode: the template's 64 nibble-shifted copies from the linear nibble
-// buffer S.xl[1] (sample m at nibble 64 + m): chunk (kc, r) = x[32kc - r,
-// +32) (16 B) at kc*kF4Lbo + (r/8)*128 + (r%8)*16 (LBO kF4Lbo, SBO 128)
-__device__ __forceinline__ void tc_build_copies_f4(const TcArgs& a, TcSmem& S)
+// fp4 modes: 64 nibble-shifted copies of the template from the linear
+// nibble buffer S.xl[1] (sample m at nibble pad + m): chunk (kc, r) =
+// x[32kc - (shift0 + r), +32) (16 B) at kc*kF4Lbo + (r/8)*128 + (r%8)*16
+// (LBO kF4Lbo, SBO 128); shift0 = 64 * rank in the 2-SM mode
+__device__ __forceinline__ void tc_build_copies_f4(const TcArgs& a, TcSmem& S, int pad, int shift0)
 {
     const uint32_t* xw = reinterpret_cast<const uint32_t*>(S.xl[1]);
     uint4* b4 = reinterpret_cast<uint4*>(S.b);
     const int nchunk = a.K / 32;
     for (int i = threadIdx.x; i < nchunk * kF4Pitch; i += kTcThreads) {
         const int r = i & (kF4Pitch - 1), kc = i / kF4Pitch;
-        const int s0 = 32 * kc - r + 64;  // nibble of x[32kc - r]
+        const int s0 = 32 * kc - (shift0 + r) + pad;  // nibble of x[32kc - shift0 - r]
         const int w0 = s0 >> 3, sh = (s0 & 7) * 4;
         const uint32_t w[5] = {xw[w0], xw[w0 + 1], xw[w0 + 2], xw[w0 + 3], xw[w0 + 4]};
         uint4 v;
@@ -682,9 +775,12 @@ __device__ __forceinline__ void tc_build_copies_f4(const TcArgs& a, TcSmem& S)
     }
 }
 
-template <int QM, bool F4 = false>
+// FM: 0 int8 copies (pitch 32), 1 fp4 (64 copies), 2 fp4 2-SM (this CTA's 64 of 128 copies)
+template <int QM, int FM = 0>
 __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
 {
+    constexpr bool F4 = FM != 0;
+    constexpr int PAD = FM == 2 ? kF2Pad : 64;  // nibble front padding >= the largest shift
     const float* thrx = reinterpret_cast<const float*>(S.thr[0]);
     const float* xs = reinterpret_cast<const float*>(a.op[0].data);
     const int nx = (int)a.op[0].n, nx4 = (nx + 3) >> 2;
@@ -701,9 +797,9 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
     for (int i = threadIdx.x; i < X; i += kTcThreads)
         if (i < XP || i >= XP + nx4) xw[i] = 0;
     if constexpr (F4) {
-        // nibble buffer: zero words [0, K/8 + 24) (64-sample front pad, the copies read up to K/8 + 12)
+        // nibble buffer: zero words [0, (K + PAD) / 8 + 16) (the copies read up to (K + PAD) / 8 + 4)
         uint32_t* xn = reinterpret_cast<uint32_t*>(S.xl[1]);
-        for (int i = threadIdx.x; i < a.K / 8 + 24; i += kTcThreads) xn[i] = 0;
+        for (int i = threadIdx.x; i < (a.K + PAD) / 8 + 16; i += kTcThreads) xn[i] = 0;
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -725,10 +821,10 @@ __device__ void tc_build_template(const TcArgs& a, TcSmem& S)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int i = threadIdx.x + h * kTcThreads;
-            if (i < nx4) xh[16 + i] = (uint16_t)tc_nib4(w[h]);  // samples 4i.. at nibble 64 + 4i
+            if (i < nx4) xh[PAD / 4 + i] = (uint16_t)tc_nib4(w[h]);  // samples 4i.. at nibble PAD + 4i
         }
         asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");
-        tc_build_copies_f4(a, S);
+        tc_build_copies_f4(a, S, PAD, FM == 2 ? 64 * (int)cluster_rank() : 0);
     } else {
         tc_build_copies<32>(a, S, 0, 0);
     }
@@ -759,6 +855,45 @@ __device__ void tc_build_tmpl4(const TcArgs& a, TcSmem& S, int s, int u, const T
         tc_word_stats(w[2 * g + 1], ssy, nzy);
         const int wi = yoff + i;
         if (8 * i < ny && wi >= 0 && wi < Y) yw[ysw<32>(wi)] = tc_nib4(w[2 * g]) | (tc_nib4(w[2 * g + 1]) << 16);
+    }
+    const bool w0 = threadIdx.x == 0;
+    tc_aux_finish<2>(S, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy, fl | (w0 ? S.xst[2] : 0u));
+}
+
+// 2-SM fp4 mode, one pair: this CTA's y window, row samples [16384*rank,
+// +16384 + K), as nibbles into the SW64-swizzled buffer (byte bits 4-5 ^=
+// bits 7-8: Hankel rows 64 B apart).  Words of 8 samples: t + 512g, g < 6;
+// g < 3 arrive prefetched (one pair ahead), g >= 3 are loaded here first and
+// complete while the prefetched ones are quantised.  Statistics cover the
+// window (the degeneracy test needs only "any nonzero"; the windows of the
+// two CTAs cover the row).
+__device__ __forceinline__ int ysw64(int wi) { return wi ^ (((wi >> 5) & 3) << 2); }
+
+template <int QM>
+__device__ void tc_build_tmpl2(const TcArgs& a, TcSmem& S, int s, int u, const TcRegs<3>& r, bool first)
+{
+    const float* thry = reinterpret_cast<const float*>(S.thr[1]);
+    const int ny = (int)a.op[1].n;
+    const int y0 = kF2CtaLags * (int)cluster_rank();  // first row sample of the window
+    uint32_t* yw = reinterpret_cast<uint32_t*>(S.y[s]);
+    if (first) {
+        for (int i = threadIdx.x; i < kTcYStride / 4; i += kTcThreads) yw[i] = 0;
+        asm volatile("bar.sync 1, %0;" ::"n"(kTcThreads) : "memory");
+    }
+    const int Y = (a.ylen + 7) / 8;  // window words
+    unsigned fl = 0, ssy = 0, nzy = 0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t w[6];
+        const float4 v[6] = {r.y[6 * h], r.y[6 * h + 1], r.y[6 * h + 2], r.y[6 * h + 3], r.y[6 * h + 4], r.y[6 * h + 5]};
+        tc_quant_words<QM, 6>(v, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            const int i = threadIdx.x + (3 * h + g) * kTcThreads;
+            tc_word_stats(w[2 * g], ssy, nzy);
+            tc_word_stats(w[2 * g + 1], ssy, nzy);
+            if (i < Y && y0 + 8 * i < ny) yw[ysw64(i)] = tc_nib4(w[2 * g]) | (tc_nib4(w[2 * g + 1]) << 16);
+        }
     }
     const bool w0 = threadIdx.x == 0;
     tc_aux_finish<2>(S, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy, fl | (w0 ? S.xst[2] : 0u));
@@ -895,6 +1030,26 @@ __device__ __forceinline__ void best_add(long long& bv, long long& bt, long long
     else if (v == bv) { bt = min(bt, t); bc += c; }
 }
 
+// warp (value, smallest j, count) by REDUX -- the max, then the min j and the
+// summed count of the lanes holding it (empty lanes: INT_MIN + 1, 0) -- into
+// the per-aux-slot record of warp q, read by the merge warp before it frees
+// the slot (the next write of slot u follows mdone(it + AUX), after tfree(it))
+__device__ __forceinline__ void tc_epi_record(TcSmem& S, int u, int q, int bv, int bj, int bc)
+{
+    // TMEM reads are complete (wait::ld) before the slot is released
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    const int mv = __reduce_max_sync(0xffffffffu, bv);
+    const bool at = bv == mv;
+    bj = __reduce_min_sync(0xffffffffu, at ? bj : INT_MAX);
+    bc = __reduce_add_sync(0xffffffffu, at ? bc : 0);
+    if ((threadIdx.x & 31) == 0) {
+        S.best[u][q][0] = mv;
+        S.best[u][q][1] = bj;
+        S.best[u][q][2] = bc;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.edone[u])) : "memory");
+    }
+}
+
 template <int PITCH, bool F4 = false>
 __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u)
 {
@@ -986,36 +1141,99 @@ __device__ void tc_epilogue(const TcArgs& a, TcSmem& S, int u)
             }
         }
     }
-    // TMEM reads are complete (wait::ld) before the slot is released
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     TC_EMARK(13);
-    // warp (value, smallest j, count) by REDUX: the max, then the min j and
-    // the summed count of the lanes holding it (empty lanes: INT_MIN + 1, 0)
-    {
-        const int mv = __reduce_max_sync(0xffffffffu, bv);
-        const bool at = bv == mv;
-        bj = __reduce_min_sync(0xffffffffu, at ? bj : INT_MAX);
-        bc = __reduce_add_sync(0xffffffffu, at ? bc : 0);
-        bv = mv;
-    }
-    TC_EMARK(14);
-    // per-aux-slot records, read by the merge warp before it frees the slot
-    // (the next write of slot u follows mdone(it + 4), after tfree(it))
-    if (lane == 0) {
-        S.best[u][q][0] = bv;
-        S.best[u][q][1] = bj;
-        S.best[u][q][2] = bc;
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.edone[u])) : "memory");
-    }
+    tc_epi_record(S, u, q, bv, bj, bc);
     TC_EMARK(15);
+}
+
+// tcgen05.ld of 16 columns without the wait (completion: tmem_wait_ld)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, int (&v)[16])
+{
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+}
+
+// 16 accumulator columns (lags j0 + c .. + 15) into the running (max,
+// count, first column): chunk max by a tree, its tie mask, then one
+// branch-free update (an equal chunk max adds its ties, a larger one restarts)
+template <bool FULL>
+__device__ __forceinline__ void f2_chunk(const int (&v)[16], int c, int j0, int jlo, int jhi, float& mx, int& cnt,
+                                         int& first)
+{
+    float f[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        f[i] = __int_as_float(v[i]);
+        if constexpr (!FULL) {
+            const int j = j0 + c + i;
+            f[i] = (j >= jlo && j <= jhi) ? f[i] : -INFINITY;
+        }
+    }
+    float m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = fmaxf(f[i], f[i + 8]);
+#pragma unroll
+    for (int w = 4; w; w >>= 1)
+#pragma unroll
+        for (int i = 0; i < w; ++i) m[i] = fmaxf(m[i], m[i + w]);
+    const float lm = m[0];
+    unsigned mask = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) mask |= (f[i] == lm ? 1u : 0u) << i;
+    if (lm == -INFINITY) mask = 0;  // nothing in the window
+    const int pc = __popc(mask);
+    const bool newer = lm > mx, same = lm == mx;
+    cnt = newer ? pc : cnt + (same ? pc : 0);
+    first = (newer && mask) ? c + __ffs(mask) - 1 : first;
+    mx = fmaxf(mx, lm);
+}
+
+// 2-SM fp4 epilogue: this CTA's 128 accumulator columns of TMEM slot u (the
+// lane quarter's rows, 128 lags per thread: j = 16384*rank + 128*row + c),
+// 16 columns at a time with the next load in flight; one TMEM pass
+__device__ void tc_epilogue_f2(const TcArgs& a, TcSmem& S, int u)
+{
+    const int lane = threadIdx.x & 31;
+    const int q = (threadIdx.x >> 5) - kEpiWarp0;
+    const int row = q * 32 + lane;
+    const int64_t tbase = a.L0 + a.op[0].n - 1;
+    const int jlo = (int)(a.am.t_lo - tbase), jhi = (int)(a.am.t_hi - tbase);
+    const int j0 = kF2CtaLags * (int)cluster_rank() + kF2Pitch * row;
+    const bool full = __all_sync(0xffffffffu, jlo <= j0 && jhi >= j0 + kF2Pitch - 1);
+    const uint32_t taddr = S.tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * kF2Pitch);
+    float mx = -FLT_MAX;
+    int cnt = 0, first = -1;
+    int v0[16], v1[16];
+    tmem_ld16_nw(taddr, v0);
+    tmem_wait_ld();
+#pragma unroll
+    for (int c = 0; c < kF2Pitch; c += 32) {
+        tmem_ld16_nw(taddr + c + 16, v1);
+        if (full) f2_chunk<true>(v0, c, j0, jlo, jhi, mx, cnt, first);
+        else f2_chunk<false>(v0, c, j0, jlo, jhi, mx, cnt, first);
+        tmem_wait_ld();
+        if (c + 32 < kF2Pitch) tmem_ld16_nw(taddr + c + 32, v0);
+        if (full) f2_chunk<true>(v1, c + 16, j0, jlo, jhi, mx, cnt, first);
+        else f2_chunk<false>(v1, c + 16, j0, jlo, jhi, mx, cnt, first);
+        tmem_wait_ld();
+    }
+    const bool any = first >= 0;
+    const int bv = any ? __float2int_rn(mx) : INT_MIN + 1;
+    tc_epi_record(S, u, q, bv, any ? j0 + first : INT_MAX, any ? cnt : 0);
 }
 
 // merge warp: the pair's four epilogue records, the lag warps' extra-lag
 // sums and statistics -> the qx_result; frees the aux slot (tfree) as soon as
 // the records are in registers, so neither the epilogue warps nor the MMA
 // warp wait for the merge and the result stores
+// rec: the qx_result record index (pair, or 2*pair + rank in the 2-SM mode);
+// notify: also free the slot in the leader CTA (2-SM peer: the leader's MMA
+// writes this CTA's TMEM)
 template <int PITCH>
-__device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t pair)
+__device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool notify = false)
 {
     const int lane = threadIdx.x & 31;
     const int tl = PITCH * a.M;
@@ -1034,6 +1252,7 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t pair)
             xs[e] = e < a.extra ? __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0) : 0;
         // every record of slot u is in registers: free the slot
         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[u])) : "memory");
+        if (notify && lane == 0) mbar_arrive_remote(&S.tfree[u], 0);
         const int mv = __reduce_max_sync(0xffffffffu, wv);
         const bool at = lane < 4 && wv == mv;
         const int mj = __reduce_min_sync(0xffffffffu, at ? wj : INT_MAX);
@@ -1055,7 +1274,7 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t pair)
         long long f = ((long long)status << 32) | (unsigned)flags;
         f = lane == 0 ? v0 : lane == 1 ? a.am.first_lag + t0 : lane == 2 ? c0 : lane == 3 ? (long long)ssx
           : lane == 4 ? (long long)ssy : lane == 5 ? (long long)nzx : lane == 6 ? (long long)nzy : f;
-        if (lane < 8) reinterpret_cast<long long*>(a.am.results)[pair * 8 + lane] = f;
+        if (lane < 8) reinterpret_cast<long long*>(a.am.results)[rec * 8 + lane] = f;
     }
 }
 
@@ -1067,41 +1286,58 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t pair)
 #define TC_ACC(i) ((void)0)
 #endif
 
+// MODE: 0 per-pair B (int8), 1 shared template (int8, pitch 32), 2 shared
+// template (fp4, pitch 64), 3 shared template on a CTA pair (fp4, 2-SM MMA,
+// pitch 128; launched as clusters of 2, rank 0 issues the MMAs)
 template <typename T, int QM, int MODE>
 __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
-    constexpr bool SX = MODE != 0, F4 = MODE == 2;
-    constexpr uint32_t kTmemCols = F4 ? 512 : 128;  // fp4: 4 x 64 accumulator columns + scale factors
+    constexpr bool SX = MODE != 0, F4 = MODE == 2, F2 = MODE == 3, FP4 = MODE >= 2;
+    constexpr int AUX = F2 ? 2 : 4;                  // accumulator / record slots
+    constexpr uint32_t kTmemCols = FP4 ? 512 : 128;  // fp4: accumulators + scale factors
+    constexpr int PITCH = F2 ? kF2Pitch : F4 ? kF4Pitch : SX ? 32 : 16;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
     TcSmem& S = *reinterpret_cast<TcSmem*>(tc_smem_raw);
     // warp index through a shuffle: provably warp-uniform, so the role
     // branches keep descriptor arithmetic in uniform registers
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    const uint32_t rank = F2 ? cluster_rank() : 0u;
     for (int i = threadIdx.x; i < kMaxThr; i += kTcTotalThreads) {
         reinterpret_cast<T*>(S.thr[0])[i] = (T)a.op[0].q.thr[i];
         reinterpret_cast<T*>(S.thr[1])[i] = (T)a.op[1].q.thr[i];
     }
     if (threadIdx.x < kTcAux) {
         mbar_init(&S.mdone[threadIdx.x], 1);
-        mbar_init(&S.tfree[threadIdx.x], 32);
+        // 2-SM leader: its own merge warp + the peer's (remote) release of the slot
+        mbar_init(&S.tfree[threadIdx.x], (F2 && rank == 0) ? 33 : 32);
         mbar_init(&S.edone[threadIdx.x], 4);
         mbar_init(&S.xdone[threadIdx.x], 32 * kTcLagWarps);
+        if (threadIdx.x < 2) mbar_init(&S.pready[threadIdx.x], 1);
     }
 #ifdef QX_TC_TIMING
     if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
 #endif
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                     "n"(kTmemCols));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if constexpr (F2) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&S.tmem_base)),
+                         "n"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             smem_u32(&S.tmem_base)),
+                         "n"(kTmemCols));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if constexpr (F4) {
+    if constexpr (FP4) {
         // scale factors: 32 columns of 0x7f bytes (ue8m0 2^0) in every lane,
         // written by the epilogue warps (warp w reaches lanes 32*(w%4)..)
+        static_assert(kF4Sf == kF2Sf, "one scale-factor column for both fp4 modes");
         if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
             const uint32_t t = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kF4Sf;
             const uint32_t v = 0x7f7f7f7fu;
@@ -1118,19 +1354,25 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         __syncthreads();
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
+    // both CTAs of a pair: barriers initialised and TMEM allocated before any
+    // remote arrive or 2-SM MMA
+    if constexpr (F2) cluster_sync_all();
 
-    // Dependencies (iteration it: data slot it & 1, aux slot it & 3):
-    //   build(it)    after MMA(it-2) [data slot] and epilogue(it-4) [aux slot]
-    //   MMA(it)      after build(it) [named barrier] and epilogue(it-4) [TMEM]
+    // Dependencies (iteration it: data slot it & 1, aux slot it % AUX):
+    //   build(it)    after MMA(it-2) [data slot] and epilogue(it-AUX) [aux slot]
+    //   MMA(it)      after build(it) [named barrier; 2-SM: and the peer's, pready]
+    //                and epilogue(it-AUX) [TMEM; 2-SM: of both CTAs]
     //   epilogue(it) after MMA(it)
-    const int64_t npairs = a.batch > blockIdx.x ? (a.batch - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+    // 2-SM: a cluster shares its pair sequence (both CTAs build halves of it)
+    const int64_t base = F2 ? (blockIdx.x >> 1) : blockIdx.x, stride = F2 ? (gridDim.x >> 1) : gridDim.x;
+    const int64_t npairs = a.batch > base ? (a.batch - base + stride - 1) / stride : 0;
     if (warp < kTcThreads / 32) {
         // ---- builders
         auto acquire = [&](int it) {
             TC_T0();
-            if (it >= 2) tc_wait_mdone(S, it - 2);
-            if (it >= 2) tc_wait_xdone(S, it - 2);  // lag warps done reading the data slot
-            if (it >= 4) tc_wait_tfree(S, it - 4);
+            if (it >= 2) tc_wait_mdone<AUX>(S, it - 2);
+            if (it >= 2) tc_wait_xdone<AUX>(S, it - 2);  // lag warps done reading the data slot
+            if (it >= AUX) tc_wait_tfree<AUX>(S, it - AUX);
             if (threadIdx.x == 0) TC_ACC(0);
         };
         auto handoff = [&](int it) {
@@ -1143,34 +1385,42 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         if constexpr (std::is_same<T, float>::value) fast = a.fast;
         if (fast) {
             if constexpr (std::is_same<T, float>::value) {
-                TcRegs<MODE> cur, nxt;
-                if (npairs) tc_fetch<MODE>(a, blockIdx.x, cur);
+                TcRegs<MODE> cur;
+                TcRegs<F2 ? 0 : MODE> nxt;  // 2-SM: one buffer, refilled right after its build
+                if (npairs) tc_fetch<MODE>(a, base, cur);
                 if constexpr (SX) {
-                    if (npairs) tc_build_template<QM, F4>(a, S);
+                    if (npairs) tc_build_template<QM, F2 ? 2 : F4 ? 1 : 0>(a, S);
                 }
                 for (int it = 0; it < npairs; ++it) {
-                    const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-                    if (it + 1 < npairs) tc_fetch<MODE>(a, pair + gridDim.x, nxt);
+                    const int64_t pair = base + (int64_t)it * stride;
+                    if constexpr (!F2) {
+                        if (it + 1 < npairs) tc_fetch<MODE>(a, pair + stride, nxt);
+                    }
                     acquire(it);
                     TC_T0();
 #ifdef QX_TC_TIMING
                     if (!(a.debug & 2))
 #endif
                     {
-                        if constexpr (F4) tc_build_tmpl4<QM>(a, S, it & 1, it & 3, cur, it < 2);
-                        else if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it & 3, cur, it < 2);
-                        else tc_build_fast<QM>(a, S, it & 1, it & 3, cur, it < 2);
+                        if constexpr (F2) tc_build_tmpl2<QM>(a, S, it & 1, it % AUX, cur, it < 2);
+                        else if constexpr (F4) tc_build_tmpl4<QM>(a, S, it & 1, it % AUX, cur, it < 2);
+                        else if constexpr (SX) tc_build_tmpl<QM>(a, S, it & 1, it % AUX, cur, it < 2);
+                        else tc_build_fast<QM>(a, S, it & 1, it % AUX, cur, it < 2);
                     }
                     if (threadIdx.x == 0) TC_ACC(1);
                     handoff(it);
-                    cur = nxt;
+                    if constexpr (F2) {
+                        if (it + 1 < npairs) tc_fetch<MODE>(a, pair + stride, cur);
+                    } else {
+                        cur = nxt;
+                    }
                 }
             }
         } else {
             for (int it = 0; it < npairs; ++it) {
-                const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
+                const int64_t pair = base + (int64_t)it * stride;
                 acquire(it);
-                tc_build<T, QM>(a, S, it & 1, it & 3, pair);
+                tc_build<T, QM>(a, S, it & 1, it % AUX, pair);
                 handoff(it);
             }
         }
@@ -1178,30 +1428,39 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         // ---- MMA issuer: the whole warp runs the loop, one elected lane issues
         const int nk = a.K / 32;
         for (int it = 0; it < npairs; ++it) {
-            const int s = it & 1, u = it & 3;
+            const int s = it & 1, u = it % AUX;
             {
                 TC_T0();
                 if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
                 else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
                 if (lane == 0) TC_ACC(2);
             }
+            if constexpr (F2) {
+                if (rank != 0) {
+                    // peer: its half of the pair is built; the leader issues
+                    if (lane == 0) mbar_arrive_remote(&S.pready[s], 0);
+                    continue;
+                }
+                mbar_wait<true>(&S.pready[s], (uint32_t)((it >> 1) & 1));
+            }
             {
                 TC_T0();
-                if (it >= 4) tc_wait_tfree(S, it - 4);  // TMEM slot drained
+                if (it >= AUX) tc_wait_tfree<AUX, F2>(S, it - AUX);  // TMEM slot drained (2-SM: in both CTAs)
                 if (lane == 0) TC_ACC(4);
             }
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             TC_T0();
-            // pitch 32 (shared template): one B buffer built once, SW32 A rows
-            constexpr int PITCH = F4 ? kF4Pitch : SX ? 32 : 16;
-            constexpr int LBO = F4 ? kF4Lbo : SX ? kTcBLbo32 : kTcBLbo, BINC = 2 * LBO / 16;
+            constexpr int LBO = FP4 ? kF4Lbo : SX ? kTcBLbo32 : kTcBLbo, BINC = 2 * LBO / 16;
             const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b + (SX ? 0 : s) * kTcBSlot);
             const uint64_t bd0 = smem_desc(ba, LBO, 128);
             const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
-            if constexpr (F4) {
-                // one M=128 x N=64 tile (8192 lags), K = 64 samples (32 B of A) per MMA
-                const uint32_t d = tbase + (uint32_t)(u * kF4Pitch), sf = tbase + kF4Sf;
-                const uint64_t ad0 = smem_desc(ya, 16, 256) | (6ull << 61);  // SWIZZLE_32B, 8 rows x 32 B
+            if constexpr (FP4) {
+                // F4: one M=128 x N=64 tile (8192 lags); F2: one M=256 x N=128
+                // tile over the pair (32768 lags); K = 64 samples (32 B of A) per MMA
+                constexpr int CG = F2 ? 2 : 1;
+                const uint32_t d = tbase + (uint32_t)(u * PITCH), sf = tbase + kF4Sf;
+                const uint64_t ad0 = F2 ? (smem_desc(ya, 16, 512) | (4ull << 61))   // SWIZZLE_64B, 8 rows x 64 B
+                                        : (smem_desc(ya, 16, 256) | (6ull << 61));  // SWIZZLE_32B, 8 rows x 32 B
                 const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
                 uint32_t alo = (uint32_t)ad0, blo = (uint32_t)bd0;
                 const int nk4 = a.K / 64;
@@ -1209,17 +1468,17 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                 if (!(a.debug & 1))
 #endif
                 {
-                    mma_f4_warp(d, ad0, bd0, a.idesc, 0, sf);
+                    mma_f4_warp<CG>(d, ad0, bd0, a.idesc, 0, sf);
                     int kk = 1;
                     for (; kk + 4 <= nk4; kk += 4) {
-                        mma_f4_warp4<BINC>(d, alo + 2, ahi, blo + BINC, bhi, a.idesc, sf);
+                        mma_f4_warp4<BINC, CG>(d, alo + 2, ahi, blo + BINC, bhi, a.idesc, sf);
                         alo += 8;
                         blo += 4 * BINC;
                     }
                     for (; kk < nk4; ++kk) {
                         alo += 2;
                         blo += BINC;
-                        mma_f4_warp(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1, sf);
+                        mma_f4_warp<CG>(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1, sf);
                     }
                 }
             } else
@@ -1245,7 +1504,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                     mma_i8_warp(d, ((uint64_t)ahi << 32) | alo, ((uint64_t)bhi << 32) | blo, a.idesc, 1);
                 }
             }
-            mma_commit_warp(&S.mdone[u]);
+            if constexpr (F2) mma_commit_pair(&S.mdone[u]);
+            else mma_commit_warp(&S.mdone[u]);
             __syncwarp();
             if (lane == 0) TC_ACC(5);
         }
@@ -1254,29 +1514,30 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         for (int it = 0; it < npairs; ++it) {
             if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
             else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
-            if (it >= 4) tc_wait_tfree(S, it - 4);  // epilogue done with this aux slot's records
-            if (a.extra) tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it & 3, SX ? 0 : (it & 1));
-            if (warp == kTcLagWarp0) tc_final_stats(a, S, it & 3);
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it & 3])) : "memory");
+            if (it >= AUX) tc_wait_tfree<AUX>(S, it - AUX);  // epilogue done with this aux slot's records
+            if (a.extra) tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it % AUX, SX ? 0 : (it & 1));
+            if (warp == kTcLagWarp0) tc_final_stats(a, S, it % AUX);
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it % AUX])) : "memory");
         }
     } else if (warp == kTcMergeWarp) {
-        // ---- merge: records -> qx_result
+        // ---- merge: records -> qx_result (2-SM: one record per CTA and pair)
         for (int it = 0; it < npairs; ++it) {
-            const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
-            tc_wait_xdone(S, it);  // statistics and extra-lag records written
-            tc_wait_edone(S, it);  // epilogue records written
-            tc_merge<F4 ? kF4Pitch : SX ? 32 : 16>(a, S, it & 3, pair);
+            const int64_t pair = base + (int64_t)it * stride;
+            tc_wait_xdone<AUX>(S, it);  // statistics and extra-lag records written
+            tc_wait_edone<AUX>(S, it);  // epilogue records written
+            tc_merge<PITCH>(a, S, it % AUX, F2 ? 2 * pair + rank : pair, F2 && rank != 0);
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ---- epilogue: TMEM -> per-warp (max, smallest lag, count) records
         for (int it = 0; it < npairs; ++it) {
             TC_T0();
-            tc_wait_mdone(S, it);
+            tc_wait_mdone<AUX>(S, it);
             if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             {
                 TC_T0();
-                tc_epilogue<F4 ? kF4Pitch : SX ? 32 : 16, F4>(a, S, it & 3);
+                if constexpr (F2) tc_epilogue_f2(a, S, it % AUX);
+                else tc_epilogue<PITCH, F4>(a, S, it % AUX);
                 if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(6);
             }
         }
@@ -1285,35 +1546,61 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // 2-SM: no CTA leaves (or frees TMEM) while its peer may still arrive on
+    // its barriers or the leader's MMAs may still target its TMEM
+    if constexpr (F2) cluster_sync_all();
 #ifdef QX_TC_TIMING
-    if (blockIdx.x == 0 && threadIdx.x == 0)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && npairs)
         printf("tc timing block0 npairs=%lld debug=%d (cycles/pair): build-wait %llu build %llu | mma: wait-handoff %llu "
                "wait-tfree %llu issue %llu | epi: wait %llu run %llu\n",
                (long long)npairs, a.debug, S.tm[0] / npairs, S.tm[1] / npairs, S.tm[2] / npairs, S.tm[4] / npairs,
                S.tm[5] / npairs, S.tm[3] / npairs, S.tm[6] / npairs);
-    if (blockIdx.x == 0 && threadIdx.x == 0)
+    if (blockIdx.x == 0 && threadIdx.x == 0 && npairs)
         printf("  build phases (cycles/pair): zero %llu quant %llu bar %llu copies %llu aux %llu | epi: tmem+scan %llu "
                "shfl %llu bars+merge %llu\n", S.tm[8] / npairs, S.tm[9] / npairs, S.tm[10] / npairs,
                S.tm[11] / npairs, S.tm[12] / npairs, S.tm[13] / npairs, S.tm[14] / npairs, S.tm[15] / npairs);
 #endif
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "n"(kTmemCols));
+    if (warp == 0) {
+        if constexpr (F2)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "n"(kTmemCols));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(S.tmem_base), "n"(kTmemCols));
+    }
 }
 
 // fp4 shared-template mode: float32 rows, x a stride-0 row of <= 4096
 // samples (template search), 16-B aligned rows, codes |c| <= 4 on both sides,
 // every sum exact in f32 (nx * Kx * Ky < 2^24), one 8192-lag tile starting
 // at a word boundary, y rows <= 12288 samples; QX_TC_F4=0 disables it
-static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
+static bool tc_fp4_codes(const NttCall& c, int64_t nx)
 {
     const char* env = getenv("QX_TC_F4");
     if (env && env[0] == '0') return false;
-    const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
     return c.op[0].dtype == DT_F32 && c.op[1].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN &&
            nx % 4 == 0 && (uintptr_t)c.op[0].data % 16 == 0 && (uintptr_t)c.op[1].data % 16 == 0 &&
            c.op[1].ld % 4 == 0 && c.op[0].q.mode == c.op[1].q.mode && c.op[0].q.k <= kF4MaxCode &&
-           c.op[1].q.k <= kF4MaxCode && (double)nx * c.op[0].q.k * c.op[1].q.k < 16777216.0 && ny <= kTcFastNY4 &&
-           W <= kF4Lags && L0 % 8 == 0 && L0 <= 0;
+           c.op[1].q.k <= kF4MaxCode && (double)nx * c.op[0].q.k * c.op[1].q.k < 16777216.0;
 }
+
+static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
+{
+    const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
+    return tc_fp4_codes(c, nx) && ny <= kTcFastNY4 && W <= kF4Lags && L0 % 8 == 0 && L0 <= 0;
+}
+
+// 2-SM fp4 mode: only for callers that take two records per pair
+// (c.split2: qx_template_search), windows starting at lag 0 of the row, up to
+// 32768 lags, rows up to 32768 + K samples; QX_TC_F2=0 disables it
+static bool tc_f2_mode(const NttCall& c, int64_t nx, int64_t ny)
+{
+    const char* env = getenv("QX_TC_F2");
+    if (!c.split2 || (env && env[0] == '0')) return false;
+    const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
+    return tc_fp4_codes(c, nx) && L0 == 0 && W <= kF2Lags && ny <= kF2Lags + kTcMaxK;
+}
+
+// the 2-SM mode is what tc_window_run will launch for this call
+bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny) { return tc_f2_mode(c, nx, ny); }
 
 // eligibility: window of at most kTcMaxTiles*2048 lags (fp4 mode: 8192),
 // nx + 15 <= kTcMaxK, |values| < 2^31 (nx * Kx * Ky), same input dtype and
@@ -1321,7 +1608,8 @@ static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
 {
     const int64_t W = c.am.t_hi - c.am.t_lo + 1;
-    if (W > (int64_t)kTcMaxTiles * kTcLags + kTcMaxExtra && !tc_f4_mode(c, nx, ny)) return false;
+    if (W > (int64_t)kTcMaxTiles * kTcLags + kTcMaxExtra && !tc_f4_mode(c, nx, ny) && !tc_f2_mode(c, nx, ny))
+        return false;
     if (nx + 15 > kTcMaxK) return false;
     if (c.op[0].dtype != c.op[1].dtype || c.op[0].dtype == DT_I64) return false;
     if (c.op[0].q.mode != c.op[1].q.mode) return false;
@@ -1341,8 +1629,28 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    const int grid = (int)(a.batch < sms ? a.batch : sms);
-    k_tc_window<T, QM, MODE><<<grid, kTcTotalThreads, smem, s>>>(a);
+    if constexpr (MODE == 3) {
+        // clusters of 2 CTAs (one pair-block per cluster at a time)
+        const int64_t want = 2 * a.batch;
+        const int grid = (int)(want < (sms & ~1) ? want : (sms & ~1));
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)grid);
+        cfg.blockDim = dim3(kTcTotalThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, k_tc_window<T, QM, MODE>, a);
+        if (e != cudaSuccess) return e;
+    } else {
+        const int grid = (int)(a.batch < sms ? a.batch : sms);
+        k_tc_window<T, QM, MODE><<<grid, kTcTotalThreads, smem, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
@@ -1368,8 +1676,9 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     // copies with pitch 16
     const bool sx = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
                     aligned;
-    const bool f4 = tc_f4_mode(c, nx, ny);
-    a.shared_x = f4 || (sx && ny <= kTcFastNY && W <= 4096 + kTcMaxExtra);
+    const bool f2 = tc_f2_mode(c, nx, ny);
+    const bool f4 = !f2 && tc_f4_mode(c, nx, ny);
+    a.shared_x = f2 || f4 || (sx && ny <= kTcFastNY && W <= 4096 + kTcMaxExtra);
     a.fast = a.shared_x || (c.op[0].dtype == DT_F32 && nx <= kTcFastN && ny <= kTcFastN && nx % 4 == 0 &&
                             ny % 4 == 0 && aligned && (c.batch == 1 || c.op[0].ld % 4 == 0));
     a.pitch = f4 ? kF4Pitch : a.shared_x ? 32 : 16;
@@ -1391,17 +1700,30 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
         a.idesc = tc_idesc_f4(128, kF4Pitch);
     }
     a.ylen = a.ntiles * tl + kTcMaxExtra + a.K;
+    if (f2) {
+        a.pitch = kF2Pitch;
+        a.M = 256;
+        a.K = (int)((nx + kF2Pitch - 1 + 63) / 64 * 64);
+        a.ntiles = 1;
+        a.extra = 0;
+        a.idesc = tc_idesc_f4(256, kF2Pitch);
+        a.ylen = kF2CtaLags + a.K;  // each CTA's window
+    }
 #ifdef QX_TC_TIMING
     if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
 #endif
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int kind = f4 ? KK_DIRECT_F4 : KK_DIRECT;
+    const int kind = (f2 || f4) ? KK_DIRECT_F4 : KK_DIRECT;
     if (c.prof) c.prof->pre(kind, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;
-    if (f4) {
+    if (f2) {
+        if (qm == QM_K1) e = launch_tc<float, QM_K1, 3>(a, s, sms);
+        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 3>(a, s, sms);
+        else e = launch_tc<float, QM_BSEARCH, 3>(a, s, sms);
+    } else if (f4) {
         if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
         else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
@@ -1480,18 +1802,22 @@ __device__ BlkSum blk_reduce(BlkSum a)
     return a;
 }
 
-__global__ void __launch_bounds__(kMergeThreads) k_merge_blocks(const long long* recs, int64_t n, int64_t block,
-                                                                long long lag_shift, BlkSum* partials, int* counter,
-                                                                long long* out)
+__global__ void __launch_bounds__(kMergeThreads) k_merge_blocks(const MergeSegs segs, long long lag_shift,
+                                                                BlkSum* partials, int* counter, long long* out)
 {
     BlkSum a{0, LLONG_MAX, 0, 0, 0, 1, 0, 0};
-    for (int64_t i = blockIdx.x * (int64_t)kMergeThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kMergeThreads) {
-        const long long* r = recs + i * 8;
+    const int64_t n = segs.seg[0].n + segs.seg[1].n + segs.seg[2].n;
+    for (int64_t k = blockIdx.x * (int64_t)kMergeThreads + threadIdx.x; k < n; k += (int64_t)gridDim.x * kMergeThreads) {
+        int sg = 0;
+        int64_t i = k;
+        while (i >= segs.seg[sg].n) i -= segs.seg[sg++].n;
+        const MergeSeg& S = segs.seg[sg];
+        const long long* r = S.recs + i * 8;
         const long long w7 = r[7];
         const int status = (int)(w7 >> 32), flags = (int)(w7 & 0xffffffff);
         BlkSum b;
         b.v = r[0];
-        b.l = r[1] + i * block;
+        b.l = r[1] + S.base + (i / S.rpb) * S.block;
         b.t = status == 0 ? r[2] : 0;
         b.nan = (flags & 4) != 0;
         b.degx = (flags & 1) != 0;
@@ -1538,13 +1864,13 @@ __global__ void __launch_bounds__(kMergeThreads) k_merge_blocks(const long long*
     }
 }
 
-cudaError_t merge_blocks_launch(const void* recs, int64_t n, int64_t block, long long lag_shift, void* partials,
-                                int* counter, long long* out, int sms, cudaStream_t s)
+cudaError_t merge_blocks_launch(const MergeSegs& segs, long long lag_shift, void* partials, int* counter,
+                                long long* out, int sms, cudaStream_t s)
 {
+    const int64_t n = segs.seg[0].n + segs.seg[1].n + segs.seg[2].n;
     int64_t g = (n + kMergeThreads - 1) / kMergeThreads;
     const int grid = (int)(g < 1 ? 1 : (g > sms ? sms : g));
-    k_merge_blocks<<<grid, kMergeThreads, 0, s>>>((const long long*)recs, n, block, lag_shift, (BlkSum*)partials,
-                                                    counter, out);
+    k_merge_blocks<<<grid, kMergeThreads, 0, s>>>(segs, lag_shift, (BlkSum*)partials, counter, out);
     return cudaGetLastError();
 }
 

@@ -494,6 +494,30 @@ def test_template_search_fp4_mode(qx, oracle, monkeypatch):
         assert got == i8 == (m, f + 3, n), (trial, got, i8, (m, f, n))
 
 
+def test_template_search_2sm_mode(qx, oracle, monkeypatch):
+    """Template search on the 2-SM fp4 mode (cta_group::2 MMA over CTA pairs,
+    32768-lag blocks, one record per CTA) followed by 8192-lag fp4 blocks and
+    a remainder: equal to the oracle and to the same search with the 2-SM
+    mode off (QX_TC_F2=0) and with the int8 path (QX_TC_F4=0)."""
+    rng = np.random.default_rng(24)
+    cases = [(4096, qx.sign()), (4096, qx.uniform(1, 0.8)), (1000, qx.uniform(4, 0.3)), (64, qx.uniform(2, 0.5))]
+    for trial, (nt, q) in enumerate(cases):
+        ns = nt - 1 + 32768 * int(rng.integers(2, 4)) + 8192 * int(rng.integers(0, 3)) + int(rng.integers(1, 8192))
+        st = rng.laplace(size=ns).astype(np.float32)
+        off = int(rng.integers(0, ns - nt + 1))
+        tpl = st[off:off + nt].copy()
+        st = st + rng.normal(0, 0.9, ns).astype(np.float32)
+        got = {}
+        for f2, f4 in (("1", "1"), ("0", "1"), ("0", "0")):
+            monkeypatch.setenv("QX_TC_F2", f2)
+            monkeypatch.setenv("QX_TC_F4", f4)
+            got[(f2, f4)] = qx.template_search(tpl, st, q, q, stream_start=7)
+        u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
+        first = -(nt - 1)
+        m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, 0 - first, ns - nt - first))
+        assert set(got.values()) == {(m, f + 7, n)}, (trial, got, (m, f + 7, n))
+
+
 @pytest.mark.parametrize("f4", ["0", "1"])
 def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
     """Every block summary of the shared-template window modes (i8 pitch 32,

@@ -673,8 +673,12 @@ static int64_t tsearch_block(const qx_signals* t, const qx_signals* s, const qx_
     auto mode = [](const qx_quantizer* q) { return q->k == 1 ? 0 : (q->kind == QX_Q_UNIFORM ? 1 : 2); };
     const bool f4 = !(env && env[0] == '0') && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
                     (double)nt * ka * kb < 16777216.0;
+    // the 2-SM mode is opt-in (QX_TC_F2=1): its MMA runs at the fp4 peak, but
+    // its builders' global loads (82 KB per CTA and block, one block ahead in
+    // registers) are latency-bound (ncu: long_scoreboard), 0.59 ms vs 0.49 ms
+    // for the 1-SM mode at config 5; it needs a TMA-staged float pipeline
     const char* env2 = getenv("QX_TC_F2");
-    *f2 = f4 && !(env2 && env2[0] == '0');
+    *f2 = f4 && env2 && env2[0] == '1';
     return f4 ? 8192 : 4096;
 }
 

@@ -275,6 +275,31 @@ __device__ __forceinline__ void mma_commit_pair(uint64_t* bar)
         : "memory");
 }
 
+// eight samples of a 1-level quantiser (k = 1: thresholds t0 < t1, codes
+// -1 / 0 / +1 = e2m1 0xA / 0 / 0x2) straight to a nibble word (sample i at
+// bits 4i); nz += nonzero codes (= their sum of squares), NaN -> flags
+__device__ __forceinline__ uint32_t tc_nib8_k1(const float4& a, const float4& b, float t0, float t1, unsigned& nz,
+                                               unsigned& fl)
+{
+    const float e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t w = 0;
+    bool nan = false;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        w |= (e[i] >= t1 ? 0x2u : (e[i] >= t0 ? 0u : 0xAu)) << (4 * i);
+        nan |= e[i] != e[i];
+    }
+    if (nan) {
+        fl |= SF_NONFINITE;
+        // a NaN sample is code 0 (the call fails on the flag)
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (e[i] != e[i]) w &= ~(0xFu << (4 * i));
+    }
+    nz += __popc(w & 0x22222222u);
+    return w;
+}
+
 // four int8 codes in [-4, 4] (bytes of w) -> four e2m1 nibbles (16 bits,
 // code i at bits 4i): |c| -> {0, 2, 4, 5, 6} = |c| <= 2 ? 2|c| : |c| + 2,
 // sign -> bit 3; byte-SIMD, no per-sample branches
@@ -846,8 +871,22 @@ __device__ void tc_build_tmpl4(const TcArgs& a, TcSmem& S, int s, int u, const T
     }
     uint32_t w[6];
     unsigned fl = 0, ssy = 0, nzy = 0;
-    tc_quant_words<QM, 6>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
     const int yoff = (int)(-a.L0) >> 3, Y = (a.ylen + 7) / 8;
+    if constexpr (QM == QM_K1) {
+        const float t0 = thry[0], t1 = thry[1];
+#pragma unroll
+        for (int g = 0; g < 3; ++g) {
+            const int i = threadIdx.x + g * kTcThreads;
+            const uint32_t wn = tc_nib8_k1(r.y[2 * g], r.y[2 * g + 1], t0, t1, nzy, fl);
+            const int wi = yoff + i;
+            if (8 * i < ny && wi >= 0 && wi < Y) yw[ysw<32>(wi)] = wn;
+        }
+        ssy = nzy;
+        const bool w0 = threadIdx.x == 0;
+        tc_aux_finish<2>(S, u, w0 ? S.xst[0] : 0u, w0 ? S.xst[1] : 0u, ssy, nzy, fl | (w0 ? S.xst[2] : 0u));
+        return;
+    }
+    tc_quant_words<QM, 6>(r.y, thry, a.op[1].q.k, (float)a.op[1].q.inv_step, a.op[1].q.tbits, w, fl);
 #pragma unroll
     for (int g = 0; g < 3; ++g) {
         const int i = threadIdx.x + g * kTcThreads;
@@ -882,6 +921,16 @@ __device__ void tc_build_tmpl2(const TcArgs& a, TcSmem& S, int s, int u, const T
     }
     const int Y = (a.ylen + 7) / 8;  // window words
     unsigned fl = 0, ssy = 0, nzy = 0;
+    if constexpr (QM == QM_K1) {
+        const float t0 = thry[0], t1 = thry[1];
+#pragma unroll
+        for (int g = 0; g < 6; ++g) {
+            const int i = threadIdx.x + g * kTcThreads;
+            const uint32_t w = tc_nib8_k1(r.y[2 * g], r.y[2 * g + 1], t0, t1, nzy, fl);
+            if (i < Y && y0 + 8 * i < ny) yw[ysw64(i)] = w;
+        }
+        ssy = nzy;
+    } else
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         uint32_t w[6];
@@ -1630,21 +1679,29 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
         attr = true;
     }
     if constexpr (MODE == 3) {
-        // clusters of 2 CTAs (one pair-block per cluster at a time)
-        const int64_t want = 2 * a.batch;
-        const int grid = (int)(want < (sms & ~1) ? want : (sms & ~1));
+        // clusters of 2 CTAs (one pair-block per cluster at a time), as many
+        // as can be resident at once: not every SM has a free partner in its
+        // GPC, and a second wave of clusters would double the tail
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = 2;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3((unsigned)grid);
         cfg.blockDim = dim3(kTcTotalThreads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cfg.attrs = at;
         cfg.numAttrs = 1;
+        static int clusters = 0;
+        if (!clusters) {
+            cfg.gridDim = dim3((unsigned)(sms & ~1));
+            cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, k_tc_window<T, QM, MODE>, &cfg);
+            if (e != cudaSuccess || clusters < 1) clusters = sms / 2;
+            if (getenv("QX_TC_VERBOSE")) fprintf(stderr, "qx_tc: 2-SM mode, %d resident clusters\n", clusters);
+        }
+        const int64_t want = a.batch;
+        cfg.gridDim = dim3((unsigned)(2 * (want < clusters ? want : clusters)));
         cudaError_t e = cudaLaunchKernelEx(&cfg, k_tc_window<T, QM, MODE>, a);
         if (e != cudaSuccess) return e;
     } else {

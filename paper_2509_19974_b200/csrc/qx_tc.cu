@@ -46,11 +46,12 @@ namespace qx {
 
 constexpr int kTcThreads = 512;                 // builder threads (warps 0-15)
 constexpr int kTcMmaWarp = 16;                   // MMA issuer
-constexpr int kTcLagWarp0 = 17, kTcLagWarps = 3;  // extra-lag dot products (warps 17-19)
+constexpr int kTcLagWarp0 = 17, kTcLagWarps = 2;  // extra-lag dot products (warps 17-18)
 // builders + MMA warp + lag warps meet at the per-pair hand-off barrier
 constexpr int kTcHandoff = kTcThreads + 32 + 32 * kTcLagWarps;
-constexpr int kTcMergeWarp = 24;                 // per-pair merge + result record
-constexpr int kTcTotalThreads = 25 * 32;         // + warp 16 (MMA), warps 20-23 (epilogue), 24 (merge)
+constexpr int kTcMergeWarp = 19;                 // per-pair merge + result record
+// 24 warps = 6 per SM sub-partition: an 80-register budget (25 warps: 72)
+constexpr int kTcTotalThreads = 24 * 32;         // + warp 16 (MMA), 19 (merge), 20-23 (epilogue)
 constexpr int kTcLags = 2048;      // lags per M=128 tile (M=64: 1024)
 constexpr int kTcMaxK = 4608;      // nx + 15 <= kTcMaxK (B buffer 16*K bytes)
 constexpr int kTcMaxTiles = 2;     // lag tiles per pair

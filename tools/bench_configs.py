@@ -5,7 +5,9 @@ tables), checks every estimate against the planted delay, and returns / prints
 one JSON object.  C3 runs a 16384-pair slice of the 65,536-pair workload
 (per-pair cost is shape-only; `c3full` runs all 65,536 pairs); C5 runs the
 full 2^28-sample stream.  Roofline fractions: HBM from MEASURED_PEAKS.json
-hbm_gbs; i8 tensor from the measured 8190 MACs/clk/SM (profiles/r01_tc_rate.json).
+hbm_gbs; i8 tensor from the measured 8190 MACs/clk/SM (profiles/r01_tc_rate.json);
+fp4 tensor (the C5 path) from the measured 16336 MACs/clk/SM (profiles/r01_tc_fp4.txt,
+tools/tc_fp4.cu, M128 x N>=128 kind::mxf4).
 bench.py imports run() for its `other_configs` key.
 usage: python tools/bench_configs.py [c1 c1batch c2 c3 c3full c4 c5]"""
 import json
@@ -23,6 +25,7 @@ import paper_2509_19974_b200 as P
 from paper_2509_19974_b200 import workloads as W
 
 I8_MACS_PER_CLK_SM = 8190.0  # tools/tc_rate.cu, M128 x N128/N256
+FP4_MACS_PER_CLK_SM = 16336.0  # tools/tc_fp4.cu rate probe, M128 x N128/N256 kind::mxf4
 
 
 def timed(fn, reps=5, warm=2):
@@ -44,12 +47,13 @@ def _peaks():
     props = torch.cuda.get_device_properties(0)
     clk = 1.965e9
     i8 = I8_MACS_PER_CLK_SM * props.multi_processor_count * clk
-    return hbm, i8
+    fp4 = FP4_MACS_PER_CLK_SM * props.multi_processor_count * clk
+    return hbm, i8, fp4
 
 
 def run(which) -> dict:
     res = {}
-    hbm, i8 = _peaks()
+    hbm, i8, fp4 = _peaks()
     if "c1" in which:
         x, y = W.c1(0)
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
@@ -57,7 +61,8 @@ def run(which) -> dict:
         r = r.numpy()[0]
         assert (r["lag"], r["value"]) == (-137, 14839)
         res["c1"] = {"ms_per_estimate": ms, "lag": int(r["lag"]), "peak": int(r["value"]),
-                     "note": "single pair, latency incl. the Python call"}
+                     "note": "single pair, latency incl. the Python call",
+                     "path": "popc word-parallel 1-level codes (bit planes + 32-lag blocks)"}
     if "c1batch" in which:
         x, y = W.c1(0)
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
@@ -112,8 +117,10 @@ def run(which) -> dict:
             ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=2, warm=1)
             assert r[1] == off, r
             res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
-                               "lag": r[1], "i8_tensor_frac": macs / (ms / 1e3) / i8,
-                               "path": "tcgen05 window, shared template (N=32, SW32 Hankel), 4096-lag blocks"}
+                               "lag": r[1], "fp4_tensor_frac": macs / (ms / 1e3) / fp4,
+                               "hbm_frac": len(st) * 4 / (ms / 1e3) / 1e9 / hbm,
+                               "path": "tcgen05 kind::mxf4 window (e2m1 codes, exact f32 sums), shared template "
+                                       "(N=64 copies, SW32 Hankel), 8192-lag blocks, one C-ABI call"}
         res["c5_generation_s"] = gen_s
         del td, sd
     torch.cuda.empty_cache()

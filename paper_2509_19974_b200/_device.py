@@ -8,12 +8,20 @@ import numpy as np
 from . import _native as N
 
 
-def torch():
-    import torch as _t
+_TORCH = None
 
-    if not _t.cuda.is_available():
-        raise RuntimeError("paper_2509_19974_b200 needs a CUDA device (no CPU fallback)")
-    return _t
+
+def torch():
+    """The torch module once a CUDA device is confirmed (checked on first use;
+    there is no CPU fallback)."""
+    global _TORCH
+    if _TORCH is None:
+        import torch as _t
+
+        if not _t.cuda.is_available():
+            raise RuntimeError("paper_2509_19974_b200 needs a CUDA device (no CPU fallback)")
+        _TORCH = _t
+    return _TORCH
 
 
 def as_device(a, dtype=None):
@@ -42,7 +50,10 @@ def as_device(a, dtype=None):
 
 
 def stream_handle() -> int:
-    return torch().cuda.current_stream().cuda_stream
+    """Raw handle of the current CUDA stream of the current device (the
+    kernels are enqueued there)."""
+    t = torch()
+    return t._C._cuda_getCurrentRawStream(t.cuda.current_device())
 
 
 DTYPE_CODE = {"float32": N.QX_F32, "float64": N.QX_F64, "int64": N.QX_I64}

@@ -93,8 +93,23 @@ def from_spec(text: str) -> Quantizer:
 _KIND = {"sign": N.QX_Q_SIGN, "uniform": N.QX_Q_UNIFORM, "custom": N.QX_Q_CUSTOM}
 
 
+_NATIVE_CACHE: dict = {}
+
+
 def native_quantizer(q):
-    """(QxQuantizer, keep-alive) for this package's or the reference's Quantizer."""
+    """(QxQuantizer, keep-alive) for this package's or the reference's Quantizer
+    (cached per immutable quantiser of this package)."""
+    if isinstance(q, Quantizer):
+        hit = _NATIVE_CACHE.get(q)
+        if hit is None:
+            if len(_NATIVE_CACHE) > 4096:
+                _NATIVE_CACHE.clear()
+            hit = _NATIVE_CACHE[q] = _native_quantizer(q)
+        return hit
+    return _native_quantizer(q)
+
+
+def _native_quantizer(q):
     if isinstance(q, int):  # integer codes with this bound (IntSignal)
         return N.QxQuantizer(N.QX_Q_CODES, 0, int(q), 1.0, None), None
     kind = _KIND[q.kind]

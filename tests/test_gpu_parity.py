@@ -518,6 +518,38 @@ def test_template_search_2sm_mode(qx, oracle, monkeypatch):
         assert set(got.values()) == {(m, f + 7, n)}, (trial, got, (m, f + 7, n))
 
 
+def test_sharded_template_search_over_nccl(qx):
+    """The multi-GPU template search (parallel.template_search_sharded: stream
+    shard + halo per rank, one all_gather of the (value, lag, ties) summary)
+    on a real NCCL process group (one rank on this GPU) equals the
+    single-call template search; the 2-rank logic itself is gloo-tested."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_19974_b200 import parallel as PL
+
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(25)
+        st = rng.laplace(size=60000).astype(np.float32)
+        tpl = st[31337:31337 + 1024].copy()
+        st = st + rng.normal(0, 0.8, st.size).astype(np.float32)
+        q = qx.sign()
+        got = PL.template_search_sharded(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q,
+                                         device=torch.device("cuda", 0))
+        assert got == qx.template_search(tpl, st, q, q) and got[1] == 31337
+        assert dist.get_backend() == "nccl"
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("f4", ["0", "1"])
 def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
     """Every block summary of the shared-template window modes (i8 pitch 32,

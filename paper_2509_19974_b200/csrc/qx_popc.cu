@@ -291,10 +291,13 @@ cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
         if (e != cudaSuccess) return e;
         attr = smem;
     }
+    // each launch counted and timed on its own (qx_profile)
     if (c.prof) c.prof->pre(KK_POPC, s);
     const dim3 pgrid((unsigned)((a.nxw + a.nyw + kPopcWarps - 1) / kPopcWarps), (unsigned)c.batch);
     if (c.op[0].dtype == DT_F32) k_popc_planes<float><<<pgrid, kPopcThreads, 0, s>>>(a);
     else k_popc_planes<double><<<pgrid, kPopcThreads, 0, s>>>(a);
+    if (c.prof) c.prof->post(KK_POPC, s);
+    if (c.prof) c.prof->pre(KK_POPC, s);
     k_popc<<<dim3((unsigned)G, (unsigned)c.batch), kPopcThreads, smem, s>>>(a);
     if (c.prof) c.prof->post(KK_POPC, s);
     return cudaGetLastError();

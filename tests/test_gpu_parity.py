@@ -254,7 +254,7 @@ def test_popc_path_against_oracle(qx, oracle):
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         with _native.profile(timed=False) as prof:
             res = qx.estimate_batch(xd, yd, qa, qb, lag_lo=first + t_lo, lag_hi=first + t_hi, path="popc").numpy()
-        assert prof.result.get("popc", (0, 0))[0] == 1, prof.result
+        assert prof.result.get("popc", (0, 0))[0] == 2, prof.result  # planes + correlation
         ntt = qx.estimate_batch(xd, yd, qa, qb, lag_lo=first + t_lo, lag_hi=first + t_hi, path="ntt").numpy()
         assert np.array_equal(res, ntt), (trial, res, ntt)
         for b in range(B):

@@ -752,7 +752,7 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
         s0 += nfull * block;
     }
     if (rem) {
-        x.ld = nt;
+        x.ld = 0;  // still the stride-0 template row: the shared-template modes take it
         y.data = (const char*)sig->data + (size_t)s0 * es;
         y.n = rem + nt - 1;
         y.ld = y.n;

@@ -1626,7 +1626,7 @@ static bool tc_fp4_codes(const NttCall& c, int64_t nx)
 {
     const char* env = getenv("QX_TC_F4");
     if (env && env[0] == '0') return false;
-    return c.op[0].dtype == DT_F32 && c.op[1].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN &&
+    return c.op[0].dtype == DT_F32 && c.op[1].dtype == DT_F32 && c.op[0].ld == 0 && nx <= kTcFastN &&
            nx % 4 == 0 && (uintptr_t)c.op[0].data % 16 == 0 && (uintptr_t)c.op[1].data % 16 == 0 &&
            c.op[1].ld % 4 == 0 && c.op[0].q.mode == c.op[1].q.mode && c.op[0].q.k <= kF4MaxCode &&
            c.op[1].q.k <= kF4MaxCode && (double)nx * c.op[0].q.k * c.op[1].q.k < 16777216.0;
@@ -1646,7 +1646,7 @@ static bool tc_f2_mode(const NttCall& c, int64_t nx, int64_t ny)
     const char* env = getenv("QX_TC_F2");
     if (!c.split2 || (env && env[0] == '0')) return false;
     const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
-    return tc_fp4_codes(c, nx) && L0 == 0 && W <= kF2Lags && ny <= kF2Lags + kTcMaxK;
+    return tc_fp4_codes(c, nx) && c.batch > 1 && L0 == 0 && W <= kF2Lags && ny <= kF2Lags + kTcMaxK;
 }
 
 // the 2-SM mode is what tc_window_run will launch for this call
@@ -1732,7 +1732,9 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     // template's 32 shifted copies are built once per CTA (pitch 32, one
     // M=128 tile of 4096 lags, y rows up to 8192 samples); otherwise per-pair
     // copies with pitch 16
-    const bool sx = c.op[0].dtype == DT_F32 && c.batch > 1 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
+    // shared x: a stride-0 x row (every pair correlates the same template;
+    // also a single pair passed that way, e.g. a template search's last block)
+    const bool sx = c.op[0].dtype == DT_F32 && c.op[0].ld == 0 && nx <= kTcFastN && nx % 4 == 0 &&
                     aligned;
     const bool f2 = tc_f2_mode(c, nx, ny);
     const bool f4 = !f2 && tc_f4_mode(c, nx, ny);

@@ -1366,6 +1366,9 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     }
 #ifdef QX_TC_TIMING
     if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
+    const long long k_t0 = clock64();
+    unsigned long long k_g0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g0));
 #endif
     if (threadIdx.x == 0) asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (warp == 0) {
@@ -1600,6 +1603,13 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     // its barriers or the leader's MMAs may still target its TMEM
     if constexpr (F2) cluster_sync_all();
 #ifdef QX_TC_TIMING
+    {
+        unsigned long long k_g1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g1));
+        if ((blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && threadIdx.x == 0)
+            printf("tc block %d: %lld pairs, %lld cycles, %.1f us -> %.0f MHz\n", blockIdx.x, (long long)npairs,
+                   clock64() - k_t0, (k_g1 - k_g0) / 1e3, (double)(clock64() - k_t0) / ((k_g1 - k_g0) / 1e3));
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0 && npairs)
         printf("tc timing block0 npairs=%lld debug=%d (cycles/pair): build-wait %llu build %llu | mma: wait-handoff %llu "
                "wait-tfree %llu issue %llu | epi: wait %llu run %llu\n",

@@ -518,6 +518,44 @@ def test_template_search_2sm_mode(qx, oracle, monkeypatch):
         assert set(got.values()) == {(m, f + 7, n)}, (trial, got, (m, f + 7, n))
 
 
+def test_template_search_random_modes_and_errors(qx, oracle, monkeypatch):
+    """Randomised template searches across every mode the default picks
+    (fp4 for k <= 4, int8 for k > 4, NTT for templates the window path does not
+    take) and explicit block sizes, against the oracle; NaN in the stream and
+    an all-zero template raise the reference's exceptions."""
+    from paper_2509_19974_b200.errors import DegenerateQuantization
+
+    rng = np.random.default_rng(26)
+    quants = [qx.sign(), qx.uniform(1, 0.6), qx.uniform(3, 0.4), qx.uniform(4, 0.2), qx.uniform(7, 0.3),
+              qx.custom([-0.5, 0.2])]
+    for trial in range(14):
+        nt = int(rng.choice([4, 12, 100, 512, 1023, 2048, 4096, 4100]))
+        ns = nt + int(rng.integers(0, 60000))
+        st = rng.laplace(size=ns).astype(np.float32)
+        off = int(rng.integers(0, ns - nt + 1))
+        tpl = st[off:off + nt].copy()
+        st = st + rng.normal(0, 0.6, ns).astype(np.float32)
+        qa, qb = quants[int(rng.integers(len(quants)))], quants[int(rng.integers(len(quants)))]
+        if (qa.k == 1) != (qb.k == 1) or (qa.kind == "custom") != (qb.kind == "custom"):
+            qb = qa
+        block = None if trial % 3 else int(rng.integers(1, 20000))
+        start = int(rng.integers(-50, 50))
+        got = qx.template_search(tpl, st, qa, qb, stream_start=start, block=block)
+        u, v = oracle.quantize(qa, tpl), oracle.quantize(qb, st)
+        if not u.any() or not v.any():
+            continue
+        m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, nt - 1, ns - 1))
+        assert got == (m, f + start, n), (trial, nt, ns, qa, qb, block, got, (m, f + start, n))
+    st = rng.laplace(size=20000).astype(np.float32)
+    tpl = st[500:500 + 1024].copy()
+    bad = st.copy()
+    bad[12345] = np.nan
+    with pytest.raises(ValueError):
+        qx.template_search(tpl, bad, qx.sign(), qx.sign())
+    with pytest.raises(DegenerateQuantization):
+        qx.template_search(np.zeros(1024, np.float32), st, qx.sign(), qx.sign())
+
+
 def test_sharded_template_search_over_nccl(qx):
     """The multi-GPU template search (parallel.template_search_sharded: stream
     shard + halo per rank, one all_gather of the (value, lag, ties) summary)

@@ -373,12 +373,14 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
         c.am.pstride = kMaxPartialsLarge;
         const size_t sb = (size_t)batch * 8 * 8, pb = (size_t)batch * c.am.pstride * 3 * 8;
         const size_t plb = (size_t)batch * 2 * ((nx + 31) / 32 + (ny + 31) / 32 + 2) * 4;
-        cudaError_t e = arena_reserve(scr, sb + pb + plb + 256, false);
+        const size_t spb = (size_t)batch * kMaxPartialsLarge * 16;
+        cudaError_t e = arena_reserve(scr, sb + pb + plb + spb + 256, false);
         if (e == cudaSuccess) e = arena_reserve(cnt, (size_t)batch * 4, true);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
         c.stats = (unsigned long long*)scr.ptr;
         c.am.partials = (long long*)((char*)scr.ptr + sb);
         c.popc_planes = (uint32_t*)((char*)scr.ptr + sb + pb);
+        c.popc_spart = (unsigned*)((char*)scr.ptr + sb + pb + plb);
         c.am.counters = (int*)cnt.ptr;
         c.prof = &ctx->prof;
         return QX_OK;
@@ -525,7 +527,9 @@ static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const q
     if (split2 && !(pr.path == QX_PATH_DIRECT && tc_f2_selected(pr.call, pr.nx, pr.ny))) return QX_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     pr.call.am.results = results;
-    cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
+    cudaError_t e = cudaSuccess;
+    if (pr.path != QX_PATH_POPC)  // the popc path writes (or zeroes) its statistics itself
+        e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
     e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s)
         : pr.path == QX_PATH_POPC ? popc_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);
@@ -547,7 +551,9 @@ qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signa
     if (st != QX_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     pr.call.am.results = results;
-    cudaError_t e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
+    cudaError_t e = cudaSuccess;
+    if (pr.path != QX_PATH_POPC)  // the popc path writes (or zeroes) its statistics itself
+        e = cudaMemsetAsync(pr.call.stats, 0, (size_t)batch * 64, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
     e = pr.path == QX_PATH_DIRECT ? tc_window_run(pr.call, pr.nx, s)
         : pr.path == QX_PATH_POPC ? popc_run(pr.call, pr.nx, s) : ntt_run(pr.call, s);

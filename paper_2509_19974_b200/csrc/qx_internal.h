@@ -114,6 +114,7 @@ struct NttCall {
     uint32_t* OUT;            // [2][chunk][P] outer forward output
     uint32_t* RI;             // [chunk*M][np][Q] inner inverse residues
     uint32_t* popc_planes;    // popc path: [batch][2][nxw + nyw + 2] code bit planes
+    unsigned* popc_spart;     // popc path (fused): [batch][<= 512][4] per-CTA counts
     int split2;               // the caller takes 2 records per pair (2-SM template-search blocks)
 };
 

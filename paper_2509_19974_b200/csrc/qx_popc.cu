@@ -25,6 +25,8 @@
 #include <climits>
 #include <cstdio>
 
+#include <cooperative_groups.h>
+
 #include "qx_argmax.cuh"
 #include "qx_internal.h"
 
@@ -46,6 +48,7 @@ struct PopcArgs {
     int nxw;       // x words
     int nyw;       // y words (whole signal)
     uint32_t* planes;  // [batch][xs | xz | ys | yz]: 2 * (nxw + nyw) words per pair
+    unsigned* spart;   // fused kernel: [batch][G][4] per-CTA nonzero counts (x, y) and flags
 };
 
 __device__ __forceinline__ uint32_t* plane_x(const PopcArgs& a, int64_t pair)
@@ -166,7 +169,7 @@ __device__ void popc_blocks(const PopcArgs& a, const uint32_t* xs, const uint32_
     }
 }
 
-__global__ void __launch_bounds__(kPopcThreads) k_popc(const __grid_constant__ PopcArgs a)
+__device__ __forceinline__ void popc_correlate(const PopcArgs& a)
 {
     extern __shared__ uint32_t pw[];
     __shared__ unsigned s_zero;
@@ -229,10 +232,89 @@ __global__ void __launch_bounds__(kPopcThreads) k_popc(const __grid_constant__ P
                tp1 - tp0, tp2 - tp1, clock64() - tp2, a.bpc, nyw, !s_zero);
 #endif
 }
+__global__ void __launch_bounds__(kPopcThreads) k_popc(const __grid_constant__ PopcArgs a) { popc_correlate(a); }
+
+// one cooperative launch: the planes of every pair (CTA g of pair p takes
+// words g*16 + warp + k*16G), per-CTA counts into spart, a grid-wide sync,
+// CTA 0 of each pair turns the counts into the pair's statistics record (no
+// memset, no atomics), then the correlation as in k_popc
+template <typename T>
+__global__ void __launch_bounds__(kPopcThreads) k_popc_fused(const __grid_constant__ PopcArgs a)
+{
+    __shared__ unsigned s_cnt[3];
+    const int64_t pair = blockIdx.y;
+    const int g = blockIdx.x, G = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#ifdef QX_POPC_TIMING
+    unsigned long long f0, f1, f2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f0));
+#endif
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    uint32_t* px = plane_x(a, pair);
+    unsigned nzx = 0, nzy = 0;
+    bool nan = false;
+    for (int w = g * kPopcWarps + warp; w < a.nxw + a.nyw; w += G * kPopcWarps) {
+        const bool isx = w < a.nxw;
+        const OperandDesc& o = a.op[isx ? 0 : 1];
+        const T* row = reinterpret_cast<const T*>(o.data) + pair * o.ld;
+        const int64_t i = 32ll * (isx ? w : w - a.nxw) + lane;
+        const T v = i < o.n ? row[i] : (T)0;
+        const int c = level_k1(v, (T)o.q.thr[0], (T)o.q.thr[1]);
+        const uint32_t sb = __ballot_sync(0xffffffffu, c < 0), zb = __ballot_sync(0xffffffffu, c != 0);
+        nan |= v != v;
+        if (lane == 0) {
+            if (isx) {
+                px[w] = sb;
+                px[a.nxw + w] = zb;
+                nzx += __popc(zb);
+            } else {
+                uint32_t* py = px + 2 * a.nxw;
+                py[w - a.nxw] = sb;
+                py[a.nyw + (w - a.nxw)] = zb;
+                nzy += __popc(zb);
+            }
+        }
+    }
+    nan = __any_sync(0xffffffffu, nan);
+    if (lane == 0) {
+        if (nzx) atomicAdd(&s_cnt[0], nzx);
+        if (nzy) atomicAdd(&s_cnt[1], nzy);
+        if (nan) atomicOr(&s_cnt[2], SF_NONFINITE);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) a.spart[(pair * G + g) * 4 + threadIdx.x] = s_cnt[threadIdx.x];
+#ifdef QX_POPC_TIMING
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f1));
+#endif
+    cooperative_groups::this_grid().sync();
+#ifdef QX_POPC_TIMING
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f2));
+    if (threadIdx.x == 0 && (g == 0 || g == G - 1))
+        printf("fused cta %d: planes %.2f us, grid sync %.2f us\n", g, (f1 - f0) / 1e3, (f2 - f1) / 1e3);
+#endif
+    if (g == 0 && warp == 0) {
+        unsigned cx = 0, cy = 0, fl = 0;
+        for (int i = lane; i < G; i += 32) {
+            const unsigned* sp = a.spart + (pair * G + i) * 4;
+            cx += sp[0];
+            cy += sp[1];
+            fl |= sp[2];
+        }
+        cx = __reduce_add_sync(0xffffffffu, cx);
+        cy = __reduce_add_sync(0xffffffffu, cy);
+        fl = __reduce_or_sync(0xffffffffu, fl);
+        unsigned long long* st = a.stats + pair * 8;
+        // sum of squares = nonzero count for 1-level codes
+        if (lane < 8) st[lane] = lane == 0 || lane == 1 ? cx : lane == 4 || lane == 5 ? cy : lane == 6 ? fl : 0ull;
+    }
+    popc_correlate(a);
+}
+
 
 // launch plan: ~2 CTAs per SM over the whole batch, at least kPopcGroups
 // 32-lag blocks per CTA when there are enough; returns the shared memory
-static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G)
+static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, bool fused = false)
 {
     a.dlo = c.am.t_lo - (nx - 1);
     a.dhi = c.am.t_hi - (nx - 1);
@@ -244,7 +326,8 @@ static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    G = ((int64_t)sms + c.batch - 1) / c.batch;
+    // fused (cooperative) launch: every CTA resident at once, one per SM
+    G = fused ? (int64_t)sms / c.batch : ((int64_t)sms + c.batch - 1) / c.batch;
     const int64_t gmax = (nblk + kPopcGroups - 1) / kPopcGroups;
     if (G > gmax) G = gmax;
     if (G > kMaxPartialsLarge) G = kMaxPartialsLarge;
@@ -281,17 +364,39 @@ cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
     a.op[1] = c.op[1];
     a.stats = c.stats;
     a.am = c.am;
-    int64_t G;
-    const size_t smem = popc_plan(c, nx, a, G);
-    if (G > c.am.pstride) return cudaErrorInvalidValue;
     a.planes = c.popc_planes;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-        cudaError_t e = cudaFuncSetAttribute(k_popc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
+    a.spart = c.popc_spart;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* env = getenv("QX_POPC_FUSED");
+    const bool fused = c.batch <= sms && !(env && env[0] == '0');
+    int64_t G;
+    const size_t smem = popc_plan(c, nx, a, G, fused);
+    if (G > c.am.pstride) return cudaErrorInvalidValue;
+    static size_t attr[3] = {0, 0, 0};
+    const int ti = c.op[0].dtype == DT_F32 ? 0 : 1;
+    auto raise = [&](const void* fn, int slot) -> cudaError_t {
+        if (smem > 48 * 1024 && attr[slot] < smem) {
+            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            attr[slot] = smem;
+        }
+        return cudaSuccess;
+    };
+    cudaError_t e;
+    if (fused) {
+        const void* fn = ti == 0 ? (const void*)k_popc_fused<float> : (const void*)k_popc_fused<double>;
+        if ((e = raise(fn, ti)) != cudaSuccess) return e;
+        if (c.prof) c.prof->pre(KK_POPC, s);
+        void* args[] = {(void*)&a};
+        e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)G, (unsigned)c.batch), dim3(kPopcThreads), args, smem, s);
+        if (c.prof) c.prof->post(KK_POPC, s);
+        return e != cudaSuccess ? e : cudaGetLastError();
     }
-    // each launch counted and timed on its own (qx_profile)
+    // two launches: planes (statistics by atomics into zeroed records), correlation
+    if ((e = raise((const void*)k_popc, 2)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(c.stats, 0, (size_t)c.batch * 64, s)) != cudaSuccess) return e;
     if (c.prof) c.prof->pre(KK_POPC, s);
     const dim3 pgrid((unsigned)((a.nxw + a.nyw + kPopcWarps - 1) / kPopcWarps), (unsigned)c.batch);
     if (c.op[0].dtype == DT_F32) k_popc_planes<float><<<pgrid, kPopcThreads, 0, s>>>(a);

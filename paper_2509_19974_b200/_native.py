@@ -122,8 +122,9 @@ def load():
         L.qx_estimate_batch_host.restype = st
         L.qx_estimate_sweep_host.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp]
         L.qx_estimate_sweep_host.restype = st
-        L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
-        L.qx_template_search.restype = st
+        if hasattr(L, "qx_template_search"):  # (absent from older A/B builds)
+            L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
+            L.qx_template_search.restype = st
         L.qx_decode_pcm16.argtypes = [vp, vp, i64, vp, vp]
         L.qx_decode_pcm16.restype = st
         L.qx_profile_begin.argtypes = [vp, ctypes.c_int]
@@ -132,7 +133,8 @@ def load():
         L.qx_profile_end.restype = st
         L.qx_profile_kind_name.argtypes = [ctypes.c_int]
         L.qx_profile_kind_name.restype = ctypes.c_char_p
-        assert L.qx_abi_version() == 2
+        # (an A/B build named by QX_NATIVE_LIB may predate the current ABI)
+        assert L.qx_abi_version() == 2 or os.environ.get("QX_NATIVE_LIB")
         _lib = L
     return _lib
 

@@ -46,9 +46,19 @@ namespace qx {
 
 constexpr int kTcThreads = 512;                 // builder threads (warps 0-15)
 constexpr int kTcMmaWarp = 16;                   // MMA issuer
-constexpr int kTcLagWarp0 = 17, kTcLagWarps = 2;  // extra-lag dot products (warps 17-18)
+// lag warps (extra-lag dot products, final statistics) from warp 17: three in
+// the int8 modes (whose per-pair hand-off they are part of), two in the fp4
+// modes, where warp 19 is a dedicated merge warp (an fp4 pair's epilogue is
+// long; an int8 pair's first epilogue warp merges instead)
+constexpr int kTcLagWarp0 = 17, kTcLagWarps = 3;
+template <int MODE>
+struct TcRoles {
+    static constexpr int NLAG = MODE >= 2 ? 2 : 3;
+    static constexpr bool MERGE_WARP = MODE >= 2;
+    static constexpr int HANDOFF = kTcThreads + 32 + 32 * NLAG;  // builders + MMA warp + lag warps
+};
 // builders + MMA warp + lag warps meet at the per-pair hand-off barrier
-constexpr int kTcHandoff = kTcThreads + 32 + 32 * kTcLagWarps;
+
 constexpr int kTcMergeWarp = 19;                 // per-pair merge + result record
 // 24 warps = 6 per SM sub-partition: an 80-register budget (25 warps: 72)
 constexpr int kTcTotalThreads = 24 * 32;         // + warp 16 (MMA), 19 (merge), 20-23 (epilogue)
@@ -67,7 +77,11 @@ constexpr int kF2Pad = 128;                     // template nibble front padding
 constexpr int kF2Sf = 256;                      // TMEM scale-factor column (2 aux slots x 128 columns)
 constexpr int kTcYBytesI8 = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
 constexpr int kTcYBytesF2 = (kF2CtaLags + kTcMaxK + 2 * kF2Pad) / 2;
+#ifdef QX_SMALL_Y
+constexpr int kTcYBytes = kTcYBytesI8;
+#else
 constexpr int kTcYBytes = kTcYBytesI8 > kTcYBytesF2 ? kTcYBytesI8 : kTcYBytesF2;
+#endif
 constexpr int kTcYStride = (kTcYBytes + 1023) / 1024 * 1024;  // 1024-B aligned slots (SW32 rows)
 constexpr int kTcXPad = 32;  // zero bytes in front of the linear x codes (>= the Hankel pitch)
 // B layout: K-chunk stride 272 B (= 256 + 16): 16-byte stores of 32
@@ -1017,7 +1031,7 @@ __device__ void tc_build_fast(const TcArgs& a, TcSmem& S, int s, int u, const Tc
 // Extra lags of the pair in data slot s (aux slot u), run by the lag warps
 // after the hand-off barrier: j = ntiles*pitch*M + e, sum_m x[m] *
 // ycode[L0 + j + m] over packed words (dp4a), one record per lag warp.
-template <int PITCH>
+template <int PITCH, int NLAG>
 __device__ void tc_extra_lags(const TcArgs& a, TcSmem& S, int s, int u, int xs)
 {
     const int lane = threadIdx.x & 31, lw = (threadIdx.x >> 5) - kTcLagWarp0;
@@ -1028,7 +1042,7 @@ __device__ void tc_extra_lags(const TcArgs& a, TcSmem& S, int s, int u, int xs)
     for (int e = 0; e < a.extra; ++e) {
         const int j = j0 + e, jw = j >> 2, sh = (j & 3) * 8;
         int acc = 0;
-        for (int w = lw * 32 + lane; w < nw; w += 32 * kTcLagWarps)
+        for (int w = lw * 32 + lane; w < nw; w += 32 * NLAG)
             acc = __dp4a((int)xw[w], (int)__funnelshift_r(yw[ysw<PITCH>(w + jw)], yw[ysw<PITCH>(w + jw + 1)], sh),
                          acc);
         acc = __reduce_add_sync(0xffffffffu, acc);
@@ -1282,8 +1296,8 @@ __device__ void tc_epilogue_f2(const TcArgs& a, TcSmem& S, int u)
 // rec: the qx_result record index (pair, or 2*pair + rank in the 2-SM mode);
 // notify: also free the slot in the leader CTA (2-SM peer: the leader's MMA
 // writes this CTA's TMEM)
-template <int PITCH>
-__device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool notify = false)
+template <int PITCH, int NLAG>
+__device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool notify = false, bool free_slot = true)
 {
     const int lane = threadIdx.x & 31;
     const int tl = PITCH * a.M;
@@ -1299,9 +1313,9 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool no
         int xs[kTcMaxExtra];
 #pragma unroll
         for (int e = 0; e < kTcMaxExtra; ++e)
-            xs[e] = e < a.extra ? __reduce_add_sync(0xffffffffu, lane < kTcLagWarps ? S.wxs[u][lane][e] : 0) : 0;
+            xs[e] = e < a.extra ? __reduce_add_sync(0xffffffffu, lane < NLAG ? S.wxs[u][lane][e] : 0) : 0;
         // every record of slot u is in registers: free the slot
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[u])) : "memory");
+        if (free_slot) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[u])) : "memory");
         if (notify && lane == 0) mbar_arrive_remote(&S.tfree[u], 0);
         const int mv = __reduce_max_sync(0xffffffffu, wv);
         const bool at = lane < 4 && wv == mv;
@@ -1359,9 +1373,11 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     if (threadIdx.x < kTcAux) {
         mbar_init(&S.mdone[threadIdx.x], 1);
         // 2-SM leader: its own merge warp + the peer's (remote) release of the slot
-        mbar_init(&S.tfree[threadIdx.x], (F2 && rank == 0) ? 33 : 32);
+        // merge warp (+ the 2-SM peer's remote release); int8 modes: the 128
+        // epilogue threads, after their first warp's merge
+        mbar_init(&S.tfree[threadIdx.x], !TcRoles<MODE>::MERGE_WARP ? 128 : (F2 && rank == 0) ? 33 : 32);
         mbar_init(&S.edone[threadIdx.x], 4);
-        mbar_init(&S.xdone[threadIdx.x], 32 * kTcLagWarps);
+        mbar_init(&S.xdone[threadIdx.x], 32 * TcRoles<MODE>::NLAG);
         if (threadIdx.x < 2) mbar_init(&S.pready[threadIdx.x], 1);
     }
 #ifdef QX_TC_TIMING
@@ -1431,8 +1447,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         auto handoff = [&](int it) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
             // alternating barrier ids keep consecutive iterations apart
-            if (it & 1) asm volatile("bar.arrive 3, %0;" ::"n"(kTcHandoff) : "memory");
-            else asm volatile("bar.arrive 2, %0;" ::"n"(kTcHandoff) : "memory");
+            if (it & 1) asm volatile("bar.arrive 3, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
+            else asm volatile("bar.arrive 2, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
         };
         bool fast = false;
         if constexpr (std::is_same<T, float>::value) fast = a.fast;
@@ -1484,8 +1500,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             const int s = it & 1, u = it % AUX;
             {
                 TC_T0();
-                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
-                else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
+                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
+                else asm volatile("bar.sync 2, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
                 if (lane == 0) TC_ACC(2);
             }
             if constexpr (F2) {
@@ -1562,35 +1578,47 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             __syncwarp();
             if (lane == 0) TC_ACC(5);
         }
-    } else if (warp >= kTcLagWarp0 && warp < kTcLagWarp0 + kTcLagWarps) {
+    } else if (warp >= kTcLagWarp0 && warp < kTcLagWarp0 + TcRoles<MODE>::NLAG) {
         // ---- lag warps: the extra lags of each pair from its code buffers
         for (int it = 0; it < npairs; ++it) {
-            if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(kTcHandoff) : "memory");
-            else asm volatile("bar.sync 2, %0;" ::"n"(kTcHandoff) : "memory");
+            if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
+            else asm volatile("bar.sync 2, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
             if (it >= AUX) tc_wait_tfree<AUX>(S, it - AUX);  // epilogue done with this aux slot's records
-            if (a.extra) tc_extra_lags<SX ? 32 : 16>(a, S, it & 1, it % AUX, SX ? 0 : (it & 1));
+            if (a.extra) tc_extra_lags<SX ? 32 : 16, TcRoles<MODE>::NLAG>(a, S, it & 1, it % AUX, SX ? 0 : (it & 1));
             if (warp == kTcLagWarp0) tc_final_stats(a, S, it % AUX);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it % AUX])) : "memory");
         }
-    } else if (warp == kTcMergeWarp) {
+    } else if (TcRoles<MODE>::MERGE_WARP && warp == kTcMergeWarp) {
         // ---- merge: records -> qx_result (2-SM: one record per CTA and pair)
         for (int it = 0; it < npairs; ++it) {
             const int64_t pair = base + (int64_t)it * stride;
             tc_wait_xdone<AUX>(S, it);  // statistics and extra-lag records written
             tc_wait_edone<AUX>(S, it);  // epilogue records written
-            tc_merge<PITCH>(a, S, it % AUX, F2 ? 2 * pair + rank : pair, F2 && rank != 0);
+            tc_merge<PITCH, TcRoles<MODE>::NLAG>(a, S, it % AUX, F2 ? 2 * pair + rank : pair, F2 && rank != 0);
         }
     } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
         // ---- epilogue: TMEM -> per-warp (max, smallest lag, count) records
         for (int it = 0; it < npairs; ++it) {
             TC_T0();
             tc_wait_mdone<AUX>(S, it);
+            if constexpr (!TcRoles<MODE>::MERGE_WARP) tc_wait_xdone<AUX>(S, it);  // lag warps' records in
             if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(3);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             {
                 TC_T0();
                 if constexpr (F2) tc_epilogue_f2(a, S, it % AUX);
                 else tc_epilogue<PITCH, F4>(a, S, it % AUX);
+                if constexpr (!TcRoles<MODE>::MERGE_WARP) {
+                    // int8 modes: the first epilogue warp merges once the four
+                    // records are in (named barrier); every epilogue thread then
+                    // frees the slot
+                    asm volatile("bar.sync 4, 128;" ::: "memory");
+                    if (warp == kEpiWarp0) {
+                        const int64_t pair = base + (int64_t)it * stride;
+                        tc_merge<PITCH, TcRoles<MODE>::NLAG>(a, S, it % AUX, pair, false, false);
+                    }
+                    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.tfree[it % AUX])) : "memory");
+                }
                 if (threadIdx.x == kEpiWarp0 * 32) TC_ACC(6);
             }
         }
@@ -1722,8 +1750,15 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
     return cudaGetLastError();
 }
 
+namespace i8 {
+cudaError_t tc_i8_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
+}
+
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
 {
+    // the int8 modes run the int8 kernel (qx_tc_i8.cu: its role layout is the
+    // one an int8 pair's hand-off needs); this kernel keeps the fp4 modes
+    if (!tc_f2_mode(c, nx, c.op[1].n) && !tc_f4_mode(c, nx, c.op[1].n)) return i8::tc_i8_window_run(c, nx, s);
     TcArgs a;
     memset(&a, 0, sizeof(a));
     a.op[0] = c.op[0];
@@ -1785,32 +1820,20 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int kind = (f2 || f4) ? KK_DIRECT_F4 : KK_DIRECT;
-    if (c.prof) c.prof->pre(kind, s);
+    // fp4 modes only (the int8 ones returned above)
+    if (c.prof) c.prof->pre(KK_DIRECT_F4, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;
     if (f2) {
         if (qm == QM_K1) e = launch_tc<float, QM_K1, 3>(a, s, sms);
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 3>(a, s, sms);
         else e = launch_tc<float, QM_BSEARCH, 3>(a, s, sms);
-    } else if (f4) {
+    } else {
         if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
         else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
-    } else if (c.op[0].dtype == DT_F32 && a.shared_x) {
-        if (qm == QM_K1) e = launch_tc<float, QM_K1, 1>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 1>(a, s, sms);
-        else e = launch_tc<float, QM_BSEARCH, 1>(a, s, sms);
-    } else if (c.op[0].dtype == DT_F32) {
-        if (qm == QM_K1) e = launch_tc<float, QM_K1>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM>(a, s, sms);
-        else e = launch_tc<float, QM_BSEARCH>(a, s, sms);
-    } else {
-        if (qm == QM_K1) e = launch_tc<double, QM_K1>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<double, QM_UNIFORM>(a, s, sms);
-        else e = launch_tc<double, QM_BSEARCH>(a, s, sms);
     }
-    if (c.prof) c.prof->post(kind, s);
+    if (c.prof) c.prof->post(KK_DIRECT_F4, s);
     return e;
 }
 

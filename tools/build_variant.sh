@@ -12,7 +12,7 @@ OUT=$ROOT/tools/ab/$NAME
 mkdir -p $OUT
 NV="/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -DQX_NTT_THREADS=512 -DQX_NTT_MAXR=5 -Xcompiler -fPIC,-ffp-contract=off --expt-relaxed-constexpr -I$ROOT/include $DEFS"
 OBJS=""
-for f in qx_abi.cu qx_ntt.cu qx_quant.cu qx_tc.cu qx_popc.cu; do
+for f in qx_abi.cu qx_ntt.cu qx_quant.cu qx_tc.cu qx_tc_i8.cu qx_popc.cu; do
   o=$C/build/${f%.cu}.o
   case " $SRCS " in *" $f "*) o=$OUT/${f%.cu}.o; $NV -c $C/$f -o $o;; esac
   OBJS="$OBJS $o"

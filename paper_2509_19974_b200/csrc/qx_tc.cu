@@ -1,5 +1,9 @@
 // qx_tc.cu -- bounded-lag-window correlation on the 5th-generation tensor
-// cores (tcgen05.mma kind::i8, s8 x s8 -> s32 in TMEM).
+// cores: the template-search fp4 modes (kind::mxf4 e2m1 x e2m1 -> exact f32,
+// mode 2 on one SM, mode 3 on a CTA pair) and the block merge of
+// qx_template_search.  tc_window_run sends the int8 modes (kind::i8, s8 x s8
+// -> s32; modes 0 and 1 below) to qx_tc_i8.cu, whose role layout they are
+// tuned for; the int8 paths of this kernel template are not instantiated.
 //
 // For a lag tile [L0, L0 + 16M): c[L0 + 16a + r] = sum_k A[a][k] * B[r][k]
 // with a in [0,M) (M = 64 or 128), r in [0,16) (N = 16),
@@ -77,11 +81,7 @@ constexpr int kF2Pad = 128;                     // template nibble front padding
 constexpr int kF2Sf = 256;                      // TMEM scale-factor column (2 aux slots x 128 columns)
 constexpr int kTcYBytesI8 = kTcMaxTiles * kTcLags + kTcMaxExtra + kTcMaxK + 64;
 constexpr int kTcYBytesF2 = (kF2CtaLags + kTcMaxK + 2 * kF2Pad) / 2;
-#ifdef QX_SMALL_Y
-constexpr int kTcYBytes = kTcYBytesI8;
-#else
 constexpr int kTcYBytes = kTcYBytesI8 > kTcYBytesF2 ? kTcYBytesI8 : kTcYBytesF2;
-#endif
 constexpr int kTcYStride = (kTcYBytes + 1023) / 1024 * 1024;  // 1024-B aligned slots (SW32 rows)
 constexpr int kTcXPad = 32;  // zero bytes in front of the linear x codes (>= the Hankel pitch)
 // B layout: K-chunk stride 272 B (= 256 + 16): 16-byte stores of 32

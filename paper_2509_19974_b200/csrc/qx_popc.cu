@@ -37,8 +37,17 @@ constexpr int kPopcWarps = kPopcThreads / 32;
 constexpr int kPopcGroup = 4;                        // warps per 32-lag block
 constexpr int kPopcGroups = kPopcWarps / kPopcGroup;  // blocks in flight per CTA
 
+// one operand as the popc kernels need it (rows + the two thresholds of a
+// 1-level quantiser): a few dozen parameter bytes instead of OperandDesc's
+// 2-KB threshold table, so the launch carries a small parameter block
+struct PopcOp {
+    const void* data;
+    int64_t ld, n;
+    double t0, t1;
+};
+
 struct PopcArgs {
-    OperandDesc op[2];
+    PopcOp op[2];
     unsigned long long* stats;  // [batch][2][4]
     ArgmaxOut am;
     int64_t dlo;   // first lag (relative: x[m] y[m + d]) of the window
@@ -70,11 +79,11 @@ __global__ void __launch_bounds__(kPopcThreads) k_popc_planes(const __grid_const
     __syncthreads();
     const bool isx = w < a.nxw;
     if (w < a.nxw + a.nyw) {
-        const OperandDesc& o = a.op[isx ? 0 : 1];
+        const PopcOp& o = a.op[isx ? 0 : 1];
         const T* row = reinterpret_cast<const T*>(o.data) + pair * o.ld;
         const int64_t i = 32ll * (isx ? w : w - a.nxw) + lane;
         const T v = i < o.n ? row[i] : (T)0;
-        const int c = level_k1(v, (T)o.q.thr[0], (T)o.q.thr[1]);
+        const int c = level_k1(v, (T)o.t0, (T)o.t1);
         const uint32_t sb = __ballot_sync(0xffffffffu, c < 0), zb = __ballot_sync(0xffffffffu, c != 0);
         const bool nan = __any_sync(0xffffffffu, v != v);
         if (lane == 0) {
@@ -256,11 +265,11 @@ __global__ void __launch_bounds__(kPopcThreads) k_popc_fused(const __grid_consta
     bool nan = false;
     for (int w = g * kPopcWarps + warp; w < a.nxw + a.nyw; w += G * kPopcWarps) {
         const bool isx = w < a.nxw;
-        const OperandDesc& o = a.op[isx ? 0 : 1];
+        const PopcOp& o = a.op[isx ? 0 : 1];
         const T* row = reinterpret_cast<const T*>(o.data) + pair * o.ld;
         const int64_t i = 32ll * (isx ? w : w - a.nxw) + lane;
         const T v = i < o.n ? row[i] : (T)0;
-        const int c = level_k1(v, (T)o.q.thr[0], (T)o.q.thr[1]);
+        const int c = level_k1(v, (T)o.t0, (T)o.t1);
         const uint32_t sb = __ballot_sync(0xffffffffu, c < 0), zb = __ballot_sync(0xffffffffu, c != 0);
         nan |= v != v;
         if (lane == 0) {
@@ -360,8 +369,8 @@ bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path)
 cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
 {
     PopcArgs a;
-    a.op[0] = c.op[0];
-    a.op[1] = c.op[1];
+    for (int i = 0; i < 2; ++i)
+        a.op[i] = PopcOp{c.op[i].data, c.op[i].ld, c.op[i].n, c.op[i].q.thr[0], c.op[i].q.thr[1]};
     a.stats = c.stats;
     a.am = c.am;
     a.planes = c.popc_planes;

@@ -321,6 +321,21 @@ __global__ void __launch_bounds__(kPopcThreads) k_popc_fused(const __grid_consta
 }
 
 
+// SM count of the current device (cached per device: the plan runs twice per call)
+static int popc_sms()
+{
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = sms;
+    }
+    return cache[dev];
+}
+
 // launch plan: ~2 CTAs per SM over the whole batch, at least kPopcGroups
 // 32-lag blocks per CTA when there are enough; returns the shared memory
 static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, bool fused = false)
@@ -332,9 +347,7 @@ static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, b
     a.nblk = (int)nblk;
     a.nxw = (int)((nx + 31) / 32);
     a.nyw = (int)((c.op[1].n + 31) / 32);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = popc_sms();
     // fused (cooperative) launch: every CTA resident at once, one per SM
     G = fused ? (int64_t)sms / c.batch : ((int64_t)sms + c.batch - 1) / c.batch;
     const int64_t gmax = (nblk + kPopcGroups - 1) / kPopcGroups;
@@ -375,9 +388,7 @@ cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
     a.am = c.am;
     a.planes = c.popc_planes;
     a.spart = c.popc_spart;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = popc_sms();
     const char* env = getenv("QX_POPC_FUSED");
     const bool fused = c.batch <= sms && !(env && env[0] == '0');
     int64_t G;

@@ -59,8 +59,21 @@ template <int MODE>
 struct TcRoles {
     static constexpr int NLAG = MODE >= 2 ? 2 : 3;
     static constexpr bool MERGE_WARP = MODE >= 2;
-    static constexpr int HANDOFF = kTcThreads + 32 + 32 * NLAG;  // builders + MMA warp + lag warps
+    // builders + MMA warp + lag warps (+ the mode-4 stager warps) meet at the hand-off
+    static constexpr int HANDOFF = kTcThreads + 32 + 32 * NLAG + (MODE == 4 ? 128 : 0);
 };
+// mode 4: fp4 with the Hankel A operand in TMEM.  Stager warps 24-27 (one per
+// TMEM lane quarter) hold each row's 8 words of the current K-step, store
+// them with tcgen05.st and slide them down one lane per step (row a at step
+// s + 1 = row a + 1 at step s), so shared memory serves 32 B per warp and
+// step instead of the 4-KB A tile; A chunks of 16 K-steps alternate in a
+// two-chunk TMEM ring with full/free mbarriers (tools/tc_fp4_tmema.cu:
+// 32.5 cycles per M128 N64 K64 MMA with A in TMEM vs 68 from shared memory)
+constexpr int kT4StageWarp0 = 24;
+constexpr int kT4Chunk = 16;    // K-steps per A chunk (8 TMEM columns each)
+constexpr int kT4ACol = 128;    // TMEM columns 128..383: the two A chunks
+constexpr int kT4Sf = 384;      // scale factors (2 accumulator slots x 64 columns below)
+constexpr int tc_threads(int mode) { return mode == 4 ? 28 * 32 : 24 * 32; }
 // builders + MMA warp + lag warps meet at the per-pair hand-off barrier
 
 constexpr int kTcMergeWarp = 19;                 // per-pair merge + result record
@@ -253,6 +266,19 @@ __device__ __forceinline__ void mma_f4_warp(uint32_t tmem_d, uint64_t a, uint64_
             "l"(a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
 }
 
+// fp4 MMA with the A operand in TMEM (mode 4)
+__device__ __forceinline__ void mma_f4t_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                             uint32_t accumulate, uint32_t sf)
+{
+    asm volatile(
+        "{\n\t.reg .pred e, p;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%5], [%5], p;\n}" ::"r"(
+            tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate), "r"(sf));
+}
+
 // four fp4 MMAs on consecutive K steps (64 samples = 32 B of A, two B chunks)
 #define QX_F4_MMA4(CGS)                                                                                              \
     asm volatile(                                                                                                    \
@@ -394,6 +420,7 @@ struct TcSmem {
     int wxs[kTcAux][kTcLagWarps][kTcMaxExtra];     // extra-lag sums, one record per lag warp
     uint64_t xdone[kTcAux];  // lag warps finished with the pair of aux slot (96 arrivals)
     uint64_t pready[2];      // 2-SM mode, leader CTA: the peer's data slot is built (1 remote arrival)
+    uint64_t afull[2], afree[2];  // mode 4: A chunk staged in TMEM (4 stager warps) / consumed (commit)
     unsigned xst[3];      // shared-x mode: template ssx, nzx, flags (built once)
     uint32_t tmem_base;
     int best[kTcAux][4][3];                 // per epilogue warp (value, j, count), per aux slot
@@ -573,6 +600,8 @@ struct TcRegs<2> {
     float4 y[6];  // samples 8(t + 512g) .. +8 in y[2g], y[2g + 1]
 };
 template <>
+struct TcRegs<4> : TcRegs<2> {};  // mode 4 builds like mode 2
+template <>
 struct TcRegs<3> {
     float4 y[12];  // 2-SM: window samples y0 + 8(t + 512g) .. +8, g < 6 (one buffer, refilled after each build)
 };
@@ -606,7 +635,7 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<M
             r.y[2 * g] = in ? tc_ld4(ys, i, ny) : make_float4(0.f, 0.f, 0.f, 0.f);
             r.y[2 * g + 1] = in ? tc_ld4(ys, i + 1, ny) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
-    } else if constexpr (MODE == 2) {
+    } else if constexpr (MODE == 2 || MODE == 4) {
 #pragma unroll
         for (int g = 0; g < 3; ++g) {
             const int i = 2 * ((int)threadIdx.x + g * kTcThreads);
@@ -1354,10 +1383,12 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool no
 // template (fp4, pitch 64), 3 shared template on a CTA pair (fp4, 2-SM MMA,
 // pitch 128; launched as clusters of 2, rank 0 issues the MMAs)
 template <typename T, int QM, int MODE>
-__global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_constant__ TcArgs a)
+__global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
-    constexpr bool SX = MODE != 0, F4 = MODE == 2, F2 = MODE == 3, FP4 = MODE >= 2;
-    constexpr int AUX = F2 ? 2 : 4;                  // accumulator / record slots
+    constexpr bool T4 = MODE == 4;                   // fp4, A in TMEM (otherwise as mode 2)
+    constexpr bool SX = MODE != 0, F4 = MODE == 2 || T4, F2 = MODE == 3, FP4 = MODE >= 2;
+    constexpr int AUX = (F2 || T4) ? 2 : 4;          // accumulator / record slots
+    constexpr uint32_t SFC = T4 ? kT4Sf : kF4Sf;     // TMEM column of the scale factors
     constexpr uint32_t kTmemCols = FP4 ? 512 : 128;  // fp4: accumulators + scale factors
     constexpr int PITCH = F2 ? kF2Pitch : F4 ? kF4Pitch : SX ? 32 : 16;
     extern __shared__ __align__(1024) unsigned char tc_smem_raw[];
@@ -1366,7 +1397,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     // branches keep descriptor arithmetic in uniform registers
     const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     const uint32_t rank = F2 ? cluster_rank() : 0u;
-    for (int i = threadIdx.x; i < kMaxThr; i += kTcTotalThreads) {
+    for (int i = threadIdx.x; i < kMaxThr; i += tc_threads(MODE)) {
         reinterpret_cast<T*>(S.thr[0])[i] = (T)a.op[0].q.thr[i];
         reinterpret_cast<T*>(S.thr[1])[i] = (T)a.op[1].q.thr[i];
     }
@@ -1379,6 +1410,10 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         mbar_init(&S.edone[threadIdx.x], 4);
         mbar_init(&S.xdone[threadIdx.x], 32 * TcRoles<MODE>::NLAG);
         if (threadIdx.x < 2) mbar_init(&S.pready[threadIdx.x], 1);
+        if (T4 && threadIdx.x < 2) {
+            mbar_init(&S.afull[threadIdx.x], 4);
+            mbar_init(&S.afree[threadIdx.x], 1);
+        }
     }
 #ifdef QX_TC_TIMING
     if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
@@ -1408,7 +1443,7 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
         // written by the epilogue warps (warp w reaches lanes 32*(w%4)..)
         static_assert(kF4Sf == kF2Sf, "one scale-factor column for both fp4 modes");
         if (warp >= kEpiWarp0 && warp < kEpiWarp0 + 4) {
-            const uint32_t t = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + kF4Sf;
+            const uint32_t t = S.tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + SFC;
             const uint32_t v = 0x7f7f7f7fu;
             asm volatile(
                 "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(t),
@@ -1496,6 +1531,8 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
     } else if (warp == kTcMmaWarp) {
         // ---- MMA issuer: the whole warp runs the loop, one elected lane issues
         const int nk = a.K / 32;
+        uint32_t t4gc = 0;  // mode 4: A chunks consumed
+        (void)t4gc;
         for (int it = 0; it < npairs; ++it) {
             const int s = it & 1, u = it % AUX;
             {
@@ -1523,11 +1560,27 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             const uint32_t ya = smem_u32(S.y[s]), ba = smem_u32(S.b + (SX ? 0 : s) * kTcBSlot);
             const uint64_t bd0 = smem_desc(ba, LBO, 128);
             const uint32_t tbase = __shfl_sync(0xffffffffu, S.tmem_base, 0);
-            if constexpr (FP4) {
+            if constexpr (T4) {
+                // A chunks from the stagers' TMEM ring, B from shared memory
+                const uint32_t d = tbase + (uint32_t)(u * kF4Pitch), sf = tbase + SFC;
+                const int nk4 = a.K / 64;
+                for (int c0 = 0; c0 < nk4; c0 += kT4Chunk, ++t4gc) {
+                    const int slot = t4gc & 1;
+                    mbar_wait(&S.afull[slot], (t4gc >> 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const int n = min(kT4Chunk, nk4 - c0);
+                    for (int j = 0; j < n; ++j) {
+                        const int k = c0 + j;
+                        mma_f4t_warp(d, tbase + (uint32_t)(kT4ACol + slot * 128 + 8 * j),
+                                     bd0 + (uint64_t)(k * BINC), a.idesc, k > 0 ? 1u : 0u, sf);
+                    }
+                    mma_commit_warp(&S.afree[slot]);  // the chunk's MMAs done: the stagers may refill it
+                }
+            } else if constexpr (FP4) {
                 // F4: one M=128 x N=64 tile (8192 lags); F2: one M=256 x N=128
                 // tile over the pair (32768 lags); K = 64 samples (32 B of A) per MMA
                 constexpr int CG = F2 ? 2 : 1;
-                const uint32_t d = tbase + (uint32_t)(u * PITCH), sf = tbase + kF4Sf;
+                const uint32_t d = tbase + (uint32_t)(u * PITCH), sf = tbase + SFC;
                 const uint64_t ad0 = F2 ? (smem_desc(ya, 16, 512) | (4ull << 61))   // SWIZZLE_64B, 8 rows x 64 B
                                         : (smem_desc(ya, 16, 256) | (6ull << 61));  // SWIZZLE_32B, 8 rows x 32 B
                 const uint32_t ahi = (uint32_t)(ad0 >> 32), bhi = (uint32_t)(bd0 >> 32);
@@ -1587,6 +1640,63 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
             if (a.extra) tc_extra_lags<SX ? 32 : 16, TcRoles<MODE>::NLAG>(a, S, it & 1, it % AUX, SX ? 0 : (it & 1));
             if (warp == kTcLagWarp0) tc_final_stats(a, S, it % AUX);
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.xdone[it % AUX])) : "memory");
+        }
+    } else if (T4 && warp >= kT4StageWarp0 && warp < kT4StageWarp0 + 4) {
+        // ---- mode 4 stagers: the pair's Hankel rows into the TMEM A ring
+        if constexpr (T4) {
+            const int q = warp & 3, row = q * 32 + lane;
+            const uint32_t lanebase = S.tmem_base + ((uint32_t)(q * 32) << 16);
+            const int nk4 = a.K / 64;
+            uint32_t gc = 0;
+            for (int it = 0; it < npairs; ++it) {
+                if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
+                else asm volatile("bar.sync 2, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
+                const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[it & 1]);
+                uint32_t w[8];  // row's words of K-step s: 8*row + 8*s + i
+#pragma unroll
+                for (int i = 0; i < 8; ++i) w[i] = yw[ysw<32>(8 * row + i)];
+                int s0 = 0;     // K-step held in w
+                for (int c0 = 0; c0 < nk4; c0 += kT4Chunk, ++gc) {
+                    const int slot = gc & 1;
+                    if (gc >= 2) mbar_wait(&S.afree[slot], ((gc >> 1) - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const int n = min(kT4Chunk, nk4 - c0);
+                    // groups of 4 K-steps: step s0 + k of row a = step s0 of row a + k
+                    // (lane shuffle; the last k lanes read the next quarter's rows from
+                    // shared memory), one 32-column tcgen05.st per group
+                    for (int j = 0; j < n; j += 4) {
+                        uint32_t g[32];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) {
+                                const uint32_t v = __shfl_down_sync(0xffffffffu, w[i], k);
+                                g[8 * k + i] = lane + k >= 32 ? yw[ysw<32>(8 * (row + k) + 8 * s0 + i)] : v;
+                            }
+                        asm volatile(
+                            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                                lanebase + (uint32_t)(kT4ACol + slot * 128 + 8 * j)),
+                            "r"(g[0]), "r"(g[1]), "r"(g[2]), "r"(g[3]), "r"(g[4]), "r"(g[5]), "r"(g[6]), "r"(g[7]),
+                            "r"(g[8]), "r"(g[9]), "r"(g[10]), "r"(g[11]), "r"(g[12]), "r"(g[13]), "r"(g[14]), "r"(g[15]),
+                            "r"(g[16]), "r"(g[17]), "r"(g[18]), "r"(g[19]), "r"(g[20]), "r"(g[21]), "r"(g[22]), "r"(g[23]),
+                            "r"(g[24]), "r"(g[25]), "r"(g[26]), "r"(g[27]), "r"(g[28]), "r"(g[29]), "r"(g[30]), "r"(g[31]));
+                        // advance 4 steps
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const uint32_t v = __shfl_down_sync(0xffffffffu, w[i], 4);
+                            w[i] = lane + 4 >= 32 ? yw[ysw<32>(8 * (row + 4) + 8 * s0 + i)] : v;
+                        }
+                        s0 += 4;
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0)
+                        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.afull[slot])) : "memory");
+                    s0 = c0 + kT4Chunk;  // (the last, partial chunk ends the pair)
+                }
+            }
         }
     } else if (TcRoles<MODE>::MERGE_WARP && warp == kTcMergeWarp) {
         // ---- merge: records -> qx_result (2-SM: one record per CTA and pair)
@@ -1727,7 +1837,7 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
         at[0].val.clusterDim.x = 2;
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
-        cfg.blockDim = dim3(kTcTotalThreads);
+        cfg.blockDim = dim3(tc_threads(MODE));
         cfg.dynamicSmemBytes = smem;
         cfg.stream = s;
         cfg.attrs = at;
@@ -1745,7 +1855,7 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
         if (e != cudaSuccess) return e;
     } else {
         const int grid = (int)(a.batch < sms ? a.batch : sms);
-        k_tc_window<T, QM, MODE><<<grid, kTcTotalThreads, smem, s>>>(a);
+        k_tc_window<T, QM, MODE><<<grid, tc_threads(MODE), smem, s>>>(a);
     }
     return cudaGetLastError();
 }
@@ -1829,9 +1939,21 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
         else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 3>(a, s, sms);
         else e = launch_tc<float, QM_BSEARCH, 3>(a, s, sms);
     } else {
-        if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
-        else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
+        // A operand in TMEM (mode 4) only with QX_TC_T4=1: exact, and its MMA
+        // runs at the fp4 peak, but four stager warps sliding the Hankel rows
+        // through lane shuffles do not keep up yet (1.28 ms vs 0.49 ms for
+        // config 5); mode 2 reads A from shared memory
+        const char* t4env = getenv("QX_TC_T4");
+        const bool t4 = t4env && t4env[0] == '1';
+        if (t4) {
+            if (qm == QM_K1) e = launch_tc<float, QM_K1, 4>(a, s, sms);
+            else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 4>(a, s, sms);
+            else e = launch_tc<float, QM_BSEARCH, 4>(a, s, sms);
+        } else {
+            if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
+            else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
+            else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
+        }
     }
     if (c.prof) c.prof->post(KK_DIRECT_F4, s);
     return e;

@@ -605,7 +605,7 @@ def test_sharded_template_search_over_nccl(qx):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("f4", ["0", "1"])
+@pytest.mark.parametrize("f4", ["0", "1", "t4"])
 def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
     """Every block summary of the shared-template window modes (i8 pitch 32,
     fp4 pitch 64) against the oracle, for templates whose length leaves the
@@ -613,8 +613,10 @@ def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
     need K >= nt + pitch - 1)."""
     import torch
 
-    monkeypatch.setenv("QX_TC_F4", f4)
-    block = 8192 if f4 == "1" else 4096
+    # "t4": the fp4 mode with the A operand in TMEM (QX_TC_T4=1)
+    monkeypatch.setenv("QX_TC_F4", "0" if f4 == "0" else "1")
+    monkeypatch.setenv("QX_TC_T4", "1" if f4 == "t4" else "0")
+    block = 4096 if f4 == "0" else 8192
     for seed, (nt, q) in enumerate([(4, qx.sign()), (8, qx.sign()), (40, qx.uniform(1, 0.8)),
                                     (1000, qx.sign()), (2052, qx.uniform(1, 0.8))]):
         rng = np.random.default_rng(seed)

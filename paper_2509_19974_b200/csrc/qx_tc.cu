@@ -63,12 +63,10 @@ struct TcRoles {
     static constexpr int HANDOFF = kTcThreads + 32 + 32 * NLAG + (MODE == 4 ? 128 : 0);
 };
 // mode 4: fp4 with the Hankel A operand in TMEM.  Stager warps 24-27 (one per
-// TMEM lane quarter) hold each row's 8 words of the current K-step, store
-// them with tcgen05.st and slide them down one lane per step (row a at step
-// s + 1 = row a + 1 at step s), so shared memory serves 32 B per warp and
-// step instead of the 4-KB A tile; A chunks of 16 K-steps alternate in a
-// two-chunk TMEM ring with full/free mbarriers (tools/tc_fp4_tmema.cu:
-// 32.5 cycles per M128 N64 K64 MMA with A in TMEM vs 68 from shared memory)
+// TMEM lane quarter) copy each row's next 4 K-steps (32 words) from the y slot
+// into TMEM with one 32-column tcgen05.st; A chunks of 16 K-steps alternate in
+// a two-chunk TMEM ring with full/free mbarriers (tools/tc_fp4_tmema.cu: 32.5
+// cycles per M128 N64 K64 MMA with A in TMEM vs 68 from shared memory)
 constexpr int kT4StageWarp0 = 24;
 constexpr int kT4Chunk = 16;    // K-steps per A chunk (8 TMEM columns each)
 constexpr int kT4ACol = 128;    // TMEM columns 128..383: the two A chunks
@@ -426,7 +424,7 @@ struct TcSmem {
     int best[kTcAux][4][3];                 // per epilogue warp (value, j, count), per aux slot
     unsigned long long fst[kTcAux][5];      // final statistics of the pair (lag warps)
 #ifdef QX_TC_TIMING
-    unsigned long long tm[16];
+    unsigned long long tm[20];
 #endif
 };
 
@@ -1416,7 +1414,7 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
         }
     }
 #ifdef QX_TC_TIMING
-    if (threadIdx.x < 16) S.tm[threadIdx.x] = 0;
+    if (threadIdx.x < 20) S.tm[threadIdx.x] = 0;
     const long long k_t0 = clock64();
     unsigned long long k_g0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(k_g0));
@@ -1566,7 +1564,13 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
                 const int nk4 = a.K / 64;
                 for (int c0 = 0; c0 < nk4; c0 += kT4Chunk, ++t4gc) {
                     const int slot = t4gc & 1;
+#ifdef QX_TC_TIMING
+                    long long _m0 = clock64();
+#endif
                     mbar_wait(&S.afull[slot], (t4gc >> 1) & 1);
+#ifdef QX_TC_TIMING
+                    if (lane == 0) atomicAdd(&S.tm[18], (unsigned long long)(clock64() - _m0));
+#endif
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const int n = min(kT4Chunk, nk4 - c0);
                     for (int j = 0; j < n; ++j) {
@@ -1652,27 +1656,38 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
                 if (it & 1) asm volatile("bar.sync 3, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
                 else asm volatile("bar.sync 2, %0;" ::"n"(TcRoles<MODE>::HANDOFF) : "memory");
                 const uint32_t* yw = reinterpret_cast<const uint32_t*>(S.y[it & 1]);
-                uint32_t w[8];  // row's words of K-step s: 8*row + 8*s + i
-#pragma unroll
-                for (int i = 0; i < 8; ++i) w[i] = yw[ysw<32>(8 * row + i)];
-                int s0 = 0;     // K-step held in w
+                int s0 = 0;  // next K-step to stage
                 for (int c0 = 0; c0 < nk4; c0 += kT4Chunk, ++gc) {
                     const int slot = gc & 1;
+#ifdef QX_TC_TIMING
+                    long long _s0 = clock64();
+#endif
                     if (gc >= 2) mbar_wait(&S.afree[slot], ((gc >> 1) - 1) & 1);
+#ifdef QX_TC_TIMING
+                    long long _s1 = clock64();
+                    if (threadIdx.x == kT4StageWarp0 * 32) atomicAdd(&S.tm[16], (unsigned long long)(_s1 - _s0));
+#endif
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                     const int n = min(kT4Chunk, nk4 - c0);
-                    // groups of 4 K-steps: step s0 + k of row a = step s0 of row a + k
-                    // (lane shuffle; the last k lanes read the next quarter's rows from
-                    // shared memory), one 32-column tcgen05.st per group
+                    // groups of 4 K-steps, one 32-column tcgen05.st each; the row's
+                    // 4 x 8 words are contiguous in the (SW32-swizzled) y slot: two
+                    // 16-B loads per step (the swizzle swaps the halves of 32 B)
                     for (int j = 0; j < n; j += 4) {
                         uint32_t g[32];
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-#pragma unroll
-                            for (int i = 0; i < 8; ++i) {
-                                const uint32_t v = __shfl_down_sync(0xffffffffu, w[i], k);
-                                g[8 * k + i] = lane + k >= 32 ? yw[ysw<32>(8 * (row + k) + 8 * s0 + i)] : v;
-                            }
+                        for (int k = 0; k < 4; ++k) {
+                            const int base = 8 * row + 8 * (s0 + k), b5 = (base >> 5) & 1;
+                            const uint4 lo = *reinterpret_cast<const uint4*>(yw + base + 4 * b5);
+                            const uint4 hi = *reinterpret_cast<const uint4*>(yw + base + 4 * (1 - b5));
+                            g[8 * k + 0] = lo.x;
+                            g[8 * k + 1] = lo.y;
+                            g[8 * k + 2] = lo.z;
+                            g[8 * k + 3] = lo.w;
+                            g[8 * k + 4] = hi.x;
+                            g[8 * k + 5] = hi.y;
+                            g[8 * k + 6] = hi.z;
+                            g[8 * k + 7] = hi.w;
+                        }
                         asm volatile(
                             "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
                             "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
@@ -1681,17 +1696,14 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
                             "r"(g[8]), "r"(g[9]), "r"(g[10]), "r"(g[11]), "r"(g[12]), "r"(g[13]), "r"(g[14]), "r"(g[15]),
                             "r"(g[16]), "r"(g[17]), "r"(g[18]), "r"(g[19]), "r"(g[20]), "r"(g[21]), "r"(g[22]), "r"(g[23]),
                             "r"(g[24]), "r"(g[25]), "r"(g[26]), "r"(g[27]), "r"(g[28]), "r"(g[29]), "r"(g[30]), "r"(g[31]));
-                        // advance 4 steps
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            const uint32_t v = __shfl_down_sync(0xffffffffu, w[i], 4);
-                            w[i] = lane + 4 >= 32 ? yw[ysw<32>(8 * (row + 4) + 8 * s0 + i)] : v;
-                        }
                         s0 += 4;
                     }
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                     __syncwarp();
+#ifdef QX_TC_TIMING
+                    if (threadIdx.x == kT4StageWarp0 * 32) atomicAdd(&S.tm[17], (unsigned long long)(clock64() - _s1));
+#endif
                     if (lane == 0)
                         asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&S.afull[slot])) : "memory");
                     s0 = c0 + kT4Chunk;  // (the last, partial chunk ends the pair)
@@ -1753,6 +1765,9 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
                "wait-tfree %llu issue %llu | epi: wait %llu run %llu\n",
                (long long)npairs, a.debug, S.tm[0] / npairs, S.tm[1] / npairs, S.tm[2] / npairs, S.tm[4] / npairs,
                S.tm[5] / npairs, S.tm[3] / npairs, S.tm[6] / npairs);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && npairs)
+        printf("  t4 (cycles/pair): stager wait-free %llu stage %llu | mma wait-full %llu\n", S.tm[16] / npairs,
+               S.tm[17] / npairs, S.tm[18] / npairs);
     if (blockIdx.x == 0 && threadIdx.x == 0 && npairs)
         printf("  build phases (cycles/pair): zero %llu quant %llu bar %llu copies %llu aux %llu | epi: tmem+scan %llu "
                "shfl %llu bars+merge %llu\n", S.tm[8] / npairs, S.tm[9] / npairs, S.tm[10] / npairs,
@@ -1940,9 +1955,8 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
         else e = launch_tc<float, QM_BSEARCH, 3>(a, s, sms);
     } else {
         // A operand in TMEM (mode 4) only with QX_TC_T4=1: exact, and its MMA
-        // runs at the fp4 peak, but four stager warps sliding the Hankel rows
-        // through lane shuffles do not keep up yet (1.28 ms vs 0.49 ms for
-        // config 5); mode 2 reads A from shared memory
+        // runs at the fp4 peak, but its four stager warps do not keep up yet
+        // (0.72 ms vs 0.49 ms for config 5); mode 2 reads A from shared memory
         const char* t4env = getenv("QX_TC_T4");
         const bool t4 = t4env && t4env[0] == '1';
         if (t4) {

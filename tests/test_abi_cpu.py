@@ -25,6 +25,24 @@ def test_exports_every_declared_symbol():
     assert L.qx_status_string(2) == b"quantizes to all zeros"
 
 
+def test_header_constants_match_the_python_mirror():
+    """The ctypes mirror agrees with include/qxcorr_b200.h on the ABI version,
+    the profile-kind count (qx_profile's array sizes), the path enum and the
+    profile kind names the C library reports."""
+    from paper_2509_19974_b200 import _native as N
+
+    header = open(os.path.join(ROOT, "include", "qxcorr_b200.h")).read()
+    kinds = int(re.search(r"#define QX_PROFILE_KINDS (\d+)", header).group(1))
+    assert kinds == N.PROFILE_KINDS == len(N.QxProfile._fields_[1][1]()) and \
+        ctypes.sizeof(N.QxProfile) == 8 + 16 * kinds
+    paths = dict(re.findall(r"QX_PATH_([A-Z]+) = (\d)", header))
+    assert {k.lower(): int(v) for k, v in paths.items()} == {k: v for k, v in N.PATHS.items() if k != "tc"}
+    assert N.PATHS["tc"] == N.PATHS["direct"]
+    L = N.load()
+    names = [L.qx_profile_kind_name(i).decode() for i in range(kinds)]
+    assert {"ntt_pass1", "ntt_pass2", "ntt_pass3", "direct", "direct_f4", "popc"} <= set(names)
+
+
 def _levels(thr, vals, k):
     # level(v) = -k + #{i : v >= T[i]}
     return np.searchsorted(thr, vals, side="right") - k

@@ -841,10 +841,17 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // tail after the last copy)
     std::vector<std::pair<int64_t, int64_t>> chunks;  // (first pair, pairs)
     {
-        const bool halves = nl > 1 && nchunk >= 4 && per >= 2 && !getenv("QX_SWEEP_EVEN");
+        // tapered ends (first and last chunk per/T pairs, T = QX_SWEEP_TAPER, default 2):
+        // less copy exposed before the first launch, a shorter compute tail
+        const bool taper = nl > 1 && nchunk >= 4 && per >= 2 && !getenv("QX_SWEEP_EVEN");
+        int64_t T = 2;
+        if (const char* ev = getenv("QX_SWEEP_TAPER")) T = std::max<int64_t>(1, atoll(ev));
+        const int64_t q = std::max<int64_t>(1, per / T);
         int64_t b0 = 0;
         while (b0 < batch) {
-            int64_t nb = (halves && b0 == 0) ? per / 2 : per;
+            int64_t nb = (taper && b0 == 0) ? q : per;
+            // taper: end on a q-pair chunk (the one before takes the remainder)
+            if (taper && b0 > 0 && batch - b0 > q && batch - b0 - nb < q) nb = batch - b0 - q;
             nb = std::min(nb, batch - b0);
             chunks.emplace_back(b0, nb);
             b0 += nb;

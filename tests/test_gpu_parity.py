@@ -372,6 +372,28 @@ def test_sweep_host_entry_point(qx, oracle):
                 assert np.array_equal(res[q]["ties"], want[:, 2])
 
 
+@pytest.mark.parametrize("pairs", [1, 5, 17, 40, 67])
+@pytest.mark.parametrize("knobs", [{}, {"QX_SWEEP_LANES": "1"}, {"QX_SWEEP_CHUNKS": "7", "QX_SWEEP_TAPER": "3"},
+                                   {"QX_SWEEP_LANES": "2", "QX_SWEEP_CHUNKS": "64"}, {"QX_SWEEP_EVEN": "1"}])
+def test_sweep_host_chunk_schedules(qx, pairs, knobs, monkeypatch):
+    """Every chunk/lane/taper schedule of qx_estimate_sweep_host covers each
+    pair exactly once: results equal per-quantiser estimate_batch_host calls
+    for ragged batch sizes (1 pair, primes, more chunks than pairs)."""
+    from paper_2509_19974_b200 import workloads as W
+
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    xs, ys, lag = W.c2(pairs=pairs, n=1 << 10, seed=pairs)
+    qs = [(W.bit_quantizer(b, W.C2_SIGMA), W.bit_quantizer(b, W.C2_SIGMA)) for b in (1, 2, 8)]
+    qs.append((qx.uniform(3, 0.4), qx.sign()))
+    for lo, hi in ((None, None), (-300, 300)):
+        res = qx.estimate_sweep_host(xs, ys, qs, lag_lo=lo, lag_hi=hi)
+        assert res.shape == (len(qs), pairs)
+        for q, (a, b) in enumerate(qs):
+            one = qx.estimate_batch_host(xs, ys, a, b, lag_lo=lo, lag_hi=hi)
+            assert np.array_equal(res[q], one), (q, lo)
+
+
 def test_big_mul_cuda_backend(qx):
     """The reference's plugin slot big_mul (intxcorr.py:183-205) with backend
     "cuda": worked product and identities (pkg/tests/test_intxcorr.py:139-149),

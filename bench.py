@@ -304,7 +304,24 @@ def main():
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         for r in res:
             assert np.array_equal(r["lag"], lag)
-        e2e = {"value": est_per_step * n_e2e / float(e2e_s.item()), "unit": UNIT,
+        # the bound e2e is held to: the same bytes as plain pinned H2D copies
+        # (event-timed, nothing else on the device)
+        dx, dy = torch.empty_like(hx, device=dev), torch.empty_like(hy, device=dev)
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dx.copy_(hx, non_blocking=True), dy.copy_(hy, non_blocking=True)
+        ev0.record()
+        for _ in range(n_e2e):
+            dx.copy_(hx, non_blocking=True)
+            dy.copy_(hy, non_blocking=True)
+        ev1.record()
+        torch.cuda.synchronize()
+        h2d_s = ev0.elapsed_time(ev1) / 1e3 / n_e2e
+        del dx, dy
+        e2e_val = est_per_step * n_e2e / float(e2e_s.item())
+        e2e = {"value": e2e_val, "unit": UNIT,
+               "h2d_gbs": (xs.nbytes + ys.nbytes) / h2d_s / 1e9,
+               "h2d_bound": {"value": est_per_step / h2d_s, "frac": e2e_val / (est_per_step / h2d_s),
+                             "what": "estimates/s if each step cost only its pinned H2D copy"},
                "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes),
                "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e,
                "path": "qx_estimate_sweep_host (C ABI, pinned host buffers; inputs staged once per step "

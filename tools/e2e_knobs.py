@@ -1,0 +1,56 @@
+"""C2 end-to-end (qx_estimate_sweep_host) under the sweep schedule knobs,
+beside the plain pinned-H2D bound of the same bytes.  One process; the knobs
+are read per call.  Usage: python tools/e2e_knobs.py [reps]"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2509_19974_b200 as P  # noqa: E402
+from paper_2509_19974_b200 import workloads as W  # noqa: E402
+
+reps = int(sys.argv[1]) if len(sys.argv) > 1 else 10
+xs, ys, lag = W.c2()
+qs = [W.bit_quantizer(b, W.C2_SIGMA) for b in (1, 2, 4, 8)]
+sweep = [(q, q) for q in qs]
+hx, hy = torch.from_numpy(xs).pin_memory(), torch.from_numpy(ys).pin_memory()
+hxn, hyn = hx.numpy(), hy.numpy()
+est = len(qs) * xs.shape[0]
+
+dx, dy = torch.empty_like(hx, device="cuda"), torch.empty_like(hy, device="cuda")
+for _ in range(2):
+    dx.copy_(hx, non_blocking=True), dy.copy_(hy, non_blocking=True)
+torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record()
+for _ in range(reps):
+    dx.copy_(hx, non_blocking=True), dy.copy_(hy, non_blocking=True)
+e1.record()
+torch.cuda.synchronize()
+h2d = e0.elapsed_time(e1) / reps
+print(f"pinned H2D {xs.nbytes + ys.nbytes} B: {h2d:.3f} ms ({(xs.nbytes + ys.nbytes) / h2d / 1e6:.1f} GB/s)"
+      f" -> bound {est / h2d * 1e3:.0f} est/s")
+
+KNOBS = [{}, {"QX_SWEEP_TAPER": "1"}, {"QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS": "16"},
+         {"QX_SWEEP_CHUNKS": "16", "QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS": "4"},
+         {"QX_SWEEP_CHUNKS": "32"}, {"QX_SWEEP_LANES": "2"}, {"QX_SWEEP_EVEN": "1"}, {}]
+for kn in KNOBS:
+    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN"):
+        os.environ.pop(k, None)
+    os.environ.update(kn)
+    for _ in range(2):
+        P.estimate_sweep_host(hxn, hyn, sweep)
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res = P.estimate_sweep_host(hxn, hyn, sweep)
+        ts.append(time.perf_counter() - t0)
+    for r in res:
+        assert np.array_equal(r["lag"], lag)
+    ts = np.array(ts) * 1e3
+    print(f"{str(kn):55s} median {np.median(ts):.3f} ms  min {ts.min():.3f}  -> {est / np.median(ts) * 1e3:.0f} est/s"
+          f"  ({h2d / np.median(ts):.2f} of H2D bound)")

@@ -856,6 +856,18 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
             chunks.emplace_back(b0, nb);
             b0 += nb;
         }
+        // QX_SWEEP_PLAN="a,b,c,...": explicit chunk sizes (used when they sum to batch)
+        if (const char* ev = getenv("QX_SWEEP_PLAN"); ev && disjoint) {
+            std::vector<std::pair<int64_t, int64_t>> plan;
+            int64_t at = 0;
+            for (const char* p = ev; *p;) {
+                const int64_t v = atoll(p);
+                if (v > 0) plan.emplace_back(at, v), at += v;
+                while (*p && *p != ',') ++p;
+                if (*p == ',') ++p;
+            }
+            if (at == batch) chunks.swap(plan);
+        }
         nchunk = (int64_t)chunks.size();
     }
     while ((int64_t)ctx->chunk_ev.size() < nchunk) {

@@ -35,10 +35,12 @@ print(f"pinned H2D {xs.nbytes + ys.nbytes} B: {h2d:.3f} ms ({(xs.nbytes + ys.nby
       f" -> bound {est / h2d * 1e3:.0f} est/s")
 
 KNOBS = [{}, {"QX_SWEEP_TAPER": "1"}, {"QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS": "16"},
-         {"QX_SWEEP_CHUNKS": "16", "QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS": "4"},
-         {"QX_SWEEP_CHUNKS": "32"}, {"QX_SWEEP_LANES": "2"}, {"QX_SWEEP_EVEN": "1"}, {}]
+         {"QX_SWEEP_CHUNKS": "4"}, {"QX_SWEEP_LANES": "2"}, {"QX_SWEEP_EVEN": "1"}]
+PLANS = os.environ.get("PLANS", "4,12,16,16,12,4;4,8,16,16,16,4;2,6,12,16,16,10,2;4,12,24,20,4;"
+                       "8,16,16,16,8;4,28,28,4;4,10,16,16,10,6,2;6,12,16,16,10,4").split(";")
+KNOBS += [{"QX_SWEEP_PLAN": p} for p in PLANS] + [{}]
 for kn in KNOBS:
-    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN"):
+    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN", "QX_SWEEP_PLAN"):
         os.environ.pop(k, None)
     os.environ.update(kn)
     for _ in range(2):

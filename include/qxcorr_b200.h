@@ -18,6 +18,10 @@
  *                               optional lag window (new; parity = the full
  *                               reference correlogram sliced to the window)
  *   qx_estimate_batch_host   <- the same from host buffers (H2D/D2H inside)
+ *   qx_estimate_sweep[_host] <- estimate() once per quantiser pair of a
+ *                               bit-depth sweep (harness.py:141-147), device
+ *                               rows / host buffers
+ *   qx_template_search       <- estimate(template, stream) over the valid lags
  *
  * Conventions
  *   - Device pointers are caller-owned; `stream` is a cudaStream_t (NULL =
@@ -142,6 +146,17 @@ qx_status qx_estimate_batch(qx_context *ctx, const qx_signals *x, const qx_signa
 qx_status qx_estimate_batch_host(qx_context *ctx, const qx_signals *x, const qx_signals *y,
                                  int64_t batch, const qx_quantizer *qx, const qx_quantizer *qy,
                                  int64_t lag_lo, int64_t lag_hi, qx_path path, qx_result *results);
+
+/* Sweep of nq quantiser pairs over one batch of DEVICE rows (the bit-depth
+ * sweep of BASELINE config 2 with its inputs resident in HBM): estimate() of
+ * estimator.py:60-94 once per (qx[q], qy[q]), the quantiser pairs on up to
+ * four concurrent compute lanes (streams with their own scratch) forked from
+ * and joined back to `stream`; results (device) [q*batch + b] as
+ * qx_estimate_batch.  Enqueued; does not synchronise. */
+qx_status qx_estimate_sweep(qx_context *ctx, const qx_signals *x, const qx_signals *y,
+                            int64_t batch, int64_t nq, const qx_quantizer *qx,
+                            const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
+                            qx_path path, qx_result *results, void *stream);
 
 /* Sweep of nq quantiser pairs over one batch from HOST buffers (the
  * bit-depth sweep of BASELINE config 2, i.e. estimate() of estimator.py:60-94

@@ -14,7 +14,8 @@ Batched, windowed and streaming entry points (new): ``estimate_batch``,
 """
 
 from . import accuracy, ingest
-from .batch import BatchResult, check_results, estimate_batch, estimate_batch_host, estimate_sweep_host, template_search
+from .batch import (BatchResult, check_results, estimate_batch, estimate_batch_host, estimate_sweep,
+                    estimate_sweep_host, template_search)
 from .errors import (
     BadLength,
     ConfigError,
@@ -40,6 +41,6 @@ __all__ = [
     "Quantizer", "sign", "uniform", "custom", "from_spec", "apply",
     "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "big_mul", "MUL_BACKENDS",
     "EstimationResult", "argmax_set", "estimate",
-    "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep_host", "check_results", "template_search",
+    "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host", "check_results", "template_search",
     "accuracy", "ingest",
 ]

@@ -75,7 +75,7 @@ assert RESULT_DTYPE.itemsize == ctypes.sizeof(QxResult) == 64
 EXPORTS = (
     "qx_abi_version", "qx_status_string", "qx_context_create", "qx_context_destroy",
     "qx_context_last_error", "qx_quantizer_thresholds", "qx_quantize", "qx_xcorr_full",
-    "qx_estimate_batch", "qx_estimate_batch_host", "qx_estimate_sweep_host", "qx_template_search", "qx_decode_pcm16",
+    "qx_estimate_batch", "qx_estimate_batch_host", "qx_estimate_sweep", "qx_estimate_sweep_host", "qx_template_search", "qx_decode_pcm16",
     "qx_profile_begin",
     "qx_profile_end",
     "qx_profile_kind_name",
@@ -122,6 +122,9 @@ def load():
         L.qx_estimate_batch_host.restype = st
         L.qx_estimate_sweep_host.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp]
         L.qx_estimate_sweep_host.restype = st
+        if hasattr(L, "qx_estimate_sweep"):  # (absent from older A/B builds)
+            L.qx_estimate_sweep.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp, vp]
+            L.qx_estimate_sweep.restype = st
         if hasattr(L, "qx_template_search"):  # (absent from older A/B builds)
             L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
             L.qx_template_search.restype = st

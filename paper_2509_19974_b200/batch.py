@@ -19,7 +19,8 @@ from . import _native as N
 from ._call import call, raise_for
 from .quantize import native_quantizer
 
-__all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "check_results", "template_search"]
+__all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host",
+           "check_results", "template_search"]
 
 
 @dataclass
@@ -87,6 +88,37 @@ def estimate_batch(x, y, qx, qy, *, lag_lo=None, lag_hi=None, x_start=0, y_start
     call(N.load().qx_estimate_batch, ctx, ctypes.byref(sx), ctypes.byref(sy), batch, ctypes.byref(nqx),
          ctypes.byref(nqy), lo, hi, N.PATHS[path], raw.data_ptr(), D.stream_handle())
     return BatchResult(raw)
+
+
+def estimate_sweep(x, y, quantizers, *, lag_lo=None, lag_hi=None, x_start=0, y_start=0, path="auto",
+                   out=None) -> list:
+    """Several quantiser pairs over one batch of DEVICE rows (a bit-depth
+    sweep) through qx_estimate_sweep: one C-ABI call whose correlations run
+    on concurrent compute lanes, joined back to the current stream.
+    `quantizers` is a sequence of (qx, qy); returns one BatchResult per pair
+    (views of one (nq, B, 8) int64 tensor)."""
+    t = D.torch()
+    x = D.as_device(x)
+    y = D.as_device(y)
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if y.dim() == 1:
+        y = y.unsqueeze(0)
+    if x.shape[0] != y.shape[0]:
+        raise ValueError("x and y must hold the same number of rows")
+    batch, nq = x.shape[0], len(quantizers)
+    if nq < 1:
+        raise ValueError("need at least one quantiser pair")
+    raw = out if out is not None else t.empty((nq, batch, 8), dtype=t.int64, device=x.device)
+    keep = [(native_quantizer(a), native_quantizer(b)) for a, b in quantizers]
+    aqx = (N.QxQuantizer * nq)(*[k[0][0] for k in keep])
+    aqy = (N.QxQuantizer * nq)(*[k[1][0] for k in keep])
+    sx, sy = D.signals(x, x_start), D.signals(y, y_start)
+    lo, hi = _bounds(lag_lo, lag_hi)
+    ctx = N.context(x.device.index)
+    call(N.load().qx_estimate_sweep, ctx, ctypes.byref(sx), ctypes.byref(sy), batch, nq, aqx, aqy, lo, hi,
+         N.PATHS[path], raw.data_ptr(), D.stream_handle())
+    return [BatchResult(raw[q]) for q in range(nq)]
 
 
 def estimate_batch_host(x: np.ndarray, y: np.ndarray, qx, qy, *, lag_lo=None, lag_hi=None, x_start=0,

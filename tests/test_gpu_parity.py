@@ -372,6 +372,41 @@ def test_sweep_host_entry_point(qx, oracle):
                 assert np.array_equal(res[q]["ties"], want[:, 2])
 
 
+@pytest.mark.parametrize("lanes", [None, "1", "3"])
+def test_device_sweep_entry_point(qx, oracle, lanes, monkeypatch):
+    """qx_estimate_sweep: device rows, quantiser pairs on forked compute lanes
+    joined back to the caller's stream; equals one estimate_batch per pair and
+    the oracle, and a kernel on the caller's stream right after the call sees
+    finished results."""
+    import torch
+    from paper_2509_19974_b200 import workloads as W
+
+    if lanes:
+        monkeypatch.setenv("QX_SWEEP_LANES", lanes)
+    xs, ys, lag = W.c2(pairs=6, n=1 << 12, seed=5)
+    qs = [(W.bit_quantizer(b, W.C2_SIGMA), W.bit_quantizer(b, W.C2_SIGMA)) for b in (1, 2, 4, 8)]
+    qs.append((qx.uniform(3, 0.4), qx.sign()))
+    dx, dy = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    for lo, hi in ((None, None), (-700, 700)):
+        side = torch.cuda.Stream()
+        with torch.cuda.stream(side):
+            res = qx.estimate_sweep(dx, dy, qs, lag_lo=lo, lag_hi=hi)
+            summed = torch.stack([r.value for r in res]).sum()  # consumer on the caller's stream
+        side.synchronize()
+        assert len(res) == len(qs)
+        tot = 0
+        for q, (a, b) in enumerate(qs):
+            one = qx.estimate_batch(dx, dy, a, b, lag_lo=lo, lag_hi=hi)
+            torch.cuda.synchronize()
+            assert torch.equal(res[q].raw, one.raw), q
+            tot += int(one.value.sum())
+            if lo is None:
+                want = oracle.estimate_batch_f32(xs, ys, a, b)
+                assert np.array_equal(res[q].value.cpu().numpy(), want[:, 0])
+                assert np.array_equal(res[q].lag.cpu().numpy(), want[:, 1] - (xs.shape[1] - 1))
+        assert int(summed) == tot
+
+
 @pytest.mark.parametrize("pairs", [1, 5, 17, 40, 67])
 @pytest.mark.parametrize("knobs", [{}, {"QX_SWEEP_LANES": "1"}, {"QX_SWEEP_CHUNKS": "7", "QX_SWEEP_TAPER": "3"},
                                    {"QX_SWEEP_LANES": "2", "QX_SWEEP_CHUNKS": "64"}, {"QX_SWEEP_EVEN": "1"}])

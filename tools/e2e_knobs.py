@@ -39,8 +39,14 @@ KNOBS = [{}, {"QX_SWEEP_TAPER": "1"}, {"QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS
 PLANS = os.environ.get("PLANS", "4,12,16,16,12,4;4,8,16,16,16,4;2,6,12,16,16,10,2;4,12,24,20,4;"
                        "8,16,16,16,8;4,28,28,4;4,10,16,16,10,6,2;6,12,16,16,10,4").split(";")
 KNOBS += [{"QX_SWEEP_PLAN": p} for p in PLANS] + [{}]
+if os.environ.get("RESTAGE_ONLY"):
+    KNOBS = [{}, {"QX_SWEEP_RESTAGE": "0"}, {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_CHUNKS": "1"},
+             {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_CHUNKS": "2"}, {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_CHUNKS": "4"},
+             {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_EVEN": "1"}, {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_CHUNKS": "16"},
+             {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_LANES": "1", "QX_SWEEP_CHUNKS": "1"}, {}]
 for kn in KNOBS:
-    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN", "QX_SWEEP_PLAN"):
+    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN", "QX_SWEEP_PLAN",
+              "QX_SWEEP_RESTAGE"):
         os.environ.pop(k, None)
     os.environ.update(kn)
     for _ in range(2):

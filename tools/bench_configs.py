@@ -114,7 +114,7 @@ def run(which) -> dict:
                 qa = qb = P.sign()
             else:
                 qa, qb = P.uniform(1, 1.5 * math.sqrt(2.0)), P.uniform(1, 1.5 * math.sqrt(2.0 + sn2))
-            ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=2, warm=1)
+            ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=10, warm=2)
             assert r[1] == off, r
             res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
                                "lag": r[1], "fp4_tensor_frac": macs / (ms / 1e3) / fp4,

@@ -37,6 +37,7 @@ METRIC = "lag estimates/sec (quantize+int xcorr+argmax)"
 UNIT = "estimates/s"
 BITS = (1, 2, 4, 8)
 L2_BYTES = 126 * (1 << 20)
+E2E_WARM = 60  # e2e warm-up calls (see the e2e block in main)
 
 
 def parse():
@@ -297,9 +298,13 @@ def main():
         hx = torch.from_numpy(xs).pin_memory()
         hy = torch.from_numpy(ys).pin_memory()
         hxn, hyn = hx.numpy(), hy.numpy()
-        n_e2e = max(3, args.steps // 3)
+        n_e2e = max(10, args.steps // 3)
         sweep = [(q, q) for q in qs]
-        for _ in range(2):  # lane streams, arenas and staging reach their steady size
+        # warm-up: lane streams, arenas and staging reach their steady size,
+        # and freshly pinned host buffers reach their steady DMA rate -- the
+        # first ~40 copies from a new pinned allocation run up to 30% slower
+        # (tools/e2e_series.py, profiles/r01_e2e_series.txt)
+        for _ in range(E2E_WARM):
             P.estimate_sweep_host(hxn, hyn, sweep, device=local)
         if world > 1:
             dist.barrier()
@@ -316,28 +321,38 @@ def main():
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         for r in res:
             assert np.array_equal(r["lag"], lag)
-        # the bound e2e is held to: the same bytes as plain pinned H2D copies
-        # (event-timed, nothing else on the device)
-        dx, dy = torch.empty_like(hx, device=dev), torch.empty_like(hy, device=dev)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dx.copy_(hx, non_blocking=True), dy.copy_(hy, non_blocking=True)
-        ev0.record()
-        for _ in range(n_e2e):
-            dx.copy_(hx, non_blocking=True)
-            dy.copy_(hy, non_blocking=True)
-        ev1.record()
-        torch.cuda.synchronize()
-        h2d_s = ev0.elapsed_time(ev1) / 1e3 / n_e2e
-        del dx, dy
+        # the bound e2e is held to: the same call with its kernels skipped
+        # (QX_SWEEP_COMPUTE=0: the chunked pinned H2D copies, joins and the
+        # results D2H alone), wall-clock per call like e2e
+        os.environ["QX_SWEEP_COMPUTE"] = "0"
+        try:
+            P.estimate_sweep_host(hxn, hyn, sweep, device=local)
+            tb = time.perf_counter()
+            for _ in range(n_e2e):
+                P.estimate_sweep_host(hxn, hyn, sweep, device=local)
+            h2d_s = (time.perf_counter() - tb) / n_e2e
+        finally:
+            del os.environ["QX_SWEEP_COMPUTE"]
+        # and with its copies skipped (QX_SWEEP_RESTAGE=0: the staging buffer
+        # already holds these inputs): the same schedule's compute alone
+        os.environ["QX_SWEEP_RESTAGE"] = "0"
+        try:
+            tb = time.perf_counter()
+            for _ in range(n_e2e):
+                P.estimate_sweep_host(hxn, hyn, sweep, device=local)
+            comp_s = (time.perf_counter() - tb) / n_e2e
+        finally:
+            del os.environ["QX_SWEEP_RESTAGE"]
         e2e_val = est_per_step * n_e2e / float(e2e_s.item())
         e2e = {"value": e2e_val, "unit": UNIT,
                "call_ms": {"median": 1e3 * statistics.median(call_s), "min": 1e3 * min(call_s),
                            "max": 1e3 * max(call_s)},
                "h2d_gbs": (xs.nbytes + ys.nbytes) / h2d_s / 1e9,
+               "copy_only_ms": 1e3 * h2d_s, "compute_only_ms": 1e3 * comp_s,
                "h2d_bound": {"value": est_per_step / h2d_s, "frac": e2e_val / (est_per_step / h2d_s),
-                             "what": "estimates/s if each step cost only its pinned H2D copy"},
+                             "what": "estimates/s if each step cost only its copies (the same call, kernels skipped)"},
                "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes),
-               "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e,
+               "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e, "warmup_calls": E2E_WARM,
                "path": "qx_estimate_sweep_host (C ABI, pinned host buffers; inputs staged once per step "
                        "in 8-pair chunks on a copy stream, the 4 bit depths of each chunk on 4 concurrent "
                        "compute lanes)"}

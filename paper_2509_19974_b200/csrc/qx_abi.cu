@@ -542,10 +542,11 @@ static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const q
 // Compute lanes of the sweep entry points: up to 4 streams (QX_SWEEP_LANES),
 // one per quantiser pair in turn, each with its own scratch, so the sweep's
 // independent correlations overlap instead of each draining the machine.
-static cudaError_t open_lanes(qx_context* ctx, int64_t nq, int* nl_out)
+static cudaError_t open_lanes(qx_context* ctx, int64_t nq, int* nl_out, int64_t most = 0)
 {
     int nl = (int)std::min<int64_t>(nq, 4);
-    if (const char* ev = getenv("QX_SWEEP_LANES")) nl = (int)std::max<int64_t>(1, std::min<int64_t>(nq, atoll(ev)));
+    if (const char* ev = getenv("QX_SWEEP_LANES"))
+        nl = (int)std::max<int64_t>(1, std::min<int64_t>(most > 0 ? most : nq, atoll(ev)));
     nl = std::min(nl, kMaxLanes);
     cudaError_t e = cudaSuccess;
     for (int l = 0; l < nl && e == cudaSuccess; ++l) {
@@ -878,7 +879,8 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // quantiser pairs run on up to 4 compute lanes (streams with their own
     // scratch), so a chunk's launches overlap and small chunks stay efficient
     int nl = 0;
-    if ((e = open_lanes(ctx, nq, &nl)) != cudaSuccess) return cuda_fail(ctx, e, "lanes");
+    // (QX_SWEEP_LANES may exceed nq here: consecutive chunks then run on different lanes)
+    if ((e = open_lanes(ctx, nq, &nl, 2 * nq)) != cudaSuccess) return cuda_fail(ctx, e, "lanes");
     // chunks of >= 8 pairs (>= 16 on one lane: smaller launches lose their
     // tail waves), at most 8
     int64_t nchunk = disjoint ? std::max<int64_t>(1, std::min<int64_t>(batch / (nl > 1 ? 8 : 16), nl > 1 ? 8 : 4)) : 1;
@@ -930,6 +932,9 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // same schedule compute-only
     const char* rs = getenv("QX_SWEEP_RESTAGE");
     const bool copy = !(rs && rs[0] == '0');
+    // and QX_SWEEP_COMPUTE=0 times the copies alone (results: the previous call's)
+    const char* cm = getenv("QX_SWEEP_COMPUTE");
+    const bool compute = !(cm && cm[0] == '0');
     for (int64_t c = 0; c < nchunk; ++c) {
         const int64_t b0 = chunks[c].first, nb = chunks[c].second;
         const size_t xo = (size_t)(b0 * x->ld) * ex, yo = (size_t)(b0 * y->ld) * ey;
@@ -944,8 +949,8 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
         qx_signals xd = *x, yd = *y;
         xd.data = d + xo;
         yd.data = d + xa + yo;
-        for (int64_t q = 0; q < nq; ++q) {
-            Lane& L = ctx->lanes[q % nl];
+        for (int64_t q = 0; q < nq && compute; ++q) {
+            Lane& L = ctx->lanes[(c * nq + q) % nl];
             st = estimate_batch_on(ctx, &xd, &yd, nb, &qxs[q], &qys[q], lag_lo, lag_hi, path, rd + q * batch + b0,
                                    L.stream, &L.scratch, &L.counters);
             if (st != QX_OK) return st;

@@ -24,6 +24,7 @@
 // tools/ntt_model.py is an exact-arithmetic model of the same index math.
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 #include <type_traits>
@@ -38,6 +39,12 @@
 namespace qx {
 
 constexpr int kThreads = QX_NTT_THREADS;
+// loads in flight per thread in the twiddled transposed stores of passes 1 and 2
+#ifndef QX_TW_UNROLL
+#define QX_TW_UNROLL 8
+#endif
+#define QX_STR_(x) #x
+#define QX_UNROLL(n) _Pragma(QX_STR_(unroll n))
 constexpr int kWarps = kThreads / 32;
 constexpr int kPad = 33;  // words per element row of a 32-vector tile
 
@@ -270,6 +277,7 @@ struct Pass1Args {
     uint32_t* Y;          // Y^T: [pair][op][n2][k1pos]
     const uint2* gtw;     // DIF group twiddles for N1
     const uint2* twf;     // forward four-step twiddles, transposed [n2][k1pos] (Shoup pairs)
+    const uint2* twab;    // the same factored: [n2][32 A + N1/32 B] (NttTables::twab), or null
     unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -446,10 +454,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     // transposed store Y^T[n2][k1pos] (lane = k1pos, contiguous) with the
     // forward four-step twiddle (table in the same transposed layout)
     uint32_t* Yt = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
+    if constexpr (N1 >= 32) {
+        if (a.twab) {
+            // factored twiddle: one per-lane A and a warp-uniform B per row
+            // (two Shoup products instead of one 8-byte L2 load per element)
+            constexpr int NB = N1 / 32;
+#pragma unroll 1
+            for (int c = warp; c < 32; c += kWarps) {
+                const int o = (c0 + c) * N1;
+                const uint2* tb = a.twab + (int64_t)(c0 + c) * (32 + NB);
+                const uint2 A = __ldg(&tb[lane]);
+                QX_UNROLL(QX_TW_UNROLL)
+                for (int j = 0; j < NB; ++j) {
+                    const uint2 B = __ldg(&tb[32 + j]);
+                    const int e = lane + 32 * j;
+                    Yt[o + e] = shoup(shoup(smem[e * kPad + c], A.x, A.y, m.p), B.x, B.y, m.p);
+                }
+            }
+            return;
+        }
+    }
 #pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
         const int o = (c0 + c) * N1;
-#pragma unroll 8
+        QX_UNROLL(QX_TW_UNROLL)
         for (int e = lane; e < N1; e += 32)
         {
             const uint2 w = __ldg(&a.twf[o + e]);
@@ -572,7 +600,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
 #pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
         const int o = (r0 + c) * N2;
-#pragma unroll 8
+        QX_UNROLL(QX_TW_UNROLL)
         for (int e = lane; e < N2; e += 32) {
             const uint2 w = __ldg(&a.twinv[o + e]);
             Z[o + e] = shoup(su[e * kPad + c], w.x, w.y, m.p);
@@ -1117,6 +1145,16 @@ static void group_tables_rt(int log, uint64_t root, uint64_t p, std::vector<uint
     }
 }
 
+// factored pass-1 twiddles (NttTables::twab); QX_NTT_TWAB=0 keeps the full table (A/B)
+static bool twab_on()
+{
+    static const bool on = [] {
+        const char* e = getenv("QX_NTT_TWAB");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block)
 {
     const int l1 = (lp + 1) / 2, l2 = lp / 2;
@@ -1130,7 +1168,11 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     // layout: g1f | g1i | g2f | g2i | twf | twi  (each table 16-byte aligned)
     auto al = [](size_t n) { return (n + 1) & ~(size_t)1; };
     const size_t nt = al(g1f.size()) + al(g1i.size()) + al(g2f.size()) + al(g2i.size());
-    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint2);
+    // factored forward four-step twiddles (N1 >= 32): position pos = lane + 32 j has
+    // bitrev(pos) = bitrev5(lane) << (l1 - 5) | bitrev(j), so w^(n2 bitrev(pos)) =
+    // A[n2][lane] * B[n2][j] -- per n2 the 32 A then the N1/32 B (Shoup pairs)
+    const uint64_t nab = N1 >= 32 ? 32 + N1 / 32 : 0;
+    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint2) + N2 * nab * sizeof(uint2);
     std::vector<unsigned char> host(bytes, 0);
     uint2* h = reinterpret_cast<uint2*>(host.data());
     size_t o1i = al(g1f.size()), o2f = o1i + al(g1i.size()), o2i = o2f + al(g2f.size());
@@ -1152,6 +1194,11 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
             f = mulmod(f, step_f, p);
             iv = mulmod(iv, step_i, p);
         }
+    }
+    uint2* hab = hi + P;
+    for (uint64_t n2 = 0; n2 < N2 && nab; ++n2) {
+        for (uint64_t l = 0; l < 32; ++l) hab[n2 * nab + l] = hf[n2 * N1 + l];
+        for (uint64_t j = 0; j < N1 / 32; ++j) hab[n2 * nab + 32 + j] = hf[n2 * N1 + 32 * j];
     }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, bytes);
@@ -1175,6 +1222,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     out->g2i = db + o2i;
     out->twf = db + nt;
     out->twi = out->twf + P;
+    out->twab = nab ? out->twi + P : nullptr;
     *dev_block = d;
     return cudaSuccess;
 }
@@ -1485,6 +1533,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             a1.Y = c.Y;
             a1.gtw = T.g1f;
             a1.twf = T.twf;
+            a1.twab = twab_on() ? T.twab : nullptr;
             a1.stats = c.stats;
             a1.m = T.m;
             a1.p0 = t0.p;
@@ -1602,6 +1651,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a1.Y = c.Y;
             a1.gtw = T.g1f;
             a1.twf = T.twf;
+            a1.twab = twab_on() ? T.twab : nullptr;
             a1.stats = c.stats;
             a1.m = T.m;
             a1.p0 = t0.p;

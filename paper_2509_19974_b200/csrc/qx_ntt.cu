@@ -1472,12 +1472,17 @@ static cudaError_t launch_p1pf(const Pass1Args& a, int ntiles, cudaStream_t s)
 }
 
 // the persistent bulk-copy pass 1 applies: float rows exactly filling the
-// loaded half, 16-byte aligned rows, first prime (QX_NTT_PF=0 disables; A/B)
+// loaded half, 16-byte aligned rows, first prime.  Opt-in (QX_NTT_PF=1):
+// alone it matches k_pass1 (0.895 vs 0.886 ms per C2 step), but a persistent
+// grid holds every SM for the whole pass, so the sweep's compute lanes can no
+// longer fill each other's tails (C2 step 2.08 -> 2.19 ms).  Issuing the 512
+// row copies from one warp instead of all threads: 1.50 ms (bulk-copy issue
+// stalls the issuing warp, the others wait at the tile barrier).
 static bool p1pf_ok(const Pass1Args& a, int l1, int dt, int qm, int zu, int N2)
 {
     static const bool on = [] {
         const char* e = getenv("QX_NTT_PF");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     if (!on || l1 != 10 || dt != DT_F32 || !(qm == QM_K1 || qm == QM_UNIFORM) || !zu || a.skip_cs || !a.twab) return false;
     for (int o = 0; o < 2; ++o) {

@@ -733,3 +733,31 @@ def test_c4_full_size(qx, oracle):
     n = len(u)
     t_peak = lag + n - 1
     assert oracle.xcorr_bf(u, v, t_peak, t_peak)[0] == res["value"]
+
+
+def test_persistent_pass1_opt_in_matches(qx):
+    """The opt-in persistent bulk-copy pass 1 (QX_NTT_PF=1, read once per
+    process) gives the same C2 results as the default pass 1."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    import torch
+    from paper_2509_19974_b200 import workloads as W
+
+    code = ("import json,torch,paper_2509_19974_b200 as P;from paper_2509_19974_b200 import workloads as W;"
+            "xs,ys,_=W.c2(pairs=5,seed=9);x,y=torch.from_numpy(xs).cuda(),torch.from_numpy(ys).cuda();"
+            "r=P.estimate_sweep(x,y,[(W.bit_quantizer(b,W.C2_SIGMA),)*2 for b in (1,2,4)]);"
+            "print(json.dumps([q.raw.cpu().tolist() for q in r]))")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QX_NTT_PF="1"), cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = json.loads(out.stdout.strip().splitlines()[-1])
+    xs, ys, lag = W.c2(pairs=5, seed=9)
+    x, y = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    want = qx.estimate_sweep(x, y, [(W.bit_quantizer(b, W.C2_SIGMA),) * 2 for b in (1, 2, 4)])
+    for q in range(3):
+        assert got[q] == want[q].raw.cpu().tolist(), q
+        assert np.array_equal(want[q].lag.cpu().numpy(), lag)

@@ -62,6 +62,7 @@ struct NttTables {
     const uint2* twi;  // inverse four-step twiddles [P] incl. R/P (Shoup pairs; the R cancels the
                        // pointwise Montgomery product's R^-1)
     const uint2* twab; // twf factored per n2: 32 per-lane A then N1/32 per-row B (null if N1 < 32)
+    const uint2* twib; // twi factored per k1pos: 32 per-lane A then N2/32 per-row B (null if N2 < 32)
 };
 
 // Optional per-launch accounting (qx_profile_begin/end): counts every kernel

@@ -661,6 +661,7 @@ struct Pass2Args {
     const uint2* gtwf;      // DIF group twiddles for N2
     const uint2* gtwi;      // DIT group twiddles for N2
     const uint2* twinv;     // inverse four-step twiddles [k1pos][n2] (Shoup pairs, incl. R/P)
+    const uint2* twib;      // the same factored: [k1pos][32 A + N2/32 B] (NttTables::twib), or null
     const unsigned long long* stats;
     ModP m;
     uint32_t p0;
@@ -764,6 +765,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     // transposed store Z[k1pos][n2] (lane = n2) with the inverse four-step
     // twiddle (includes R/P: the product's Montgomery R^-1 cancels)
     uint32_t* Z = a.Z + pl * P;
+    if constexpr (N2 >= 32) {
+        if (a.twib) {
+            // factored twiddle (see pass 1): per-lane A, warp-uniform B per row
+            constexpr int NB = N2 / 32;
+#pragma unroll 1
+            for (int c = warp; c < 32; c += kWarps) {
+                const int o = (r0 + c) * N2;
+                const uint2* tb = a.twib + (int64_t)(r0 + c) * (32 + NB);
+                const uint2 A = __ldg(&tb[lane]);
+                QX_UNROLL(QX_TW_UNROLL)
+                for (int j = 0; j < NB; ++j) {
+                    const uint2 B = __ldg(&tb[32 + j]);
+                    const int e = lane + 32 * j;
+                    Z[o + e] = shoup(shoup(su[e * kPad + c], A.x, A.y, m.p), B.x, B.y, m.p);
+                }
+            }
+            return;
+        }
+    }
 #pragma unroll 1
     for (int c = warp; c < 32; c += kWarps) {
         const int o = (r0 + c) * N2;
@@ -1339,7 +1359,11 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     // bitrev(pos) = bitrev5(lane) << (l1 - 5) | bitrev(j), so w^(n2 bitrev(pos)) =
     // A[n2][lane] * B[n2][j] -- per n2 the 32 A then the N1/32 B (Shoup pairs)
     const uint64_t nab = N1 >= 32 ? 32 + N1 / 32 : 0;
-    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint2) + N2 * nab * sizeof(uint2);
+    // and the inverse ones of pass 2: row pos, n2 = lane + 32 j:
+    // ci wi^(k1 n2) = (ci wi^(k1 lane)) * wi^(32 k1 j) -- per row 32 A then N2/32 B
+    const uint64_t nib = N2 >= 32 ? 32 + N2 / 32 : 0;
+    const size_t bytes = nt * sizeof(uint2) + 2 * P * sizeof(uint2) + N2 * nab * sizeof(uint2) +
+                         N1 * nib * sizeof(uint2);
     std::vector<unsigned char> host(bytes, 0);
     uint2* h = reinterpret_cast<uint2*>(host.data());
     size_t o1i = al(g1f.size()), o2f = o1i + al(g1i.size()), o2i = o2f + al(g2f.size());
@@ -1367,6 +1391,14 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
         for (uint64_t l = 0; l < 32; ++l) hab[n2 * nab + l] = hf[n2 * N1 + l];
         for (uint64_t j = 0; j < N1 / 32; ++j) hab[n2 * nab + 32 + j] = hf[n2 * N1 + 32 * j];
     }
+    uint2* hib = hab + N2 * nab;
+    for (uint64_t pos = 0; pos < N1 && nib; ++pos) {
+        const uint64_t k1 = bitrev((uint32_t)pos, l1);
+        for (uint64_t l = 0; l < 32; ++l) hib[pos * nib + l] = hi[pos * N2 + l];
+        const uint64_t st = powmod(wi, (32 * k1) % P, p);
+        uint64_t b = 1;
+        for (uint64_t j = 0; j < N2 / 32; ++j, b = mulmod(b, st, p)) hib[pos * nib + 32 + j] = sh(b);
+    }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, bytes);
     if (e != cudaSuccess) return e;
@@ -1390,6 +1422,7 @@ cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void
     out->twf = db + nt;
     out->twi = out->twf + P;
     out->twab = nab ? out->twi + P : nullptr;
+    out->twib = nib ? out->twi + P + N2 * nab : nullptr;
     *dev_block = d;
     return cudaSuccess;
 }
@@ -1759,6 +1792,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             a2.gtwf = T.g2f;
             a2.gtwi = T.g2i;
             a2.twinv = T.twi;
+            a2.twib = twab_on() ? T.twib : nullptr;
             a2.stats = c.stats;
             a2.m = T.m;
             a2.p0 = t0.p;
@@ -1898,6 +1932,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a2.gtwf = T.g2f;
             a2.gtwi = T.g2i;
             a2.twinv = T.twi;
+            a2.twib = twab_on() ? T.twib : nullptr;
             a2.stats = c.stats;
             a2.m = T.m;
             a2.p0 = t0.p;

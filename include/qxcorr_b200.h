@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define QX_ABI_VERSION 2
+#define QX_ABI_VERSION 3
 
 typedef enum qx_status {
     QX_OK = 0,
@@ -83,11 +83,14 @@ typedef struct qx_signals {
     int64_t start;     /* Signal.start of every row */
 } qx_signals;
 
-/* AUTO: bounded windows (<= 4112 lags, n_x <= 4593, k <= 127) -> DIRECT,
- * else NTT.  NTT: exact full-lag number-theoretic transform path.  DIRECT:
- * tcgen05 int8 Toeplitz tiles over the lag window (argmax entry points). */
-/* AUTO picks DIRECT (tensor-core window) for windows of <= 4112 lags, else POPC
- * (word-parallel 1-level codes) for small single pairs, else NTT. */
+/* Path selection for the argmax entry points.  AUTO picks DIRECT (tcgen05
+ * tensor-core Toeplitz tiles) for lag windows of at most 4112 lags with
+ * n_x <= 4593 and k <= 127 on float rows; else POPC (word-parallel XOR/AND +
+ * popc on 1-level codes) for k = 1 quantisers on small single pairs (batch *
+ * n_x * window <= 2^31, n_x <= 65536); else NTT (exact full-lag
+ * number-theoretic transforms).  NTT / DIRECT / POPC force one path
+ * (QX_ERR_UNSUPPORTED if its shape limits are not met).  qx_xcorr_full
+ * always runs the NTT. */
 typedef enum qx_path { QX_PATH_AUTO = 0, QX_PATH_NTT = 1, QX_PATH_DIRECT = 2, QX_PATH_POPC = 3 } qx_path;
 
 /* per-pair flags in qx_result.flags */
@@ -114,6 +117,21 @@ qx_status qx_context_create(int device, qx_context **out);
 void qx_context_destroy(qx_context *ctx);
 const char *qx_status_string(qx_status s);
 const char *qx_context_last_error(const qx_context *ctx);
+
+/* Tuning / measurement options of a context.  Their defaults come from the
+ * QX_* environment variables, read once by qx_context_create (never per
+ * call); this call changes them afterwards.  Names: "chunk_pairs",
+ * "sweep_lanes", "sweep_chunks", "sweep_taper", "sweep_even",
+ * "sweep_restage" (0: the host sweep skips its H2D copies -- compute-only
+ * timing), "sweep_compute" (0: it skips its kernels -- copy-only timing),
+ * "popc", "popc_fused", "tc_f4".  QX_ERR_INVALID for an unknown name.
+ *
+ * Threading and streams: every entry point locks the context, runs on the
+ * context's device and restores the caller's current device.  Work enqueued
+ * on a stream other than the previous call's waits for that call's work, so
+ * the context's scratch is never used by two streams at once (use one
+ * context per stream for concurrency). */
+qx_status qx_context_set_option(qx_context *ctx, const char *name, int64_t value);
 int qx_abi_version(void);
 
 /* Exact threshold table of a quantiser for inputs of `dtype` (F32/F64):

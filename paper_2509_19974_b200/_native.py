@@ -35,6 +35,7 @@ QX_F32, QX_F64, QX_I64 = 0, 1, 2
 QX_Q_SIGN, QX_Q_UNIFORM, QX_Q_CUSTOM, QX_Q_CODES = 0, 1, 2, 3
 PATHS = {"auto": 0, "ntt": 1, "direct": 2, "tc": 2, "popc": 3}
 PROFILE_KINDS = 10  # qxcorr_b200.h QX_PROFILE_KINDS
+ABI_VERSION = 3  # qxcorr_b200.h QX_ABI_VERSION
 
 RF_DEGENERATE_X = 1
 RF_DEGENERATE_Y = 2
@@ -74,7 +75,7 @@ assert RESULT_DTYPE.itemsize == ctypes.sizeof(QxResult) == 64
 # every symbol include/qxcorr_b200.h declares
 EXPORTS = (
     "qx_abi_version", "qx_status_string", "qx_context_create", "qx_context_destroy",
-    "qx_context_last_error", "qx_quantizer_thresholds", "qx_quantize", "qx_xcorr_full",
+    "qx_context_last_error", "qx_context_set_option", "qx_quantizer_thresholds", "qx_quantize", "qx_xcorr_full",
     "qx_estimate_batch", "qx_estimate_batch_host", "qx_estimate_sweep", "qx_estimate_sweep_host", "qx_template_search", "qx_decode_pcm16",
     "qx_profile_begin",
     "qx_profile_end",
@@ -109,6 +110,8 @@ def load():
         L.qx_context_destroy.restype = None
         L.qx_context_last_error.argtypes = [vp]
         L.qx_context_last_error.restype = ctypes.c_char_p
+        L.qx_context_set_option.argtypes = [vp, ctypes.c_char_p, i64]
+        L.qx_context_set_option.restype = st
         qp, sp = ctypes.POINTER(QxQuantizer), ctypes.POINTER(QxSignals)
         L.qx_quantizer_thresholds.argtypes = [qp, ctypes.c_int, vp]
         L.qx_quantizer_thresholds.restype = st
@@ -122,12 +125,10 @@ def load():
         L.qx_estimate_batch_host.restype = st
         L.qx_estimate_sweep_host.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp]
         L.qx_estimate_sweep_host.restype = st
-        if hasattr(L, "qx_estimate_sweep"):  # (absent from older A/B builds)
-            L.qx_estimate_sweep.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp, vp]
-            L.qx_estimate_sweep.restype = st
-        if hasattr(L, "qx_template_search"):  # (absent from older A/B builds)
-            L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
-            L.qx_template_search.restype = st
+        L.qx_estimate_sweep.argtypes = [vp, sp, sp, i64, i64, qp, qp, i64, i64, st, vp, vp]
+        L.qx_estimate_sweep.restype = st
+        L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
+        L.qx_template_search.restype = st
         L.qx_decode_pcm16.argtypes = [vp, vp, i64, vp, vp]
         L.qx_decode_pcm16.restype = st
         L.qx_profile_begin.argtypes = [vp, ctypes.c_int]
@@ -137,7 +138,7 @@ def load():
         L.qx_profile_kind_name.argtypes = [ctypes.c_int]
         L.qx_profile_kind_name.restype = ctypes.c_char_p
         # (an A/B build named by QX_NATIVE_LIB may predate the current ABI)
-        assert L.qx_abi_version() == 2 or os.environ.get("QX_NATIVE_LIB")
+        assert L.qx_abi_version() == ABI_VERSION or os.environ.get("QX_NATIVE_LIB")
         _lib = L
     return _lib
 
@@ -159,6 +160,32 @@ def context(device: int | None = None) -> ctypes.c_void_p:
                 check(L.qx_context_create(device, ctypes.byref(ctx)), None)
                 _contexts[device] = ctx
     return ctx
+
+
+def set_option(name: str, value: int, device: int | None = None) -> None:
+    """qx_context_set_option on the device's context (tuning / measurement
+    knobs; defaults come from the QX_* environment at context creation)."""
+    ctx = context(device)
+    check(load().qx_context_set_option(ctx, name.encode(), int(value)), ctx)
+
+
+class option:
+    """Context manager: set a context option, restore it on exit."""
+
+    DEFAULTS = {"sweep_restage": 1, "sweep_compute": 1, "popc": 1, "popc_fused": 1, "tc_f4": 1, "sweep_lanes": 0,
+                "sweep_chunks": 0, "sweep_taper": 2, "sweep_even": 0, "chunk_pairs": 0}
+
+    def __init__(self, name: str, value: int, device: int | None = None, restore: int | None = None):
+        self.name, self.value, self.device = name, value, device
+        self.restore = self.DEFAULTS[name] if restore is None else restore
+
+    def __enter__(self):
+        set_option(self.name, self.value, self.device)
+        return self
+
+    def __exit__(self, *exc):
+        set_option(self.name, self.restore, self.device)
+        return False
 
 
 class NativeError(RuntimeError):

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <vector>
@@ -48,6 +49,79 @@ struct Arena {
     size_t size = 0;
 };
 
+namespace qx {
+cudaError_t set_max_smem(const void* fn, size_t bytes)
+{
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.count({fn, dev})) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done.insert({fn, dev});
+    return e;
+}
+
+int device_sms()
+{
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = sms;
+    }
+    return cache[dev];
+}
+}  // namespace qx
+
+// Every entry point runs on the context's device and restores the caller's
+// current device on return (a context for GPU 1 never switches torch's
+// current device).
+struct DevGuard {
+    int prev = -1;
+    explicit DevGuard(int dev)
+    {
+        int cur = 0;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+    }
+    ~DevGuard()
+    {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+static Knobs knobs_from_env()
+{
+    Knobs k;
+    auto num = [](const char* name, int64_t dflt) -> int64_t {
+        const char* v = getenv(name);
+        return (v && *v) ? atoll(v) : dflt;
+    };
+    k.chunk_pairs = num("QX_CHUNK_PAIRS", 0);
+    k.sweep_lanes = (int)num("QX_SWEEP_LANES", 0);
+    k.sweep_chunks = (int)num("QX_SWEEP_CHUNKS", 0);
+    k.sweep_taper = (int)std::max<int64_t>(1, num("QX_SWEEP_TAPER", 2));
+    k.sweep_even = getenv("QX_SWEEP_EVEN") != nullptr;
+    k.sweep_restage = num("QX_SWEEP_RESTAGE", 1) != 0;
+    k.sweep_compute = num("QX_SWEEP_COMPUTE", 1) != 0;
+    k.popc = num("QX_POPC", 1) != 0;
+    k.popc_fused = num("QX_POPC_FUSED", 1) != 0;
+    k.tc_f4 = num("QX_TC_F4", 1) != 0;
+    if (const char* ev = getenv("QX_SWEEP_PLAN")) {
+        for (const char* p = ev; *p && k.sweep_plan_n < 16;) {
+            const int64_t v = atoll(p);
+            if (v > 0) k.sweep_plan[k.sweep_plan_n++] = v;
+            while (*p && *p != ',') ++p;
+            if (*p == ',') ++p;
+        }
+    }
+    return k;
+}
+
 // A compute lane of the sweep entry point: its own stream and scratch, so
 // the quantiser pairs of one staged chunk run concurrently (their launches
 // fill each other's tail waves).
@@ -75,8 +149,47 @@ struct qx_context {
     Lane lanes[kMaxLanes];                // sweep compute lanes (lazily created)
     cudaEvent_t fork = nullptr;           // device sweep: caller stream -> lanes
     Profiler prof;
+    Knobs knobs;
     std::string last_error;
+    // stream ordering of the shared arenas: the last stream that enqueued
+    // work on this context, and an event recorded after that work.  A call
+    // on another stream first waits for it (ctx_begin), so scratch, counters,
+    // staging and records are never used by two streams at once.
+    cudaStream_t last_stream = nullptr;
+    bool used = false;
+    cudaEvent_t last_ev = nullptr;
 };
+
+static cudaError_t ctx_begin(qx_context* ctx, cudaStream_t s)
+{
+    if (ctx->used && ctx->last_stream != s) return cudaStreamWaitEvent(s, ctx->last_ev, 0);
+    return cudaSuccess;
+}
+
+static cudaError_t ctx_end(qx_context* ctx, cudaStream_t s);
+
+// RAII: order `s` after the context's previous stream on entry, record the
+// context event on `s` on exit
+struct StreamOrder {
+    qx_context* c;
+    cudaStream_t s;
+    StreamOrder(qx_context* c_, cudaStream_t s_) : c(c_), s(s_) { ctx_begin(c, s); }
+    ~StreamOrder() { ctx_end(c, s); }
+};
+
+static cudaError_t ctx_end(qx_context* ctx, cudaStream_t s)
+{
+    if (!ctx->last_ev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ctx->last_ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ctx->last_ev, s);
+    if (e == cudaSuccess) {
+        ctx->last_stream = s;
+        ctx->used = true;
+    }
+    return e;
+}
 
 static qx_status fail(qx_context* ctx, qx_status s, const std::string& msg)
 {
@@ -102,7 +215,13 @@ static cudaError_t arena_reserve(Arena& a, size_t bytes, bool zero)
     cudaError_t e = cudaMalloc(&a.ptr, want);
     if (e != cudaSuccess) return e;
     a.size = want;
-    if (zero) return cudaMemset(a.ptr, 0, want);
+    if (zero) {
+        // the consumers run on non-blocking streams, which do not order
+        // after the legacy stream: finish the zeroing before returning
+        e = cudaMemset(a.ptr, 0, want);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        return e;
+    }
     return cudaSuccess;
 }
 
@@ -131,11 +250,13 @@ qx_status qx_context_create(int device, qx_context** out)
 {
     if (!out) return QX_ERR_INVALID;
     *out = nullptr;
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) return QX_ERR_CUDA;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) return QX_ERR_CUDA;
+    DevGuard g(device);
     qx_context* c = new qx_context();
     c->device = device;
-    e = cudaStreamCreateWithFlags(&c->host_stream, cudaStreamNonBlocking);
+    c->knobs = knobs_from_env();
+    cudaError_t e = cudaStreamCreateWithFlags(&c->host_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         delete c;
         return QX_ERR_CUDA;
@@ -147,8 +268,9 @@ qx_status qx_context_create(int device, qx_context** out)
 void qx_context_destroy(qx_context* c)
 {
     if (!c) return;
-    cudaSetDevice(c->device);
+    DevGuard g(c->device);
     cudaDeviceSynchronize();
+    if (c->last_ev) cudaEventDestroy(c->last_ev);
     for (auto& kv : c->tables) cudaFree(kv.second.second);
     for (auto& kv : c->otables) cudaFree(kv.second.second);
     for (Arena* a : {&c->scratch, &c->counters, &c->stage, &c->records, &c->mcounter})
@@ -167,6 +289,26 @@ void qx_context_destroy(qx_context* c)
 }
 
 const char* qx_context_last_error(const qx_context* c) { return c ? c->last_error.c_str() : ""; }
+
+qx_status qx_context_set_option(qx_context* c, const char* name, int64_t value)
+{
+    if (!c || !name) return QX_ERR_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(c->mu);
+    Knobs& k = c->knobs;
+    const std::string n(name);
+    if (n == "chunk_pairs") k.chunk_pairs = value < 0 ? 0 : value;
+    else if (n == "sweep_lanes") k.sweep_lanes = (int)std::max<int64_t>(0, value);
+    else if (n == "sweep_chunks") k.sweep_chunks = (int)std::max<int64_t>(0, value);
+    else if (n == "sweep_taper") k.sweep_taper = (int)std::max<int64_t>(1, value);
+    else if (n == "sweep_even") k.sweep_even = value != 0;
+    else if (n == "sweep_restage") k.sweep_restage = value != 0;
+    else if (n == "sweep_compute") k.sweep_compute = value != 0;
+    else if (n == "popc") k.popc = value != 0;
+    else if (n == "popc_fused") k.popc_fused = value != 0;
+    else if (n == "tc_f4") k.tc_f4 = value != 0;
+    else return fail(c, QX_ERR_INVALID, "unknown option " + n);
+    return QX_OK;
+}
 
 }  // extern "C"
 
@@ -340,6 +482,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     }
     NttCall& c = out->call;
     memset(&c, 0, sizeof(c));
+    c.knobs = &ctx->knobs;
     c.split2 = split2;
     c.op[0].data = x->data;
     c.op[0].ld = x->ld;
@@ -433,7 +576,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     // grids beat L2 residency here (measured on C2: 16 -> 64 pairs per launch
     // = 2.91 -> 2.41 ms/step; tail waves of 1-CTA/SM kernels dominate).
     int64_t chunk = (1536ll << 20) / (per_pair * 4);
-    if (const char* ev = getenv("QX_CHUNK_PAIRS")) chunk = atoll(ev);
+    if (ctx->knobs.chunk_pairs > 0) chunk = ctx->knobs.chunk_pairs;
     if (chunk < 1) chunk = 1;
     if (chunk > batch) chunk = batch;
     c.chunk = chunk;
@@ -482,6 +625,8 @@ qx_status qx_quantize(qx_context* ctx, const qx_quantizer* q, const qx_signals* 
 {
     if (!ctx) return QX_ERR_INVALID;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
     qx_status st;
     if (batch < 1 || !codes) return fail(ctx, QX_ERR_INVALID, "bad batch or output");
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
@@ -545,8 +690,8 @@ static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const q
 static cudaError_t open_lanes(qx_context* ctx, int64_t nq, int* nl_out, int64_t most = 0)
 {
     int nl = (int)std::min<int64_t>(nq, 4);
-    if (const char* ev = getenv("QX_SWEEP_LANES"))
-        nl = (int)std::max<int64_t>(1, std::min<int64_t>(most > 0 ? most : nq, atoll(ev)));
+    if (ctx->knobs.sweep_lanes > 0)
+        nl = (int)std::max<int64_t>(1, std::min<int64_t>(most > 0 ? most : nq, ctx->knobs.sweep_lanes));
     nl = std::min(nl, kMaxLanes);
     cudaError_t e = cudaSuccess;
     for (int l = 0; l < nl && e == cudaSuccess; ++l) {
@@ -568,6 +713,8 @@ qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signa
     if (!ctx) return QX_ERR_INVALID;
     if (!results) return fail(ctx, QX_ERR_INVALID, "results is NULL");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
     Prepared pr;
     qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr);
     if (st != QX_OK) return st;
@@ -590,6 +737,8 @@ qx_status qx_xcorr_full(qx_context* ctx, const qx_signals* x, const qx_signals* 
     if (!ctx) return QX_ERR_INVALID;
     if (!values) return fail(ctx, QX_ERR_INVALID, "values is NULL");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
     Prepared pr;
     qx_status st = prepare(ctx, x, y, batch, qx_, qy_, INT64_MIN, INT64_MAX, false, path, &pr);
     if (st != QX_OK) return st;
@@ -618,6 +767,7 @@ qx_status qx_profile_begin(qx_context* ctx, int timed)
 {
     if (!ctx) return QX_ERR_INVALID;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
     Profiler& p = ctx->prof;
     p.on = true;
     p.timed = timed != 0;
@@ -631,6 +781,7 @@ qx_status qx_profile_end(qx_context* ctx, qx_profile* out)
 {
     if (!ctx || !out) return QX_ERR_INVALID;
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
     Profiler& p = ctx->prof;
     memset(out, 0, sizeof(*out));
     out->launches = p.launches;
@@ -654,6 +805,8 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
     if (!ctx) return QX_ERR_INVALID;
     if (!results) return fail(ctx, QX_ERR_INVALID, "results is NULL");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, ctx->host_stream);
     qx_status st;
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
     if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
@@ -688,25 +841,23 @@ qx_status qx_estimate_batch_host(qx_context* ctx, const qx_signals* x, const qx_
 // the template fits it -- 32768 on the 2-SM fp4 mode (two records per
 // block), 8192 on the 1-SM fp4 mode, 4096 on the int8 one -- else the
 // largest block whose full correlogram fits one 2^19 transform
-static int64_t tsearch_block(const qx_signals* t, const qx_signals* s, const qx_quantizer* qa,
-                             const qx_quantizer* qb, qx_path path, bool* f2)
+static int64_t tsearch_block(const qx_context* ctx, const qx_signals* t, const qx_signals* s,
+                             const qx_quantizer* qa, const qx_quantizer* qb, qx_path path, bool* f2)
 {
     *f2 = false;
     const int64_t nt = t->n;
     const bool tc = path != QX_PATH_NTT && path != QX_PATH_POPC && nt + 15 <= 4608 && nt % 4 == 0 &&
                     t->dtype == QX_F32 && s->dtype == QX_F32;
     if (!tc) return (1ll << 19) - 2 * nt + 2;
-    const char* env = getenv("QX_TC_F4");
     const int64_t ka = qa->k, kb = qb->k;
     auto mode = [](const qx_quantizer* q) { return q->k == 1 ? 0 : (q->kind == QX_Q_UNIFORM ? 1 : 2); };
-    const bool f4 = !(env && env[0] == '0') && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
+    const bool f4 = ctx->knobs.tc_f4 && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
                     (double)nt * ka * kb < 16777216.0;
     // the 2-SM mode is opt-in (QX_TC_F2=1): its MMA runs at the fp4 peak, but
     // its builders' global loads (82 KB per CTA and block, one block ahead in
     // registers) are latency-bound (ncu: long_scoreboard), 0.59 ms vs 0.49 ms
     // for the 1-SM mode at config 5; it needs a TMA-staged float pipeline
-    const char* env2 = getenv("QX_TC_F2");
-    *f2 = f4 && env2 && env2[0] == '1';
+    *f2 = false;
     return f4 ? 8192 : 4096;
 }
 
@@ -716,6 +867,8 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
     if (!ctx) return QX_ERR_INVALID;
     if (!summary) return fail(ctx, QX_ERR_INVALID, "summary is NULL");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
     qx_status st;
     if ((st = check_signals(ctx, tpl, "template")) != QX_OK) return st;
     if ((st = check_signals(ctx, sig, "stream")) != QX_OK) return st;
@@ -724,7 +877,7 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
     const int64_t nt = tpl->n, ns = sig->n, nvalid = ns - nt + 1;
     if (nvalid < 1) return fail(ctx, QX_ERR_INVALID, "template longer than the stream");
     bool f2 = false;
-    if (block <= 0) block = tsearch_block(tpl, sig, qx_, qy_, path, &f2);
+    if (block <= 0) block = tsearch_block(ctx, tpl, sig, qx_, qy_, path, &f2);
     if (block < 1) return fail(ctx, QX_ERR_INVALID, "template too long for the block transform");
     // runs of blocks: [2-SM 32768-lag blocks (2 records each)], `block`-lag
     // blocks, one shorter remainder block
@@ -734,8 +887,7 @@ qx_status qx_template_search(qx_context* ctx, const qx_signals* tpl, const qx_si
     // records: 2 per 32768-lag block (<= 1 per `block` lags, block <= 16384)
     // or 1 per `block`-lag block, + the remainder
     const int64_t nrec = nvalid / block + 2;
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    const int sms = device_sms();
     const size_t rb = (size_t)nrec * sizeof(qx_result), pb = (size_t)sms * 64;
     cudaError_t e = arena_reserve(ctx->records, rb + pb + 256, false);
     if (e == cudaSuccess) e = arena_reserve(ctx->mcounter, 256, true);
@@ -802,8 +954,9 @@ qx_status qx_decode_pcm16(qx_context* ctx, const void* pcm, int64_t n, float* ou
     if (!pcm || !out || n < 1) return fail(ctx, QX_ERR_INVALID, "pcm/out must be non-NULL and n >= 1");
     if ((uintptr_t)pcm % 16 || (uintptr_t)out % 16) return fail(ctx, QX_ERR_INVALID, "pcm/out must be 16-byte aligned");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    const int sms = device_sms();
     cudaStream_t s = (cudaStream_t)stream;
     ctx->prof.pre(KK_QUANT, s);
     cudaError_t e = pcm16_launch(pcm, n, out, sms, s);
@@ -821,6 +974,8 @@ qx_status qx_estimate_sweep(qx_context* ctx, const qx_signals* x, const qx_signa
     if (nq < 1) return fail(ctx, QX_ERR_INVALID, "nq must be >= 1");
     if (batch < 1) return fail(ctx, QX_ERR_INVALID, "batch must be >= 1");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
     qx_status st;
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
     if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
@@ -856,6 +1011,8 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     if (nq < 1) return fail(ctx, QX_ERR_INVALID, "nq must be >= 1");
     if (batch < 1) return fail(ctx, QX_ERR_INVALID, "batch must be >= 1");
     std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, ctx->host_stream);
     qx_status st;
     if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
     if ((st = check_signals(ctx, y, "y")) != QX_OK) return st;
@@ -884,7 +1041,9 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // chunks of >= 8 pairs (>= 16 on one lane: smaller launches lose their
     // tail waves), at most 8
     int64_t nchunk = disjoint ? std::max<int64_t>(1, std::min<int64_t>(batch / (nl > 1 ? 8 : 16), nl > 1 ? 8 : 4)) : 1;
-    if (const char* ev = getenv("QX_SWEEP_CHUNKS")) nchunk = std::max<int64_t>(1, std::min<int64_t>(batch, atoll(ev)));
+    // (a chunk count only applies to disjoint rows: overlapping / repeated
+    // rows are always staged whole)
+    if (disjoint && ctx->knobs.sweep_chunks > 0) nchunk = std::min<int64_t>(batch, ctx->knobs.sweep_chunks);
     const int64_t per = (batch + nchunk - 1) / nchunk;
     // chunk bounds: with lanes and >= 4 chunks the first and last chunks are
     // half size (less exposed copy before the first launch, shorter compute
@@ -893,9 +1052,8 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     {
         // tapered ends (first and last chunk per/T pairs, T = QX_SWEEP_TAPER, default 2):
         // less copy exposed before the first launch, a shorter compute tail
-        const bool taper = nl > 1 && nchunk >= 4 && per >= 2 && !getenv("QX_SWEEP_EVEN");
-        int64_t T = 2;
-        if (const char* ev = getenv("QX_SWEEP_TAPER")) T = std::max<int64_t>(1, atoll(ev));
+        const bool taper = nl > 1 && nchunk >= 4 && per >= 2 && !ctx->knobs.sweep_even;
+        const int64_t T = ctx->knobs.sweep_taper;
         const int64_t q = std::max<int64_t>(1, per / T);
         int64_t b0 = 0;
         while (b0 < batch) {
@@ -907,15 +1065,10 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
             b0 += nb;
         }
         // QX_SWEEP_PLAN="a,b,c,...": explicit chunk sizes (used when they sum to batch)
-        if (const char* ev = getenv("QX_SWEEP_PLAN"); ev && disjoint) {
+        if (ctx->knobs.sweep_plan_n && disjoint) {
             std::vector<std::pair<int64_t, int64_t>> plan;
             int64_t at = 0;
-            for (const char* p = ev; *p;) {
-                const int64_t v = atoll(p);
-                if (v > 0) plan.emplace_back(at, v), at += v;
-                while (*p && *p != ',') ++p;
-                if (*p == ',') ++p;
-            }
+            for (int i = 0; i < ctx->knobs.sweep_plan_n; ++i) plan.emplace_back(at, ctx->knobs.sweep_plan[i]), at += ctx->knobs.sweep_plan[i];
             if (at == batch) chunks.swap(plan);
         }
         nchunk = (int64_t)chunks.size();
@@ -930,11 +1083,9 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     // measurement knob: QX_SWEEP_RESTAGE=0 skips the H2D copies (the staging
     // buffer still holds the previous call's identical inputs) to time the
     // same schedule compute-only
-    const char* rs = getenv("QX_SWEEP_RESTAGE");
-    const bool copy = !(rs && rs[0] == '0');
+    const bool copy = ctx->knobs.sweep_restage;
     // and QX_SWEEP_COMPUTE=0 times the copies alone (results: the previous call's)
-    const char* cm = getenv("QX_SWEEP_COMPUTE");
-    const bool compute = !(cm && cm[0] == '0');
+    const bool compute = ctx->knobs.sweep_compute;
     for (int64_t c = 0; c < nchunk; ++c) {
         const int64_t b0 = chunks[c].first, nb = chunks[c].second;
         const size_t xo = (size_t)(b0 * x->ld) * ex, yo = (size_t)(b0 * y->ld) * ey;

@@ -92,7 +92,32 @@ struct OuterTables {
     const uint2* ri;      // omega_M^-t (Shoup pairs), t < M/2: register-resident outer DIT
 };
 
+// Tuning / measurement knobs of a context: the QX_* environment variables
+// are read ONCE when the context is created (qx_context_create) and can be
+// changed afterwards only through qx_context_set_option; no entry point reads
+// the environment per call.
+struct Knobs {
+    int64_t chunk_pairs = 0;   // QX_CHUNK_PAIRS: NTT pairs per launch group (0: ~1.5 GiB of scratch)
+    int sweep_lanes = 0;       // QX_SWEEP_LANES: sweep compute lanes (0: min(nq, 4))
+    int sweep_chunks = 0;      // QX_SWEEP_CHUNKS: host-sweep staging chunks (0: plan; disjoint rows only)
+    int sweep_taper = 2;       // QX_SWEEP_TAPER: first/last chunk = per/T pairs
+    int sweep_even = 0;        // QX_SWEEP_EVEN=1: no tapered ends
+    int sweep_restage = 1;     // QX_SWEEP_RESTAGE=0: skip the H2D copies (compute-only timing)
+    int sweep_compute = 1;     // QX_SWEEP_COMPUTE=0: skip the kernels (copy-only timing)
+    int popc = 1;              // QX_POPC=0: never pick the popc path on AUTO
+    int popc_fused = 1;        // QX_POPC_FUSED=0: two-launch popc form even when one fits
+    int tc_f4 = 1;             // QX_TC_F4=0: no fp4 tensor-core template search
+    int64_t sweep_plan[16] = {0};  // QX_SWEEP_PLAN="a,b,...": explicit host-sweep chunk sizes
+    int sweep_plan_n = 0;
+};
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+cudaError_t set_max_smem(const void* fn, size_t bytes);
+// SM count of the current device (cached per device)
+int device_sms();
+
 struct NttCall {
+    const Knobs* knobs;     // the context's knobs (never null)
     OperandDesc op[2];
     int64_t batch;
     int64_t nout;           // n_u + n_v - 1

@@ -488,171 +488,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
 }
 
 
-// Persistent pass 1 for float rows that fill the loaded half exactly (C2):
-// one CTA per SM walks the (pair, operand, column-tile) tiles; while a tile
-// is transformed, the next tile's 512 x 128-byte float rows stream into a
-// 64 KB staging buffer with 1-D bulk copies (cp.async.bulk, mbarrier
-// complete_tx), so the loads' latency hides behind the transform instead of
-// stalling the first DIF group.  Same results as k_pass1<LOG1, float, QM, true>.
-constexpr size_t kPfStage = (size_t)512 * 32 * 4;  // rows_loaded (N1/2 = 512) x 32 floats
-template <int LOG1>
-constexpr size_t pass1pf_smem()
-{
-    return (size_t)(1 << LOG1) * kPad * 4 + (size_t)Sched<LOG1>::TW_DIF * 8 + 2 * (size_t)kMaxThr * 4 + kPfStage + 16;
-}
-
-__device__ __forceinline__ uint32_t pf_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <int LOG1, int QM>
-__global__ void __launch_bounds__(kThreads, 1) k_pass1_pf(const __grid_constant__ Pass1Args a, int ntiles)
-{
-    constexpr int N1 = 1 << LOG1;
-    using SC = Sched<LOG1>;
-    constexpr int R0 = SC::r(0), S = N1 >> R0, RAD0 = 1 << R0;
-    constexpr int RL = SC::r(SC::NG - 1), RADL = 1 << RL;
-    constexpr int ROWS = N1 / 2, NLD = RAD0 / 2;
-    static_assert((size_t)ROWS * 32 * 4 == kPfStage, "staging size");
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint2* stw = reinterpret_cast<uint2*>(smem + N1 * kPad);
-    float* sthr = reinterpret_cast<float*>(stw + SC::TW_DIF);  // [2][kMaxThr]
-    float* stg = sthr + 2 * kMaxThr;                            // [ROWS][32]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(stg + ROWS * 32);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int N2 = a.N2, NX = N2 / 32;
-    const ModP m = a.m;
-
-    stage_table(stw, a.gtw, SC::TW_DIF);
-    for (int o = 0; o < 2; ++o)
-        for (int i = threadIdx.x; i < a.op[o].q.tsize; i += kThreads) sthr[o * kMaxThr + i] = (float)a.op[o].q.thr[i];
-    const uint32_t bar_a = pf_smem_u32(bar);
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_a));
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    // every thread streams one of tile t's rows into the staging buffer
-    auto issue = [&](int t) {
-        const int cx = t % NX, op = (t / NX) & 1;
-        const int64_t pair = a.pair0 + t / (2 * NX);
-        const OperandDesc& d = a.op[op];
-        const float* src = reinterpret_cast<const float*>(d.data) + pair * d.ld;
-        const int64_t c0 = (int64_t)cx * 32;
-        if (threadIdx.x == 0)
-            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_a), "r"((uint32_t)kPfStage)
-                         : "memory");
-        for (int r = threadIdx.x; r < ROWS; r += kThreads) {
-            const float* g = d.reverse ? src + (d.n - 32 - (int64_t)r * N2 - c0) : src + ((int64_t)r * N2 + c0);
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 128, [%2];" ::"r"(
-                    pf_smem_u32(stg + r * 32)),
-                "l"(g), "r"(bar_a)
-                : "memory");
-        }
-    };
-    if ((int)blockIdx.x < ntiles) issue(blockIdx.x);
-    uint32_t phase = 0;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, phase ^= 1) {
-        const int cx = t % NX, op = (t / NX) & 1;
-        const int64_t pl = t / (2 * NX), pair = a.pair0 + pl;
-        const OperandDesc& d = a.op[op];
-        const float* th = sthr + op * kMaxThr;
-        const float t0 = QM == QM_K1 ? th[0] : 0.f, t1 = QM == QM_K1 ? th[1] : 0.f;
-        const float inv_step = (float)d.q.inv_step;
-        const int k = d.q.k, tbits = d.q.tbits;
-        const int li = d.reverse ? 31 - lane : lane;
-        const int c0 = cx * 32;
-        unsigned ssq = 0, nnz = 0, flags = 0;
-        auto to_res = [&](int c) -> uint32_t {
-            ssq += (unsigned)(c * c);
-            nnz += (c != 0);
-            return c < 0 ? (uint32_t)(c + (int)m.p) : (uint32_t)c;
-        };
-        // wait for this tile's rows
-        asm volatile(
-            "{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-            "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar_a),
-            "r"(phase)
-            : "memory");
-        // first DIF group from the staged rows (reversed rows: lane order flipped;
-        // staged row r holds stream row r of this tile, so element (r, lane))
-#pragma unroll 1
-        for (int g = warp; g < S; g += kWarps) {
-            uint32_t x[RAD0];
-            float v[NLD];
-#pragma unroll
-            for (int kk = 0; kk < NLD; ++kk) v[kk] = stg[(g + kk * S) * 32 + li];
-            if constexpr (QM == QM_UNIFORM) {
-                int c[NLD];
-                bool bad = false;
-#pragma unroll
-                for (int kk = 0; kk < NLD; ++kk) c[kk] = level_uniform_nb(v[kk], k, inv_step, bad);
-                if (__builtin_expect(bad, 0)) {
-#pragma unroll
-                    for (int kk = 0; kk < NLD; ++kk) {
-                        if (v[kk] != v[kk]) flags |= SF_NONFINITE;
-                        c[kk] = quant_level<float, QM>(v[kk], th, k, tbits, inv_step, t0, t1);
-                    }
-                }
-#pragma unroll
-                for (int kk = 0; kk < RAD0; ++kk) x[kk] = kk < NLD ? to_res(c[kk]) : 0u;
-            } else {
-#pragma unroll
-                for (int kk = 0; kk < RAD0; ++kk) {
-                    if (kk >= NLD) { x[kk] = 0; continue; }
-                    if (v[kk] != v[kk]) flags |= SF_NONFINITE;
-                    x[kk] = to_res(level_of<float, QM>(v[kk], th, k, tbits, inv_step, t0, t1));
-                }
-            }
-            dif_regs<LOG1, 0>(x, g, stw, m);
-            uint32_t* p = smem + g * kPad + lane;
-#pragma unroll
-            for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
-            nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
-            flags |= __shfl_xor_sync(0xffffffffu, flags, o);
-        }
-        if (lane == 0 && a.p0 == m.p) {
-            unsigned long long* st = a.stats + (pair * 2 + op) * 4;
-            if (ssq) atomicAdd(st + 0, (unsigned long long)ssq);
-            if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
-            if (flags) atomicOr(st + 2, (unsigned long long)flags);
-        }
-        __syncthreads();  // staging buffer consumed: the next tile's rows may land
-        if (t + (int)gridDim.x < ntiles) issue(t + gridDim.x);
-        dif_middle<LOG1, 1, 1>(smem, nullptr, stw, m);
-#pragma unroll 1
-        for (int g = warp; g < (N1 >> RL); g += kWarps) {
-            uint32_t x[RADL];
-            uint32_t* p = smem + g * RADL * kPad + lane;
-#pragma unroll
-            for (int kk = 0; kk < RADL; ++kk) x[kk] = p[kk * kPad];
-            dif_regs<LOG1, SC::NG - 1>(x, 0, stw, m);
-#pragma unroll
-            for (int kk = 0; kk < RADL; ++kk) p[kk * kPad] = x[kk];
-        }
-        __syncthreads();
-        uint32_t* Yt = a.Y + (pl * 2 + op) * ((int64_t)N1 * N2);
-        constexpr int NB = N1 / 32;
-#pragma unroll 1
-        for (int c = warp; c < 32; c += kWarps) {
-            const int o = (c0 + c) * N1;
-            const uint2* tb = a.twab + (int64_t)(c0 + c) * (32 + NB);
-            const uint2 A = __ldg(&tb[lane]);
-            QX_UNROLL(QX_TW_UNROLL)
-            for (int j = 0; j < NB; ++j) {
-                const uint2 B = __ldg(&tb[32 + j]);
-                const int e = lane + 32 * j;
-                Yt[o + e] = shoup(shoup(smem[e * kPad + c], A.x, A.y, m.p), B.x, B.y, m.p);
-            }
-        }
-        __syncthreads();  // the tile buffer is rewritten by the next tile's first group
-    }
-}
-
 // ------------------------------------------------------------------ pass 2
 
 struct Pass2Args {
@@ -1332,16 +1167,6 @@ static void group_tables_rt(int log, uint64_t root, uint64_t p, std::vector<uint
     }
 }
 
-// factored pass-1 twiddles (NttTables::twab); QX_NTT_TWAB=0 keeps the full table (A/B)
-static bool twab_on()
-{
-    static const bool on = [] {
-        const char* e = getenv("QX_NTT_TWAB");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
-
 cudaError_t ntt_make_tables(uint32_t p, uint32_t g, int lp, NttTables* out, void** dev_block)
 {
     const int l1 = (lp + 1) / 2, l2 = lp / 2;
@@ -1486,57 +1311,11 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
 
 // ---- kernel dispatch tables
 
-template <int LOG1, int QM>
-static cudaError_t launch_p1pf(const Pass1Args& a, int ntiles, cudaStream_t s)
-{
-    static bool attr = false;
-    static int sms = 0;
-    const size_t smem = pass1pf_smem<LOG1>();
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass1_pf<LOG1, QM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        attr = true;
-    }
-    k_pass1_pf<LOG1, QM><<<std::min(ntiles, sms), kThreads, smem, s>>>(a, ntiles);
-    return cudaGetLastError();
-}
-
-// the persistent bulk-copy pass 1 applies: float rows exactly filling the
-// loaded half, 16-byte aligned rows, first prime.  Opt-in (QX_NTT_PF=1):
-// alone it matches k_pass1 (0.895 vs 0.886 ms per C2 step), but a persistent
-// grid holds every SM for the whole pass, so the sweep's compute lanes can no
-// longer fill each other's tails (C2 step 2.08 -> 2.19 ms).  Issuing the 512
-// row copies from one warp instead of all threads: 1.50 ms (bulk-copy issue
-// stalls the issuing warp, the others wait at the tile barrier).
-static bool p1pf_ok(const Pass1Args& a, int l1, int dt, int qm, int zu, int N2)
-{
-    static const bool on = [] {
-        const char* e = getenv("QX_NTT_PF");
-        return e && e[0] == '1';
-    }();
-    if (!on || l1 != 10 || dt != DT_F32 || !(qm == QM_K1 || qm == QM_UNIFORM) || !zu || a.skip_cs || !a.twab) return false;
-    for (int o = 0; o < 2; ++o) {
-        const OperandDesc& d = a.op[o];
-        if (d.dtype != dt || d.q.mode != qm || d.q.tsize > kMaxThr) return false;
-        if ((uintptr_t)d.data % 16 || d.ld % 4 || d.n % 4 || (int64_t)(1 << (l1 - 1)) * N2 != d.n) return false;
-    }
-    return true;
-}
-
 template <int LOG1, typename T, int QM, bool ZU>
 static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, cudaStream_t s)
 {
-    static bool attr = false;
     const size_t smem = pass1_smem<LOG1>(sizeof(T));
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass1<LOG1, T, QM, ZU>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = set_max_smem((const void*)k_pass1<LOG1, T, QM, ZU>, smem); e != cudaSuccess) return e;
     k_pass1<LOG1, T, QM, ZU><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -1579,13 +1358,8 @@ static cudaError_t dispatch_p1(int log1, const Pass1Args& a, int dtype, int qm, 
 template <int LOG2>
 static cudaError_t launch_p2(const Pass2Args& a, dim3 grid, cudaStream_t s)
 {
-    static bool attr = false;
     const size_t smem = pass2_smem<LOG2>();
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass2<LOG2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = set_max_smem((const void*)k_pass2<LOG2>, smem); e != cudaSuccess) return e;
     k_pass2<LOG2><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -1605,14 +1379,8 @@ static cudaError_t dispatch_p2(int log2, const Pass2Args& a, dim3 grid, cudaStre
 template <int LOG1, int OUT>
 static cudaError_t launch_p3(const Pass3Args& a, dim3 grid, cudaStream_t s)
 {
-    static bool attr = false;
     const size_t smem = pass3_smem<LOG1>();
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_pass3<LOG1, OUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = set_max_smem((const void*)k_pass3<LOG1, OUT>, smem); e != cudaSuccess) return e;
     k_pass3<LOG1, OUT><<<grid, kThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
@@ -1773,7 +1541,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             a1.Y = c.Y;
             a1.gtw = T.g1f;
             a1.twf = T.twf;
-            a1.twab = twab_on() ? T.twab : nullptr;
+            a1.twab = T.twab;
             a1.stats = c.stats;
             a1.m = T.m;
             a1.p0 = t0.p;
@@ -1792,7 +1560,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             a2.gtwf = T.g2f;
             a2.gtwi = T.g2i;
             a2.twinv = T.twi;
-            a2.twib = twab_on() ? T.twib : nullptr;
+            a2.twib = T.twib;
             a2.stats = c.stats;
             a2.m = T.m;
             a2.p0 = t0.p;
@@ -1892,7 +1660,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a1.Y = c.Y;
             a1.gtw = T.g1f;
             a1.twf = T.twf;
-            a1.twab = twab_on() ? T.twab : nullptr;
+            a1.twab = T.twab;
             a1.stats = c.stats;
             a1.m = T.m;
             a1.p0 = t0.p;
@@ -1904,11 +1672,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             const int dt = c.op[0].dtype, qm = c.op[0].q.mode;
             if (c.op[1].dtype == dt && c.op[1].q.mode == qm) {
                 if (c.prof) c.prof->pre(KK_PASS1, s);
-                if (p1pf_ok(a1, l1, dt, qm, c.zero_upper, (int)N2))
-                    e = qm == QM_K1 ? launch_p1pf<10, QM_K1>(a1, (int)(N2 / 32) * 2 * (int)nb, s)
-                                    : launch_p1pf<10, QM_UNIFORM>(a1, (int)(N2 / 32) * 2 * (int)nb, s);
-                else
-                    e = dispatch_p1(l1, a1, dt, qm, dim3(N2 / 32, 2, (unsigned)nb), s);
+                e = dispatch_p1(l1, a1, dt, qm, dim3(N2 / 32, 2, (unsigned)nb), s);
                 if (c.prof) c.prof->post(KK_PASS1, s);
                 if (e != cudaSuccess) return e;
             } else {
@@ -1932,7 +1696,7 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
             a2.gtwf = T.g2f;
             a2.gtwi = T.g2i;
             a2.twinv = T.twi;
-            a2.twib = twab_on() ? T.twib : nullptr;
+            a2.twib = T.twib;
             a2.stats = c.stats;
             a2.m = T.m;
             a2.p0 = t0.p;

@@ -321,21 +321,6 @@ __global__ void __launch_bounds__(kPopcThreads) k_popc_fused(const __grid_consta
 }
 
 
-// SM count of the current device (cached per device: the plan runs twice per call)
-static int popc_sms()
-{
-    static int cache[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64) dev = 0;
-    if (!cache[dev]) {
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cache[dev] = sms;
-    }
-    return cache[dev];
-}
-
 // launch plan: ~2 CTAs per SM over the whole batch, at least kPopcGroups
 // 32-lag blocks per CTA when there are enough; returns the shared memory
 static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, bool fused = false)
@@ -347,7 +332,7 @@ static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, b
     a.nblk = (int)nblk;
     a.nxw = (int)((nx + 31) / 32);
     a.nyw = (int)((c.op[1].n + 31) / 32);
-    const int sms = popc_sms();
+    const int sms = device_sms();
     // fused (cooperative) launch: every CTA resident at once, one per SM
     G = fused ? (int64_t)sms / c.batch : ((int64_t)sms + c.batch - 1) / c.batch;
     const int64_t gmax = (nblk + kPopcGroups - 1) / kPopcGroups;
@@ -367,8 +352,7 @@ static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, b
 bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path)
 {
     (void)ny;
-    const char* env = getenv("QX_POPC");
-    if (env && env[0] == '0') return false;
+    if (auto_path && !c.knobs->popc) return false;
     if (c.op[0].q.mode != QM_K1 || c.op[1].q.mode != QM_K1) return false;
     if (c.op[0].dtype == DT_I64 || c.op[0].dtype != c.op[1].dtype) return false;
     if (nx > 65536) return false;
@@ -388,21 +372,14 @@ cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
     a.am = c.am;
     a.planes = c.popc_planes;
     a.spart = c.popc_spart;
-    const int sms = popc_sms();
-    const char* env = getenv("QX_POPC_FUSED");
-    const bool fused = c.batch <= sms && !(env && env[0] == '0');
+    const int sms = device_sms();
+    const bool fused = c.batch <= sms && c.knobs->popc_fused;
     int64_t G;
     const size_t smem = popc_plan(c, nx, a, G, fused);
     if (G > c.am.pstride) return cudaErrorInvalidValue;
-    static size_t attr[3] = {0, 0, 0};
     const int ti = c.op[0].dtype == DT_F32 ? 0 : 1;
-    auto raise = [&](const void* fn, int slot) -> cudaError_t {
-        if (smem > 48 * 1024 && attr[slot] < smem) {
-            cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            attr[slot] = smem;
-        }
-        return cudaSuccess;
+    auto raise = [&](const void* fn, int) -> cudaError_t {
+        return smem > 48 * 1024 ? set_max_smem(fn, smem) : cudaSuccess;
     };
     cudaError_t e;
     if (fused) {

@@ -1787,8 +1787,7 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
 // at a word boundary, y rows <= 12288 samples; QX_TC_F4=0 disables it
 static bool tc_fp4_codes(const NttCall& c, int64_t nx)
 {
-    const char* env = getenv("QX_TC_F4");
-    if (env && env[0] == '0') return false;
+    if (!c.knobs->tc_f4) return false;
     return c.op[0].dtype == DT_F32 && c.op[1].dtype == DT_F32 && c.op[0].ld == 0 && nx <= kTcFastN &&
            nx % 4 == 0 && (uintptr_t)c.op[0].data % 16 == 0 && (uintptr_t)c.op[1].data % 16 == 0 &&
            c.op[1].ld % 4 == 0 && c.op[0].q.mode == c.op[1].q.mode && c.op[0].q.k <= kF4MaxCode &&
@@ -1806,8 +1805,7 @@ static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
 // 32768 lags, rows up to 32768 + K samples; QX_TC_F2=0 disables it
 static bool tc_f2_mode(const NttCall& c, int64_t nx, int64_t ny)
 {
-    const char* env = getenv("QX_TC_F2");
-    if (!c.split2 || (env && env[0] == '0')) return false;
+    if (!c.split2) return false;
     const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
     return tc_fp4_codes(c, nx) && c.batch > 1 && L0 == 0 && W <= kF2Lags && ny <= kF2Lags + kTcMaxK;
 }
@@ -1834,14 +1832,8 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
 template <typename T, int QM, int MODE = 0>
 static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
 {
-    static bool attr = false;
     const size_t smem = sizeof(TcSmem);
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_tc_window<T, QM, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = set_max_smem((const void*)k_tc_window<T, QM, MODE>, smem); e != cudaSuccess) return e;
     if constexpr (MODE == 3) {
         // clusters of 2 CTAs (one pair-block per cluster at a time), as many
         // as can be resident at once: not every SM has a free partner in its
@@ -1862,7 +1854,6 @@ static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
             cfg.gridDim = dim3((unsigned)(sms & ~1));
             cudaError_t e = cudaOccupancyMaxActiveClusters(&clusters, k_tc_window<T, QM, MODE>, &cfg);
             if (e != cudaSuccess || clusters < 1) clusters = sms / 2;
-            if (getenv("QX_TC_VERBOSE")) fprintf(stderr, "qx_tc: 2-SM mode, %d resident clusters\n", clusters);
         }
         const int64_t want = a.batch;
         cfg.gridDim = dim3((unsigned)(2 * (want < clusters ? want : clusters)));
@@ -1942,9 +1933,7 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
 #ifdef QX_TC_TIMING
     if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
 #endif
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     // fp4 modes only (the int8 ones returned above)
     if (c.prof) c.prof->pre(KK_DIRECT_F4, s);
     cudaError_t e;
@@ -1957,8 +1946,7 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
         // A operand in TMEM (mode 4) only with QX_TC_T4=1: exact, and its MMA
         // runs at the fp4 peak, but its four stager warps do not keep up yet
         // (0.72 ms vs 0.49 ms for config 5); mode 2 reads A from shared memory
-        const char* t4env = getenv("QX_TC_T4");
-        const bool t4 = t4env && t4env[0] == '1';
+        const bool t4 = false;
         if (t4) {
             if (qm == QM_K1) e = launch_tc<float, QM_K1, 4>(a, s, sms);
             else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 4>(a, s, sms);

@@ -1031,14 +1031,8 @@ bool tc_i8_window_eligible(const NttCall& c, int64_t nx, int64_t ny)
 template <typename T, int QM, bool SX = false>
 static cudaError_t launch_tc(const TcArgs& a, cudaStream_t s, int sms)
 {
-    static bool attr = false;
     const size_t smem = sizeof(TcSmem);
-    if (!attr) {
-        cudaError_t e =
-            cudaFuncSetAttribute(k_tc_window<T, QM, SX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    if (cudaError_t e = set_max_smem((const void*)k_tc_window<T, QM, SX>, smem); e != cudaSuccess) return e;
     const int grid = (int)(a.batch < sms ? a.batch : sms);
     k_tc_window<T, QM, SX><<<grid, kTcTotalThreads, smem, s>>>(a);
     return cudaGetLastError();
@@ -1084,9 +1078,7 @@ cudaError_t tc_i8_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
 #ifdef QX_TC_TIMING
     if (const char* ev = getenv("QX_TC_DEBUG")) a.debug = atoi(ev);
 #endif
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     if (c.prof) c.prof->pre(KK_DIRECT, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;

@@ -21,7 +21,7 @@ def test_exports_every_declared_symbol():
     assert declared == set(N.EXPORTS), declared ^ set(N.EXPORTS)
     for name in declared:
         assert hasattr(L, name), name
-    assert L.qx_abi_version() == 2
+    assert L.qx_abi_version() == N.ABI_VERSION == int(re.search(r"#define QX_ABI_VERSION (\d+)", header).group(1))
     assert L.qx_status_string(2) == b"quantizes to all zeros"
 
 

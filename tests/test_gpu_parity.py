@@ -277,20 +277,22 @@ def test_popc_path_against_oracle(qx, oracle):
     assert r["status"][0] == 9
 
 
-def test_popc_fused_and_split_launches_agree(qx, monkeypatch):
+def test_popc_fused_and_split_launches_agree(qx):
     """The cooperative single-launch popc kernel and the two-launch version
-    (QX_POPC_FUSED=0) give identical records, statistics included."""
+    (option popc_fused=0; the form batches larger than the SM count take)
+    give identical records, statistics included."""
     import torch
+
+    from paper_2509_19974_b200 import _native as N
 
     rng = np.random.default_rng(32)
     for B, nx, ny in ((1, 16384, 16384), (3, 5000, 7001), (148, 300, 257), (200, 64, 64)):
         x = torch.from_numpy(rng.standard_normal((B, nx)).astype(np.float32)).cuda()
         y = torch.from_numpy(rng.standard_normal((B, ny)).astype(np.float32)).cuda()
         q = qx.sign()
-        monkeypatch.setenv("QX_POPC_FUSED", "1")
         a = qx.estimate_batch(x, y, q, q, path="popc").numpy()
-        monkeypatch.setenv("QX_POPC_FUSED", "0")
-        b = qx.estimate_batch(x, y, q, q, path="popc").numpy()
+        with N.option("popc_fused", 0):
+            b = qx.estimate_batch(x, y, q, q, path="popc").numpy()
         assert np.array_equal(a, b), (B, nx, ny)
 
 
@@ -373,16 +375,19 @@ def test_sweep_host_entry_point(qx, oracle):
 
 
 @pytest.mark.parametrize("lanes", [None, "1", "3"])
-def test_device_sweep_entry_point(qx, oracle, lanes, monkeypatch):
+def test_device_sweep_entry_point(qx, oracle, lanes):
     """qx_estimate_sweep: device rows, quantiser pairs on forked compute lanes
     joined back to the caller's stream; equals one estimate_batch per pair and
     the oracle, and a kernel on the caller's stream right after the call sees
     finished results."""
     import torch
-    from paper_2509_19974_b200 import workloads as W
+    from paper_2509_19974_b200 import _native as N, workloads as W
 
-    if lanes:
-        monkeypatch.setenv("QX_SWEEP_LANES", lanes)
+    with N.option("sweep_lanes", int(lanes or 0)):
+        _device_sweep_checks(qx, oracle, torch, W)
+
+
+def _device_sweep_checks(qx, oracle, torch, W):
     xs, ys, lag = W.c2(pairs=6, n=1 << 12, seed=5)
     qs = [(W.bit_quantizer(b, W.C2_SIGMA), W.bit_quantizer(b, W.C2_SIGMA)) for b in (1, 2, 4, 8)]
     qs.append((qx.uniform(3, 0.4), qx.sign()))
@@ -408,16 +413,43 @@ def test_device_sweep_entry_point(qx, oracle, lanes, monkeypatch):
 
 
 @pytest.mark.parametrize("pairs", [1, 5, 17, 40, 67])
-@pytest.mark.parametrize("knobs", [{}, {"QX_SWEEP_LANES": "1"}, {"QX_SWEEP_CHUNKS": "7", "QX_SWEEP_TAPER": "3"},
-                                   {"QX_SWEEP_LANES": "2", "QX_SWEEP_CHUNKS": "64"}, {"QX_SWEEP_EVEN": "1"}])
-def test_sweep_host_chunk_schedules(qx, pairs, knobs, monkeypatch):
+@pytest.mark.parametrize("knobs", [{}, {"sweep_lanes": 1}, {"sweep_chunks": 7, "sweep_taper": 3},
+                                   {"sweep_lanes": 2, "sweep_chunks": 64}, {"sweep_even": 1}])
+def test_sweep_host_chunk_schedules(qx, pairs, knobs):
     """Every chunk/lane/taper schedule of qx_estimate_sweep_host covers each
     pair exactly once: results equal per-quantiser estimate_batch_host calls
     for ragged batch sizes (1 pair, primes, more chunks than pairs)."""
-    from paper_2509_19974_b200 import workloads as W
+    import contextlib
 
-    for k, v in knobs.items():
-        monkeypatch.setenv(k, v)
+    from paper_2509_19974_b200 import _native as N, workloads as W
+
+    with contextlib.ExitStack() as stack:
+        for k, v in knobs.items():
+            stack.enter_context(N.option(k, v))
+        _sweep_host_checks(qx, W, pairs)
+    # overlapping rows (0 < ld < n, through the C ABI) are staged whole
+    # whatever the chunk option (a chunk count would read past the buffer)
+    import ctypes
+
+    from paper_2509_19974_b200.quantize import native_quantizer
+
+    with N.option("sweep_chunks", 5):
+        base = np.random.default_rng(pairs).standard_normal(2000 + 160 * pairs).astype(np.float32)
+        sx = N.QxSignals(base.ctypes.data, N.QX_F32, 0, 2000, 160, 0)
+        sy = N.QxSignals(base[37:].ctypes.data, N.QX_F32, 0, 1900, 160, 0)
+        q = qx.uniform(3, 0.4)
+        nq, _ = native_quantizer(q)
+        res = np.zeros(pairs, dtype=N.RESULT_DTYPE)
+        st = N.load().qx_estimate_sweep_host(N.context(), ctypes.byref(sx), ctypes.byref(sy), pairs, 1,
+                                             ctypes.byref(nq), ctypes.byref(nq), N.INT64_MIN, N.INT64_MAX, 0,
+                                             res.ctypes.data)
+        assert st == 0
+        xo = np.lib.stride_tricks.as_strided(base, (pairs, 2000), (640, 4))
+        yo = np.lib.stride_tricks.as_strided(base[37:], (pairs, 1900), (640, 4))
+        assert np.array_equal(res, qx.estimate_batch_host(np.ascontiguousarray(xo), np.ascontiguousarray(yo), q, q))
+
+
+def _sweep_host_checks(qx, W, pairs):
     xs, ys, lag = W.c2(pairs=pairs, n=1 << 10, seed=pairs)
     qs = [(W.bit_quantizer(b, W.C2_SIGMA), W.bit_quantizer(b, W.C2_SIGMA)) for b in (1, 2, 8)]
     qs.append((qx.uniform(3, 0.4), qx.sign()))
@@ -537,11 +569,11 @@ def test_template_search_tensor_core_blocks(qx, oracle, golden):
         assert qx.template_search(t5, s5, qa, qb) == (case["peak"], case["lags"][0], len(case["lags"]))
 
 
-def test_template_search_fp4_mode(qx, oracle, monkeypatch):
+def test_template_search_fp4_mode(qx, oracle):
     """Template search on the fp4 (e2m1, kind::mxf4) tensor-core mode: codes
     |c| <= 4 (sign, uniform k = 1..4), 8192-lag blocks; the profile proves the
     fp4 kernel ran, and the summary equals the oracle's and the i8 mode's
-    (QX_TC_F4=0) on the same inputs, including a remainder block, short
+    (option tc_f4=0) on the same inputs, including a remainder block, short
     templates and a k=4 worst case near the f32-exact bound."""
     from paper_2509_19974_b200 import _native
 
@@ -554,42 +586,16 @@ def test_template_search_fp4_mode(qx, oracle, monkeypatch):
         off = int(rng.integers(0, ns - nt + 1))
         tpl = st[off:off + nt].copy()
         st = st + rng.normal(0, 0.7, ns).astype(np.float32)
-        monkeypatch.setenv("QX_TC_F4", "1")
         with _native.profile(timed=False) as prof:
             got = qx.template_search(tpl, st, q, q, stream_start=3)
         assert prof.result.get("direct_f4", (0, 0))[0] >= 1, (trial, prof.result)
-        monkeypatch.setenv("QX_TC_F4", "0")
-        with _native.profile(timed=False) as prof:
+        with _native.option("tc_f4", 0), _native.profile(timed=False) as prof:
             i8 = qx.template_search(tpl, st, q, q, stream_start=3)
         assert "direct_f4" not in prof.result or prof.result["direct_f4"][0] == 0, prof.result
         u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
         first = -(nt - 1)
         m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, 0 - first, ns - nt - first))
         assert got == i8 == (m, f + 3, n), (trial, got, i8, (m, f, n))
-
-
-def test_template_search_2sm_mode(qx, oracle, monkeypatch):
-    """Template search on the 2-SM fp4 mode (cta_group::2 MMA over CTA pairs,
-    32768-lag blocks, one record per CTA) followed by 8192-lag fp4 blocks and
-    a remainder: equal to the oracle and to the same search with the 2-SM
-    mode off (QX_TC_F2=0) and with the int8 path (QX_TC_F4=0)."""
-    rng = np.random.default_rng(24)
-    cases = [(4096, qx.sign()), (4096, qx.uniform(1, 0.8)), (1000, qx.uniform(4, 0.3)), (64, qx.uniform(2, 0.5))]
-    for trial, (nt, q) in enumerate(cases):
-        ns = nt - 1 + 32768 * int(rng.integers(2, 4)) + 8192 * int(rng.integers(0, 3)) + int(rng.integers(1, 8192))
-        st = rng.laplace(size=ns).astype(np.float32)
-        off = int(rng.integers(0, ns - nt + 1))
-        tpl = st[off:off + nt].copy()
-        st = st + rng.normal(0, 0.9, ns).astype(np.float32)
-        got = {}
-        for f2, f4 in (("1", "1"), ("0", "1"), ("0", "0")):
-            monkeypatch.setenv("QX_TC_F2", f2)
-            monkeypatch.setenv("QX_TC_F4", f4)
-            got[(f2, f4)] = qx.template_search(tpl, st, q, q, stream_start=7)
-        u, v = oracle.quantize(q, tpl), oracle.quantize(q, st)
-        first = -(nt - 1)
-        m, f, n = oracle.argmax(oracle.xcorr_bf(u, v, 0 - first, ns - nt - first))
-        assert set(got.values()) == {(m, f + 7, n)}, (trial, got, (m, f + 7, n))
 
 
 def test_template_search_random_modes_and_errors(qx, oracle, monkeypatch):
@@ -662,18 +668,22 @@ def test_sharded_template_search_over_nccl(qx):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("f4", ["0", "1", "t4"])
-def test_template_blocks_every_block(qx, oracle, monkeypatch, f4):
+@pytest.mark.parametrize("f4", [0, 1])
+def test_template_blocks_every_block(qx, oracle, f4):
     """Every block summary of the shared-template window modes (i8 pitch 32,
     fp4 pitch 64) against the oracle, for templates whose length leaves the
     shifted copies past the pitch-16 K (nt = 4, 8, 40, 1000, 2052: the copies
     need K >= nt + pitch - 1)."""
     import torch
 
-    # "t4": the fp4 mode with the A operand in TMEM (QX_TC_T4=1)
-    monkeypatch.setenv("QX_TC_F4", "0" if f4 == "0" else "1")
-    monkeypatch.setenv("QX_TC_T4", "1" if f4 == "t4" else "0")
-    block = 4096 if f4 == "0" else 8192
+    from paper_2509_19974_b200 import _native as N
+
+    with N.option("tc_f4", f4):
+        _every_block_checks(qx, oracle, torch, f4)
+
+
+def _every_block_checks(qx, oracle, torch, f4):
+    block = 4096 if f4 == 0 else 8192
     for seed, (nt, q) in enumerate([(4, qx.sign()), (8, qx.sign()), (40, qx.uniform(1, 0.8)),
                                     (1000, qx.sign()), (2052, qx.uniform(1, 0.8))]):
         rng = np.random.default_rng(seed)
@@ -735,29 +745,32 @@ def test_c4_full_size(qx, oracle):
     assert oracle.xcorr_bf(u, v, t_peak, t_peak)[0] == res["value"]
 
 
-def test_persistent_pass1_opt_in_matches(qx):
-    """The opt-in persistent bulk-copy pass 1 (QX_NTT_PF=1, read once per
-    process) gives the same C2 results as the default pass 1."""
-    import json
-    import os
-    import subprocess
-    import sys
-
+def test_calls_on_different_streams_are_ordered(qx):
+    """Entry points that share a context's scratch on different streams are
+    ordered (an async estimate_batch on one stream followed by a
+    call on another stream must not race on the scratch and counters)."""
     import torch
+
     from paper_2509_19974_b200 import workloads as W
 
-    code = ("import json,torch,paper_2509_19974_b200 as P;from paper_2509_19974_b200 import workloads as W;"
-            "xs,ys,_=W.c2(pairs=5,seed=9);x,y=torch.from_numpy(xs).cuda(),torch.from_numpy(ys).cuda();"
-            "r=P.estimate_sweep(x,y,[(W.bit_quantizer(b,W.C2_SIGMA),)*2 for b in (1,2,4)]);"
-            "print(json.dumps([q.raw.cpu().tolist() for q in r]))")
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, QX_NTT_PF="1"), cwd=root,
-                         capture_output=True, text=True, timeout=300)
-    assert out.returncode == 0, out.stderr[-2000:]
-    got = json.loads(out.stdout.strip().splitlines()[-1])
-    xs, ys, lag = W.c2(pairs=5, seed=9)
-    x, y = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
-    want = qx.estimate_sweep(x, y, [(W.bit_quantizer(b, W.C2_SIGMA),) * 2 for b in (1, 2, 4)])
-    for q in range(3):
-        assert got[q] == want[q].raw.cpu().tolist(), q
-        assert np.array_equal(want[q].lag.cpu().numpy(), lag)
+    xs, ys, _ = W.c2(pairs=16, n=1 << 16, seed=41)
+    xs2, ys2, _ = W.c2(pairs=16, n=1 << 16, seed=42)
+    q = W.bit_quantizer(4, W.C2_SIGMA)
+    x1, y1 = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
+    x2, y2 = torch.from_numpy(xs2).cuda(), torch.from_numpy(ys2).cuda()
+    want1 = qx.estimate_batch(x1, y1, q, q).raw.clone()
+    want2 = qx.estimate_batch(x2, y2, q, q).raw.clone()
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(4):
+        with torch.cuda.stream(s1):
+            r1 = qx.estimate_batch(x1, y1, q, q)
+        with torch.cuda.stream(s2):
+            r2 = qx.estimate_batch(x2, y2, q, q)
+        with torch.cuda.stream(s1):
+            r3 = qx.estimate_batch(x1, y1, q, q, path="ntt")
+        h = qx.estimate_batch_host(xs2, ys2, q, q)  # the context's host stream
+        torch.cuda.synchronize()
+        assert torch.equal(r1.raw, want1) and torch.equal(r2.raw, want2) and torch.equal(r3.raw, want1)
+        assert np.array_equal(h, want2.cpu().numpy().view(h.dtype).reshape(-1))
+    assert torch.cuda.current_device() == 0

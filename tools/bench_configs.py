@@ -1,7 +1,8 @@
 """Per-config throughput of the engine on one GPU (BASELINE configs 1-5).
 
 Times each config's hot path with CUDA events (inputs resident in HBM, warm
-tables), checks every estimate against the planted delay, and returns / prints
+tables), checks every estimate against the pinned oracle's full-size records
+(tests/golden/fullsize.*, tools/fullsize_golden.py), and returns / prints
 one JSON object.  C3 runs a 16384-pair slice of the 65,536-pair workload
 (per-pair cost is shape-only; `c3full` runs all 65,536 pairs); C5 runs the
 full 2^28-sample stream.  Roofline fractions: HBM from MEASURED_PEAKS.json
@@ -23,6 +24,9 @@ import torch
 
 import paper_2509_19974_b200 as P
 from paper_2509_19974_b200 import workloads as W
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import fullsize_golden as G  # noqa: E402
 
 I8_MACS_PER_CLK_SM = 8190.0  # tools/tc_rate.cu, M128 x N128/N256
 FP4_MACS_PER_CLK_SM = 16336.0  # tools/tc_fp4.cu rate probe, M128 x N128/N256 kind::mxf4
@@ -59,7 +63,7 @@ def run(which) -> dict:
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         ms, r = timed(lambda: P.estimate_batch(xd, yd, P.sign(), P.sign()), reps=50)
         r = r.numpy()[0]
-        assert (r["lag"], r["value"]) == (-137, 14839)
+        G.check_c1(int(r["lag"]), int(r["value"]))
         res["c1"] = {"ms_per_estimate": ms, "lag": int(r["lag"]), "peak": int(r["value"]),
                      "note": "single pair, latency incl. the Python call",
                      "path": "popc word-parallel 1-level codes (bit planes + 32-lag blocks)"}
@@ -68,7 +72,9 @@ def run(which) -> dict:
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         xb, yb = xd.expand(1024, -1), yd.expand(1024, -1)
         ms, r = timed(lambda: P.estimate_batch(xb, yb, P.sign(), P.sign()), reps=10)
-        assert (r.numpy()["lag"] == -137).all()
+        rr = r.numpy()
+        G.check_c1(int(rr["lag"][0]), int(rr["value"][0]))
+        assert (G.records(rr) == G.records(rr[:1])).all()
         res["c1_batch1024"] = {"ms": ms, "estimates_per_s": 1024 / ms * 1e3}
     if "c2" in which:
         xs, ys, lag = W.c2()
@@ -76,7 +82,7 @@ def run(which) -> dict:
         for b in (1, 2, 4, 8):
             q = W.bit_quantizer(b, W.C2_SIGMA)
             ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q))
-            assert np.array_equal(r.numpy()["lag"], lag)
+            G.check_c2((1, 2, 4, 8).index(b), 0, r.numpy())
             res[f"c2_b{b}"] = {"ms": ms, "estimates_per_s": 64 / ms * 1e3,
                                "gsamples_per_s": 64 * 2 * W.C2_N / ms / 1e6}
     if "c3" in which or "c3full" in which:
@@ -88,7 +94,7 @@ def run(which) -> dict:
             q = W.bit_quantizer(b, W.C3_SIGMA)
             ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q, lag_lo=-512, lag_hi=512), reps=3)
             ok = float(np.mean(r.numpy()["lag"] == lag))
-            assert ok == 1.0, ok
+            G.check_c3((2, 4).index(b), 0, r.numpy())
             res[f"c3_b{b}"] = {"pairs": npairs, "ms": ms, "estimates_per_s": npairs / ms * 1e3,
                                "gsamples_per_s": npairs * 2 * W.C3_N / ms / 1e6, "frac_correct_lag": ok,
                                "hbm_frac": npairs * 2 * W.C3_N * 4 / (ms / 1e3) / 1e9 / hbm,
@@ -99,7 +105,7 @@ def run(which) -> dict:
         xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
         q = W.bit_quantizer(4, W.C4_SIGMA)
         ms, r = timed(lambda: P.estimate_batch(xd, yd, q, q), reps=3)
-        assert r.numpy()["lag"][0] == lag
+        G.check_c4(r.numpy()[0])
         res["c4"] = {"ms": ms, "gsamples_per_s": 2 * W.C4_N / ms / 1e6,
                      "path": "ntt P=2^25 (outer 2^6 x inner 2^19)"}
         del xd, yd
@@ -115,7 +121,7 @@ def run(which) -> dict:
             else:
                 qa, qb = P.uniform(1, 1.5 * math.sqrt(2.0)), P.uniform(1, 1.5 * math.sqrt(2.0 + sn2))
             ms, r = timed(lambda: P.template_search(td, sd, qa, qb), reps=10, warm=2)
-            assert r[1] == off, r
+            G.check_c5(b, r)
             res[f"c5_b{b}"] = {"ms": ms, "gsamples_per_s": (len(st) + len(tpl)) / ms / 1e6, "peak": r[0],
                                "lag": r[1], "fp4_tensor_frac": macs / (ms / 1e3) / fp4,
                                "hbm_frac": len(st) * 4 / (ms / 1e3) / 1e9 / hbm,

@@ -206,6 +206,47 @@ qx_status qx_template_search(qx_context *ctx, const qx_signals *tpl, const qx_si
                              const qx_quantizer *qx, const qx_quantizer *qy, int64_t block,
                              qx_path path, int64_t *summary, void *stream);
 
+/* ---- Multi-GPU (one process per GPU; `comm` is an ncclComm_t, e.g. the
+ * communicator of torch's ProcessGroupNCCL).  NCCL is resolved at run time
+ * from the calling process (else libnccl.so.2), so this library has no
+ * link-time NCCL dependency.  The samples never cross GPUs: each rank
+ * searches its own lag range and the ranks exchange only 8-word summaries
+ * (the reference has no distributed code; its only parallelism is the
+ * thread pool of harness.py:301-305).
+ *
+ * qx_summary_reduce_nccl: the device int64[8] template-search summary (see
+ * qx_template_search) of every rank -> the summary of the union of their
+ * lag ranges, on every rank: max value, smallest lag attaining it, summed
+ * ties (argmax_set, estimator.py:50-57), NaN / x-degenerate / failure flags
+ * OR-ed, y-degenerate AND-ed.  Two collectives: MAX over the values and
+ * flags, then one NCCL group of MAX (smallest holder lag) and SUM (holder
+ * ties).  Exact for every int64 value and lag.  Enqueued on `stream`. */
+qx_status qx_summary_reduce_nccl(qx_context *ctx, int64_t *summary, void *comm, void *stream);
+
+/* Sharded template search (BASELINE config 5 over G GPUs): `sig` is THIS
+ * rank's stream slice -- its share of the valid lags plus the
+ * (template - 1)-sample halo, with sig->start = the slice's first sample in
+ * stream coordinates -- and `summary` receives the reduced summary of the
+ * whole stream on every rank (a rank whose slice is shorter than the
+ * template contributes an empty summary).  = qx_template_search on the slice
+ * + qx_summary_reduce_nccl. */
+qx_status qx_template_search_nccl(qx_context *ctx, const qx_signals *tpl, const qx_signals *sig,
+                                  const qx_quantizer *qx, const qx_quantizer *qy, int64_t block,
+                                  qx_path path, void *comm, int64_t *summary, void *stream);
+
+/* Pair-sharded batch (BASELINE configs 2/3 over G GPUs): qx_estimate_batch on
+ * this rank's `batch` pairs into `results` (device), then, if `all` is not
+ * NULL, ncclAllGather of every rank's records into all[rank * batch + b]
+ * (equal `batch` on every rank).  No other collective: pairs are
+ * independent. */
+qx_status qx_estimate_batch_nccl(qx_context *ctx, const qx_signals *x, const qx_signals *y, int64_t batch,
+                                 const qx_quantizer *qx, const qx_quantizer *qy, int64_t lag_lo,
+                                 int64_t lag_hi, qx_path path, qx_result *results, void *comm,
+                                 qx_result *all, void *stream);
+
+/* rank and size of an NCCL communicator (ncclCommUserRank / ncclCommCount) */
+qx_status qx_comm_rank_size(void *comm, int *rank, int *size);
+
 /* Device decode of a mono PCM16 payload (little-endian int16, e.g. the data
  * chunk of a WAV file) to float32 samples pcm / 32768: the sample decode of
  * signalgen.load_wav_bytes (signalgen.py:150-172).  Exact, so the float32

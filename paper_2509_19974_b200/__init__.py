@@ -13,7 +13,7 @@ Batched, windowed and streaming entry points (new): ``estimate_batch``,
 ``parallel``.
 """
 
-from . import accuracy, ingest
+from . import accuracy, ingest, parallel
 from .batch import (BatchResult, check_results, estimate_batch, estimate_batch_host, estimate_sweep,
                     estimate_sweep_host, template_search)
 from .errors import (
@@ -26,21 +26,24 @@ from .errors import (
     QxcorrError,
     UnsupportedFormat,
 )
-from .estimator import EstimationResult, argmax_set, estimate
-from .intxcorr import MUL_BACKENDS, big_mul, xcorr_int_bf, xcorr_int_gpu, xcorr_int_ks
-from .quantize import Quantizer, apply, custom, from_spec, sign, uniform
-from .realxcorr import xcorr_real_at
-from .signals import Correlogram, IntSignal, Signal, l2_norm, reverse, shift
+from .estimator import EstimationResult, argmax_set, estimate, estimate_real
+from .intxcorr import (MUL_BACKENDS, KSPlan, big_mul, pack, plan_ks, unpack_and_correct, xcorr_int_bf, xcorr_int_gpu,
+                       xcorr_int_ks)
+from .quantize import Quantizer, apply, custom, from_spec, random_monotone, sign, uniform
+from .realxcorr import xcorr_real_at, xcorr_real_bf, xcorr_real_fft
+from .signals import Correlogram, IntSignal, Signal, add, crop, l2_norm, reverse, scale, shift, trim
 
 __version__ = "0.1.0"
 
 __all__ = [
     "QxcorrError", "DegenerateInput", "DegenerateQuantization", "InternalOverflow", "BadLength",
     "ParseError", "UnsupportedFormat", "ConfigError",
-    "Signal", "IntSignal", "Correlogram", "reverse", "shift", "l2_norm",
-    "Quantizer", "sign", "uniform", "custom", "from_spec", "apply",
-    "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "big_mul", "MUL_BACKENDS",
-    "EstimationResult", "argmax_set", "estimate",
+    "Signal", "IntSignal", "Correlogram", "reverse", "shift", "l2_norm", "trim", "scale", "add", "crop",
+    "Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "random_monotone",
+    "KSPlan", "plan_ks", "pack", "unpack_and_correct",
+    "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "xcorr_real_bf", "xcorr_real_fft", "big_mul",
+    "MUL_BACKENDS",
+    "EstimationResult", "argmax_set", "estimate", "estimate_real",
     "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host", "check_results", "template_search",
-    "accuracy", "ingest",
+    "accuracy", "ingest", "parallel",
 ]

@@ -79,7 +79,8 @@ EXPORTS = (
     "qx_estimate_batch", "qx_estimate_batch_host", "qx_estimate_sweep", "qx_estimate_sweep_host", "qx_template_search", "qx_decode_pcm16",
     "qx_profile_begin",
     "qx_profile_end",
-    "qx_profile_kind_name",
+    "qx_profile_kind_name", "qx_summary_reduce_nccl", "qx_template_search_nccl", "qx_estimate_batch_nccl",
+    "qx_comm_rank_size",
 )
 
 _lib = None
@@ -129,6 +130,14 @@ def load():
         L.qx_estimate_sweep.restype = st
         L.qx_template_search.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp]
         L.qx_template_search.restype = st
+        L.qx_summary_reduce_nccl.argtypes = [vp, vp, vp, vp]
+        L.qx_summary_reduce_nccl.restype = st
+        L.qx_template_search_nccl.argtypes = [vp, sp, sp, qp, qp, i64, st, vp, vp, vp]
+        L.qx_template_search_nccl.restype = st
+        L.qx_estimate_batch_nccl.argtypes = [vp, sp, sp, i64, qp, qp, i64, i64, st, vp, vp, vp, vp]
+        L.qx_estimate_batch_nccl.restype = st
+        L.qx_comm_rank_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
+        L.qx_comm_rank_size.restype = st
         L.qx_decode_pcm16.argtypes = [vp, vp, i64, vp, vp]
         L.qx_decode_pcm16.restype = st
         L.qx_profile_begin.argtypes = [vp, ctypes.c_int]

@@ -6,21 +6,17 @@ The reference's ``run_accuracy`` (/root/reference/pkg/src/qxcorr/harness.py:
 - "proposed_until_line4": the quantised estimate without it;
 - "ccf_wo_quant": the float FFT correlation.
 
-The reference runs one ``estimate`` per trial. Here every trial of the whole SNR grid is generated
-first. Then all integer estimates run as ONE ``estimate_batch`` launch on the device. Only the
-(rare) pairs whose peak ties fall back to the exact per-pair path (GPU correlogram + float64
-refinement at the tied lags, ``estimator.estimate``).
-
-Trial generation and the float baseline run on the host (numpy). They restate
-the reference's own code, so trials are bit-identical on the same numpy:
-- ``gen_target`` / ``_bandlimited`` / ``_unit_rms`` (signalgen.py:52-97);
-- ``sinc_shift`` (100-116), ``mix_at_snr`` (119-127), ``make_trial`` (130-147);
-- the per-trial seeding of ``_accuracy_trial`` (harness.py:238-257);
-- the float CCF: the radix-2 ``fft`` and ``ccf_fft_array`` (realxcorr.py:35-116).
+The reference runs one ``estimate`` per trial. Here the caller supplies the
+trials (``trial_fn(config, snr_idx, trial_idx) -> (x, y, true_lag)``, e.g.
+the restated reference generator in oracle/refport.py) and the float
+baseline (``baseline_fn(x, y) -> lags``); every quantised estimate of the
+whole SNR grid then runs as ONE ``estimate_batch`` launch on the device.
+Only the (rare) pairs whose peak ties take the exact per-pair path (GPU
+correlogram + float64 refinement at the tied lags, ``estimator.estimate``).
+Without a baseline_fn the "ccf_wo_quant" row is not scored (None).
 
 Parity: tests/golden/accuracy.json holds the reference's per-trial outcomes,
 rows and diagnostics for small configurations (tests/golden/make_golden_accuracy.py).
-Synthetic targets only (wav_dir is not supported: WAV ingestion is out of scope).
 """
 
 from __future__ import annotations
@@ -32,13 +28,11 @@ import numpy as np
 
 from . import _device as D
 from .batch import estimate_batch
-from .errors import DegenerateInput, DegenerateQuantization
-from .estimator import argmax_set, estimate
+from .errors import DegenerateQuantization
+from .estimator import estimate
 from .quantize import from_spec
-from .signals import Correlogram, Signal
 
-__all__ = ["AccuracyConfig", "AccuracyRow", "ACCURACY_MODES", "gen_target", "make_trial", "ccf_fft_array",
-           "run_accuracy", "accuracy_trials"]
+__all__ = ["AccuracyConfig", "AccuracyRow", "ACCURACY_MODES", "run_accuracy", "accuracy_trials"]
 
 ACCURACY_MODES = ("proposed", "proposed_until_line4", "ccf_wo_quant")  # harness.py:56
 
@@ -80,181 +74,23 @@ class AccuracyRow:
     accuracy: float
 
 
-# ------------------------------------------------------- trial generation
-
-
-def _bandlimited(rng: np.random.Generator, length: int, band) -> np.ndarray:
-    freqs = np.fft.rfftfreq(length)
-    mask = (freqs >= band[0]) & (freqs <= band[1])
-    if not mask.any():
-        raise ValueError(f"length {length} has no DFT bins inside band {band}")
-    spectrum = np.fft.rfft(rng.standard_normal(length)) * mask
-    return np.fft.irfft(spectrum, length)
-
-
-def _unit_rms(samples: np.ndarray) -> np.ndarray:
-    return samples / math.sqrt(np.mean(samples * samples))
-
-
-def gen_target(seed: int, length: int, kind: str = "white", *, band=(0.02, 0.2)) -> Signal:
-    """Deterministic unit-RMS test signal anchored at 0 (signalgen.py:65-97)."""
-    if length < 1:
-        raise ValueError("length must be >= 1")
-    rng = np.random.default_rng(seed)
-    if kind == "white":
-        samples = rng.standard_normal(length)
-    elif kind == "bandlimited":
-        samples = _bandlimited(rng, length, band)
-    elif kind == "am_bursts":
-        carrier = _bandlimited(rng, length, band)
-        envelope = np.zeros(length)
-        for _ in range(max(1, length // 512)):
-            width = max(3, int(round(rng.uniform(length / 16, length / 4))))
-            center = rng.uniform(0, length)
-            amp = rng.uniform(0.3, 1.0)
-            lo = int(round(center - width / 2))
-            bump = amp * np.hanning(width)
-            a, b = max(0, lo), min(length, lo + width)
-            if a < b:
-                envelope[a:b] += bump[a - lo:b - lo]
-        samples = carrier * envelope
-        if not samples.any():
-            samples = carrier
-    else:
-        raise ValueError(f"unknown target kind {kind!r}")
-    return Signal(0, _unit_rms(samples))
-
-
-def _window(s: Signal, start: int, length: int) -> np.ndarray:
-    out = np.zeros(length, dtype=s.samples.dtype)
-    lo, hi = max(start, s.start), min(start + length, s.start + len(s.samples))
-    if lo < hi:
-        out[lo - start:hi - start] = s.samples[lo - s.start:hi - s.start]
-    return out
-
-
-def _sinc_shift(s: Signal, d: float, half_width: int = 64) -> Signal:
-    """result[n] ~= s[n + d], Hann-windowed sinc (signalgen.py:100-116)."""
-    whole = math.floor(d)
-    frac = float(d) - whole
-    if frac == 0.0:
-        return Signal(s.start - int(whole), s.samples)
-    w = half_width
-    u = frac - np.arange(-w + 1, w + 1)
-    taps = np.sinc(u) * (0.5 + 0.5 * np.cos(np.pi * u / w))
-    return Signal(s.start - whole - w, np.convolve(s.samples, taps[::-1]))
-
-
-def _l2(s: Signal) -> float:
-    return math.sqrt(math.fsum(v * v for v in s.samples.tolist()))
-
-
-def _mix_at_snr(target: Signal, background: Signal, snr_db: float) -> Signal:
-    """target + g*background at the requested energy ratio (signalgen.py:119-127)."""
-    e_t, e_b = _l2(target) ** 2, _l2(background) ** 2
-    if e_t == 0.0 or e_b == 0.0:
-        raise DegenerateInput("cannot set an SNR against an all-zero signal")
-    g = math.sqrt((e_t / len(target.samples)) / (e_b / len(background.samples))) * 10.0 ** (-snr_db / 20.0)
-    lo = min(target.start, background.start)
-    hi = max(target.start + len(target.samples), background.start + len(background.samples)) - 1
-    out = np.zeros(hi - lo + 1, dtype=np.float64)
-    out[target.start - lo:target.start - lo + len(target.samples)] += target.samples
-    out[background.start - lo:background.start - lo + len(background.samples)] += background.samples * g
-    return Signal(lo, out)
-
-
-def make_trial(target: Signal, background: Signal, true_delay: float, snr_db: float, scene_len: int):
-    """(x = scene, y = target, true lag) (signalgen.py:130-147)."""
-    if len(background.samples) < scene_len:
-        raise DegenerateInput("background is shorter than the scene")
-    placed = _sinc_shift(target, -true_delay)
-    scene_bg = Signal(0, _window(background, 0, scene_len))
-    mixed = _mix_at_snr(placed, scene_bg, snr_db)
-    return Signal(0, _window(mixed, 0, scene_len)), target, -float(true_delay)
-
-
-def _trial(config: AccuracyConfig, snr_idx: int, trial_idx: int):
-    """The seeded draws of _accuracy_trial (harness.py:238-257)."""
-    rng = np.random.default_rng(np.random.SeedSequence([config.seed, snr_idx, trial_idx]))
-    delay = float(rng.uniform(0.0, config.scene_len - config.target_len))
-    target_seed = int(rng.integers(0, 2**63))
-    background_seed = int(rng.integers(0, 2**63))
-    background = gen_target(background_seed, config.scene_len, config.background_kind)
-    target = gen_target(target_seed, config.target_len, config.target_kind)
-    return make_trial(target, background, delay, config.snr_db_list[snr_idx], config.scene_len)
-
-
-# ------------------------------------------------------------ float CCF
-
-
-def _bit_reverse_indices(n: int) -> np.ndarray:
-    bits = n.bit_length() - 1
-    idx = np.arange(n)
-    rev = np.zeros(n, dtype=np.int64)
-    for _ in range(bits):
-        rev = (rev << 1) | (idx & 1)
-        idx >>= 1
-    return rev
-
-
-def _fft(values: np.ndarray, inverse: bool = False) -> np.ndarray:
-    """Iterative radix-2 DFT (realxcorr.py:46-88)."""
-    a = np.asarray(values)
-    n = a.shape[0]
-    cdtype = np.complex64 if a.dtype in (np.float32, np.complex64) else np.complex128
-    out = a.astype(cdtype)[_bit_reverse_indices(n)]
-    m = 2
-    while m <= n:
-        half = m // 2
-        ang = (2j if inverse else -2j) * np.pi / m
-        twiddle = np.exp(ang * np.arange(half)).astype(cdtype)
-        blocks = out.reshape(-1, m)
-        lo = blocks[:, :half].copy()
-        hi = blocks[:, half:] * twiddle
-        blocks[:, :half] = lo + hi
-        blocks[:, half:] = lo - hi
-        m *= 2
-    if inverse:
-        out /= n
-    return out
-
-
-def ccf_fft_array(xs: np.ndarray, ys: np.ndarray) -> np.ndarray:
-    """Full-overlap float CCF via zero-padded spectra (realxcorr.py:99-116)."""
-    n_x, n_y = len(xs), len(ys)
-    count = n_x + n_y - 1
-    padded = 1 << (count - 1).bit_length()
-    dtype = xs.dtype if xs.dtype == np.float32 else np.float64
-    x_pad = np.zeros(padded, dtype=dtype)
-    y_pad = np.zeros(padded, dtype=dtype)
-    x_pad[:n_x] = xs
-    y_pad[:n_y] = ys
-    circ = _fft(np.conj(_fft(x_pad)) * _fft(y_pad), inverse=True).real
-    return circ[(np.arange(count) - (n_x - 1)) % padded].astype(dtype)
-
-
-def _baseline_lags(x: Signal, y: Signal) -> list[int]:
-    """estimate_real(x, y, "fft").lags (estimator.py:104-117)."""
-    if not x.samples.any() or not y.samples.any():
-        raise DegenerateInput("all-zero signal")
-    first = y.start - (x.start + len(x.samples) - 1)
-    return argmax_set(Correlogram(first, ccf_fft_array(x.samples, y.samples)))
-
-
 # ---------------------------------------------------------------- driver
 
 
-def accuracy_trials(config: AccuracyConfig, *, device=None):
+def accuracy_trials(config: AccuracyConfig, trial_fn, baseline_fn=None, *, device=None):
     """Per (snr_idx, trial_idx): (ok_proposed, ok_raw, ok_baseline,
     tie_changed, errored), as _accuracy_trial returns (harness.py:238-280).
-    All quantised estimates of the grid run as one GPU batch."""
+    ``trial_fn(config, snr_idx, trial_idx) -> (x, y, true_lag)`` supplies the
+    trials; ``baseline_fn(x, y) -> lags`` the float baseline (ok_baseline is
+    None without it).  All quantised estimates of the grid run as one GPU
+    batch."""
     t = D.torch()
     q = from_spec(config.quantizer_spec)
     keys, xs, ys, truths, out = [], [], [], [], {}
     for si in range(len(config.snr_db_list)):
         for ti in range(config.trials):
             try:
-                x, y, nu = _trial(config, si, ti)
+                x, y, nu = trial_fn(config, si, ti)
             except Exception:
                 out[(si, ti)] = (False, False, False, False, True)
                 continue
@@ -279,7 +115,7 @@ def accuracy_trials(config: AccuracyConfig, *, device=None):
                 e = estimate(x, y, q, q, config.method)
                 lags = e.lags
                 raw = tuple(lag for lag, _ in e.tie_break_values) if e.tie_broken else e.lags
-            base = _baseline_lags(x, y)
+            base = baseline_fn(x, y) if baseline_fn is not None else None
         except Exception:
             out[key] = (False, False, False, False, True)
             continue
@@ -287,13 +123,16 @@ def accuracy_trials(config: AccuracyConfig, *, device=None):
         def close(ls):
             return all(abs(lag - nu) < 1.0 for lag in ls)
 
-        out[key] = (close(lags), close(raw), close(base), tuple(lags) != tuple(raw), False)
+        out[key] = (close(lags), close(raw), close(base) if base is not None else None, tuple(lags) != tuple(raw),
+                    False)
     return out
 
 
-def run_accuracy(config: AccuracyConfig, *, device=None) -> tuple[list[AccuracyRow], dict]:
-    """The reference's run_accuracy rows and diagnostics (harness.py:283-327)."""
-    trials = accuracy_trials(config, device=device)
+def run_accuracy(config: AccuracyConfig, trial_fn, baseline_fn=None, *,
+                 device=None) -> tuple[list[AccuracyRow], dict]:
+    """The reference's run_accuracy rows and diagnostics (harness.py:283-327)
+    over caller-supplied trials (see accuracy_trials)."""
+    trials = accuracy_trials(config, trial_fn, baseline_fn, device=device)
     rows: list[AccuracyRow] = []
     tie_changed_fraction: dict[float, float] = {}
     trial_errors = 0
@@ -304,10 +143,12 @@ def run_accuracy(config: AccuracyConfig, *, device=None) -> tuple[list[AccuracyR
             okp, okr, okb, tie_changed, errored = trials[(si, ti)]
             correct[0] += okp
             correct[1] += okr
-            correct[2] += okb
+            correct[2] += bool(okb)
             changed += tie_changed
             trial_errors += errored
         for mode, n in zip(ACCURACY_MODES, correct):
+            if mode == "ccf_wo_quant" and baseline_fn is None:
+                continue
             rows.append(AccuracyRow(float(snr), config.quantizer_spec, mode, config.trials, int(n),
                                     n / config.trials))
         tie_changed_fraction[float(snr)] = changed / config.trials

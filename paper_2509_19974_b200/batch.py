@@ -20,7 +20,7 @@ from ._call import call, raise_for
 from .quantize import native_quantizer
 
 __all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host",
-           "check_results", "template_search"]
+           "check_results", "template_search", "template_search_summary"]
 
 
 @dataclass
@@ -178,21 +178,12 @@ def estimate_sweep_host(x: np.ndarray, y: np.ndarray, quantizers, *, lag_lo=None
     return res
 
 
-def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
-                    path: str = "auto") -> tuple[int, int, int]:
-    """Peak summary (value, smallest lag, ties) of estimate(x=template, y=stream)
-    over the VALID lags (template fully inside the stream):
-    lag in [stream_start, stream_start + len(stream) - len(template)].
-
-    One C-ABI call (qx_template_search): the valid-lag range is cut into
-    blocks of `block` lags (default: the tensor-core tile, 8192 lags on the
-    fp4 mode / 4096 on the int8 one, else the largest one-transform NTT
-    block); block b correlates the template (a stride-0 row, never copied)
-    with the stream window [b*block, b*block + block + len(template) - 1)
-    (overlapping strided rows of the same buffer) and the per-block summaries
-    are merged on the device.  Each block's lags use only samples inside its
-    window, so the result equals the reference's argmax_set summary of the
-    full correlogram restricted to the valid lags (estimator.py:50-57)."""
+def template_search_summary(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
+                            path: str = "auto"):
+    """The device int64[8] summary of template_search (value, smallest lag,
+    ties, NaN seen, x all-zero, y all-zero in every block, a block failed,
+    its status), enqueued on the current stream and not inspected (the
+    multi-GPU reduction combines these before any exception is raised)."""
     t = D.torch()
     x = D.as_device(template).reshape(-1)
     y = D.as_device(stream).reshape(-1)
@@ -207,6 +198,24 @@ def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: i
     ctx = N.context(x.device.index)
     call(N.load().qx_template_search, ctx, ctypes.byref(sx), ctypes.byref(sy), ctypes.byref(nqx), ctypes.byref(nqy),
          0 if block is None else int(block), N.PATHS[path], out.data_ptr(), D.stream_handle())
+    return out
+
+
+def template_search(template, stream, qx, qy, *, stream_start: int = 0, block: int | None = None,
+                    path: str = "auto") -> tuple[int, int, int]:
+    """Peak summary (value, smallest lag, ties) of estimate(x=template, y=stream)
+    over the VALID lags (template fully inside the stream):
+    lag in [stream_start, stream_start + len(stream) - len(template)].
+
+    One C-ABI call (qx_template_search): the valid-lag range is cut into
+    blocks of `block` lags (default: the tensor-core tile, else the largest
+    one-transform NTT block); block b correlates the template (a stride-0
+    row, never copied) with the stream window [b*block, b*block + block +
+    len(template) - 1) and the per-block summaries are merged on the device.
+    Each block's lags use only samples inside its window, so the result
+    equals the reference's argmax_set summary of the full correlogram
+    restricted to the valid lags (estimator.py:50-57)."""
+    out = template_search_summary(template, stream, qx, qy, stream_start=stream_start, block=block, path=path)
     vmax, lmin, nties, nan, degx, degy, anybad, badst = out.cpu().tolist()
     if nan:
         raise ValueError("input contains NaN")

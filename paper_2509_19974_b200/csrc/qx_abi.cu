@@ -29,6 +29,9 @@ cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s);
 bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t merge_blocks_launch(const MergeSegs& segs, long long lag_shift, void* partials, int* counter,
                                 long long* out, int sms, cudaStream_t s);
+const char* summary_allreduce(void* comm, long long* summary, long long* scratch, cudaStream_t s);
+const char* records_allgather(void* comm, const void* mine, size_t bytes, void* out, cudaStream_t s);
+const char* comm_rank_size(void* comm, int* rank, int* size);
 }  // namespace qx
 
 using namespace qx;
@@ -143,6 +146,7 @@ struct qx_context {
     Arena stage;       // host-API staging (x, y, results)
     Arena records;     // template search: per-block results, merge partials
     Arena mcounter;    // template search: merge counter (zeroed once, reset by the kernel)
+    Arena dist;        // multi-GPU summary reduction scratch (16 int64)
     cudaStream_t host_stream = nullptr;
     cudaStream_t copy_stream = nullptr;   // H2D of the sweep entry point
     std::vector<cudaEvent_t> chunk_ev;    // per staged chunk (lazily created)
@@ -273,7 +277,7 @@ void qx_context_destroy(qx_context* c)
     if (c->last_ev) cudaEventDestroy(c->last_ev);
     for (auto& kv : c->tables) cudaFree(kv.second.second);
     for (auto& kv : c->otables) cudaFree(kv.second.second);
-    for (Arena* a : {&c->scratch, &c->counters, &c->stage, &c->records, &c->mcounter})
+    for (Arena* a : {&c->scratch, &c->counters, &c->stage, &c->records, &c->mcounter, &c->dist})
         if (a->ptr) cudaFree(a->ptr);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1118,6 +1122,70 @@ qx_status qx_estimate_sweep_host(qx_context* ctx, const qx_signals* x, const qx_
     for (int64_t i = 0; i < nq * batch; ++i)
         if (results[i].status) return (qx_status)results[i].status;
     return QX_OK;
+}
+
+// ---------------------------------------------------------------- multi-GPU
+
+qx_status qx_summary_reduce_nccl(qx_context* ctx, int64_t* summary, void* comm, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!summary || !comm) return fail(ctx, QX_ERR_INVALID, "summary/comm is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    cudaError_t e = arena_reserve(ctx->dist, 16 * 8, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "dist scratch");
+    if (const char* why = summary_allreduce(comm, (long long*)summary, (long long*)ctx->dist.ptr, (cudaStream_t)stream))
+        return fail(ctx, QX_ERR_CUDA, std::string("summary reduction: ") + why);
+    return QX_OK;
+}
+
+qx_status qx_template_search_nccl(qx_context* ctx, const qx_signals* tpl, const qx_signals* sig, const qx_quantizer* qx_,
+                                  const qx_quantizer* qy_, int64_t block, qx_path path, void* comm, int64_t* summary,
+                                  void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!summary || !comm) return fail(ctx, QX_ERR_INVALID, "summary/comm is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    qx_status st;
+    if ((st = check_signals(ctx, tpl, "template")) != QX_OK) return st;
+    if (!sig || sig->n < 0) return fail(ctx, QX_ERR_INVALID, "stream is NULL");
+    if (sig->n >= tpl->n) {
+        st = qx_template_search(ctx, tpl, sig, qx_, qy_, block, path, summary, stream);
+        if (st != QX_OK) return st;
+    } else {
+        // this rank's slice holds no valid lag: an empty summary (ties = 0,
+        // y all-zero so the AND over ranks ignores it) joins the reduction
+        static const int64_t empty[8] = {0, 0, 0, 0, 0, 1, 0, 0};
+        cudaError_t e = cudaMemcpyAsync(summary, empty, sizeof(empty), cudaMemcpyHostToDevice, (cudaStream_t)stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);  // `empty` is pageable
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "empty summary");
+    }
+    return qx_summary_reduce_nccl(ctx, summary, comm, stream);
+}
+
+qx_status qx_estimate_batch_nccl(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                                 const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
+                                 qx_path path, qx_result* results, void* comm, qx_result* all, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    if (!results || !comm) return fail(ctx, QX_ERR_INVALID, "results/comm is NULL");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    qx_status st = qx_estimate_batch(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, path, results, stream);
+    if (st != QX_OK || !all) return st;
+    if (const char* why = records_allgather(comm, results, (size_t)batch * sizeof(qx_result), all, (cudaStream_t)stream))
+        return fail(ctx, QX_ERR_CUDA, std::string("result gather: ") + why);
+    return QX_OK;
+}
+
+qx_status qx_comm_rank_size(void* comm, int* rank, int* size)
+{
+    if (!comm || !rank || !size) return QX_ERR_INVALID;
+    return comm_rank_size(comm, rank, size) ? QX_ERR_CUDA : QX_OK;
 }
 
 }  // extern "C"

@@ -20,9 +20,10 @@ from . import _native as N
 from .batch import estimate_batch
 from .errors import DegenerateQuantization
 from .intxcorr import xcorr_full_device
-from .realxcorr import xcorr_real_at
+from .errors import DegenerateInput
+from .realxcorr import xcorr_real_at, xcorr_real_bf, xcorr_real_fft
 
-__all__ = ["EstimationResult", "argmax_set", "estimate", "METHODS"]
+__all__ = ["EstimationResult", "argmax_set", "estimate", "estimate_real", "METHODS"]
 
 METHODS = ("ks", "bf", "gpu")
 
@@ -93,3 +94,19 @@ def estimate(x, y, qx, qy, method: str = "ks", *, refine_ties: bool = True,
         survivors = tuple(lag for lag, val in zip(lags, real_values) if val == best)
         return EstimationResult(survivors, peak, True, pairs, method)
     return EstimationResult(tuple(lags), peak, False, (), method)
+
+
+def estimate_real(x, y, method: str = "fft") -> EstimationResult:
+    """The unquantised baseline: argmax set of the real correlation
+    (estimator.py:104-117), same exceptions and result fields."""
+    if not np.asarray(x.samples).any():
+        raise DegenerateInput("x is all-zero")
+    if not np.asarray(y.samples).any():
+        raise DegenerateInput("y is all-zero")
+    if method == "fft":
+        c = xcorr_real_fft(x, y)
+    elif method == "bf":
+        c = xcorr_real_bf(x, y)
+    else:
+        raise ValueError(f"unknown real correlation method {method!r}")
+    return EstimationResult(tuple(argmax_set(c)), float(c.values.max()), False, (), f"real_{method}")

@@ -15,18 +15,19 @@ from __future__ import annotations
 
 import ctypes
 import math
+from dataclasses import dataclass
 
 import numpy as np
 
 from . import _device as D
 from . import _native as N
 from ._call import call
-from .errors import DegenerateInput
+from .errors import DegenerateInput, InternalOverflow
 from .quantize import native_quantizer
-from .signals import Correlogram
+from .signals import Correlogram, l2_norm
 
 __all__ = ["xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "MAX_COEFF_BOUND", "xcorr_full_device", "big_mul",
-           "MUL_BACKENDS"]
+           "MUL_BACKENDS", "KSPlan", "plan_ks", "pack", "unpack_and_correct"]
 
 MAX_COEFF_BOUND = 1 << 59  # intxcorr.py:50
 # intxcorr.py:52 plus "cuda"; "auto" takes "cuda" from CUDA_MIN_BITS up
@@ -143,3 +144,106 @@ def big_mul(a: int, b: int, backend: str = "auto") -> int:
     if a == 0 or b == 0:
         return 0
     return sign * _big_mul_cuda(a, b)
+
+
+# ------------------------------------------------ Kronecker substitution (host)
+# The reference's KS plumbing (intxcorr.py:55-142, 208-256) with the same
+# names, plan and exceptions, for callers that drive it step by step
+# (pack -> big_mul -> unpack_and_correct).  The engine itself never packs:
+# its exact NTT correlation replaces the packed product,
+# and big_mul "cuda" multiplies packed naturals on the GPU.  Packing and slot
+# extraction here are vectorised bit-plane operations (numpy packbits), not
+# per-slot Python loops.
+
+
+@dataclass(frozen=True)
+class KSPlan:
+    """Slot width L and biases of one Kronecker correlation (intxcorr.py:55-82):
+    2^L > 4 * n_min * k_u * k_v, so biased slots never collide."""
+
+    slot_bits: int
+    n_min: int
+    k_u: int
+    k_v: int
+
+    def __post_init__(self):
+        if self.slot_bits < 1:
+            raise ValueError("slot_bits must be >= 1")
+        if (1 << self.slot_bits) <= 4 * self.n_min * self.k_u * self.k_v:
+            raise ValueError("slot width too narrow for biased coefficients")
+
+    @property
+    def bias_u(self) -> int:
+        return self.k_u
+
+    @property
+    def bias_v(self) -> int:
+        return self.k_v
+
+    @property
+    def coeff_bound(self) -> int:
+        return self.n_min * self.k_u * self.k_v
+
+
+def plan_ks(u, v) -> KSPlan:
+    """L = floor(log2(N_min K_u K_v)) + 3 (intxcorr.py:103-115)."""
+    if not np.asarray(u.samples).any() or not np.asarray(v.samples).any():
+        raise DegenerateInput("cannot plan a Kronecker correlation for an all-zero signal")
+    n_min = min(len(u.samples), len(v.samples))
+    _check_coeff_bound(n_min, int(u.bound), int(v.bound))
+    return KSPlan(slot_bits=(n_min * int(u.bound) * int(v.bound)).bit_length() + 2, n_min=n_min,
+                  k_u=int(u.bound), k_v=int(v.bound))
+
+
+def _slots_to_int(vals: np.ndarray, L: int) -> int:
+    """sum_n vals[n] * 2^(L n) for 0 <= vals < 2^L: the L low bits of every
+    value laid end to end, little-endian."""
+    if vals.size == 0:
+        return 0
+    bits = ((vals.astype(np.uint64)[:, None] >> np.arange(L, dtype=np.uint64)[None, :]) & np.uint64(1)).astype(np.uint8)
+    return int.from_bytes(np.packbits(bits.reshape(-1), bitorder="little").tobytes(), "little")
+
+
+def _int_to_slots(p: int, L: int, count: int) -> np.ndarray:
+    """count L-bit slots of the natural p (the inverse of _slots_to_int)."""
+    nbytes = (L * count + 7) // 8
+    raw = np.frombuffer(p.to_bytes(max(nbytes, (p.bit_length() + 7) // 8), "little")[:nbytes], dtype=np.uint8)
+    bits = np.unpackbits(raw, bitorder="little")[:L * count].reshape(count, L).astype(np.uint64)
+    return (bits << np.arange(L, dtype=np.uint64)[None, :]).sum(axis=1).astype(np.int64)
+
+
+def pack(w, plan: KSPlan, *, bias: int) -> int:
+    """sum_n (w[n] + bias) * 2^(L n) as one natural (intxcorr.py:133-142);
+    InternalOverflow when a biased coefficient leaves [0, 2^L)."""
+    shifted = np.asarray(w.samples, dtype=np.int64) + np.int64(bias)
+    if shifted.size and (int(shifted.min()) < 0 or int(shifted.max()) >> plan.slot_bits):
+        raise InternalOverflow("biased coefficient does not fit its slot")
+    if plan.slot_bits > 63:
+        return sum(int(x) << (plan.slot_bits * i) for i, x in enumerate(shifted.tolist()))
+    return _slots_to_int(shifted, plan.slot_bits)
+
+
+def unpack_and_correct(p: int, plan: KSPlan, u, v) -> Correlogram:
+    """The exact signed correlation from the packed product of
+    (reverse(u) + B_u) and (v + B_v) (intxcorr.py:226-256): the slots minus
+    the three bias cross terms (window sums by prefix sums); InternalOverflow
+    if a value exceeds N_min K_u K_v."""
+    nu, nv = len(u.samples), len(v.samples)
+    count = nu + nv - 1
+    if plan.slot_bits > 63:
+        mask = (1 << plan.slot_bits) - 1
+        slots = np.array([(p >> (plan.slot_bits * n)) & mask for n in range(count)], dtype=object)
+    else:
+        slots = _int_to_slots(p, plan.slot_bits, count)
+    cu = np.concatenate(([0], np.cumsum(np.asarray(u.samples, dtype=np.int64)[::-1])))
+    cv = np.concatenate(([0], np.cumsum(np.asarray(v.samples, dtype=np.int64))))
+    t = np.arange(count)
+    ilo, ihi = np.maximum(0, t - nv + 1), np.minimum(nu - 1, t)
+    jlo, jhi = np.maximum(0, t - nu + 1), np.minimum(nv - 1, t)
+    values = (slots - plan.bias_v * (cu[ihi + 1] - cu[ilo]) - plan.bias_u * (cv[jhi + 1] - cv[jlo])
+              - plan.bias_u * plan.bias_v * (ihi - ilo + 1))
+    values = np.asarray(values, dtype=np.int64)
+    if int(np.abs(values).max()) > plan.coeff_bound:
+        raise InternalOverflow("corrected coefficient exceeds N_min*K_u*K_v")
+    first_lag = int(v.start) - (int(u.start) + nu - 1)
+    return Correlogram(first_lag, values, norm_x=l2_norm(u), norm_y=l2_norm(v))

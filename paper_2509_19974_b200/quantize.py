@@ -19,8 +19,8 @@ from . import _device as D
 from . import _native as N
 from .signals import IntSignal, Signal
 
-__all__ = ["Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "native_quantizer",
-           "thresholds"]
+__all__ = ["Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "random_monotone",
+           "native_quantizer", "thresholds"]
 
 
 @dataclass(frozen=True)
@@ -88,6 +88,21 @@ def from_spec(text: str) -> Quantizer:
         except ValueError as exc:
             raise ValueError(f"bad uniform quantizer spec {text!r}: {exc}") from exc
     raise ValueError(f"unknown quantizer spec {text!r} (expected 'sign' or 'uniform:K:STEP')")
+
+
+def random_monotone(seed: int, k: int, levels: int | None = None, scale: float = 1.0) -> Quantizer:
+    """Seeded random custom staircase for property tests (quantize.py:110-131):
+    depth d (drawn in [1, k], or (levels - 1) // 2 capped to [1, k]), 2d
+    strictly increasing thresholds spanning ~[-scale, scale] with 0 inside the
+    middle step.  Same draws in the same order as the reference, so a seed
+    gives the reference's quantiser."""
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    rng = np.random.default_rng(seed)
+    d = int(rng.integers(1, k + 1)) if levels is None else max(1, min(k, (levels - 1) // 2))
+    edges = np.cumsum(rng.uniform(0.05, 1.0, size=2 * d))
+    edges = edges / edges[-1] * 2.0 * scale  # (this float operation order keeps the thresholds bit-identical)
+    return custom(edges - rng.uniform(edges[d - 1], edges[d]))
 
 
 _KIND = {"sign": N.QX_Q_SIGN, "uniform": N.QX_Q_UNIFORM, "custom": N.QX_Q_CUSTOM}

@@ -636,16 +636,19 @@ def test_template_search_random_modes_and_errors(qx, oracle, monkeypatch):
         qx.template_search(np.zeros(1024, np.float32), st, qx.sign(), qx.sign())
 
 
-def test_sharded_template_search_over_nccl(qx):
-    """The multi-GPU template search (parallel.template_search_sharded: stream
-    shard + halo per rank, one all_gather of the (value, lag, ties) summary)
-    on a real NCCL process group (one rank on this GPU) equals the
-    single-call template search; the 2-rank logic itself is gloo-tested."""
+def test_sharded_paths_over_nccl(qx):
+    """The multi-GPU entry points on a real NCCL process group (one rank on
+    this GPU; the 2-rank protocol itself is gloo-tested on the CPU and on
+    this GPU in test_multigpu_gpu.py): qx_template_search_nccl (via
+    parallel.template_search_sharded) equals the single-call template search;
+    qx_summary_reduce_nccl keeps a summary; qx_estimate_batch_nccl gathers
+    the records of estimate_batch."""
     import socket
 
     import torch
     import torch.distributed as dist
 
+    from paper_2509_19974_b200 import _native as N
     from paper_2509_19974_b200 import parallel as PL
 
     sock = socket.socket()
@@ -660,10 +663,19 @@ def test_sharded_template_search_over_nccl(qx):
         tpl = st[31337:31337 + 1024].copy()
         st = st + rng.normal(0, 0.8, st.size).astype(np.float32)
         q = qx.sign()
-        got = PL.template_search_sharded(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q,
-                                         device=torch.device("cuda", 0))
-        assert got == qx.template_search(tpl, st, q, q) and got[1] == 31337
-        assert dist.get_backend() == "nccl"
+        with N.profile(timed=False) as prof:
+            got = PL.template_search_sharded(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q,
+                                             stream_start=-5)
+        assert got == qx.template_search(tpl, st, q, q, stream_start=-5) and got[1] == 31337 - 5
+        assert dist.get_backend() == "nccl" and prof.launches >= 2
+        s = torch.tensor([17, -3, 2, 0, 1, 0, 0, 0], dtype=torch.int64, device="cuda")
+        assert PL.reduce_summary(s).tolist() == [17, -3, 2, 0, 1, 0, 0, 0]
+        xs = torch.from_numpy(rng.standard_normal((8, 4096)).astype(np.float32)).cuda()
+        ys = torch.roll(xs, 100, dims=1) + 0.1
+        qu = qx.uniform(7, 0.4)
+        mine, allr = PL.estimate_batch_sharded(xs, ys, qu, qu, lag_lo=-512, lag_hi=512)
+        want = qx.estimate_batch(xs, ys, qu, qu, lag_lo=-512, lag_hi=512).raw
+        assert torch.equal(mine.raw, want) and torch.equal(allr, want)
     finally:
         dist.destroy_process_group()
 

@@ -28,6 +28,15 @@ def test_merge_peaks_semantics():
         PL.merge_peaks([(1, 1, 0)])
 
 
+def test_merge_summaries_semantics():
+    e = PL.SUMMARY_EMPTY
+    assert PL.merge_summaries([(5, 10, 1, 0, 0, 0, 0, 0), (7, 30, 2, 1, 0, 0, 0, 0), (7, 20, 1, 0, 0, 1, 0, 0)]) == \
+        (7, 20, 3, 1, 0, 0, 0, 0)
+    assert PL.merge_summaries([e, (-4, -9, 2, 0, 1, 1, 0, 0)]) == (-4, -9, 2, 0, 1, 1, 0, 0)
+    assert PL.merge_summaries([e, e]) == (0, 0, 0, 0, 0, 1, 0, 0)
+    assert PL.merge_summaries([(3, 1, 1, 0, 0, 1, 1, 7), (3, 0, 1, 0, 0, 1, 1, 5)]) == (3, 0, 2, 0, 0, 1, 1, 7)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -95,3 +104,52 @@ def test_template_search_two_ranks_matches_unsharded():
     m, f, n = O.argmax(c)
     assert got[0] == got[1] == (m, f, n)
     assert f == 1234
+
+
+def _reduce_worker(rank, world, port, cases, out):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    got = []
+    for case in cases:
+        s = torch.tensor(case[rank], dtype=torch.int64)
+        got.append(tuple(PL.reduce_summary(s).tolist()))
+    out.put((rank, got))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_summary_reduction_protocol(world):
+    """The two-round summary reduction (the device protocol of qx_dist.cu,
+    here through gloo) equals merge_summaries on random per-rank summaries:
+    negative and int64-extreme values, ties across ranks, empty shards and
+    every flag."""
+    rng = np.random.default_rng(world)
+    cases = []
+    for trial in range(40):
+        ranks = []
+        for r in range(world):
+            if rng.random() < 0.2:
+                ranks.append(PL.SUMMARY_EMPTY)
+                continue
+            v = int(rng.choice([-(1 << 62), -5, 0, 3, 7, (1 << 62)])) if trial % 2 else int(rng.integers(0, 3))
+            lag = int(rng.integers(-(1 << 40), 1 << 40))
+            ranks.append((v, lag, int(rng.integers(1, 4)), int(rng.random() < 0.1), int(rng.random() < 0.1),
+                          int(rng.random() < 0.5), int(rng.random() < 0.1), int(rng.integers(0, 8))))
+        cases.append(ranks)
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reduce_worker, args=(r, world, port, cases, out)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = dict(out.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i, ranks in enumerate(cases):
+        want = PL.merge_summaries(ranks)
+        assert all(got[r][i] == want for r in range(world)), (i, ranks, [got[r][i] for r in range(world)], want)

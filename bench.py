@@ -7,7 +7,7 @@ synthetic data with BASELINE's shapes and statistics (workloads.c2); they are
 resident in HBM before timing (`value`) or copied from pinned host memory
 inside the timed region through the C ABI's host entry point (`e2e`).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 
 Under torchrun every rank processes its own 64-pair batch (weak scaling; the
 pairs are independent, so there is no data-path collective); the timed region
@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"],
+                    help="BASELINE config (default c2, the headline; the others: tools/bench_run.py)")
     ap.add_argument("--pairs", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -148,6 +150,13 @@ def cpu_arm(pairs_sample, threads, xs, ys, min_seconds=0.0):
     return n_est / dt, dt, passes
 
 
+def _cpu_info():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import cpu_baselines
+
+    return cpu_baselines.cpu_info()
+
+
 def reference_arm(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -155,7 +164,7 @@ def reference_arm(args):
     from paper_2509_19974_b200 import workloads as W
 
     threads = os.cpu_count() or 1
-    sample = max(1, min(args.pairs, 2 * threads))
+    sample = args.pairs  # the same 64-pair, 4-depth workload as the GPU arm's step
     xs, ys, lag = W.c2(pairs=sample)
     times = []
     for i in range(args.warmup + args.steps):
@@ -169,8 +178,9 @@ def reference_arm(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (seeded, BASELINE config 2 shapes)",
             "config": config_desc(sample, 1) | {"sample": f"{sample} pairs x 4 bit depths per step"},
+            "same_config": True,
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{sample} pairs x {len(BITS)} bit depths of config 2 per step"},
+                             "sample": f"{sample} pairs x {len(BITS)} bit depths of config 2 per step"} | _cpu_info(),
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -178,6 +188,11 @@ def reference_arm(args):
 # ------------------------------------------------------------------ GPU arm
 def main():
     args = parse()
+    if args.config != "c2":
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_run
+
+        return bench_run.run_reference(args) if args.impl == "reference" else bench_run.run(args)
     if args.impl == "reference":
         return reference_arm(args)
     import torch
@@ -341,6 +356,16 @@ def main():
             for _ in range(n_e2e):
                 P.estimate_sweep_host(hxn, hyn, sweep, device=local)
             comp_s = (time.perf_counter() - tb) / n_e2e
+        # the same call from PAGEABLE numpy arrays (what a reference caller using
+        # INTEGRATION.md section 3 passes): the driver stages them synchronously
+        xs_pg, ys_pg = np.array(xs, copy=True), np.array(ys, copy=True)
+        P.estimate_sweep_host(xs_pg, ys_pg, sweep, device=local)
+        tb = time.perf_counter()
+        for _ in range(n_e2e):
+            rp = P.estimate_sweep_host(xs_pg, ys_pg, sweep, device=local)
+        pageable_s = (time.perf_counter() - tb) / n_e2e
+        for bi, r in enumerate(rp):
+            G.check_c2(bi, rank * pairs, r)
         e2e_val = est_per_step * n_e2e / float(e2e_s.item())
         e2e = {"value": e2e_val, "unit": UNIT,
                "call_ms": {"median": 1e3 * statistics.median(call_s), "min": 1e3 * min(call_s),
@@ -349,6 +374,8 @@ def main():
                "copy_only_ms": 1e3 * h2d_s, "compute_only_ms": 1e3 * comp_s,
                "h2d_bound": {"value": est_per_step / h2d_s, "frac": e2e_val / (est_per_step / h2d_s),
                              "what": "estimates/s if each step cost only its copies (the same call, kernels skipped)"},
+               "pageable": {"value": est_per_step / pageable_s, "call_ms": 1e3 * pageable_s,
+                            "what": "the same call from pageable numpy arrays (no pinning by the caller)"},
                "h2d_bytes_per_step": int(xs.nbytes + ys.nbytes),
                "d2h_bytes_per_step": int(len(BITS) * pairs * 64), "steps": n_e2e, "warmup_calls": E2E_WARM,
                "path": "qx_estimate_sweep_host (C ABI, pinned host buffers; inputs staged once per step "
@@ -360,9 +387,16 @@ def main():
         threads = os.cpu_count() or 1
         sample = min(pairs, max(8, threads))
         rate, dt, passes = cpu_arm(sample, threads, xs, ys, min_seconds=10.0)
+        import cpu_baselines as CB
+
+        fft = CB.fft_pairs(xs, ys, threads, min_seconds=8.0, max_pairs=threads)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"{passes} passes over {sample} pairs x {len(BITS)} bit depths of config 2 ({dt:.1f} s): "
-                         "C oracle = reference algorithm (float64 quantise, KS + GMP mpn_mul, argmax)"}
+                         "C oracle = reference algorithm (float64 quantise, KS + GMP mpn_mul, argmax)",
+               "fft": {"value": fft["value"], "unit": UNIT, "cores": threads, "kind": "port",
+                       "sample": fft["sample"] + f" ({fft['seconds']:.1f} s): the reference's Real-FFT path "
+                                 "(realxcorr.py:99-116 restated in oracle/refport.py), one estimate per pair "
+                                 "(independent of the bit depth)"}} | CB.cpu_info()
 
     # the other BASELINE configs on this GPU (rank 0 of a single-GPU run):
     # each checked against its planted delay, failures reported, not fatal

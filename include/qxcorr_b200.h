@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define QX_ABI_VERSION 3
+#define QX_ABI_VERSION 4
 
 typedef enum qx_status {
     QX_OK = 0,
@@ -124,7 +124,8 @@ const char *qx_context_last_error(const qx_context *ctx);
  * "sweep_lanes", "sweep_chunks", "sweep_taper", "sweep_even",
  * "sweep_restage" (0: the host sweep skips its H2D copies -- compute-only
  * timing), "sweep_compute" (0: it skips its kernels -- copy-only timing),
- * "popc", "popc_fused", "tc_f4".  QX_ERR_INVALID for an unknown name.
+ * "popc", "popc_timing" (1: the popc correlation kernel prints its phase
+ * times), "tc_f4".  QX_ERR_INVALID for an unknown name.
  *
  * Threading and streams: every entry point locks the context, runs on the
  * context's device and restores the caller's current device.  Work enqueued
@@ -157,6 +158,23 @@ qx_status qx_estimate_batch(qx_context *ctx, const qx_signals *x, const qx_signa
                             int64_t batch, const qx_quantizer *qx, const qx_quantizer *qy,
                             int64_t lag_lo, int64_t lag_hi, qx_path path, qx_result *results,
                             void *stream);
+
+/* Prepared estimate_batch call (the low-latency form of qx_estimate_batch
+ * for repeated calls of one shape, e.g. BASELINE config 1 served pair after
+ * pair): qx_plan_create validates the shapes (x/y data may be NULL), builds
+ * the quantiser tables, picks the path and lays out the scratch once;
+ * qx_plan_run then takes only the row pointers (same shapes, dtypes, ld and
+ * start as at creation) and enqueues exactly what qx_estimate_batch would,
+ * with identical results.  A plan belongs to its context (destroy it first)
+ * and, like the context, is used by one thread at a time. */
+typedef struct qx_plan qx_plan;
+qx_status qx_plan_create(qx_context *ctx, const qx_signals *x, const qx_signals *y, int64_t batch,
+                         const qx_quantizer *qx, const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
+                         qx_path path, qx_plan **out);
+qx_status qx_plan_run(qx_plan *plan, const void *x, const void *y, qx_result *results, void *stream);
+/* the qx_path the plan runs (never QX_PATH_AUTO) */
+int qx_plan_path(const qx_plan *plan);
+void qx_plan_destroy(qx_plan *plan);
 
 /* As qx_estimate_batch, but x/y data and results are HOST pointers; the
  * library stages the inputs to the device, runs, copies results back and

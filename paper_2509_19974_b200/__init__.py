@@ -14,7 +14,7 @@ Batched, windowed and streaming entry points (new): ``estimate_batch``,
 """
 
 from . import accuracy, ingest, parallel
-from .batch import (BatchResult, check_results, estimate_batch, estimate_batch_host, estimate_sweep,
+from .batch import (BatchResult, EstimatePlan, check_results, estimate_batch, estimate_batch_host, estimate_sweep,
                     estimate_sweep_host, template_search)
 from .errors import (
     BadLength,
@@ -44,6 +44,6 @@ __all__ = [
     "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "xcorr_real_bf", "xcorr_real_fft", "big_mul",
     "MUL_BACKENDS",
     "EstimationResult", "argmax_set", "estimate", "estimate_real",
-    "BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host", "check_results", "template_search",
+    "BatchResult", "EstimatePlan", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host", "check_results", "template_search",
     "accuracy", "ingest", "parallel",
 ]

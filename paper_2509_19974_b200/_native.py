@@ -35,7 +35,7 @@ QX_F32, QX_F64, QX_I64 = 0, 1, 2
 QX_Q_SIGN, QX_Q_UNIFORM, QX_Q_CUSTOM, QX_Q_CODES = 0, 1, 2, 3
 PATHS = {"auto": 0, "ntt": 1, "direct": 2, "tc": 2, "popc": 3}
 PROFILE_KINDS = 10  # qxcorr_b200.h QX_PROFILE_KINDS
-ABI_VERSION = 3  # qxcorr_b200.h QX_ABI_VERSION
+ABI_VERSION = 4  # qxcorr_b200.h QX_ABI_VERSION
 
 RF_DEGENERATE_X = 1
 RF_DEGENERATE_Y = 2
@@ -80,7 +80,7 @@ EXPORTS = (
     "qx_profile_begin",
     "qx_profile_end",
     "qx_profile_kind_name", "qx_summary_reduce_nccl", "qx_template_search_nccl", "qx_estimate_batch_nccl",
-    "qx_comm_rank_size",
+    "qx_comm_rank_size", "qx_plan_create", "qx_plan_run", "qx_plan_path", "qx_plan_destroy",
 )
 
 _lib = None
@@ -138,6 +138,14 @@ def load():
         L.qx_estimate_batch_nccl.restype = st
         L.qx_comm_rank_size.argtypes = [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]
         L.qx_comm_rank_size.restype = st
+        L.qx_plan_create.argtypes = [vp, sp, sp, i64, qp, qp, i64, i64, st, ctypes.POINTER(vp)]
+        L.qx_plan_create.restype = st
+        L.qx_plan_run.argtypes = [vp, vp, vp, vp, vp]
+        L.qx_plan_run.restype = st
+        L.qx_plan_path.argtypes = [vp]
+        L.qx_plan_path.restype = ctypes.c_int
+        L.qx_plan_destroy.argtypes = [vp]
+        L.qx_plan_destroy.restype = None
         L.qx_decode_pcm16.argtypes = [vp, vp, i64, vp, vp]
         L.qx_decode_pcm16.restype = st
         L.qx_profile_begin.argtypes = [vp, ctypes.c_int]
@@ -181,7 +189,7 @@ def set_option(name: str, value: int, device: int | None = None) -> None:
 class option:
     """Context manager: set a context option, restore it on exit."""
 
-    DEFAULTS = {"sweep_restage": 1, "sweep_compute": 1, "popc": 1, "popc_fused": 1, "tc_f4": 1, "sweep_lanes": 0,
+    DEFAULTS = {"sweep_restage": 1, "sweep_compute": 1, "popc": 1, "popc_timing": 0, "tc_f4": 1, "sweep_lanes": 0,
                 "sweep_chunks": 0, "sweep_taper": 2, "sweep_even": 0, "chunk_pairs": 0}
 
     def __init__(self, name: str, value: int, device: int | None = None, restore: int | None = None):

@@ -19,8 +19,8 @@ from . import _native as N
 from ._call import call, raise_for
 from .quantize import native_quantizer
 
-__all__ = ["BatchResult", "estimate_batch", "estimate_batch_host", "estimate_sweep", "estimate_sweep_host",
-           "check_results", "template_search", "template_search_summary"]
+__all__ = ["BatchResult", "EstimatePlan", "estimate_batch", "estimate_batch_host", "estimate_sweep",
+           "estimate_sweep_host", "check_results", "template_search", "template_search_summary"]
 
 
 @dataclass
@@ -88,6 +88,69 @@ def estimate_batch(x, y, qx, qy, *, lag_lo=None, lag_hi=None, x_start=0, y_start
     call(N.load().qx_estimate_batch, ctx, ctypes.byref(sx), ctypes.byref(sy), batch, ctypes.byref(nqx),
          ctypes.byref(nqy), lo, hi, N.PATHS[path], raw.data_ptr(), D.stream_handle())
     return BatchResult(raw)
+
+
+class EstimatePlan:
+    """estimate_batch prepared once for repeated calls of one shape (the
+    low-latency form for serving pair after pair, e.g. BASELINE config 1):
+    validation, threshold tables, path choice and scratch layout happen at
+    construction (qx_plan_create); each call passes only the row pointers to
+    qx_plan_run and returns exactly what estimate_batch returns for the same
+    rows.  `x` and `y` at construction give the shapes, dtypes, row stride and
+    device (tensors or arrays; their data is not used)."""
+
+    def __init__(self, x, y, qx, qy, *, lag_lo=None, lag_hi=None, x_start=0, y_start=0, path="auto"):
+        t = D.torch()
+        x = D.as_device(x)
+        y = D.as_device(y)
+        if x.dim() == 1:
+            x = x.unsqueeze(0)
+        if y.dim() == 1:
+            y = y.unsqueeze(0)
+        if x.shape[0] != y.shape[0]:
+            raise ValueError("x and y must hold the same number of rows")
+        self.batch = x.shape[0]
+        self.device = x.device
+        # what every call must match: row length, dtype, row stride
+        self._chk = (x.shape[1], x.dtype, x.stride(0) if x.shape[0] > 1 else None,
+                     y.shape[1], y.dtype, y.stride(0) if y.shape[0] > 1 else None)
+        nqx, _ = native_quantizer(qx)
+        nqy, _ = native_quantizer(qy)
+        sx, sy = D.signals(x, x_start), D.signals(y, y_start)
+        lo, hi = _bounds(lag_lo, lag_hi)
+        self._ctx = N.context(self.device.index)
+        self._lib = N.load()
+        h = ctypes.c_void_p()
+        call(self._lib.qx_plan_create, self._ctx, ctypes.byref(sx), ctypes.byref(sy), self.batch,
+             ctypes.byref(nqx), ctypes.byref(nqy), lo, hi, N.PATHS[path], ctypes.byref(h))
+        self._h = h
+        self._run = self._lib.qx_plan_run
+        self._t = t
+        self.path = {v: k for k, v in N.PATHS.items() if k != "tc"}[self._lib.qx_plan_path(h)]
+
+    def __call__(self, x, y, out=None) -> BatchResult:
+        """Enqueue the estimate of rows `x`, `y` (CUDA tensors of the plan's
+        shapes, dtypes and row stride) on the current stream."""
+        nx, dx, lx, ny, dy, ly = self._chk
+        if x.shape[-1] != nx or y.shape[-1] != ny or x.dtype != dx or y.dtype != dy or not (x.is_cuda and y.is_cuda) \
+                or (lx is not None and x.stride(0) != lx) or (ly is not None and y.stride(0) != ly):
+            raise ValueError("rows do not match the plan's length / dtype / row stride, or are not CUDA tensors")
+        raw = out if out is not None else self._t.empty((self.batch, 8), dtype=self._t.int64, device=self.device)
+        st = self._run(self._h, x.data_ptr(), y.data_ptr(), raw.data_ptr(),
+                       self._t._C._cuda_getCurrentRawStream(self.device.index))
+        if st != N.QX_OK:
+            raise_for(st, self._lib.qx_context_last_error(self._ctx).decode() or
+                      self._lib.qx_status_string(st).decode())
+        return BatchResult(raw)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                self._lib.qx_plan_destroy(h)
+            except Exception:  # noqa: BLE001  (interpreter shutdown)
+                pass
+            self._h = None
 
 
 def estimate_sweep(x, y, quantizers, *, lag_lo=None, lag_hi=None, x_start=0, y_start=0, path="auto",

@@ -26,6 +26,8 @@ bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s);
 bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path);
 cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s);
+size_t popc_planes_words(int64_t batch, int64_t nx, int64_t ny);
+void popc_schedule(const NttCall& c, int64_t nx, int* G_out, std::vector<int>& out);
 bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t merge_blocks_launch(const MergeSegs& segs, long long lag_shift, void* partials, int* counter,
                                 long long* out, int sms, cudaStream_t s);
@@ -50,6 +52,7 @@ static const PrimeInfo kPrimes[] = {
 struct Arena {
     void* ptr = nullptr;
     size_t size = 0;
+    uint64_t gen = 0;  // bumped on every reallocation (plans re-derive their pointers)
 };
 
 namespace qx {
@@ -112,7 +115,7 @@ static Knobs knobs_from_env()
     k.sweep_restage = num("QX_SWEEP_RESTAGE", 1) != 0;
     k.sweep_compute = num("QX_SWEEP_COMPUTE", 1) != 0;
     k.popc = num("QX_POPC", 1) != 0;
-    k.popc_fused = num("QX_POPC_FUSED", 1) != 0;
+    k.popc_timing = num("QX_POPC_TIMING", 0) != 0;
     k.tc_f4 = num("QX_TC_F4", 1) != 0;
     if (const char* ev = getenv("QX_SWEEP_PLAN")) {
         for (const char* p = ev; *p && k.sweep_plan_n < 16;) {
@@ -141,6 +144,8 @@ struct qx_context {
     std::map<std::pair<uint32_t, int>, std::pair<NttTables, void*>> tables;
     std::map<std::pair<uint32_t, int>, std::pair<OuterTables, void*>> otables;
     std::map<std::string, std::vector<double>> thr_cache;
+    // popc path: per-shape CTA schedules (device int[G + 1]) and their G
+    std::map<std::tuple<int64_t, int64_t, int64_t, int64_t, int64_t>, std::pair<void*, int>> popc_sched;
     Arena scratch;     // Y/R/stats/partials
     Arena counters;    // zero-initialised ints, reset by the kernels
     Arena stage;       // host-API staging (x, y, results)
@@ -164,10 +169,25 @@ struct qx_context {
     cudaEvent_t last_ev = nullptr;
 };
 
+// The ordering event is recorded lazily, on the previous stream, only when a
+// call arrives on a different one: it then covers everything enqueued there
+// so far (a superset of the previous call's work), and same-stream calls --
+// the common case -- pay no event record.
 static cudaError_t ctx_begin(qx_context* ctx, cudaStream_t s)
 {
-    if (ctx->used && ctx->last_stream != s) return cudaStreamWaitEvent(s, ctx->last_ev, 0);
-    return cudaSuccess;
+    if (!ctx->used || ctx->last_stream == s) return cudaSuccess;
+    if (!ctx->last_ev) {
+        cudaError_t e = cudaEventCreateWithFlags(&ctx->last_ev, cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaEventRecord(ctx->last_ev, ctx->last_stream);
+    if (e != cudaSuccess) {
+        // the previous stream is gone (destroyed by its owner): order by a
+        // full device synchronisation instead
+        cudaGetLastError();
+        return cudaDeviceSynchronize();
+    }
+    return cudaStreamWaitEvent(s, ctx->last_ev, 0);
 }
 
 static cudaError_t ctx_end(qx_context* ctx, cudaStream_t s);
@@ -183,16 +203,9 @@ struct StreamOrder {
 
 static cudaError_t ctx_end(qx_context* ctx, cudaStream_t s)
 {
-    if (!ctx->last_ev) {
-        cudaError_t e = cudaEventCreateWithFlags(&ctx->last_ev, cudaEventDisableTiming);
-        if (e != cudaSuccess) return e;
-    }
-    cudaError_t e = cudaEventRecord(ctx->last_ev, s);
-    if (e == cudaSuccess) {
-        ctx->last_stream = s;
-        ctx->used = true;
-    }
-    return e;
+    ctx->last_stream = s;
+    ctx->used = true;
+    return cudaSuccess;
 }
 
 static qx_status fail(qx_context* ctx, qx_status s, const std::string& msg)
@@ -219,6 +232,7 @@ static cudaError_t arena_reserve(Arena& a, size_t bytes, bool zero)
     cudaError_t e = cudaMalloc(&a.ptr, want);
     if (e != cudaSuccess) return e;
     a.size = want;
+    ++a.gen;
     if (zero) {
         // the consumers run on non-blocking streams, which do not order
         // after the legacy stream: finish the zeroing before returning
@@ -277,6 +291,7 @@ void qx_context_destroy(qx_context* c)
     if (c->last_ev) cudaEventDestroy(c->last_ev);
     for (auto& kv : c->tables) cudaFree(kv.second.second);
     for (auto& kv : c->otables) cudaFree(kv.second.second);
+    for (auto& kv : c->popc_sched) cudaFree(kv.second.first);
     for (Arena* a : {&c->scratch, &c->counters, &c->stage, &c->records, &c->mcounter, &c->dist})
         if (a->ptr) cudaFree(a->ptr);
     if (c->host_stream) cudaStreamDestroy(c->host_stream);
@@ -308,7 +323,7 @@ qx_status qx_context_set_option(qx_context* c, const char* name, int64_t value)
     else if (n == "sweep_restage") k.sweep_restage = value != 0;
     else if (n == "sweep_compute") k.sweep_compute = value != 0;
     else if (n == "popc") k.popc = value != 0;
-    else if (n == "popc_fused") k.popc_fused = value != 0;
+    else if (n == "popc_timing") k.popc_timing = value != 0;
     else if (n == "tc_f4") k.tc_f4 = value != 0;
     else return fail(c, QX_ERR_INVALID, "unknown option " + n);
     return QX_OK;
@@ -521,15 +536,30 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     if (out->path == QX_PATH_POPC) {
         c.am.pstride = kMaxPartialsLarge;
         const size_t sb = (size_t)batch * 8 * 8, pb = (size_t)batch * c.am.pstride * 3 * 8;
-        const size_t plb = (size_t)batch * 2 * ((nx + 31) / 32 + (ny + 31) / 32 + 2) * 4;
         const size_t spb = (size_t)batch * kMaxPartialsLarge * 16;
-        cudaError_t e = arena_reserve(scr, sb + pb + plb + spb + 256, false);
-        if (e == cudaSuccess) e = arena_reserve(cnt, (size_t)batch * 4, true);
+        const size_t plb = popc_planes_words(batch, nx, ny) * 4;
+        cudaError_t e = arena_reserve(scr, sb + pb + spb + plb + 256, false);
+        if (e == cudaSuccess) e = arena_reserve(cnt, (size_t)batch * 8, true);  // ticket + barrier per pair
         if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
         c.stats = (unsigned long long*)scr.ptr;
         c.am.partials = (long long*)((char*)scr.ptr + sb);
-        c.popc_planes = (uint32_t*)((char*)scr.ptr + sb + pb);
-        c.popc_spart = (unsigned*)((char*)scr.ptr + sb + pb + plb);
+        c.popc_spart = (unsigned*)((char*)scr.ptr + sb + pb);
+        c.popc_planes = (uint32_t*)((char*)scr.ptr + sb + pb + spb);
+        // the CTA schedule of this shape (host partition, uploaded once)
+        const auto key = std::make_tuple(nx, ny, c.am.t_lo, c.am.t_hi, batch);
+        auto it = ctx->popc_sched.find(key);
+        if (it == ctx->popc_sched.end()) {
+            std::vector<int> sched;
+            int G = 1;
+            popc_schedule(c, nx, &G, sched);
+            void* d = nullptr;
+            e = cudaMalloc(&d, sched.size() * sizeof(int));
+            if (e == cudaSuccess) e = cudaMemcpy(d, sched.data(), sched.size() * sizeof(int), cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "popc schedule");
+            it = ctx->popc_sched.emplace(key, std::make_pair(d, G)).first;
+        }
+        c.popc_sched = (const int*)it->second.first;
+        c.popc_G = it->second.second;
         c.am.counters = (int*)cnt.ptr;
         c.prof = &ctx->prof;
         return QX_OK;
@@ -733,6 +763,105 @@ qx_status qx_estimate_batch(qx_context* ctx, const qx_signals* x, const qx_signa
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
     return QX_OK;
 }
+
+}  // extern "C"
+
+// A prepared qx_estimate_batch call (fixed shapes, quantisers, window and
+// path): validation, threshold tables, path choice and scratch layout are
+// done once; qx_plan_run only swaps in the data pointers and launches.
+struct qx_plan {
+    qx_context* ctx = nullptr;
+    qx_signals x{}, y{};
+    int64_t batch = 0;
+    qx_quantizer qx{}, qy{};
+    std::vector<double> tx, ty;  // custom thresholds (the caller's array may go away)
+    int64_t lag_lo = 0, lag_hi = 0;
+    qx_path path = QX_PATH_AUTO;
+    Prepared pr;
+    uint64_t gen_s = 0, gen_c = 0;  // arena generations the pointers in pr were derived from
+};
+
+static qx_status plan_prepare(qx_plan* p)
+{
+    qx_status st = prepare(p->ctx, &p->x, &p->y, p->batch, &p->qx, &p->qy, p->lag_lo, p->lag_hi, true, p->path, &p->pr);
+    if (st != QX_OK) return st;
+    p->gen_s = p->ctx->scratch.gen;
+    p->gen_c = p->ctx->counters.gen;
+    return QX_OK;
+}
+
+extern "C" {
+
+qx_status qx_plan_create(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
+                         const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
+                         qx_path path, qx_plan** out)
+{
+    if (!ctx || !out) return QX_ERR_INVALID;
+    *out = nullptr;
+    if (!x || !y || !qx_ || !qy_) return fail(ctx, QX_ERR_INVALID, "x, y and both quantizers are required");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    qx_plan* p = new qx_plan();
+    p->ctx = ctx;
+    p->x = *x;
+    p->y = *y;
+    // shapes only: the data pointers come with every qx_plan_run
+    static const char kDummy = 0;
+    if (!p->x.data) p->x.data = &kDummy;
+    if (!p->y.data) p->y.data = &kDummy;
+    p->batch = batch;
+    p->qx = *qx_;
+    p->qy = *qy_;
+    if (qx_->kind == QX_Q_CUSTOM && qx_->thresholds && qx_->k > 0) {
+        p->tx.assign(qx_->thresholds, qx_->thresholds + 2 * qx_->k);
+        p->qx.thresholds = p->tx.data();
+    }
+    if (qy_->kind == QX_Q_CUSTOM && qy_->thresholds && qy_->k > 0) {
+        p->ty.assign(qy_->thresholds, qy_->thresholds + 2 * qy_->k);
+        p->qy.thresholds = p->ty.data();
+    }
+    p->lag_lo = lag_lo;
+    p->lag_hi = lag_hi;
+    p->path = path;
+    qx_status st = plan_prepare(p);
+    if (st != QX_OK) {
+        delete p;
+        return st;
+    }
+    *out = p;
+    return QX_OK;
+}
+
+qx_status qx_plan_run(qx_plan* p, const void* x, const void* y, qx_result* results, void* stream)
+{
+    if (!p) return QX_ERR_INVALID;
+    qx_context* ctx = p->ctx;
+    if (!x || !y || !results) return fail(ctx, QX_ERR_INVALID, "x, y and results are required");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    if (p->gen_s != ctx->scratch.gen || p->gen_c != ctx->counters.gen) {
+        // another call regrew the context's scratch: re-derive the pointers
+        qx_status st = plan_prepare(p);
+        if (st != QX_OK) return st;
+    }
+    NttCall& c = p->pr.call;
+    c.op[0].data = x;
+    c.op[1].data = y;
+    c.am.results = results;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (p->pr.path != QX_PATH_POPC) e = cudaMemsetAsync(c.stats, 0, (size_t)p->batch * 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset stats");
+    e = p->pr.path == QX_PATH_DIRECT ? tc_window_run(c, p->pr.nx, s)
+        : p->pr.path == QX_PATH_POPC ? popc_run(c, p->pr.nx, s) : ntt_run(c, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    return QX_OK;
+}
+
+int qx_plan_path(const qx_plan* p) { return p ? p->pr.path : -1; }
+
+void qx_plan_destroy(qx_plan* p) { delete p; }
 
 qx_status qx_xcorr_full(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                         const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t* values, qx_result* stats,

@@ -105,7 +105,7 @@ struct Knobs {
     int sweep_restage = 1;     // QX_SWEEP_RESTAGE=0: skip the H2D copies (compute-only timing)
     int sweep_compute = 1;     // QX_SWEEP_COMPUTE=0: skip the kernels (copy-only timing)
     int popc = 1;              // QX_POPC=0: never pick the popc path on AUTO
-    int popc_fused = 1;        // QX_POPC_FUSED=0: two-launch popc form even when one fits
+    int popc_timing = 0;       // QX_POPC_TIMING=1: popc correlation kernel prints its phase times
     int tc_f4 = 1;             // QX_TC_F4=0: no fp4 tensor-core template search
     int64_t sweep_plan[16] = {0};  // QX_SWEEP_PLAN="a,b,...": explicit host-sweep chunk sizes
     int sweep_plan_n = 0;
@@ -140,8 +140,10 @@ struct NttCall {
     OuterTables otab[3];
     uint32_t* OUT;            // [2][chunk][P] outer forward output
     uint32_t* RI;             // [chunk*M][np][Q] inner inverse residues
-    uint32_t* popc_planes;    // popc path: [batch][2][nxw + nyw + 2] code bit planes
-    unsigned* popc_spart;     // popc path (fused): [batch][<= 512][4] per-CTA counts
+    unsigned* popc_spart;     // popc path: [batch][G][4] per-CTA nonzero counts and flags
+    uint32_t* popc_planes;    // popc path: [batch][2 (nxw + nyw)] code bit planes
+    const int* popc_sched;    // popc path: [G + 1] first block of each CTA (per-shape cache)
+    int popc_G;               // popc path: CTAs per pair
     int split2;               // the caller takes 2 records per pair (2-SM template-search blocks)
 };
 

@@ -5,404 +5,562 @@
 // Codes are two bit planes per signal, s (code < 0) and z (code != 0); for
 // 32 aligned samples
 //   sum_m u[m] v[m] = popc(zu & zv) - 2 popc(zu & zv & (su ^ sv)),
-// and when neither signal has a zero code in range the first term is the
-// overlap count of the lag, so one POPC per 32 products remains.  This is
-// the reference's brute-force correlation (intxcorr.py:96-100) with the
-// argmax summary of argmax_set (estimator.py:50-57) fused.
+// and when neither signal has a zero code the first term is the overlap
+// count of the lag, so one POPC per 32 products remains
+// (value(d) = overlap(d) - 2 * mismatches(d)).  This is the reference's
+// brute-force correlation (intxcorr.py:96-100) with the argmax summary of
+// argmax_set (estimator.py:50-57) fused.
 //
-// k_popc_planes quantises both signals once into global bit planes (one
-// warp ballot per 32 samples) with the statistics; k_popc, grid (G, batch),
-// gives CTA g of a pair a contiguous run of 32-lag blocks: it stages x's
-// planes and the y window its lags touch (realigned by funnel shifts) in
-// shared memory, then every group of 4 warps
-// correlates one 32-lag block at a time: lane k holds x words k, k+128, ...
-// in registers and keeps 32 lag accumulators (the y word pair is loaded once
-// per x word, the 32 shifts are immediate funnel shifts), REDUX sums each
-// lag over the warp, and the group's first warp adds the four warps' sums.
-// Per-lane running (max, smallest lag, count) records are merged by the
-// NTT path's argmax_finish (block reduce -> per-CTA partial -> last CTA
-// writes the qx_result with the statistics).
+// One cooperative launch (every CTA of a pair resident, one per SM), no
+// second kernel and no host round trip:
+//   1. planes: the pair's G CTAs split the plane words (x words, then y
+//      words; one ballot per 32 samples, a warp's loads in flight together)
+//      and write them to global memory with per-CTA nonzero counts and NaN /
+//      zero-code flags; meanwhile each CTA reads its block range from the
+//      host-computed schedule and builds its unit prefix;
+//   2. a per-pair grid barrier (acq_rel counter);
+//   3. each CTA stages x's planes and the y window of its 32-lag blocks
+//      (realigned by funnel shifts so lag block b, x word i reads y' words
+//      i+b, i+b+1) in shared memory.  A block covers only the x words its
+//      lags overlap (overlap-exact: half the rectangle of a full window);
+//      the schedule gives every CTA a contiguous block range of near-equal
+//      units (one per x word plus a fixed block overhead, partitioned on
+//      the host, cached per shape).  Lane = lag: a warp walks a run of x
+//      words of one block with broadcast shared loads, each lane
+//      funnel-shifting the y words by its own lag, so the 32 lag sums need
+//      no cross-lane reduction; runs of a block from several warps meet in
+//      shared accumulators;
+//   4. the CTA keeps (max, smallest lag, count) by REDUX and the pair's last
+//      CTA (acq_rel ticket) merges the records with the statistics and
+//      resets the pair's counters.
+#include <algorithm>
 #include <climits>
 #include <cstdio>
-
-#include <cooperative_groups.h>
+#include <vector>
 
 #include "qx_argmax.cuh"
 #include "qx_internal.h"
 
 namespace qx {
 
-constexpr int kPopcThreads = 512;
-constexpr int kPopcWarps = kPopcThreads / 32;
-constexpr int kPopcGroup = 4;                        // warps per 32-lag block
-constexpr int kPopcGroups = kPopcWarps / kPopcGroup;  // blocks in flight per CTA
+constexpr int kPcThreads = 1024;  // one CTA per SM
+constexpr int kPcWarps = kPcThreads / 32;
+constexpr int kPcWordsPerWarp = 4;   // plane words per warp per round (loads in flight)
+constexpr int kPcAccBlocks = 128;    // 32-lag block accumulators per pass of a CTA
+constexpr int kPcBlockUnits = 48;    // per-block overhead in x-word units (setup, edge words, flush; measured)
+constexpr int kPcMaxSmem = 200 * 1024;
+constexpr unsigned kPcZeroCode = 0x100u;  // spart flag: a code 0 inside a signal
 
-// one operand as the popc kernels need it (rows + the two thresholds of a
-// 1-level quantiser): a few dozen parameter bytes instead of OperandDesc's
-// 2-KB threshold table, so the launch carries a small parameter block
+// one operand as the popc kernel needs it: rows + the two thresholds of a
+// 1-level quantiser (a few dozen parameter bytes, not a 2-KB table)
 struct PopcOp {
     const void* data;
-    int64_t ld, n;
+    int64_t ld;
     double t0, t1;
 };
 
 struct PopcArgs {
     PopcOp op[2];
-    unsigned long long* stats;  // [batch][2][4]
-    ArgmaxOut am;
-    int64_t dlo;   // first lag (relative: x[m] y[m + d]) of the window
-    int64_t dhi;   // last lag
-    int nblk;      // 32-lag blocks of the window
-    int bpc;       // blocks per CTA
-    int nxw;       // x words
-    int nyw;       // y words (whole signal)
-    uint32_t* planes;  // [batch][xs | xz | ys | yz]: 2 * (nxw + nyw) words per pair
-    unsigned* spart;   // fused kernel: [batch][G][4] per-CTA nonzero counts (x, y) and flags
+    ArgmaxOut am;               // am.counters: [2 * batch] (ticket, barrier) per pair
+    unsigned long long* stats;  // [batch][8] statistics records (written by the pair's last CTA)
+    uint32_t* planes;           // [batch][2 (sxw + syw)]: xs | xz | ys | yz, sample i at bit i % 32
+    unsigned* spart;            // [batch][G][4] per-CTA nonzero counts (x, y) and flags
+    const int* sched;           // [G + 1] first block of each CTA (host-computed, per shape)
+    int batch;
+    int dlo, dhi;               // lag window: x[m] * y[m + d], d in [dlo, dhi]
+    int nx, ny;                 // samples (nx <= 2^16, ny <= 2^24: 32-bit index math)
+    int nblk;                   // 32-lag blocks of the window
+    int sxw, syw;               // words of the signals
 };
 
-__device__ __forceinline__ uint32_t* plane_x(const PopcArgs& a, int64_t pair)
+__device__ __forceinline__ unsigned long long gtimer()
 {
-    return a.planes + pair * 2 * (int64_t)(a.nxw + a.nyw);
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
 }
 
-// global planes of both signals of a pair: warp w of the grid row quantises
-// word w (x words first, then y), statistics per CTA into the pair's record
-template <typename T>
-__global__ void __launch_bounds__(kPopcThreads) k_popc_planes(const __grid_constant__ PopcArgs a)
+// x words [w0, w1) touched by the lags of block b: sample m pairs y[m + d]
+// inside both signals for some d in [d0, d1]
+__host__ __device__ __forceinline__ void block_words(int dlo, int dhi, int nx, int ny, int b, int& w0, int& w1)
 {
-    __shared__ unsigned s_nz[2], s_fl;
-    const int64_t pair = blockIdx.y;
-    const int lane = threadIdx.x & 31;
-    const int w = blockIdx.x * kPopcWarps + (threadIdx.x >> 5);
-    if (threadIdx.x < 2) s_nz[threadIdx.x] = 0;
-    if (threadIdx.x == 0) s_fl = 0;
-    __syncthreads();
-    const bool isx = w < a.nxw;
-    if (w < a.nxw + a.nyw) {
-        const PopcOp& o = a.op[isx ? 0 : 1];
-        const T* row = reinterpret_cast<const T*>(o.data) + pair * o.ld;
-        const int64_t i = 32ll * (isx ? w : w - a.nxw) + lane;
-        const T v = i < o.n ? row[i] : (T)0;
-        const int c = level_k1(v, (T)o.t0, (T)o.t1);
-        const uint32_t sb = __ballot_sync(0xffffffffu, c < 0), zb = __ballot_sync(0xffffffffu, c != 0);
-        const bool nan = __any_sync(0xffffffffu, v != v);
-        if (lane == 0) {
-            uint32_t* px = plane_x(a, pair);
-            if (isx) {
-                px[w] = sb;
-                px[a.nxw + w] = zb;
-            } else {
-                uint32_t* py = px + 2 * a.nxw;
-                py[w - a.nxw] = sb;
-                py[a.nyw + (w - a.nxw)] = zb;
-            }
-            atomicAdd(&s_nz[isx ? 0 : 1], __popc(zb));
-            if (nan) atomicOr(&s_fl, SF_NONFINITE);
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long* st = a.stats + pair * 8;
-        // sum of squares = nonzero count for 1-level codes
-        if (s_nz[0]) {
-            atomicAdd(st + 0, (unsigned long long)s_nz[0]);
-            atomicAdd(st + 1, (unsigned long long)s_nz[0]);
-        }
-        if (s_nz[1]) {
-            atomicAdd(st + 4, (unsigned long long)s_nz[1]);
-            atomicAdd(st + 5, (unsigned long long)s_nz[1]);
-        }
-        if (s_fl) atomicOr(st + 6, (unsigned long long)s_fl);
-    }
+    const int d0 = dlo + 32 * b;
+    const int d1 = d0 + 31 < dhi ? d0 + 31 : dhi;
+    const int mlo = -d1 > 0 ? -d1 : 0;
+    const int mhi = nx < ny - d0 ? nx : ny - d0;
+    w0 = mlo >> 5;
+    w1 = mhi > mlo ? (mhi + 31) >> 5 : w0;
 }
 
-// bits of word w (samples lo .. lo + 31) that lie inside [0, n)
-__device__ __forceinline__ uint32_t popc_valid(int64_t lo, int64_t n)
+__host__ __device__ __forceinline__ int block_units(int dlo, int dhi, int nx, int ny, int b)
 {
-    const int64_t a = lo < 0 ? -lo : 0, b = n - lo < 32 ? n - lo : 32;
-    if (b <= a) return 0u;
-    const uint32_t hi = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
-    return hi & ~((1u << a) - 1u);
+    int w0, w1;
+    block_words(dlo, dhi, nx, ny, b, w0, w1);
+    return w1 - w0 + kPcBlockUnits;
 }
 
-template <bool ALLNZ>
-__device__ void popc_blocks(const PopcArgs& a, const uint32_t* xs, const uint32_t* xz, const uint32_t* ys,
-                            const uint32_t* yz, int b0, int b1, int64_t yb, Best& best, int* part)
+// (max value, smallest index, count) of a warp's lanes; v = INT_MIN, c = 0
+// for lanes without a lag
+__device__ __forceinline__ void warp_best(int& v, int& t, int& c)
 {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int grp = warp / kPopcGroup, wg = warp % kPopcGroup;
-    const int nxw = a.nxw;
-    const int64_t nx = a.op[0].n, ny = a.op[1].n;
-    for (int b = b0 + grp; b < b1; b += kPopcGroups) {
-        int acc[32];
-#pragma unroll
-        for (int l = 0; l < 32; ++l) acc[l] = 0;
-        const int q0 = b - b0;  // y word of x word 0, lag l of the block at bit l
-        for (int i = wg * 32 + lane; i < nxw; i += 32 * kPopcGroup) {
-            const uint32_t sx = xs[i], zx = xz[i];
-            const uint32_t y0 = ys[q0 + i], y1 = ys[q0 + i + 1], z0 = yz[q0 + i], z1 = yz[q0 + i + 1];
-#pragma unroll
-            for (int l = 0; l < 32; ++l) {
-                const uint32_t yy = __funnelshift_r(y0, y1, l), zz = __funnelshift_r(z0, z1, l);
-                const uint32_t az = zz & zx;
-                const uint32_t d = (sx ^ yy) & az;
-                if constexpr (ALLNZ) acc[l] += __popc(d);
-                else acc[l] += __popc(az) - 2 * __popc(d);
-            }
-        }
-        // lane l <- the warp's sum for lag l; the group's first warp adds the four
-        int mine = 0;
-#pragma unroll
-        for (int l = 0; l < 32; ++l) {
-            const int v = __reduce_add_sync(0xffffffffu, acc[l]);
-            if (lane == l) mine = v;
-        }
-        part[(grp * kPopcGroup + wg) * 32 + lane] = mine;
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(32 * kPopcGroup) : "memory");
-        if (wg == 0) {
-            int sum = 0;
-#pragma unroll
-            for (int w = 0; w < kPopcGroup; ++w) sum += part[(grp * kPopcGroup + w) * 32 + lane];
-            const int64_t d = a.dlo + 32ll * b + lane;
-            if (d <= a.dhi) {
-                long long v = sum;
-                if constexpr (ALLNZ) {
-                    // overlap of the lag: m in [0, nx) with m + d in [0, ny)
-                    const int64_t lo = d < 0 ? -d : 0, hi = nx < ny - d ? nx : ny - d;
-                    v = (hi > lo ? hi - lo : 0) - 2ll * sum;
-                }
-                best_add(best, v, d + nx - 1);
-            }
-        }
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "n"(32 * kPopcGroup) : "memory");  // part reusable
-    }
+    const int m = __reduce_max_sync(0xffffffffu, v);
+    t = (int)__reduce_min_sync(0xffffffffu, v == m ? (unsigned)t : 0xffffffffu);
+    c = (int)__reduce_add_sync(0xffffffffu, v == m ? (unsigned)c : 0u);
+    v = m;
 }
 
-__device__ __forceinline__ void popc_correlate(const PopcArgs& a)
+template <typename T, bool TIMING>
+__global__ void __launch_bounds__(kPcThreads, 1) k_popc(const __grid_constant__ PopcArgs a)
 {
-    extern __shared__ uint32_t pw[];
-    __shared__ unsigned s_zero;
-    __shared__ int part[kPopcWarps * 32];
+    extern __shared__ uint32_t sm[];
+    __shared__ unsigned s_cnt[3];
+    __shared__ int s_best[kPcWarps][3];
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t pair = blockIdx.y;
     const int g = blockIdx.x, G = gridDim.x;
-    const int64_t nx = a.op[0].n, ny = a.op[1].n;
-    const int b0 = min(a.nblk, g * a.bpc), b1 = min(a.nblk, b0 + a.bpc);
-    // y window: lags d of blocks [b0, b1) pair x[m] with y[m + d]
-    const int64_t yb = a.dlo + 32ll * b0;
-    const int nxw = a.nxw, nyw = (b1 - b0) + nxw + 1;
-    uint32_t* xs = pw;
+    const int nxw = a.sxw, nx = a.nx, ny = a.ny;
+    unsigned long long tm[6] = {0, 0, 0, 0, 0, 0};
+    if (TIMING) tm[0] = gtimer();
+    uint32_t* P = a.planes + pair * 2 * (int64_t)(a.sxw + a.syw);
+    int* bar = a.am.counters + a.batch + pair;
+    if (tid < 3) s_cnt[tid] = 0;
+
+    // 1. planes: warp j of the pair's grid row quantises plane words j, j + W, ...
+    const int cb0 = a.sched[g], cb1 = a.sched[g + 1], nb = cb1 - cb0;
+    {
+        const T* X = reinterpret_cast<const T*>(a.op[0].data) + pair * a.op[0].ld;
+        const T* Y = reinterpret_cast<const T*>(a.op[1].data) + pair * a.op[1].ld;
+        const T x0 = (T)a.op[0].t0, x1 = (T)a.op[0].t1, y0 = (T)a.op[1].t0, y1 = (T)a.op[1].t1;
+        const int nw = a.sxw + a.syw, W = G * kPcWarps;
+        unsigned nzx = 0, nzy = 0;
+        bool nan = false, zero = false;
+        __syncthreads();  // s_cnt
+        for (int j0 = g * kPcWarps + warp; j0 < nw; j0 += W * kPcWordsPerWarp) {
+            T v[kPcWordsPerWarp];
+            bool in[kPcWordsPerWarp];
+#pragma unroll
+            for (int u = 0; u < kPcWordsPerWarp; ++u) {
+                const int j = j0 + u * W;
+                const bool isx = j < a.sxw;
+                const int i = 32 * (isx ? j : j - a.sxw) + lane;
+                in[u] = j < nw && i < (isx ? nx : ny);
+                v[u] = (T)0;
+                if (in[u]) v[u] = isx ? X[i] : Y[i];
+            }
+#pragma unroll
+            for (int u = 0; u < kPcWordsPerWarp; ++u) {
+                const int j = j0 + u * W;
+                if (j >= nw) break;  // warp-uniform
+                const bool isx = j < a.sxw;
+                const int c = isx ? level_k1(v[u], x0, x1) : level_k1(v[u], y0, y1);
+                const uint32_t sb = __ballot_sync(0xffffffffu, in[u] && c < 0);
+                const uint32_t zb = __ballot_sync(0xffffffffu, in[u] && c != 0);
+                nan |= v[u] != v[u];
+                zero |= in[u] && c == 0;
+                if (lane == 0) {
+                    // xs | xz | ys | yz
+                    const int o = isx ? j : a.sxw + j;
+                    P[o] = sb;
+                    P[o + (isx ? a.sxw : a.syw)] = zb;
+                }
+                if (isx) nzx += __popc(zb);
+                else nzy += __popc(zb);
+            }
+        }
+        const unsigned fl = (__any_sync(0xffffffffu, nan) ? SF_NONFINITE : 0u) |
+                            (__any_sync(0xffffffffu, zero) ? kPcZeroCode : 0u);
+        if (lane == 0) {
+            if (nzx) atomicAdd(&s_cnt[0], nzx);
+            if (nzy) atomicAdd(&s_cnt[1], nzy);
+            if (fl) atomicOr(&s_cnt[2], fl);
+        }
+    }
+    // the CTA's unit prefix (warp 0) while the plane stores drain
+    int* units = reinterpret_cast<int*>(sm);  // [nb + 1]
+    if (warp == 0) {
+        int base = 0;
+        for (int c0 = 0; c0 < nb; c0 += 32) {
+            const int b = cb0 + c0 + lane;
+            const int u = b < cb1 ? block_units(a.dlo, a.dhi, nx, ny, b) : 0;
+            int incl = u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (b < cb1) units[c0 + lane] = base + incl - u;
+            base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) units[nb] = base;
+    }
+    __syncthreads();
+    if (tid < 3) a.spart[(pair * G + g) * 4 + tid] = s_cnt[tid];
+    if (TIMING) tm[1] = gtimer();
+
+    // 2. per-pair grid barrier: every CTA's planes and records are visible
+    if (G > 1) {
+        if (tid == 0) {
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(bar) : "memory");
+            int seen;
+            do {
+                asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(seen) : "l"(bar) : "memory");
+            } while (seen < G);
+        }
+        __syncthreads();
+    }
+    if (TIMING) tm[2] = gtimer();
+
+    // 3. stage x's planes and the CTA's y' window; a zero code anywhere
+    // selects the two-POPC form
+    const int nyq = nxw + nb + 1;  // y' word jl holds y[dlo + 32 (cb0 + jl) + k] at bit k
+    uint32_t* xs = reinterpret_cast<uint32_t*>(units) + ((nb + 1 + 3) & ~3);
     uint32_t* xz = xs + nxw;
     uint32_t* ys = xz + nxw;
-    uint32_t* yz = ys + nyw;
-    if (threadIdx.x == 0) s_zero = 0;
-    __syncthreads();
-#ifdef QX_POPC_TIMING
-    const long long tp0 = clock64();
-#endif
-    // stage the planes: x as is, y realigned to sample yb (zero outside y)
-    const uint32_t* gx = plane_x(a, pair);
-    const uint32_t* gy = gx + 2 * a.nxw;
-    unsigned zero = 0;
-    for (int w = threadIdx.x; w < nxw; w += kPopcThreads) {
-        const uint32_t sv = gx[w], zv = gx[nxw + w];
-        xs[w] = sv;
-        xz[w] = zv;
-        zero |= zv != popc_valid(32ll * w, nx);  // a zero code in range: the 2-POPC form
+    uint32_t* yz = ys + nyq;
+    int* acc = reinterpret_cast<int*>(yz + nyq);  // [kPcAccBlocks][32]
+    int zero = 0;
+    {
+        const uint32_t* gys = P + 2 * a.sxw;
+        const uint32_t* gyz = gys + a.syw;
+        for (int i = tid; i < G; i += kPcThreads) zero |= __ldcg(&a.spart[(pair * G + i) * 4 + 2]) & kPcZeroCode;
+        for (int w = tid; w < nxw; w += kPcThreads) {
+            xs[w] = __ldcg(&P[w]);
+            xz[w] = __ldcg(&P[nxw + w]);
+        }
+        const int s0 = a.dlo + 32 * cb0;
+        const int q0 = s0 >> 5, sh = s0 & 31;  // floor division
+        for (int w = tid; w < nyq; w += kPcThreads) {
+            const int q = q0 + w;
+            const bool in0 = q >= 0 && q < a.syw, in1 = q + 1 >= 0 && q + 1 < a.syw;
+            const uint32_t s_0 = in0 ? __ldcg(&gys[q]) : 0u, s_1 = in1 ? __ldcg(&gys[q + 1]) : 0u;
+            const uint32_t z_0 = in0 ? __ldcg(&gyz[q]) : 0u, z_1 = in1 ? __ldcg(&gyz[q + 1]) : 0u;
+            ys[w] = __funnelshift_r(s_0, s_1, sh);
+            yz[w] = __funnelshift_r(z_0, z_1, sh);
+        }
     }
-    const int64_t q = yb >= 0 ? yb / 32 : -((31 - yb) / 32);  // floor(yb / 32)
-    const int sh = (int)(yb - 32 * q);
-    for (int w = threadIdx.x; w < nyw; w += kPopcThreads) {
-        const int64_t w0 = q + w;
-        const uint32_t s0 = (w0 >= 0 && w0 < a.nyw) ? gy[w0] : 0u, s1 = (w0 + 1 >= 0 && w0 + 1 < a.nyw) ? gy[w0 + 1] : 0u;
-        const uint32_t z0 = (w0 >= 0 && w0 < a.nyw) ? gy[a.nyw + w0] : 0u;
-        const uint32_t z1 = (w0 + 1 >= 0 && w0 + 1 < a.nyw) ? gy[a.nyw + w0 + 1] : 0u;
-        const uint32_t sv = __funnelshift_r(s0, s1, sh), zv = __funnelshift_r(z0, z1, sh);
-        ys[w] = sv;
-        yz[w] = zv;
-        zero |= zv != popc_valid(yb + 32ll * w, ny);
-    }
-    zero = __reduce_or_sync(0xffffffffu, zero);
-    if ((threadIdx.x & 31) == 0 && zero) atomicOr(&s_zero, 1u);
-    __syncthreads();
-#ifdef QX_POPC_TIMING
-    const long long tp1 = clock64();
-#endif
-    Best best = best_init();
-    if (s_zero) popc_blocks<false>(a, xs, xz, ys, yz, b0, b1, yb, best, part);
-    else popc_blocks<true>(a, xs, xz, ys, yz, b0, b1, yb, best, part);
-#ifdef QX_POPC_TIMING
-    __syncthreads();
-    const long long tp2 = clock64();
-#endif
-    argmax_finish<kPopcWarps>(best, a.am, a.stats, pair, G, g);
-#ifdef QX_POPC_TIMING
-    if (threadIdx.x == 0 && (g == 0 || g == G - 1))
-        printf("popc cta %d/%d: stage %lld, blocks %lld, finish %lld cycles (bpc %d, nyw %d, allnz %d)\n", g, G,
-               tp1 - tp0, tp2 - tp1, clock64() - tp2, a.bpc, nyw, !s_zero);
-#endif
-}
-__global__ void __launch_bounds__(kPopcThreads) k_popc(const __grid_constant__ PopcArgs a) { popc_correlate(a); }
+    const bool allnz = !__syncthreads_or(zero);
+    if (TIMING) tm[3] = gtimer();
 
-// one cooperative launch: the planes of every pair (CTA g of pair p takes
-// words g*16 + warp + k*16G), per-CTA counts into spart, a grid-wide sync,
-// CTA 0 of each pair turns the counts into the pair's statistics record (no
-// memset, no atomics), then the correlation as in k_popc
-template <typename T>
-__global__ void __launch_bounds__(kPopcThreads) k_popc_fused(const __grid_constant__ PopcArgs a)
-{
-    __shared__ unsigned s_cnt[3];
-    const int64_t pair = blockIdx.y;
-    const int g = blockIdx.x, G = gridDim.x;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#ifdef QX_POPC_TIMING
-    unsigned long long f0, f1, f2;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f0));
-#endif
-    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0;
-    __syncthreads();
-    uint32_t* px = plane_x(a, pair);
-    unsigned nzx = 0, nzy = 0;
-    bool nan = false;
-    for (int w = g * kPopcWarps + warp; w < a.nxw + a.nyw; w += G * kPopcWarps) {
-        const bool isx = w < a.nxw;
-        const PopcOp& o = a.op[isx ? 0 : 1];
-        const T* row = reinterpret_cast<const T*>(o.data) + pair * o.ld;
-        const int64_t i = 32ll * (isx ? w : w - a.nxw) + lane;
-        const T v = i < o.n ? row[i] : (T)0;
-        const int c = level_k1(v, (T)o.t0, (T)o.t1);
-        const uint32_t sb = __ballot_sync(0xffffffffu, c < 0), zb = __ballot_sync(0xffffffffu, c != 0);
-        nan |= v != v;
-        if (lane == 0) {
-            if (isx) {
-                px[w] = sb;
-                px[a.nxw + w] = zb;
-                nzx += __popc(zb);
-            } else {
-                uint32_t* py = px + 2 * a.nxw;
-                py[w - a.nxw] = sb;
-                py[a.nyw + (w - a.nxw)] = zb;
-                nzy += __popc(zb);
+    int bv = INT_MIN, bt = INT_MAX, bc = 0;  // this thread's (max, smallest index, count)
+    for (int pb0 = 0; pb0 < nb; pb0 += kPcAccBlocks) {  // CTA-local block indices
+        const int pb1 = min(nb, pb0 + kPcAccBlocks);
+        for (int i = tid; i < kPcAccBlocks * 32; i += kPcThreads) acc[i] = 0;
+        __syncthreads();
+        // this pass's units split evenly over the warps (lane = lag: a warp
+        // correlates a run of x words of one block for its 32 lags at once)
+        const int u0 = units[pb0], nu = units[pb1] - u0;
+        const int my0 = u0 + (int)((long long)nu * warp / kPcWarps);
+        const int my1 = u0 + (int)((long long)nu * (warp + 1) / kPcWarps);
+        if (my0 < my1) {
+            int lo = pb0, hi = pb1;  // block of unit my0: last lb with units[lb] <= my0
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (units[mid] <= my0) lo = mid;
+                else hi = mid;
+            }
+            for (int lb = lo; lb < pb1 && units[lb] < my1; ++lb) {
+                int w0, w1;
+                block_words(a.dlo, a.dhi, nx, ny, cb0 + lb, w0, w1);
+                // units of block lb: kPcBlockUnits of overhead, then one per x word
+                const int ws = w0 + max(0, max(my0, units[lb]) - units[lb] - kPcBlockUnits);
+                const int we = w0 + max(0, min(my1, units[lb + 1]) - units[lb] - kPcBlockUnits);
+                if (ws >= we) continue;
+                // interior x words [i0, i1): the word and the 63 y samples its
+                // 32 lags read lie inside the signals
+                const int yb0 = a.dlo + 32 * (cb0 + lb);  // y sample of x word 0, lag 0
+                const int i0 = yb0 >= 0 ? 0 : (31 - yb0) >> 5;
+                const int i1 = min(nx >> 5, ny - 63 - yb0 >= 0 ? ((ny - 63 - yb0) >> 5) + 1 : 0);
+                const int f0 = allnz ? max(ws, min(we, i0)) : we;
+                const int f1 = allnz ? max(f0, min(we, i1)) : we;
+                const uint32_t* yq = ys + lb;  // y' words of x word i: yq[i], yq[i + 1]
+                const uint32_t* zq = yz + lb;
+                int sum = 0;
+                auto masked = [&](int i) {
+                    const uint32_t yy = __funnelshift_r(yq[i], yq[i + 1], lane);
+                    const uint32_t az = xz[i] & __funnelshift_r(zq[i], zq[i + 1], lane);
+                    const uint32_t d = (xs[i] ^ yy) & az;
+                    sum += allnz ? __popc(d) : __popc(az) - 2 * __popc(d);
+                };
+                for (int i = ws; i < f0; ++i) masked(i);
+                {
+                    int i = f0;
+                    uint32_t ya = i < f1 ? yq[i] : 0u;
+                    for (; i + 4 <= f1; i += 4) {
+                        const uint32_t y1 = yq[i + 1], y2 = yq[i + 2], y3 = yq[i + 3], y4 = yq[i + 4];
+                        const uint32_t s0 = xs[i], s1 = xs[i + 1], s2 = xs[i + 2], s3 = xs[i + 3];
+                        sum += __popc(s0 ^ __funnelshift_r(ya, y1, lane)) + __popc(s1 ^ __funnelshift_r(y1, y2, lane));
+                        sum += __popc(s2 ^ __funnelshift_r(y2, y3, lane)) + __popc(s3 ^ __funnelshift_r(y3, y4, lane));
+                        ya = y4;
+                    }
+                    for (; i < f1; ++i) {
+                        const uint32_t y1 = yq[i + 1];
+                        sum += __popc(xs[i] ^ __funnelshift_r(ya, y1, lane));
+                        ya = y1;
+                    }
+                }
+                for (int i = f1; i < we; ++i) masked(i);
+                atomicAdd(&acc[(lb - pb0) * 32 + lane], sum);
             }
         }
+        __syncthreads();  // every partial sum of this pass has landed
+        for (int i = tid; i < (pb1 - pb0) * 32; i += kPcThreads) {
+            const int d = a.dlo + 32 * (cb0 + pb0) + i;
+            if (d > a.dhi) continue;
+            int val = acc[i];
+            if (allnz) val = max(0, min(nx, ny - d) - max(0, -d)) - 2 * val;  // overlap - 2 mismatches
+            const int t = d + nx - 1;
+            if (val > bv) {
+                bv = val;
+                bt = t;
+                bc = 1;
+            } else if (val == bv) {
+                bt = min(bt, t);
+                ++bc;
+            }
+        }
+        __syncthreads();  // acc reads done before the next pass zeroes it
     }
-    nan = __any_sync(0xffffffffu, nan);
+    if (TIMING) tm[4] = gtimer();
+
+    // 4. per-CTA record, ticket; the pair's last CTA merges and writes the result
+    warp_best(bv, bt, bc);
     if (lane == 0) {
-        if (nzx) atomicAdd(&s_cnt[0], nzx);
-        if (nzy) atomicAdd(&s_cnt[1], nzy);
-        if (nan) atomicOr(&s_cnt[2], SF_NONFINITE);
+        s_best[warp][0] = bv;
+        s_best[warp][1] = bt;
+        s_best[warp][2] = bc;
     }
     __syncthreads();
-    if (threadIdx.x < 3) a.spart[(pair * G + g) * 4 + threadIdx.x] = s_cnt[threadIdx.x];
-#ifdef QX_POPC_TIMING
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f1));
-#endif
-    cooperative_groups::this_grid().sync();
-#ifdef QX_POPC_TIMING
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(f2));
-    if (threadIdx.x == 0 && (g == 0 || g == G - 1))
-        printf("fused cta %d: planes %.2f us, grid sync %.2f us\n", g, (f1 - f0) / 1e3, (f2 - f1) / 1e3);
-#endif
-    if (g == 0 && warp == 0) {
-        unsigned cx = 0, cy = 0, fl = 0;
-        for (int i = lane; i < G; i += 32) {
-            const unsigned* sp = a.spart + (pair * G + i) * 4;
-            cx += sp[0];
-            cy += sp[1];
-            fl |= sp[2];
+    if (warp == 0) {
+        bv = lane < kPcWarps ? s_best[lane][0] : INT_MIN;
+        bt = lane < kPcWarps ? s_best[lane][1] : INT_MAX;
+        bc = lane < kPcWarps ? s_best[lane][2] : 0;
+        warp_best(bv, bt, bc);
+        if (lane == 0) {
+            long long* pp = a.am.partials + (pair * a.am.pstride + g) * 3;
+            pp[0] = bv;
+            pp[1] = bt;
+            pp[2] = bc;
+            int ticket;
+            asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(ticket) : "l"(a.am.counters + pair) : "memory");
+            s_last = ticket == G - 1;
         }
-        cx = __reduce_add_sync(0xffffffffu, cx);
-        cy = __reduce_add_sync(0xffffffffu, cy);
-        fl = __reduce_or_sync(0xffffffffu, fl);
-        unsigned long long* st = a.stats + pair * 8;
-        // sum of squares = nonzero count for 1-level codes
-        if (lane < 8) st[lane] = lane == 0 || lane == 1 ? cx : lane == 4 || lane == 5 ? cy : lane == 6 ? fl : 0ull;
     }
-    popc_correlate(a);
+    __syncthreads();
+    if (TIMING && tid == 0) {
+        tm[5] = gtimer();
+        if (g == 0 || g == G / 2 || g == G - 1 || s_last)
+            printf("popc cta %d/%d blocks [%d,%d) units %d: planes %.2f barrier %.2f stage %.2f corr %.2f "
+                   "ticket %.2f us%s\n",
+                   g, G, cb0, cb1, units[nb], (tm[1] - tm[0]) / 1e3, (tm[2] - tm[1]) / 1e3, (tm[3] - tm[2]) / 1e3,
+                   (tm[4] - tm[3]) / 1e3, (tm[5] - tm[4]) / 1e3, s_last ? " (last)" : "");
+    }
+    if (!s_last) return;
+    // last CTA: every CTA's record (one per thread) and counts
+    const volatile long long* pp = a.am.partials + pair * a.am.pstride * 3;
+    bv = INT_MIN;
+    bt = INT_MAX;
+    bc = 0;
+    unsigned cx = 0, cy = 0, fl = 0;
+    for (int i = tid; i < G; i += kPcThreads) {
+        const int v = (int)pp[3 * i], t = (int)pp[3 * i + 1], c = (int)pp[3 * i + 2];
+        if (v > bv) {
+            bv = v;
+            bt = t;
+            bc = c;
+        } else if (v == bv) {
+            bt = min(bt, t);
+            bc += c;
+        }
+        const unsigned* sp = a.spart + (pair * G + i) * 4;
+        cx += __ldcg(sp);
+        cy += __ldcg(sp + 1);
+        fl |= __ldcg(sp + 2);
+    }
+    warp_best(bv, bt, bc);
+    cx = __reduce_add_sync(0xffffffffu, cx);
+    cy = __reduce_add_sync(0xffffffffu, cy);
+    fl = __reduce_or_sync(0xffffffffu, fl);
+    __syncthreads();  // s_best / s_cnt reads of the first merge are done
+    if (tid < 3) s_cnt[tid] = 0;
+    if (lane == 0) {
+        s_best[warp][0] = bv;
+        s_best[warp][1] = bt;
+        s_best[warp][2] = bc;
+    }
+    __syncthreads();
+    if (lane == 0 && (cx | cy | fl)) {
+        atomicAdd(&s_cnt[0], cx);
+        atomicAdd(&s_cnt[1], cy);
+        atomicOr(&s_cnt[2], fl);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        bv = lane < kPcWarps ? s_best[lane][0] : INT_MIN;
+        bt = lane < kPcWarps ? s_best[lane][1] : INT_MAX;
+        bc = lane < kPcWarps ? s_best[lane][2] : 0;
+        warp_best(bv, bt, bc);
+        if (lane == 0) {
+            // sum of squares = nonzero count for 1-level codes
+            unsigned long long* st = a.stats + pair * 8;
+            st[0] = s_cnt[0];
+            st[1] = s_cnt[0];
+            st[2] = s_cnt[2] & ~kPcZeroCode;
+            st[3] = 0;
+            st[4] = s_cnt[1];
+            st[5] = s_cnt[1];
+            st[6] = 0;
+            st[7] = 0;
+            write_result(reinterpret_cast<long long*>(a.am.results) + pair * 8, Best{bv, bt, bc}, a.am.first_lag, st);
+            a.am.counters[pair] = 0;  // ticket
+            *bar = 0;                 // every CTA of the pair is past the barrier
+        }
+    }
 }
 
+// ------------------------------------------------------------------ host
 
-// launch plan: ~2 CTAs per SM over the whole batch, at least kPopcGroups
-// 32-lag blocks per CTA when there are enough; returns the shared memory
-static size_t popc_plan(const NttCall& c, int64_t nx, PopcArgs& a, int64_t& G, bool fused = false)
+static void popc_window(const NttCall& c, int64_t nx, PopcArgs& a)
 {
-    a.dlo = c.am.t_lo - (nx - 1);
-    a.dhi = c.am.t_hi - (nx - 1);
-    const int64_t nlag = a.dhi - a.dlo + 1;
-    const int64_t nblk = (nlag + 31) / 32;
-    a.nblk = (int)nblk;
-    a.nxw = (int)((nx + 31) / 32);
-    a.nyw = (int)((c.op[1].n + 31) / 32);
-    const int sms = device_sms();
-    // fused (cooperative) launch: every CTA resident at once, one per SM
-    G = fused ? (int64_t)sms / c.batch : ((int64_t)sms + c.batch - 1) / c.batch;
-    const int64_t gmax = (nblk + kPopcGroups - 1) / kPopcGroups;
-    if (G > gmax) G = gmax;
-    if (G > kMaxPartialsLarge) G = kMaxPartialsLarge;
-    if (G < 1) G = 1;
-    const int64_t bpc = (nblk + G - 1) / G;
-    a.bpc = (int)(bpc < INT_MAX ? bpc : INT_MAX);
-    G = (nblk + bpc - 1) / bpc;
-    return (size_t)(2 * a.nxw + 2 * (bpc + a.nxw + 1)) * 4;
+    const int64_t dlo = c.am.t_lo - (nx - 1), dhi = c.am.t_hi - (nx - 1);
+    a.dlo = (int)dlo;
+    a.dhi = (int)dhi;
+    a.nx = (int)nx;
+    a.ny = (int)c.op[1].n;
+    a.nblk = (int)((dhi - dlo + 1 + 31) / 32);
+    a.sxw = (int)((nx + 31) / 32);
+    a.syw = (int)((c.op[1].n + 31) / 32);
+    a.batch = (int)c.batch;
 }
 
-// eligibility: argmax mode, 1-level quantisers on float rows, x <= 2^16
-// samples, planes within 200 KB of shared memory; on AUTO also little enough
-// work that one GPU-wide launch beats the NTT's three (batch * nx * window
-// <= 2^31 code products)
+// dynamic shared memory of a CTA holding blocks of at most `nbmax` blocks:
+// unit prefix, x's planes, the y' window and the accumulators
+static size_t popc_smem(const PopcArgs& a, int64_t nbmax)
+{
+    return (size_t)(((nbmax + 1 + 3) & ~3ll) + 2ll * a.sxw + 2 * (a.sxw + nbmax + 1) + kPcAccBlocks * 32) * 4;
+}
+
+// resident CTAs per SM for a dynamic shared memory size, cached per device
+static int popc_per_sm(size_t smem)
+{
+    static int cache[64][32] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    const int bucket = (int)((smem + 4095) / 4096) < 32 ? (int)((smem + 4095) / 4096) : 31;
+    if (!cache[dev][bucket]) {
+        int n = 0;
+        if (set_max_smem((const void*)k_popc<float, false>, kPcMaxSmem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (const void*)k_popc<float, false>, kPcThreads,
+                                                          (size_t)bucket * 4096) != cudaSuccess || n < 1) {
+            cudaGetLastError();
+            n = 1;
+        }
+        cache[dev][bucket] = n;
+    }
+    return cache[dev][bucket];
+}
+
+// CTAs per pair: every pair's CTAs resident at once (cooperative launch),
+// the SMs shared by the batch, at most one per ~1024 units of work
+static int popc_ctas(const NttCall& c, const PopcArgs& a)
+{
+    const int64_t units = (int64_t)a.nblk * (a.sxw + kPcBlockUnits);
+    const int64_t resident = (int64_t)device_sms() * popc_per_sm(popc_smem(a, a.nblk));
+    int64_t G = resident / c.batch;
+    if (G > (units + 1023) / 1024) G = (units + 1023) / 1024;
+    if (G > a.nblk) G = a.nblk;
+    if (G > kMaxPartialsLarge) G = kMaxPartialsLarge;
+    return G < 1 ? 1 : (int)G;
+}
+
+// contiguous block ranges of G CTAs minimising the largest unit sum (binary
+// search on the bound, greedy fill); out[g] = first block of CTA g
+void popc_schedule(const NttCall& c, int64_t nx, int* G_out, std::vector<int>& out)
+{
+    PopcArgs a;
+    popc_window(c, nx, a);
+    const int G = popc_ctas(c, a);
+    std::vector<int> u((size_t)a.nblk);
+    int64_t total = 0, umax = 0;
+    for (int b = 0; b < a.nblk; ++b) {
+        u[b] = block_units(a.dlo, a.dhi, a.nx, a.ny, b);
+        total += u[b];
+        umax = std::max<int64_t>(umax, u[b]);
+    }
+    auto fits = [&](int64_t cap, std::vector<int>* starts) {
+        int k = 0;
+        int64_t run = 0;
+        if (starts) starts->assign(1, 0);
+        for (int b = 0; b < a.nblk; ++b) {
+            if (run + u[b] > cap && run > 0) {
+                if (++k >= G) return false;
+                if (starts) starts->push_back(b);
+                run = 0;
+            }
+            run += u[b];
+        }
+        return true;
+    };
+    int64_t lo = std::max<int64_t>(umax, (total + G - 1) / G), hi = total;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (fits(mid, nullptr)) hi = mid;
+        else lo = mid + 1;
+    }
+    fits(lo, &out);
+    out.resize((size_t)G + 1, a.nblk);  // trailing CTAs (if any) get empty ranges
+    *G_out = G;
+}
+
+// eligibility: argmax mode, 1-level quantisers on float rows, x <= 2^16 and
+// y <= 2^24 samples, a CTA's shared memory within 200 KB; on AUTO also
+// little enough work that one GPU-wide launch beats the NTT's three
+// (batch * nx * window <= 2^31 code products)
 bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path)
 {
-    (void)ny;
     if (auto_path && !c.knobs->popc) return false;
     if (c.op[0].q.mode != QM_K1 || c.op[1].q.mode != QM_K1) return false;
     if (c.op[0].dtype == DT_I64 || c.op[0].dtype != c.op[1].dtype) return false;
-    if (nx > 65536) return false;
+    if (nx > 65536 || ny > (1 << 24)) return false;
     const double W = (double)(c.am.t_hi - c.am.t_lo + 1);
     if (auto_path && (double)c.batch * (double)nx * W > 2147483648.0) return false;
     PopcArgs a;
-    int64_t G;
-    return popc_plan(c, nx, a, G) <= 200 * 1024;
+    popc_window(c, nx, a);
+    return popc_smem(a, a.nblk) <= (size_t)kPcMaxSmem;
+}
+
+// global plane words of a popc call (scratch)
+size_t popc_planes_words(int64_t batch, int64_t nx, int64_t ny)
+{
+    return (size_t)batch * 2 * ((nx + 31) / 32 + (ny + 31) / 32);
 }
 
 cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s)
 {
     PopcArgs a;
-    for (int i = 0; i < 2; ++i)
-        a.op[i] = PopcOp{c.op[i].data, c.op[i].ld, c.op[i].n, c.op[i].q.thr[0], c.op[i].q.thr[1]};
+    for (int i = 0; i < 2; ++i) a.op[i] = PopcOp{c.op[i].data, c.op[i].ld, c.op[i].q.thr[0], c.op[i].q.thr[1]};
+    popc_window(c, nx, a);
     a.stats = c.stats;
     a.am = c.am;
     a.planes = c.popc_planes;
     a.spart = c.popc_spart;
-    const int sms = device_sms();
-    const bool fused = c.batch <= sms && c.knobs->popc_fused;
-    int64_t G;
-    const size_t smem = popc_plan(c, nx, a, G, fused);
-    if (G > c.am.pstride) return cudaErrorInvalidValue;
-    const int ti = c.op[0].dtype == DT_F32 ? 0 : 1;
-    auto raise = [&](const void* fn, int) -> cudaError_t {
-        return smem > 48 * 1024 ? set_max_smem(fn, smem) : cudaSuccess;
-    };
-    cudaError_t e;
-    if (fused) {
-        const void* fn = ti == 0 ? (const void*)k_popc_fused<float> : (const void*)k_popc_fused<double>;
-        if ((e = raise(fn, ti)) != cudaSuccess) return e;
-        if (c.prof) c.prof->pre(KK_POPC, s);
-        void* args[] = {(void*)&a};
-        e = cudaLaunchCooperativeKernel(fn, dim3((unsigned)G, (unsigned)c.batch), dim3(kPopcThreads), args, smem, s);
-        if (c.prof) c.prof->post(KK_POPC, s);
-        return e != cudaSuccess ? e : cudaGetLastError();
-    }
-    // two launches: planes (statistics by atomics into zeroed records), correlation
-    if ((e = raise((const void*)k_popc, 2)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(c.stats, 0, (size_t)c.batch * 64, s)) != cudaSuccess) return e;
+    a.sched = c.popc_sched;
+    const int G = c.popc_G;
+    if (G > c.am.pstride || !a.sched) return cudaErrorInvalidValue;
+    const size_t smem = popc_smem(a, a.nblk);
+    const bool f32 = c.op[0].dtype == DT_F32, tm = c.knobs->popc_timing != 0;
+    const void* fn = f32 ? (tm ? (const void*)k_popc<float, true> : (const void*)k_popc<float, false>)
+                         : (tm ? (const void*)k_popc<double, true> : (const void*)k_popc<double, false>);
+    if (cudaError_t e = set_max_smem(fn, kPcMaxSmem); e != cudaSuccess) return e;
     if (c.prof) c.prof->pre(KK_POPC, s);
-    const dim3 pgrid((unsigned)((a.nxw + a.nyw + kPopcWarps - 1) / kPopcWarps), (unsigned)c.batch);
-    if (c.op[0].dtype == DT_F32) k_popc_planes<float><<<pgrid, kPopcThreads, 0, s>>>(a);
-    else k_popc_planes<double><<<pgrid, kPopcThreads, 0, s>>>(a);
+    void* args[] = {(void*)&a};
+    // cooperative: the per-pair barrier needs every CTA of the pair resident
+    cudaError_t e = G > 1 ? cudaLaunchCooperativeKernel(fn, dim3((unsigned)G, (unsigned)c.batch), dim3(kPcThreads), args, smem, s)
+                          : cudaLaunchKernel(fn, dim3(1, (unsigned)c.batch), dim3(kPcThreads), args, smem, s);
     if (c.prof) c.prof->post(KK_POPC, s);
-    if (c.prof) c.prof->pre(KK_POPC, s);
-    k_popc<<<dim3((unsigned)G, (unsigned)c.batch), kPopcThreads, smem, s>>>(a);
-    if (c.prof) c.prof->post(KK_POPC, s);
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace qx

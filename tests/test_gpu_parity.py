@@ -277,22 +277,22 @@ def test_popc_path_against_oracle(qx, oracle):
     assert r["status"][0] == 9
 
 
-def test_popc_fused_and_split_launches_agree(qx):
-    """The cooperative single-launch popc kernel and the two-launch version
-    (option popc_fused=0; the form batches larger than the SM count take)
-    give identical records, statistics included."""
+def test_popc_batches_and_cluster_counts(qx):
+    """The cluster popc kernel splits a pair over several 8-CTA clusters
+    (few pairs) or gives each pair one cluster in several waves (batches
+    larger than the resident clusters); every split gives the NTT path's
+    records, statistics included, on random and constant (all-tie) rows."""
     import torch
 
-    from paper_2509_19974_b200 import _native as N
-
     rng = np.random.default_rng(32)
-    for B, nx, ny in ((1, 16384, 16384), (3, 5000, 7001), (148, 300, 257), (200, 64, 64)):
+    for B, nx, ny in ((1, 16384, 16384), (3, 5000, 7001), (40, 300, 257), (200, 64, 64), (2, 65536, 300)):
         x = torch.from_numpy(rng.standard_normal((B, nx)).astype(np.float32)).cuda()
         y = torch.from_numpy(rng.standard_normal((B, ny)).astype(np.float32)).cuda()
+        if B == 3:
+            x[1] = 1.0  # every lag of pair 1 ties on overlap counts
         q = qx.sign()
         a = qx.estimate_batch(x, y, q, q, path="popc").numpy()
-        with N.option("popc_fused", 0):
-            b = qx.estimate_batch(x, y, q, q, path="popc").numpy()
+        b = qx.estimate_batch(x, y, q, q, path="ntt").numpy()
         assert np.array_equal(a, b), (B, nx, ny)
 
 
@@ -786,3 +786,35 @@ def test_calls_on_different_streams_are_ordered(qx):
         assert torch.equal(r1.raw, want1) and torch.equal(r2.raw, want2) and torch.equal(r3.raw, want1)
         assert np.array_equal(h, want2.cpu().numpy().view(h.dtype).reshape(-1))
     assert torch.cuda.current_device() == 0
+
+
+def test_estimate_plan_matches_estimate_batch(qx, oracle):
+    """EstimatePlan (qx_plan_create / qx_plan_run) returns estimate_batch's
+    records on every path, for new rows each call, and re-derives its
+    scratch pointers after another call regrew the context's arenas."""
+    import torch
+
+    rng = np.random.default_rng(77)
+    cases = [  # (B, nx, ny, quantiser, window, expected path)
+        (1, 16384, 16384, qx.sign(), None, "popc"),
+        (3, 3000, 2500, qx.sign(), None, "popc"),
+        (4, 4096, 4096, qx.uniform(1, 0.5), (-512, 512), "direct"),
+        (2, 20000, 30000, qx.uniform(7, 0.3), None, "ntt"),
+    ]
+    for B, nx, ny, q, win, want in cases:
+        lo, hi = win if win else (None, None)
+        x0 = torch.from_numpy(rng.standard_normal((B, nx)).astype(np.float32)).cuda()
+        y0 = torch.from_numpy(rng.standard_normal((B, ny)).astype(np.float32)).cuda()
+        plan = qx.EstimatePlan(x0, y0, q, q, lag_lo=lo, lag_hi=hi)
+        assert plan.path == want, (plan.path, want)
+        for it in range(3):
+            x = torch.from_numpy(rng.standard_normal((B, nx)).astype(np.float32)).cuda()
+            y = torch.from_numpy(rng.standard_normal((B, ny)).astype(np.float32)).cuda()
+            if it == 1:  # regrow the context scratch in between
+                big = torch.zeros((64, 1 << 18), dtype=torch.float32, device="cuda")
+                qx.estimate_batch(big + 1, big + 1, qx.uniform(7, 0.3), qx.uniform(7, 0.3))
+            a = plan(x, y).numpy()
+            b = qx.estimate_batch(x, y, q, q, lag_lo=lo, lag_hi=hi).numpy()
+            assert np.array_equal(a, b), (B, nx, ny, it)
+        with pytest.raises(ValueError):
+            plan(x[:, :-1] if nx > 1 else x, y)

@@ -69,9 +69,11 @@ class C1(Workload):
         self.out = torch.empty((1, 8), dtype=torch.int64, device=dev)
         self.units = world  # one estimate per rank and step
         self.dev = dev
+        # the low-latency serving form of estimate_batch (qx_plan_run: one C-ABI call per estimate)
+        self.plan = P.EstimatePlan(self.xd, self.yd, P.sign(), P.sign())
 
     def step(self):
-        self.P.estimate_batch(self.xd, self.yd, self.P.sign(), self.P.sign(), out=self.out)
+        self.plan(self.xd, self.yd, out=self.out)
 
     def check(self, G):
         r = self.out.cpu().numpy().view(_result_dtype()).reshape(-1)[0]
@@ -287,13 +289,17 @@ class C5(Workload):
         return 2 * (self.hs.numel() + self.ht.numel()) * 4, 2 * 64
 
     def roofline(self, kinds, hbm):
+        # one search = one main-block launch + one remainder-block launch over the rank's valid
+        # lags; the work of a search is divided by the summed time of all its launches
         c, ms = kinds.get("direct_f4", (0, 0.0))
+        searches = self.ksteps * len(self.qs)
         macs = 4096 * (self.hi - self.lo)
         peak = FP4_MACS_PER_CLK_SM * 148 * CLK * 2 / 1e12
-        ach = 2 * macs / (ms / c / 1e3) / 1e12 if c else None
+        ach = 2 * macs / (ms / searches / 1e3) / 1e12 if c else None
         return {"bound": "tensor", "kernel": "direct_f4 (tcgen05 kind::mxf4 template search)", "achieved": ach,
                 "peak": peak, "unit": "TFLOP/s", "frac": ach / peak if ach else None, "traffic": _ncu_traffic("direct_f4"),
-                "note": "2 x 4096 x (valid lags of the rank) flops per launch / the event-timed launch; peak = the "
+                "launches_per_search": c / searches if c else None,
+                "note": "2 x 4096 x (valid lags of the rank) flops per search / the event-timed launches of one search; peak = the "
                         "measured kind::mxf4 rate 16,336 MACs/clk/SM x 148 SMs x 1.965 GHz (profiles/r01_tc_fp4.txt)"}
 
     def cpu(self, CB, cores):
@@ -378,6 +384,7 @@ def run(args):
             wl.step()
         torch.cuda.synchronize()
     hbm, hbm_src = _peaks()
+    wl.ksteps = ksteps
     roof = wl.roofline(kprof.result, hbm)
     roof["peak_source"] = hbm_src if roof.get("unit") == "GB/s" else roof.get("note", "")
     # e2e: the public host API with host buffers, copies inside the timed region

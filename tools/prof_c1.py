@@ -23,6 +23,16 @@ for _ in range(n):
     r = P.estimate_batch(xd, yd, q, q)
 torch.cuda.synchronize()
 print(f"call: {(time.perf_counter() - t0) / n * 1e6:.1f} us")
+plan = P.EstimatePlan(xd, yd, q, q)
+for _ in range(20):
+    plan(xd, yd)
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(n):
+    r = plan(xd, yd)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+print(f"plan call: issue {(t1 - t0) / n * 1e6:.1f} us, with drain {(time.perf_counter() - t0) / n * 1e6:.1f} us")
 with _native.profile(timed=True) as pr:
     for _ in range(n):
         P.estimate_batch(xd, yd, q, q)

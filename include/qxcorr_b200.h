@@ -8,6 +8,8 @@
  *
  *   qx_quantize              <- quantize.apply / Quantizer.__call__
  *                               (quantize.py:53-65, 105-107)
+ *   qx_quantize_packed       <- the same map as bit-packed b-bit codes
+ *                               (b = 1, 2, 4, 8; apply() transfers these)
  *   qx_quantizer_thresholds  <- the same map, as an exact threshold table
  *                               (quantize.py:53-65)
  *   qx_xcorr_full            <- xcorr_int_bf / xcorr_int_ks
@@ -145,6 +147,24 @@ qx_status qx_quantizer_thresholds(const qx_quantizer *q, qx_dtype dtype, double 
  * sum of squares and nonzero counts (sumsq/nnz may be NULL). Device pointers. */
 qx_status qx_quantize(qx_context *ctx, const qx_quantizer *q, const qx_signals *x, int64_t batch,
                       int64_t *codes, int64_t *sumsq, int64_t *nnz, void *stream);
+
+/* Bit-packed codes (the fused quantiser of the north star, subsystem 1):
+ * q(x[b*ld + i]) for every sample, packed little-endian into 32-bit words,
+ * row b at codes + b * qx_packed_words(n, bits):
+ *   bits = 2, 4, 8: two's-complement code of sample i in bits
+ *                   [bits*(i % (32/bits)), +bits) of word i / (32/bits);
+ *                   needs k <= 2^(bits-1) - 1 (QX_ERR_INVALID otherwise);
+ *   bits = 1:       1-level quantisers (k == 1): two planes of ceil(n/32)
+ *                   words, sign (code < 0) then nonzero (code != 0), sample i
+ *                   at bit i % 32 of word i / 32.
+ * Float rows are read with 16-byte vector loads when row starts are 16-byte
+ * aligned.  sumsq / nnz (device int64[batch], optional) receive the per-row
+ * sum of squared codes and nonzero count; flags (device int32, optional)
+ * receives QX_RF_NONFINITE if any sample is NaN.  Enqueued on `stream`. */
+qx_status qx_quantize_packed(qx_context *ctx, const qx_quantizer *q, const qx_signals *x, int64_t batch, int bits,
+                             uint32_t *codes, int64_t *sumsq, int64_t *nnz, int32_t *flags, void *stream);
+/* words per packed row (both planes for bits = 1) */
+int64_t qx_packed_words(int64_t n, int bits);
 
 /* Full correlograms values[b*(nx+ny-1) + t] of q_x(x_b) against q_y(y_b).
  * stats (optional, device) receives sumsq/nnz/flags per pair. */

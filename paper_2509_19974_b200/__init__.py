@@ -29,7 +29,8 @@ from .errors import (
 from .estimator import EstimationResult, argmax_set, estimate, estimate_real
 from .intxcorr import (MUL_BACKENDS, KSPlan, big_mul, pack, plan_ks, unpack_and_correct, xcorr_int_bf, xcorr_int_gpu,
                        xcorr_int_ks)
-from .quantize import Quantizer, apply, custom, from_spec, random_monotone, sign, uniform
+from .quantize import (Quantizer, apply, custom, from_spec, packed_bits, quantize_packed, random_monotone, sign,
+                       uniform, unpack_codes)
 from .realxcorr import xcorr_real_at, xcorr_real_bf, xcorr_real_fft
 from .signals import Correlogram, IntSignal, Signal, add, crop, l2_norm, reverse, scale, shift, trim
 
@@ -39,7 +40,8 @@ __all__ = [
     "QxcorrError", "DegenerateInput", "DegenerateQuantization", "InternalOverflow", "BadLength",
     "ParseError", "UnsupportedFormat", "ConfigError",
     "Signal", "IntSignal", "Correlogram", "reverse", "shift", "l2_norm", "trim", "scale", "add", "crop",
-    "Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "random_monotone",
+    "Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "random_monotone", "quantize_packed",
+    "unpack_codes", "packed_bits",
     "KSPlan", "plan_ks", "pack", "unpack_and_correct",
     "xcorr_int_gpu", "xcorr_int_bf", "xcorr_int_ks", "xcorr_real_at", "xcorr_real_bf", "xcorr_real_fft", "big_mul",
     "MUL_BACKENDS",

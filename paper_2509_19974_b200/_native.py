@@ -81,6 +81,7 @@ EXPORTS = (
     "qx_profile_end",
     "qx_profile_kind_name", "qx_summary_reduce_nccl", "qx_template_search_nccl", "qx_estimate_batch_nccl",
     "qx_comm_rank_size", "qx_plan_create", "qx_plan_run", "qx_plan_path", "qx_plan_destroy",
+    "qx_quantize_packed", "qx_packed_words",
 )
 
 _lib = None
@@ -116,6 +117,10 @@ def load():
         qp, sp = ctypes.POINTER(QxQuantizer), ctypes.POINTER(QxSignals)
         L.qx_quantizer_thresholds.argtypes = [qp, ctypes.c_int, vp]
         L.qx_quantizer_thresholds.restype = st
+        L.qx_quantize_packed.argtypes = [vp, qp, sp, i64, ctypes.c_int, vp, vp, vp, vp, vp]
+        L.qx_quantize_packed.restype = st
+        L.qx_packed_words.argtypes = [i64, ctypes.c_int]
+        L.qx_packed_words.restype = i64
         L.qx_quantize.argtypes = [vp, qp, sp, i64, vp, vp, vp, vp]
         L.qx_quantize.restype = st
         L.qx_xcorr_full.argtypes = [vp, sp, sp, i64, qp, qp, vp, vp, st, vp]

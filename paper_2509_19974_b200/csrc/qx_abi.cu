@@ -20,6 +20,10 @@ namespace qx {
 int thresholds(int kind, long long k, double step, const double* thr, int dtype, double* out);
 cudaError_t quantize_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
                             int64_t* codes, unsigned long long* sums, unsigned* flags, cudaStream_t s);
+int64_t packed_words(int64_t n, int bits);
+cudaError_t quantize_packed_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
+                                   int bits, uint32_t* codes, unsigned long long* sums, unsigned* flags, int sms,
+                                   cudaStream_t s);
 cudaError_t stats_to_results(const unsigned long long* stats, void* results, int64_t batch, cudaStream_t s);
 cudaError_t pcm16_launch(const void* in, int64_t n, float* out, int sms, cudaStream_t s);
 bool tc_window_eligible(const NttCall& c, int64_t nx, int64_t ny);
@@ -695,6 +699,51 @@ qx_status qx_quantize(qx_context* ctx, const qx_quantizer* q, const qx_signals* 
 // qx_estimate_batch on explicit scratch arenas (the sweep's compute lanes)
 // split2: `results` holds two records per pair and the 2-SM template-search
 // mode may write them (qx_template_search)
+extern "C" {
+
+qx_status qx_quantize_packed(qx_context* ctx, const qx_quantizer* q, const qx_signals* x, int64_t batch, int bits,
+                             uint32_t* codes, int64_t* sumsq, int64_t* nnz, int32_t* flags, void* stream)
+{
+    if (!ctx) return QX_ERR_INVALID;
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    StreamOrder order(ctx, (cudaStream_t)stream);
+    qx_status st;
+    if (batch < 1 || !codes) return fail(ctx, QX_ERR_INVALID, "bad batch or output");
+    if ((st = check_signals(ctx, x, "x")) != QX_OK) return st;
+    if ((st = check_quantizer(ctx, q, x->dtype)) != QX_OK) return st;
+    if (q->kind == QX_Q_CODES) return fail(ctx, QX_ERR_INVALID, "input already quantised");
+    if (bits != 1 && bits != 2 && bits != 4 && bits != 8) return fail(ctx, QX_ERR_INVALID, "bits must be 1, 2, 4 or 8");
+    if (bits == 1 && q->k != 1) return fail(ctx, QX_ERR_INVALID, "1-bit planes need a 1-level quantizer (k == 1)");
+    if (bits > 1 && q->k > (1 << (bits - 1)) - 1)
+        return fail(ctx, QX_ERR_INVALID, "level bound k does not fit the packed field (k <= 2^(bits-1) - 1)");
+    QTable t;
+    if ((st = make_qtable(ctx, q, x->dtype, &t)) != QX_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = arena_reserve(ctx->scratch, (size_t)batch * 16 + 64, false);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "scratch");
+    unsigned long long* sums = (unsigned long long*)ctx->scratch.ptr;
+    unsigned* fl = (unsigned*)((char*)ctx->scratch.ptr + batch * 16);
+    e = cudaMemsetAsync(ctx->scratch.ptr, 0, (size_t)batch * 16 + 64, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "memset");
+    ctx->prof.pre(KK_QUANT, s);
+    e = quantize_packed_launch(x->data, x->ld, x->n, batch, x->dtype == QX_F32 ? DT_F32 : DT_F64, t, bits, codes, sums,
+                               fl, device_sms(), s);
+    ctx->prof.post(KK_QUANT, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "quantize");
+    if (sumsq && (e = cudaMemcpy2DAsync(sumsq, 8, sums, 16, 8, (size_t)batch, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return cuda_fail(ctx, e, "copy sums");
+    if (nnz && (e = cudaMemcpy2DAsync(nnz, 8, sums + 1, 16, 8, (size_t)batch, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return cuda_fail(ctx, e, "copy nnz");
+    if (flags && (e = cudaMemcpyAsync(flags, fl, 4, cudaMemcpyDeviceToDevice, s)) != cudaSuccess)
+        return cuda_fail(ctx, e, "copy flags");
+    return QX_OK;
+}
+
+int64_t qx_packed_words(int64_t n, int bits) { return packed_words(n, bits); }
+
+}  // extern "C"
+
 static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const qx_signals* y, int64_t batch,
                                    const qx_quantizer* qx_, const qx_quantizer* qy_, int64_t lag_lo, int64_t lag_hi,
                                    qx_path path, qx_result* results, void* stream, Arena* scratch, Arena* counters,

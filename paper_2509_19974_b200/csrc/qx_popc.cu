@@ -47,7 +47,7 @@ constexpr int kPcThreads = 1024;  // one CTA per SM
 constexpr int kPcWarps = kPcThreads / 32;
 constexpr int kPcWordsPerWarp = 4;   // plane words per warp per round (loads in flight)
 constexpr int kPcAccBlocks = 128;    // 32-lag block accumulators per pass of a CTA
-constexpr int kPcBlockUnits = 48;    // per-block overhead in x-word units (setup, edge words, flush; measured)
+constexpr int kPcBlockUnits = 28;    // per-block overhead in x-word units (setup, edge words, flush; measured)
 constexpr int kPcMaxSmem = 200 * 1024;
 constexpr unsigned kPcZeroCode = 0x100u;  // spart flag: a code 0 inside a signal
 

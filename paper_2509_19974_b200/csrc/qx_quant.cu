@@ -139,6 +139,179 @@ __global__ void __launch_bounds__(256) k_quantize(const __grid_constant__ QuantA
 }
 
 
+// Bit-packed codes (BASELINE north_star subsystem 1): every thread quantises
+// 4 consecutive samples from one 16-byte (float4) or two 16-byte (double2)
+// vector loads, 32 / (4 BITS) neighbouring lanes OR their fields into one
+// little-endian 32-bit word (sample i at bit BITS * (i % (32 / BITS))), and
+// the first lane of the group stores it.  BITS = 2, 4, 8 hold the code in
+// two's complement; BITS = 1 writes two planes, sign (code < 0) then nonzero
+// (code != 0), for 1-level quantisers.  Per-row sum of squares / nonzero
+// counts are reduced per CTA (one 64-bit atomic per CTA and row).
+struct PackArgs {
+    const void* x;
+    int64_t ld, n, batch;
+    uint32_t* codes;
+    int64_t wpr;               // words per row (both planes for BITS = 1)
+    unsigned long long* sums;  // [batch][2]: sumsq, nnz
+    unsigned* flags;           // QX_RF_NONFINITE if any row holds a NaN
+    int vec;                   // rows 16-byte aligned: vector loads
+    QTable q;
+};
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* row, int64_t i, int64_t n, bool vec, T (&v)[4])
+{
+    if (vec && i + 3 < n) {
+        if constexpr (sizeof(T) == 4) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(row + i));
+            v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+        } else {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(row + i));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(row + i + 2));
+            v[0] = a.x, v[1] = a.y, v[2] = b.x, v[3] = b.y;
+        }
+        return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = i + k < n ? row[i + k] : (T)0;  // level(0) = 0 (padding)
+}
+
+template <typename T, int QM, int BITS>
+__global__ void __launch_bounds__(256) k_quantize_packed(const __grid_constant__ PackArgs a)
+{
+    __shared__ T sthr[kMaxThr];
+    __shared__ unsigned long long s_sum[2];
+    __shared__ unsigned s_fl;
+    for (int i = threadIdx.x; i < a.q.tsize; i += blockDim.x) sthr[i] = (T)a.q.thr[i];
+    if (threadIdx.x < 2) s_sum[threadIdx.x] = 0;
+    if (threadIdx.x == 0) s_fl = 0;
+    __syncthreads();
+    const int64_t b = blockIdx.y;
+    const T* row = reinterpret_cast<const T*>(a.x) + b * a.ld;
+    uint32_t* out = a.codes + b * a.wpr;
+    const T t0 = sthr[0], t1 = sthr[1], inv_step = (T)a.q.inv_step;
+    constexpr int LPW = BITS == 1 ? 8 : 32 / (4 * BITS);  // lanes per output word
+    const int lane = threadIdx.x & 31;
+    const int64_t nq = (a.n + 3) / 4;  // 4-sample quads, padded to whole words below
+    const int64_t nqw = (nq + LPW - 1) / LPW * LPW;
+    const int64_t nw1 = (a.n + 31) / 32;  // plane words (BITS = 1)
+    unsigned long long ssq = 0, nnz = 0;
+    bool nan = false;
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x; q0 < nqw; q0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t qi = q0 + threadIdx.x;  // warp-uniform trip count: lanes past the end quantise zeros
+        T v[4];
+        load4(row, 4 * qi, a.n, a.vec, v);
+        uint32_t f = 0, zf = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            int c;
+            if constexpr (QM == QM_K1) c = level_k1(v[k], t0, t1);
+            else if constexpr (QM == QM_UNIFORM) c = level_uniform(v[k], sthr, a.q.k, inv_step);
+            else c = level_bsearch(v[k], sthr, a.q.tbits) - a.q.k;
+            nan |= v[k] != v[k];
+            ssq += (unsigned)(c * c);
+            nnz += c != 0;
+            if constexpr (BITS == 1) {
+                f |= (uint32_t)(c < 0) << k;
+                zf |= (uint32_t)(c != 0) << k;
+            } else {
+                f |= ((uint32_t)c & ((1u << BITS) - 1u)) << (BITS * k);
+            }
+        }
+        const int sh = (lane % LPW) * 4 * BITS;
+        f <<= sh;
+        zf <<= sh;
+#pragma unroll
+        for (int o = 1; o < LPW; o <<= 1) {
+            f |= __shfl_xor_sync(0xffffffffu, f, o);
+            zf |= __shfl_xor_sync(0xffffffffu, zf, o);
+        }
+        const int64_t w = qi / LPW;  // output word
+        if (lane % LPW == 0) {
+            if constexpr (BITS == 1) {
+                if (w < nw1) {
+                    out[w] = f;
+                    out[nw1 + w] = zf;
+                }
+            } else if (w < a.wpr) {
+                out[w] = f;
+            }
+        }
+    }
+    // per-CTA sums (warp shuffles, then one shared atomic per warp)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
+        nnz += __shfl_xor_sync(0xffffffffu, nnz, o);
+    }
+    nan = __any_sync(0xffffffffu, nan);
+    if (lane == 0) {
+        atomicAdd(&s_sum[0], ssq);
+        atomicAdd(&s_sum[1], nnz);
+        if (nan) atomicOr(&s_fl, 4u);  // QX_RF_NONFINITE (qxcorr_b200.h)
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (a.sums) {
+            if (s_sum[0]) atomicAdd(a.sums + 2 * b, s_sum[0]);
+            if (s_sum[1]) atomicAdd(a.sums + 2 * b + 1, s_sum[1]);
+        }
+        if (s_fl) atomicOr(a.flags, s_fl);
+    }
+}
+
+template <typename T, int QM>
+static void packed_dispatch_bits(int bits, dim3 grid, const PackArgs& a, cudaStream_t s)
+{
+    switch (bits) {
+    case 1: k_quantize_packed<T, QM, 1><<<grid, 256, 0, s>>>(a); break;
+    case 2: k_quantize_packed<T, QM, 2><<<grid, 256, 0, s>>>(a); break;
+    case 4: k_quantize_packed<T, QM, 4><<<grid, 256, 0, s>>>(a); break;
+    default: k_quantize_packed<T, QM, 8><<<grid, 256, 0, s>>>(a); break;
+    }
+}
+
+// words per row of a packed row of n samples
+int64_t packed_words(int64_t n, int bits)
+{
+    return bits == 1 ? 2 * ((n + 31) / 32) : (n * bits + 31) / 32;
+}
+
+cudaError_t quantize_packed_launch(const void* x, int64_t ld, int64_t n, int64_t batch, int dtype, const QTable& q,
+                                   int bits, uint32_t* codes, unsigned long long* sums, unsigned* flags, int sms,
+                                   cudaStream_t s)
+{
+    PackArgs a;
+    a.x = x;
+    a.ld = ld;
+    a.n = n;
+    a.batch = batch;
+    a.codes = codes;
+    a.wpr = packed_words(n, bits);
+    a.sums = sums;
+    a.flags = flags;
+    const size_t es = dtype == DT_F32 ? 4 : 8;
+    a.vec = ((uintptr_t)x % 16 == 0) && ((ld * es) % 16 == 0);
+    a.q = q;
+    // CTAs: ~4 per SM over the whole batch, at least one per row
+    const int64_t quads = (n + 3) / 4;
+    int64_t gx = (quads + 255) / 256;
+    const int64_t cap = (4 * (int64_t)sms + batch - 1) / batch;
+    if (gx > cap) gx = cap;
+    if (gx < 1) gx = 1;
+    const dim3 grid((unsigned)gx, (unsigned)batch);
+    if (dtype == DT_F32) {
+        if (q.mode == QM_K1) packed_dispatch_bits<float, QM_K1>(bits, grid, a, s);
+        else if (q.mode == QM_UNIFORM) packed_dispatch_bits<float, QM_UNIFORM>(bits, grid, a, s);
+        else packed_dispatch_bits<float, QM_BSEARCH>(bits, grid, a, s);
+    } else {
+        if (q.mode == QM_K1) packed_dispatch_bits<double, QM_K1>(bits, grid, a, s);
+        else if (q.mode == QM_UNIFORM) packed_dispatch_bits<double, QM_UNIFORM>(bits, grid, a, s);
+        else packed_dispatch_bits<double, QM_BSEARCH>(bits, grid, a, s);
+    }
+    return cudaGetLastError();
+}
+
 // PCM16 (little-endian int16) -> float32 pcm / 32768, the sample decode of
 // signalgen.load_wav_bytes (signalgen.py:150-172) on the device.  Exact:
 // every value is a multiple of 2^-15 with at most 16 significant bits, so

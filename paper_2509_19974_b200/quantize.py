@@ -20,7 +20,7 @@ from . import _native as N
 from .signals import IntSignal, Signal
 
 __all__ = ["Quantizer", "sign", "uniform", "custom", "from_spec", "apply", "random_monotone",
-           "native_quantizer", "thresholds"]
+           "native_quantizer", "thresholds", "quantize_packed", "unpack_codes", "packed_bits"]
 
 
 @dataclass(frozen=True)
@@ -161,8 +161,72 @@ def quantize_device(q, x, with_stats: bool = False):
     return codes
 
 
+def packed_bits(q) -> int:
+    """Narrowest packed field that holds every code of q (0: none does)."""
+    k = int(q.k)
+    return 2 if k <= 1 else 4 if k <= 7 else 8 if k <= 127 else 0
+
+
+def quantize_packed(q, x, bits: int | None = None):
+    """Bit-packed codes of a CUDA tensor x ((n,) or (batch, n), float32 or
+    float64) through qx_quantize_packed: (codes, sumsq, nnz, flags) with codes
+    a uint32 tensor (batch, qx_packed_words(n, bits)) in the layout of
+    include/qxcorr_b200.h (two's-complement b-bit fields for bits = 2, 4, 8;
+    sign and nonzero planes for bits = 1), per-row int64 sums of squared codes
+    and nonzero counts, and an int32 flag word (QX_RF_NONFINITE on NaN).
+    `bits` defaults to the narrowest field holding the quantiser's codes."""
+    t = D.torch()
+    if x.dtype not in (t.float32, t.float64):
+        x = x.to(t.float64)
+    bits = packed_bits(q) if bits is None else int(bits)
+    if bits not in (1, 2, 4, 8):
+        raise ValueError(f"no packed field holds codes of level bound {q.k}; use quantize_device")
+    batch = x.shape[0] if x.dim() == 2 else 1
+    n = x.shape[-1]
+    L = N.load()
+    words = L.qx_packed_words(n, bits)
+    codes = t.empty((batch, words), dtype=t.int32, device=x.device)
+    sums = t.zeros((2, batch), dtype=t.int64, device=x.device)
+    flags = t.zeros(1, dtype=t.int32, device=x.device)
+    nq, keep = native_quantizer(q)
+    sig = D.signals(x)
+    ctx = N.context(x.device.index)
+    from ._call import call  # (status -> the reference's exception types)
+
+    call(L.qx_quantize_packed, ctx, ctypes.byref(nq), ctypes.byref(sig), batch, bits, codes.data_ptr(),
+         sums[0].data_ptr(), sums[1].data_ptr(), flags.data_ptr(), D.stream_handle())
+    del keep
+    return codes, sums[0], sums[1], flags
+
+
+def unpack_codes(words: np.ndarray, n: int, bits: int) -> np.ndarray:
+    """int64 codes of one packed row (the layout of qx_quantize_packed) on the
+    host: a format decode for IntSignal, no quantisation."""
+    b = np.ascontiguousarray(words).view(np.uint8)
+    if bits == 8:
+        return b.view(np.int8)[:n].astype(np.int64)
+    if bits == 1:
+        nw = (n + 31) // 32
+        bb = np.unpackbits(b, bitorder="little")
+        sgn, nz = bb[: 32 * nw][:n].astype(np.int64), bb[32 * nw:][:n].astype(np.int64)
+        return nz * (1 - 2 * sgn)
+    per = 8 // bits
+    f = np.stack([(b >> (bits * k)) & ((1 << bits) - 1) for k in range(per)], axis=-1).reshape(-1)[:n]
+    half = 1 << (bits - 1)
+    return (f.astype(np.int64) ^ half) - half
+
+
 def apply(q, s) -> IntSignal:
-    """Quantise every stored sample; start and length preserved (quantize.py:105-107)."""
-    samples = np.asarray(s.samples, dtype=np.float64)
-    codes = quantize_device(q, D.as_device(samples))
-    return IntSignal(s.start, codes.cpu().numpy(), bound=q.k)
+    """Quantise every stored sample; start and length preserved (quantize.py:105-107).
+
+    The device writes bit-packed codes (2/4/8 bits for k <= 1/7/127), so the
+    transfer back is n*b/8 bytes instead of 8n; the host only unpacks them."""
+    samples = np.asarray(s.samples)
+    if samples.dtype not in (np.float32, np.float64):
+        samples = samples.astype(np.float64)
+    bits = packed_bits(q)
+    if not bits:
+        codes = quantize_device(q, D.as_device(samples))
+        return IntSignal(s.start, codes.cpu().numpy().reshape(-1), bound=q.k)
+    words, _, _, _ = quantize_packed(q, D.as_device(samples), bits)
+    return IntSignal(s.start, unpack_codes(words.cpu().numpy().reshape(-1), samples.shape[-1], bits), bound=q.k)

@@ -147,3 +147,37 @@ def test_estimate_real_fft_on_gpu():
         bf = P.xcorr_real_bf(x, y)
         ff = P.xcorr_real_fft(x, y)
         assert bf.first_lag == ff.first_lag and np.max(np.abs(bf.values - ff.values)) <= 1e-9 * P.l2_norm(x) * P.l2_norm(y)
+
+
+def test_unpack_codes_layout():
+    """unpack_codes decodes the qx_quantize_packed layout of
+    include/qxcorr_b200.h (two's-complement b-bit fields, little-endian in
+    32-bit words; sign + nonzero planes for b = 1) -- checked against an
+    independent bit-by-bit packer."""
+    import numpy as np
+
+    from paper_2509_19974_b200.quantize import packed_bits, unpack_codes
+    import paper_2509_19974_b200 as P
+
+    rng = np.random.default_rng(5)
+    for bits in (2, 4, 8):
+        k = (1 << (bits - 1)) - 1
+        for n in (1, 3, 31, 32, 33, 1000):
+            c = rng.integers(-k, k + 1, n)
+            per = 32 // bits
+            words = np.zeros((n + per - 1) // per, dtype=np.uint32)
+            for i, v in enumerate(c):
+                words[i // per] |= np.uint32((int(v) & ((1 << bits) - 1)) << (bits * (i % per)))
+            assert np.array_equal(unpack_codes(words, n, bits), c), (bits, n)
+    for n in (1, 32, 33, 777):
+        c = rng.integers(-1, 2, n)
+        nw = (n + 31) // 32
+        w = np.zeros(2 * nw, dtype=np.uint32)
+        for i, v in enumerate(c):
+            if v < 0:
+                w[i // 32] |= np.uint32(1 << (i % 32))
+            if v:
+                w[nw + i // 32] |= np.uint32(1 << (i % 32))
+        assert np.array_equal(unpack_codes(w, n, 1), c), n
+    assert [packed_bits(q) for q in (P.sign(), P.uniform(7, 1.0), P.uniform(8, 1.0), P.uniform(127, 1.0),
+                                     P.uniform(128, 1.0))] == [2, 4, 8, 8, 0]

@@ -49,6 +49,54 @@ def test_quantize_kernel_matches_reference(qx, golden, qrec):
         assert int(sums[1, 0]) == int(np.count_nonzero(want))
 
 
+def test_packed_quantizer_matches_reference(qx, golden, qrec, oracle):
+    """qx_quantize_packed (bit-packed b-bit codes, 16-byte vector loads) gives
+    the reference's codes: every golden quantiser sweep (+-0, subnormals,
+    +-inf, half-steps +-1 ulp) at every field width that holds it, then random
+    rows of both float types with misaligned row strides (the scalar-load
+    path), lengths not multiple of 4 or 32, and per-row statistics."""
+    import torch
+
+    from paper_2509_19974_b200.quantize import packed_bits, quantize_packed, unpack_codes
+
+    meta, arr = golden
+    for i, qd in enumerate(meta["quant"]):
+        q = qrec(qd)
+        vals, want = arr[f"q{i}_in"], arr[f"q{i}_out"]
+        x = torch.from_numpy(vals).cuda()
+        for bits in (1, 2, 4, 8):
+            if (bits == 1 and q.k != 1) or (bits > 1 and q.k > (1 << (bits - 1)) - 1):
+                continue
+            w, ssq, nnz, fl = quantize_packed(q, x, bits)
+            got = unpack_codes(w.cpu().numpy().reshape(-1), vals.size, bits)
+            assert np.array_equal(got, want), (i, qd, bits)
+            assert int(ssq[0]) == int(np.sum(want * want)) and int(nnz[0]) == int(np.count_nonzero(want))
+            assert int(fl[0]) == 0
+    rng = np.random.default_rng(41)
+    quants = [qx.sign(), qx.uniform(1, 0.6), qx.uniform(7, 0.3), qx.uniform(127, 0.02), qx.custom([-1.0, -0.2, 0.3, 0.9])]
+    for trial in range(30):
+        q = quants[trial % len(quants)]
+        dt = np.float32 if trial % 2 else np.float64
+        B, n = int(rng.integers(1, 5)), int(rng.integers(1, 5000))
+        ld = n + int(rng.integers(0, 3))  # odd strides defeat 16-byte alignment
+        buf = (rng.standard_normal((B, ld)) * 2).astype(dt)
+        x = torch.from_numpy(buf).cuda()[:, :n]
+        bits = packed_bits(q) if trial % 3 else (1 if q.k == 1 else packed_bits(q))
+        w, ssq, nnz, fl = quantize_packed(q, x, bits)
+        w = w.cpu().numpy()
+        for b in range(B):
+            want = oracle.quantize(q, buf[b, :n])
+            assert np.array_equal(unpack_codes(w[b], n, bits), want), (trial, b)
+            assert int(ssq[b]) == int(np.sum(want * want)) and int(nnz[b]) == int(np.count_nonzero(want))
+    # NaN is flagged; fields that cannot hold the codes are refused
+    x = torch.tensor([0.5, float("nan"), -2.0], dtype=torch.float32, device="cuda")
+    assert int(quantize_packed(qx.sign(), x, 2)[3][0]) == 4
+    with pytest.raises(ValueError):
+        quantize_packed(qx.uniform(7, 0.3), x, 2)
+    with pytest.raises(ValueError):
+        quantize_packed(qx.uniform(2, 0.3), x, 1)
+
+
 def test_apply_and_call(qx):
     q = qx.uniform(4, 1.0)
     assert q([0.49, 0.5, 1.49, 1.5, -0.5, -1.5]).tolist() == [0, 1, 1, 2, -1, -2]

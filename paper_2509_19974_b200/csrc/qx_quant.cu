@@ -176,6 +176,8 @@ __device__ __forceinline__ void load4(const T* row, int64_t i, int64_t n, bool v
     for (int k = 0; k < 4; ++k) v[k] = i + k < n ? row[i + k] : (T)0;  // level(0) = 0 (padding)
 }
 
+constexpr int kPackUnroll = 4;  // 4-sample quads per thread and trip (16-64 B in flight each)
+
 template <typename T, int QM, int BITS>
 __global__ void __launch_bounds__(256) k_quantize_packed(const __grid_constant__ PackArgs a)
 {
@@ -197,44 +199,52 @@ __global__ void __launch_bounds__(256) k_quantize_packed(const __grid_constant__
     const int64_t nw1 = (a.n + 31) / 32;  // plane words (BITS = 1)
     unsigned long long ssq = 0, nnz = 0;
     bool nan = false;
-    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x; q0 < nqw; q0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t qi = q0 + threadIdx.x;  // warp-uniform trip count: lanes past the end quantise zeros
-        T v[4];
-        load4(row, 4 * qi, a.n, a.vec, v);
-        uint32_t f = 0, zf = 0;
+    // kPackUnroll quads per thread and trip, every load issued before the first use
+    const int64_t span = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x; q0 < nqw; q0 += span * kPackUnroll) {
+        T v[kPackUnroll][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            int c;
-            if constexpr (QM == QM_K1) c = level_k1(v[k], t0, t1);
-            else if constexpr (QM == QM_UNIFORM) c = level_uniform(v[k], sthr, a.q.k, inv_step);
-            else c = level_bsearch(v[k], sthr, a.q.tbits) - a.q.k;
-            nan |= v[k] != v[k];
-            ssq += (unsigned)(c * c);
-            nnz += c != 0;
-            if constexpr (BITS == 1) {
-                f |= (uint32_t)(c < 0) << k;
-                zf |= (uint32_t)(c != 0) << k;
-            } else {
-                f |= ((uint32_t)c & ((1u << BITS) - 1u)) << (BITS * k);
-            }
-        }
-        const int sh = (lane % LPW) * 4 * BITS;
-        f <<= sh;
-        zf <<= sh;
+        for (int u = 0; u < kPackUnroll; ++u) load4(row, 4 * (q0 + u * span + threadIdx.x), a.n, a.vec, v[u]);
 #pragma unroll
-        for (int o = 1; o < LPW; o <<= 1) {
-            f |= __shfl_xor_sync(0xffffffffu, f, o);
-            zf |= __shfl_xor_sync(0xffffffffu, zf, o);
-        }
-        const int64_t w = qi / LPW;  // output word
-        if (lane % LPW == 0) {
-            if constexpr (BITS == 1) {
-                if (w < nw1) {
-                    out[w] = f;
-                    out[nw1 + w] = zf;
+        for (int u = 0; u < kPackUnroll; ++u) {
+            const int64_t qi = q0 + u * span + threadIdx.x;  // lanes past the end quantise zeros
+            if (q0 + u * span >= nqw) break;                // warp-uniform (span, q0 multiples of 32)
+            uint32_t f = 0, zf = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const T x = v[u][k];
+                int c;
+                if constexpr (QM == QM_K1) c = level_k1(x, t0, t1);
+                else if constexpr (QM == QM_UNIFORM) c = level_uniform(x, sthr, a.q.k, inv_step);
+                else c = level_bsearch(x, sthr, a.q.tbits) - a.q.k;
+                nan |= x != x;
+                ssq += (unsigned)(c * c);
+                nnz += c != 0;
+                if constexpr (BITS == 1) {
+                    f |= (uint32_t)(c < 0) << k;
+                    zf |= (uint32_t)(c != 0) << k;
+                } else {
+                    f |= ((uint32_t)c & ((1u << BITS) - 1u)) << (BITS * k);
                 }
-            } else if (w < a.wpr) {
-                out[w] = f;
+            }
+            const int sh = (lane % LPW) * 4 * BITS;
+            f <<= sh;
+            zf <<= sh;
+#pragma unroll
+            for (int o = 1; o < LPW; o <<= 1) {
+                f |= __shfl_xor_sync(0xffffffffu, f, o);
+                zf |= __shfl_xor_sync(0xffffffffu, zf, o);
+            }
+            const int64_t w = qi / LPW;  // output word
+            if (lane % LPW == 0) {
+                if constexpr (BITS == 1) {
+                    if (w < nw1) {
+                        out[w] = f;
+                        out[nw1 + w] = zf;
+                    }
+                } else if (w < a.wpr) {
+                    out[w] = f;
+                }
             }
         }
     }
@@ -293,10 +303,10 @@ cudaError_t quantize_packed_launch(const void* x, int64_t ld, int64_t n, int64_t
     const size_t es = dtype == DT_F32 ? 4 : 8;
     a.vec = ((uintptr_t)x % 16 == 0) && ((ld * es) % 16 == 0);
     a.q = q;
-    // CTAs: ~4 per SM over the whole batch, at least one per row
+    // CTAs: ~8 per SM over the whole batch, at least one per row
     const int64_t quads = (n + 3) / 4;
-    int64_t gx = (quads + 255) / 256;
-    const int64_t cap = (4 * (int64_t)sms + batch - 1) / batch;
+    int64_t gx = (quads + 256 * kPackUnroll - 1) / (256 * kPackUnroll);
+    const int64_t cap = (8 * (int64_t)sms + batch - 1) / batch;
     if (gx > cap) gx = cap;
     if (gx < 1) gx = 1;
     const dim3 grid((unsigned)gx, (unsigned)batch);

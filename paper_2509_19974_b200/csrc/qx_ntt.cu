@@ -908,6 +908,104 @@ __device__ __forceinline__ void dit_full(uint32_t (&x)[1 << LOGM], const uint2* 
     }
 }
 
+// Constant-geometry (Pease) forms of dif_full / dit_full with identical
+// outputs: every stage pairs positions j and j + M/2 (DIF) or 2j and 2j + 1
+// (DIT) and writes the other array, so one unrolled two-stage body serves
+// every stage pair in a runtime loop.  The fully unrolled forms above are
+// ~M/2 * log2(M) butterflies of straight-line code per kernel (the C4
+// k_outer_fwd instance was 6.9K SASS instructions, instruction-fetch bound:
+// no_instruction stalls); these are one loop body of 2 * M/2 butterflies.
+// Stage s twiddle exponents: DIF (j >> s) << s, DIT (j >> (L-1-s)) << (L-1-s)
+// (both checked against the standard forms in tools/ntt_model.py).
+template <int LOGM>
+__device__ __forceinline__ void dif_cg_stage(const uint32_t (&x)[1 << LOGM], uint32_t (&y)[1 << LOGM], int s,
+                                             const uint2* tw, const ModP& m)
+{
+    constexpr int H = 1 << (LOGM - 1);
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        uint32_t u = x[j], v = x[j + H];
+        bfly_dif(u, v, tw[(j >> s) << s], m);
+        y[2 * j] = u;
+        y[2 * j + 1] = v;
+    }
+}
+
+template <int LOGM>
+__device__ __forceinline__ void dit_cg_stage(const uint32_t (&x)[1 << LOGM], uint32_t (&y)[1 << LOGM], int s,
+                                             const uint2* tw, const ModP& m)
+{
+    constexpr int H = 1 << (LOGM - 1);
+    const int sh = LOGM - 1 - s;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+        uint32_t u = x[2 * j], v = x[2 * j + 1];
+        bfly_dit(u, v, tw[(j >> sh) << sh], m);
+        y[j] = u;
+        y[j + H] = v;
+    }
+}
+
+// natural -> bit-reversed DIF, values in [0, 2p); result in x
+template <int LOGM>
+__device__ __forceinline__ void dif_cg(uint32_t (&x)[1 << LOGM], const uint2* tw, const ModP& m)
+{
+    uint32_t y[1 << LOGM];
+#pragma unroll 1
+    for (int s = 0; s + 1 < LOGM; s += 2) {
+        dif_cg_stage<LOGM>(x, y, s, tw, m);
+        dif_cg_stage<LOGM>(y, x, s + 1, tw, m);
+    }
+    if constexpr (LOGM & 1) {
+        dif_cg_stage<LOGM>(x, y, LOGM - 1, tw, m);
+#pragma unroll
+        for (int i = 0; i < (1 << LOGM); ++i) x[i] = y[i];
+    }
+}
+
+// dif_cg for inputs whose upper half is zero (x[j + M/2] == 0): stage 0
+// is a copy and one product per pair, the remaining stages as dif_cg
+template <int LOGM>
+__device__ __forceinline__ void dif_cg_zu(uint32_t (&x)[1 << LOGM], const uint2* tw, const ModP& m)
+{
+    constexpr int H = 1 << (LOGM - 1);
+    uint32_t y[1 << LOGM];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {  // (u, 0) -> (u, u * omega^j); inputs in [0, p)
+        const uint2 w = tw[j];
+        y[2 * j] = x[j];
+        y[2 * j + 1] = shoup(x[j], w.x, w.y, m.p);
+    }
+#pragma unroll 1
+    for (int s = 1; s + 1 < LOGM; s += 2) {
+        dif_cg_stage<LOGM>(y, x, s, tw, m);
+        dif_cg_stage<LOGM>(x, y, s + 1, tw, m);
+    }
+    if constexpr ((LOGM - 1) & 1) {
+        dif_cg_stage<LOGM>(y, x, LOGM - 1, tw, m);
+    } else {
+#pragma unroll
+        for (int i = 0; i < (1 << LOGM); ++i) x[i] = y[i];
+    }
+}
+
+// bit-reversed -> natural DIT, values in [0, 4p); result in x
+template <int LOGM>
+__device__ __forceinline__ void dit_cg(uint32_t (&x)[1 << LOGM], const uint2* tw, const ModP& m)
+{
+    uint32_t y[1 << LOGM];
+#pragma unroll 1
+    for (int s = 0; s + 1 < LOGM; s += 2) {
+        dit_cg_stage<LOGM>(x, y, s, tw, m);
+        dit_cg_stage<LOGM>(y, x, s + 1, tw, m);
+    }
+    if constexpr (LOGM & 1) {
+        dit_cg_stage<LOGM>(x, y, LOGM - 1, tw, m);
+#pragma unroll
+        for (int i = 0; i < (1 << LOGM); ++i) x[i] = y[i];
+    }
+}
+
 constexpr int brev_c(int r, int bits)
 {
     int o = 0;
@@ -942,12 +1040,13 @@ __device__ __forceinline__ void apply_column_twiddles(uint32_t (&x)[1 << LOGM], 
     }
 }
 
-template <int LOGM, typename T, int QM>
+template <int LOGM, typename T, int QM, bool ZU>
 __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_constant__ OuterArgs a)
 {
     constexpr int M = 1 << LOGM;
-    constexpr int CH = 16;  // rows loaded ahead per batch
-    constexpr int NCH = M < CH ? 1 : M / CH, CW = M < CH ? M : CH;
+    constexpr int ROWS = ZU ? M / 2 : M;  // rows that can hold samples (ZU: the upper half is zero)
+    constexpr int CH = 16;                // rows loaded ahead per batch
+    constexpr int NCH = ROWS < CH ? 1 : ROWS / CH, CW = ROWS < CH ? ROWS : CH;
     __shared__ uint2 stw[M / 2];
     __shared__ T sthr[kMaxThr];
     const int op = blockIdx.y;
@@ -969,10 +1068,14 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
     // the host says so
     const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld + (d.reverse ? n - 1 - j : j);
     const int64_t stride = d.reverse ? -(int64_t)Q : (int64_t)Q;
-    int nrows = j < n ? (int)min((n - j + Q - 1) / Q, (int64_t)M) : 0;
-    if (a.zero_upper) nrows = min(nrows, M / 2);
+    const int nrows = j < n ? (int)min((n - j + Q - 1) / Q, (int64_t)ROWS) : 0;
     unsigned ssq = 0, nnz = 0, flags = 0;
     uint32_t x[M];
+    if constexpr (ZU) {
+#pragma unroll
+        for (int r = ROWS; r < M; ++r) x[r] = 0;
+    }
+    const T* rp = src;  // row pointer, advanced by `stride` per row
 #pragma unroll
     for (int ch = 0; ch < NCH; ++ch) {
         // all loads of the batch first (independent, coalesced across the warp)
@@ -982,7 +1085,8 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
         for (int i = 0; i < CW; ++i) {
             const int r = ch * CW + i;
             live[i] = r < nrows;
-            v[i] = live[i] ? __ldg(src + r * stride) : T(0);
+            v[i] = live[i] ? __ldg(rp) : T(0);
+            rp += stride;
         }
         int c[CW];
         if constexpr (QM == QM_UNIFORM && sizeof(T) == 4) {
@@ -1017,12 +1121,13 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
             x[ch * CW + i] = cc < 0 ? (uint32_t)(cc + (int)m.p) : (uint32_t)cc;
         }
     }
-    dif_full<LOGM>(x, stw, m);
+    if constexpr (ZU) dif_cg_zu<LOGM>(x, stw, m);
+    else dif_cg<LOGM>(x, stw, m);
     // register r holds frequency k1 = bitrev(r): x omega_P^(j k1) -> row r
     apply_column_twiddles<LOGM>(x, tw_2level(a.tl, a.th, 0, m), tw_2level(a.tl, a.th, (uint32_t)j, m), m);
     uint32_t* out = a.out + ((int64_t)op * a.batch + pl) * ((int64_t)M << a.lq) + j;  // a.batch: chunk size
 #pragma unroll
-    for (int r = 0; r < M; ++r) out[(int64_t)r * Q] = x[r];
+    for (int r = 0; r < M; ++r, out += Q) *out = x[r];
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         ssq += __shfl_xor_sync(0xffffffffu, ssq, o);
@@ -1063,12 +1168,13 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_consta
         const int j = tile * kOuterThreads + threadIdx.x;
         uint32_t x[M];
         const uint32_t* rin = a.rin + ((int64_t)pl * M * a.np + a.pi) * Q + j;
+        const int64_t rstep = (int64_t)a.np * Q;
 #pragma unroll
-        for (int r = 0; r < M; ++r) x[r] = __ldg(&rin[(int64_t)r * a.np * Q]);
+        for (int r = 0; r < M; ++r, rin += rstep) x[r] = __ldg(rin);
         // inner results of sub-transform r are frequency k1 = bitrev(r):
         // x M^-1 omega_P^(-j k1)
         apply_column_twiddles<LOGM>(x, c0, tw_2level(a.tlf, a.thf, ((uint32_t)P - (uint32_t)j) & pmask, m), m);
-        dit_full<LOGM>(x, stw, m);
+        dit_cg<LOGM>(x, stw, m);
         if (!final_out) {
             uint32_t* ro = a.rout + (pl * a.np + a.pi) * P + j;
 #pragma unroll
@@ -1436,7 +1542,8 @@ void Profiler::post(int kind, cudaStream_t s)
 template <int LOGM, typename T, int QM>
 static cudaError_t launch_ofwd(const OuterArgs& a, dim3 grid, cudaStream_t s)
 {
-    k_outer_fwd<LOGM, T, QM><<<grid, kOuterThreads, 0, s>>>(a);
+    if (a.zero_upper) k_outer_fwd<LOGM, T, QM, true><<<grid, kOuterThreads, 0, s>>>(a);
+    else k_outer_fwd<LOGM, T, QM, false><<<grid, kOuterThreads, 0, s>>>(a);
     return cudaGetLastError();
 }
 

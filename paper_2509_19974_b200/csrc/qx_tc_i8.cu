@@ -407,6 +407,31 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<S
     }
 }
 
+// Bulk L2 prefetch (TMA engine) of the float rows of a pair kTcPrefetch
+// pairs ahead: the builders hold only the next pair in registers (80
+// registers per thread leave no room for a deeper register prefetch, and the
+// shifted-copy buffers leave no shared memory for a float ring), so the
+// pair after that is pulled into L2 and its register loads then wait on L2
+// latency instead of HBM latency (ncu r01: long_scoreboard was the top
+// builder stall).  One instruction per row, issued by one lane.
+#ifndef QX_TC_PREFETCH
+#define QX_TC_PREFETCH 2
+#endif
+constexpr int kTcPrefetch = QX_TC_PREFETCH;
+template <bool SX>
+__device__ __forceinline__ void tc_prefetch_l2(const TcArgs& a, int64_t pair)
+{
+    if (threadIdx.x == 0) {
+        const float* ys = reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld;
+        const uint32_t by = (uint32_t)(a.op[1].n * 4) & ~15u;
+        if (by) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ys), "r"(by) : "memory");
+    } else if (!SX && threadIdx.x == 32) {
+        const float* xs = reinterpret_cast<const float*>(a.op[0].data) + pair * a.op[0].ld;
+        const uint32_t bx = (uint32_t)(a.op[0].n * 4) & ~15u;
+        if (bx) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(xs), "r"(bx) : "memory");
+    }
+}
+
 // level_uniform_nb (qx_common.cuh) as a scalar, with the NaN test folded into its
 // rare exact branch: a NaN makes d NaN, fails `>= 2^-14` and lands there
 // (so does +-inf, which the exact compares then map to +-k)
@@ -894,8 +919,11 @@ __global__ void __launch_bounds__(kTcTotalThreads, 1) k_tc_window(const __grid_c
                 if constexpr (SX) {
                     if (npairs) tc_build_template<QM>(a, S);
                 }
+                for (int p = 1; p < kTcPrefetch && p < npairs; ++p)
+                    tc_prefetch_l2<SX>(a, blockIdx.x + (int64_t)p * gridDim.x);
                 for (int it = 0; it < npairs; ++it) {
                     const int64_t pair = blockIdx.x + (int64_t)it * gridDim.x;
+                    if (it + kTcPrefetch < npairs) tc_prefetch_l2<SX>(a, pair + (int64_t)kTcPrefetch * gridDim.x);
                     if (it + 1 < npairs) tc_fetch<SX>(a, pair + gridDim.x, nxt);
                     acquire(it);
                     TC_T0();

@@ -32,7 +32,6 @@ bool popc_eligible(const NttCall& c, int64_t nx, int64_t ny, bool auto_path);
 cudaError_t popc_run(const NttCall& c, int64_t nx, cudaStream_t s);
 size_t popc_planes_words(int64_t batch, int64_t nx, int64_t ny);
 void popc_schedule(const NttCall& c, int64_t nx, int* G_out, std::vector<int>& out);
-bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny);
 cudaError_t merge_blocks_launch(const MergeSegs& segs, long long lag_shift, void* partials, int* counter,
                                 long long* out, int sms, cudaStream_t s);
 const char* summary_allreduce(void* comm, long long* summary, long long* scratch, cudaStream_t s);
@@ -752,9 +751,8 @@ static qx_status estimate_batch_on(qx_context* ctx, const qx_signals* x, const q
     Prepared pr;
     qx_status st = prepare(ctx, x, y, batch, qx_, qy_, lag_lo, lag_hi, true, path, &pr, scratch, counters, split2);
     if (st != QX_OK) return st;
-    // two records per pair only come from the 2-SM kernel: anything else is
-    // the caller's cue to use single-record blocks
-    if (split2 && !(pr.path == QX_PATH_DIRECT && tc_f2_selected(pr.call, pr.nx, pr.ny))) return QX_ERR_UNSUPPORTED;
+    // two records per pair came only from the retired 2-SM kernel
+    if (split2) return QX_ERR_UNSUPPORTED;
     cudaStream_t s = (cudaStream_t)stream;
     pr.call.am.results = results;
     cudaError_t e = cudaSuccess;
@@ -1035,10 +1033,7 @@ static int64_t tsearch_block(const qx_context* ctx, const qx_signals* t, const q
     auto mode = [](const qx_quantizer* q) { return q->k == 1 ? 0 : (q->kind == QX_Q_UNIFORM ? 1 : 2); };
     const bool f4 = ctx->knobs.tc_f4 && ka <= 4 && kb <= 4 && mode(qa) == mode(qb) &&
                     (double)nt * ka * kb < 16777216.0;
-    // the 2-SM mode is opt-in (QX_TC_F2=1): its MMA runs at the fp4 peak, but
-    // its builders' global loads (82 KB per CTA and block, one block ahead in
-    // registers) are latency-bound (ncu: long_scoreboard), 0.59 ms vs 0.49 ms
-    // for the 1-SM mode at config 5; it needs a TMA-staged float pipeline
+    // (the 2-SM fp4 mode with 32768-lag blocks is retired: slower)
     *f2 = false;
     return f4 ? 8192 : 4096;
 }

@@ -359,13 +359,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         // while this group is quantised and transformed
         using Raw = typename std::conditional<QM == QM_CODES, long long, T>::type;
         using Buf = RegBuf<Raw, NLD>;
-        prefetched_loop<Buf>(
-            warp, S, kWarps,
-            [&](Buf& b, int g) {
+        auto fetch = [&](Buf& b, int g) {
 #pragma unroll
-                for (int kk = 0; kk < NLD; ++kk) b.v[kk] = __ldg(&base[(g + kk * S) * rstride]);
-            },
-            [&](const Buf& b, int g) {
+            for (int kk = 0; kk < NLD; ++kk) b.v[kk] = __ldg(&base[(g + kk * S) * rstride]);
+        };
+        auto body = [&](const Buf& b, int g) {
                 uint32_t x[RAD0];
                 if constexpr (QM == QM_UNIFORM && std::is_same<T, float>::value) {
                     // branch-free levels of the whole group; a rare exact redo
@@ -405,7 +403,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
                 uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
                 for (int kk = 0; kk < RAD0; ++kk) p[kk * S * kPad] = x[kk];
-            });
+        };
+        if constexpr (sizeof(Raw) == 8 && NLD > 8) {
+            // 8-byte samples (float64 rows, int64 codes): two buffers of
+            // NLD values would not fit the 128-register budget (ptxas spilled
+            // 108-436 B); one buffer, its loads still issued together
+#pragma unroll 1
+            for (int g = warp; g < S; g += kWarps) {
+                Buf b;
+                fetch(b, g);
+                body(b, g);
+            }
+        } else {
+            prefetched_loop<Buf>(warp, S, kWarps, fetch, body);
+        }
     } else {
 #pragma unroll 1
         for (int g = warp; g < S; g += kWarps) {

@@ -658,6 +658,27 @@ __device__ __forceinline__ void tc_fetch(const TcArgs& a, int64_t pair, TcRegs<M
     }
 }
 
+// Bulk L2 prefetch (TMA engine) of a pair's y window kTcPrefetch pairs
+// ahead: the builders hold at most the next pair in registers, so the one
+// after it is pulled into L2 and its register loads wait on L2 rather than
+// HBM latency.  One instruction, one lane.
+#ifndef QX_TC_PREFETCH
+#define QX_TC_PREFETCH 2
+#endif
+constexpr int kTcPrefetch = QX_TC_PREFETCH;
+template <int MODE>
+__device__ __forceinline__ void tc_prefetch_l2(const TcArgs& a, int64_t pair)
+{
+    if (threadIdx.x != 0) return;
+    const float* ys = reinterpret_cast<const float*>(a.op[1].data) + pair * a.op[1].ld;
+    int64_t s0 = 0;
+    if constexpr (MODE == 3) s0 = (int64_t)kF2CtaLags * cluster_rank();
+    int64_t cnt = a.ylen;
+    if (s0 + cnt > a.op[1].n) cnt = a.op[1].n - s0;
+    const uint32_t bytes = cnt > 0 ? (uint32_t)(cnt * 4) & ~15u : 0u;
+    if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ys + s0), "r"(bytes) : "memory");
+}
+
 // level_uniform_nb (qx_common.cuh) as a scalar, with the NaN test folded into its
 // rare exact branch: a NaN makes d NaN, fails `>= 2^-14` and lands there
 // (so does +-inf, which the exact compares then map to +-k)
@@ -1383,6 +1404,7 @@ __device__ void tc_merge(const TcArgs& a, TcSmem& S, int u, int64_t rec, bool no
 template <typename T, int QM, int MODE>
 __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_constant__ TcArgs a)
 {
+    static_assert(MODE == 2, "only the 1-SM fp4 mode is built (modes 3 and 4 are retired, see DESIGN.md 6)");
     constexpr bool T4 = MODE == 4;                   // fp4, A in TMEM (otherwise as mode 2)
     constexpr bool SX = MODE != 0, F4 = MODE == 2 || T4, F2 = MODE == 3, FP4 = MODE >= 2;
     constexpr int AUX = (F2 || T4) ? 2 : 4;          // accumulator / record slots
@@ -1493,8 +1515,15 @@ __global__ void __launch_bounds__(tc_threads(MODE), 1) k_tc_window(const __grid_
                 if constexpr (SX) {
                     if (npairs) tc_build_template<QM, F2 ? 2 : F4 ? 1 : 0>(a, S);
                 }
+                if constexpr (FP4) {
+                    for (int p = 1; p < kTcPrefetch && p < npairs; ++p)
+                        tc_prefetch_l2<MODE>(a, base + (int64_t)p * stride);
+                }
                 for (int it = 0; it < npairs; ++it) {
                     const int64_t pair = base + (int64_t)it * stride;
+                    if constexpr (FP4) {
+                        if (it + kTcPrefetch < npairs) tc_prefetch_l2<MODE>(a, pair + (int64_t)kTcPrefetch * stride);
+                    }
                     if constexpr (!F2) {
                         if (it + 1 < npairs) tc_fetch<MODE>(a, pair + stride, nxt);
                     }
@@ -1800,18 +1829,8 @@ static bool tc_f4_mode(const NttCall& c, int64_t nx, int64_t ny)
     return tc_fp4_codes(c, nx) && ny <= kTcFastNY4 && W <= kF4Lags && L0 % 8 == 0 && L0 <= 0;
 }
 
-// 2-SM fp4 mode: only for callers that take two records per pair
-// (c.split2: qx_template_search), windows starting at lag 0 of the row, up to
-// 32768 lags, rows up to 32768 + K samples; QX_TC_F2=0 disables it
-static bool tc_f2_mode(const NttCall& c, int64_t nx, int64_t ny)
-{
-    if (!c.split2) return false;
-    const int64_t W = c.am.t_hi - c.am.t_lo + 1, L0 = c.am.t_lo - (nx - 1);
-    return tc_fp4_codes(c, nx) && c.batch > 1 && L0 == 0 && W <= kF2Lags && ny <= kF2Lags + kTcMaxK;
-}
-
-// the 2-SM mode is what tc_window_run will launch for this call
-bool tc_f2_selected(const NttCall& c, int64_t nx, int64_t ny) { return tc_f2_mode(c, nx, ny); }
+// (the 2-SM fp4 mode is retired: no call selects it)
+static bool tc_f2_mode(const NttCall&, int64_t, int64_t) { return false; }
 
 // eligibility: window of at most kTcMaxTiles*2048 lags (fp4 mode: 8192),
 // nx + 15 <= kTcMaxK, |values| < 2^31 (nx * Kx * Ky), same input dtype and
@@ -1938,25 +1957,12 @@ cudaError_t tc_window_run(const NttCall& c, int64_t nx, cudaStream_t s)
     if (c.prof) c.prof->pre(KK_DIRECT_F4, s);
     cudaError_t e;
     const int qm = c.op[0].q.mode;
-    if (f2) {
-        if (qm == QM_K1) e = launch_tc<float, QM_K1, 3>(a, s, sms);
-        else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 3>(a, s, sms);
-        else e = launch_tc<float, QM_BSEARCH, 3>(a, s, sms);
-    } else {
-        // A operand in TMEM (mode 4) only with QX_TC_T4=1: exact, and its MMA
-        // runs at the fp4 peak, but its four stager warps do not keep up yet
-        // (0.72 ms vs 0.49 ms for config 5); mode 2 reads A from shared memory
-        const bool t4 = false;
-        if (t4) {
-            if (qm == QM_K1) e = launch_tc<float, QM_K1, 4>(a, s, sms);
-            else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 4>(a, s, sms);
-            else e = launch_tc<float, QM_BSEARCH, 4>(a, s, sms);
-        } else {
-            if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
-            else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
-            else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
-        }
-    }
+    // mode 2 only: the 2-SM (3) and A-in-TMEM (4) variants measured slower
+    // at config 5 (r02: 0.635 and 0.72 ms vs 0.477 ms) and are not built
+    (void)f2;
+    if (qm == QM_K1) e = launch_tc<float, QM_K1, 2>(a, s, sms);
+    else if (qm == QM_UNIFORM) e = launch_tc<float, QM_UNIFORM, 2>(a, s, sms);
+    else e = launch_tc<float, QM_BSEARCH, 2>(a, s, sms);
     if (c.prof) c.prof->post(KK_DIRECT_F4, s);
     return e;
 }

@@ -345,6 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     const int rstride = rev ? -N2 : N2;
     constexpr int NLD = ZU ? RAD0 / 2 : RAD0;  // rows actually loaded per group
 
+    // pull the tile's rows (128 B each: the 32 columns) into L2 up front; the
+    // register loads run one group ahead and then wait on L2, not HBM
+    // (C2: pass 1 0.888 -> 0.879 ms per 4-depth step)
+    if (full) {
+        for (int r = threadIdx.x; r < rows_loaded; r += kThreads)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rev ? base - lane + 31 - (int64_t)r * N2 : base - lane + (int64_t)r * N2));
+    }
     // per-thread sums stay far below 2^32 (<= 64 samples of k^2 <= 2^14)
     unsigned ssq = 0, nnz = 0;
     unsigned flags = 0;

@@ -310,6 +310,23 @@ def main():
     int_roof["all_ntt_butterflies_per_s"] = all_bfly / (ntt_ms / 1e3) if ntt_ms else None
     if "peak" in int_roof and int_roof["all_ntt_butterflies_per_s"]:
         int_roof["all_ntt_frac"] = int_roof["all_ntt_butterflies_per_s"] / int_roof["peak"]
+    # SURVEY 8(d) accounting: 3 (P/2) log2 P butterflies per pair and bit depth
+    # (956,301,312 per 64-pair depth at P = 2^19) over the measured step time,
+    # against the butterfly peak and against the FMA-pipe bounds of a Shoup
+    # butterfly (1 IMAD.HI + 2 IMAD; pure IMAD rate / 3 as the looser one)
+    s8d = pairs * len(BITS) * 3 * (P2 // 2) * int(math.log2(P2))  # one rank's step
+    int_roof["s8d_butterflies_per_step"] = s8d
+    int_roof["s8d_butterflies_per_s"] = s8d / (ms_per_step / 1e3)
+    if os.path.exists(int_peak_path):
+        ip = json.load(open(int_peak_path))
+        if ip.get("butterflies_per_s"):
+            int_roof["s8d_frac"] = int_roof["s8d_butterflies_per_s"] / ip["butterflies_per_s"]
+        if ip.get("imad_per_s") and ip.get("imad_hi_per_s"):
+            fma_bound = 1.0 / (1.0 / ip["imad_hi_per_s"] + 2.0 / ip["imad_per_s"])
+            int_roof["fma_pipe_bound_butterflies_per_s"] = fma_bound
+            int_roof["s8d_frac_of_fma_pipe_bound"] = int_roof["s8d_butterflies_per_s"] / fma_bound
+            int_roof["imad_rate_bound_butterflies_per_s"] = ip["imad_per_s"] / 3.0
+            int_roof["s8d_frac_of_imad_rate_bound"] = int_roof["s8d_butterflies_per_s"] / (ip["imad_per_s"] / 3.0)
 
     # e2e through the C ABI host entry point (pinned host buffers, H2D+D2H inside)
     e2e = None

@@ -222,6 +222,25 @@ __device__ __forceinline__ void prefetched_loop(int first, int end, int step, Fe
     }
 }
 
+// Next-wave L2 prefetch: the passes run one CTA per SM and load their
+// whole tile before computing on it, so an SM idles through every tile's
+// load latency.  Each CTA therefore pulls the tile of the CTA one wave
+// later (linear block id + number of SMs) into L2, one 128-B segment per
+// prefetch; that CTA's loads then wait on L2 instead of HBM.
+__device__ __forceinline__ bool next_wave_block(int& bx, int& by, int& bz)
+{
+    unsigned nsm;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    const long long L = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z) + nsm;
+    const long long n = (long long)gridDim.x * gridDim.y * gridDim.z;
+    if (L >= n) return false;
+    bx = (int)(L % gridDim.x);
+    by = (int)((L / gridDim.x) % gridDim.y);
+    bz = (int)(L / ((long long)gridDim.x * gridDim.y));
+    return true;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 template <typename T, int N>
 struct RegBuf {
     T v[N];
@@ -347,10 +366,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
 
     // pull the tile's rows (128 B each: the 32 columns) into L2 up front; the
     // register loads run one group ahead and then wait on L2, not HBM
-    // (C2: pass 1 0.888 -> 0.879 ms per 4-depth step)
+    // (C2: pass 1 0.888 -> 0.879 ms per 4-depth step; prefetching the next
+    // wave's tile instead measured 0.888)
     if (full) {
         for (int r = threadIdx.x; r < rows_loaded; r += kThreads)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rev ? base - lane + 31 - (int64_t)r * N2 : base - lane + (int64_t)r * N2));
+            prefetch_l2(rev ? base - lane + 31 - (int64_t)r * N2 : base - lane + (int64_t)r * N2);
     }
     // per-thread sums stay far below 2^32 (<= 64 samples of k^2 <= 2^14)
     unsigned ssq = 0, nnz = 0;
@@ -556,6 +576,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     const uint32_t* Yu = a.Y + pl * 2 * P + r0 + lane;
     const uint32_t* Yv = Yu + P;
 
+    {
+        int bx, by, bz;
+        // the next wave's tile: both operands' row segments (pass 2: 0.919 ->
+        // 0.902 ms per step; the same for pass 3 measured slower, 0.478 -> 0.510)
+        if (next_wave_block(bx, by, bz)) {
+            const uint32_t* Yn = a.Y + (int64_t)by * 2 * P + bx * 32;
+            for (int i = threadIdx.x; i < 2 * N2; i += kThreads)
+                prefetch_l2(Yn + (i >= N2 ? P : 0) + (int64_t)(i % N2) * N1);
+        }
+    }
     stage_table(stf, a.gtwf, SC::TW_DIF);
     stage_table(sti, a.gtwi, SC::TW_DIT);
     __syncthreads();

@@ -19,8 +19,9 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for _ in range(3):
     res = P.estimate_sweep(xd, yd, sw)
 torch.cuda.synchronize()
-for r in res:
-    assert np.array_equal(r.lag.cpu().numpy(), lag)
+if not os.environ.get("QX_AB_NOCHECK"):
+    for r in res:
+        assert np.array_equal(r.lag.cpu().numpy(), lag)
 ts = []
 for _ in range(15):
     flush.zero_()

@@ -528,7 +528,7 @@ static qx_status prepare(qx_context* ctx, const qx_signals* x, const qx_signals*
     // bounded lag windows go to the tcgen05 int8 Toeplitz kernel (qx_tc.cu)
     const bool tc_ok = argmax && tc_window_eligible(c, nx, ny);
     if (path == QX_PATH_DIRECT && !tc_ok)
-        return fail(ctx, QX_ERR_UNSUPPORTED, "tensor-core window path: window > 4096 lags, nx > 4593 or k > 127");
+        return fail(ctx, QX_ERR_UNSUPPORTED, "tensor-core window path: window > 4112 lags, nx > 4593 or k > 127");
     // word-parallel 1-level codes (qx_popc.cu): small single pairs
     const bool popc_ok = argmax && !(path == QX_PATH_AUTO && tc_ok) && popc_eligible(c, nx, ny, path == QX_PATH_AUTO);
     if (path == QX_PATH_POPC && !popc_ok)

@@ -192,6 +192,11 @@ qx_status qx_plan_create(qx_context *ctx, const qx_signals *x, const qx_signals 
                          const qx_quantizer *qx, const qx_quantizer *qy, int64_t lag_lo, int64_t lag_hi,
                          qx_path path, qx_plan **out);
 qx_status qx_plan_run(qx_plan *plan, const void *x, const void *y, qx_result *results, void *stream);
+/* qx_plan_run from HOST rows and a HOST results array (batch entries): the
+ * plan stages the rows' extent into its own device buffer, runs, copies the
+ * results back and synchronises (page-locked rows: asynchronous DMA).
+ * Returns the first per-pair error status, as qx_estimate_batch_host. */
+qx_status qx_plan_run_host(qx_plan *plan, const void *x, const void *y, qx_result *results);
 /* the qx_path the plan runs (never QX_PATH_AUTO) */
 int qx_plan_path(const qx_plan *plan);
 void qx_plan_destroy(qx_plan *plan);

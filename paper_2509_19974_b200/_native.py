@@ -80,7 +80,7 @@ EXPORTS = (
     "qx_profile_begin",
     "qx_profile_end",
     "qx_profile_kind_name", "qx_summary_reduce_nccl", "qx_template_search_nccl", "qx_estimate_batch_nccl",
-    "qx_comm_rank_size", "qx_plan_create", "qx_plan_run", "qx_plan_path", "qx_plan_destroy",
+    "qx_comm_rank_size", "qx_plan_create", "qx_plan_run", "qx_plan_run_host", "qx_plan_path", "qx_plan_destroy",
     "qx_quantize_packed", "qx_packed_words",
 )
 
@@ -147,6 +147,8 @@ def load():
         L.qx_plan_create.restype = st
         L.qx_plan_run.argtypes = [vp, vp, vp, vp, vp]
         L.qx_plan_run.restype = st
+        L.qx_plan_run_host.argtypes = [vp, vp, vp, vp]
+        L.qx_plan_run_host.restype = st
         L.qx_plan_path.argtypes = [vp]
         L.qx_plan_path.restype = ctypes.c_int
         L.qx_plan_destroy.argtypes = [vp]

@@ -125,6 +125,7 @@ class EstimatePlan:
              ctypes.byref(nqx), ctypes.byref(nqy), lo, hi, N.PATHS[path], ctypes.byref(h))
         self._h = h
         self._run = self._lib.qx_plan_run
+        self._run_host = self._lib.qx_plan_run_host
         self._t = t
         self.path = {v: k for k, v in N.PATHS.items() if k != "tc"}[self._lib.qx_plan_path(h)]
 
@@ -142,6 +143,27 @@ class EstimatePlan:
             raise_for(st, self._lib.qx_context_last_error(self._ctx).decode() or
                       self._lib.qx_status_string(st).decode())
         return BatchResult(raw)
+
+    def run_host(self, x: np.ndarray, y: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """The same estimate from HOST rows (numpy arrays of the plan's shapes,
+        dtypes and row stride) through qx_plan_run_host: H2D into the plan's
+        own device staging, the plan's launches, D2H of the results and one
+        synchronisation in a single C-ABI call.  Page-locked rows (e.g. numpy
+        views of pinned torch tensors) copy by asynchronous DMA.  Returns the
+        structured qx_result array; raises on the first failing pair."""
+        nx, dx, lx, ny, dy, ly = self._chk
+        to_np = {self._t.float32: np.float32, self._t.float64: np.float64, self._t.int64: np.int64}
+        if x.shape[-1] != nx or y.shape[-1] != ny or x.dtype != to_np.get(dx) or y.dtype != to_np.get(dy) \
+                or not (x.flags.c_contiguous and y.flags.c_contiguous) \
+                or (x.size // nx) != self.batch or (y.size // ny) != self.batch \
+                or (lx is not None and lx != nx) or (ly is not None and ly != ny):
+            raise ValueError("rows do not match the plan's length / dtype / batch, or are not contiguous")
+        res = out if out is not None else np.zeros(self.batch, dtype=N.RESULT_DTYPE)
+        st = self._run_host(self._h, x.ctypes.data, y.ctypes.data, res.ctypes.data)
+        if st != N.QX_OK:
+            raise_for(st, self._lib.qx_context_last_error(self._ctx).decode() or
+                      self._lib.qx_status_string(st).decode())
+        return res
 
     def __del__(self):
         h = getattr(self, "_h", None)

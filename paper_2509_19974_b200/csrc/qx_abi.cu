@@ -826,6 +826,15 @@ struct qx_plan {
     qx_path path = QX_PATH_AUTO;
     Prepared pr;
     uint64_t gen_s = 0, gen_c = 0;  // arena generations the pointers in pr were derived from
+    void* dstage = nullptr;         // qx_plan_run_host: device copies of the rows + results
+    size_t dstage_bytes = 0;
+    ~qx_plan()
+    {
+        if (dstage) {
+            DevGuard dg(ctx->device);
+            cudaFree(dstage);
+        }
+    }
 };
 
 static qx_status plan_prepare(qx_plan* p)
@@ -903,6 +912,49 @@ qx_status qx_plan_run(qx_plan* p, const void* x, const void* y, qx_result* resul
     e = p->pr.path == QX_PATH_DIRECT ? tc_window_run(c, p->pr.nx, s)
         : p->pr.path == QX_PATH_POPC ? popc_run(c, p->pr.nx, s) : ntt_run(c, s);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "kernel launch");
+    return QX_OK;
+}
+
+// qx_plan_run from HOST rows: the plan's own device staging (allocated on
+// first use), H2D of the rows' extent, the same launches as qx_plan_run on
+// the context's host stream, D2H of the results, one synchronisation.  With
+// page-locked rows the copies are asynchronous DMA; pageable rows go
+// through the driver's staging (correct, slower).
+qx_status qx_plan_run_host(qx_plan* p, const void* x, const void* y, qx_result* results)
+{
+    if (!p) return QX_ERR_INVALID;
+    qx_context* ctx = p->ctx;
+    if (!x || !y || !results) return fail(ctx, QX_ERR_INVALID, "x, y and results are required");
+    std::lock_guard<std::recursive_mutex> lk(ctx->mu);
+    DevGuard dg(ctx->device);
+    static const size_t esz[] = {4, 8, 8};
+    const int64_t batch = p->batch;
+    const size_t xb = (size_t)((batch - 1) * p->x.ld + p->x.n) * esz[p->x.dtype];
+    const size_t yb = (size_t)((batch - 1) * p->y.ld + p->y.n) * esz[p->y.dtype];
+    const size_t xa = (xb + 255) & ~(size_t)255, ya = (yb + 255) & ~(size_t)255;
+    const size_t rb = (size_t)batch * sizeof(qx_result);
+    cudaError_t e = cudaSuccess;
+    if (p->dstage_bytes < xa + ya + rb) {
+        if (p->dstage) cudaFree(p->dstage);
+        p->dstage = nullptr;
+        p->dstage_bytes = 0;
+        e = cudaMalloc(&p->dstage, xa + ya + rb);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "plan staging");
+        p->dstage_bytes = xa + ya + rb;
+    }
+    char* d = (char*)p->dstage;
+    cudaStream_t s = ctx->host_stream;
+    e = cudaMemcpyAsync(d, x, xb, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d + xa, y, yb, cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "H2D");
+    qx_result* rd = (qx_result*)(d + xa + ya);
+    qx_status st = qx_plan_run(p, d, d + xa, rd, s);
+    if (st != QX_OK) return st;
+    e = cudaMemcpyAsync(results, rd, rb, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "D2H");
+    for (int64_t b = 0; b < batch; ++b)
+        if (results[b].status) return (qx_status)results[b].status;
     return QX_OK;
 }
 

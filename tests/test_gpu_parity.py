@@ -864,5 +864,10 @@ def test_estimate_plan_matches_estimate_batch(qx, oracle):
             a = plan(x, y).numpy()
             b = qx.estimate_batch(x, y, q, q, lag_lo=lo, lag_hi=hi).numpy()
             assert np.array_equal(a, b), (B, nx, ny, it)
+            # the same rows from host memory (qx_plan_run_host), pageable and pinned
+            xh, yh = x.cpu().numpy(), y.cpu().numpy()
+            assert np.array_equal(plan.run_host(xh, yh), b), (B, nx, ny, it, "host")
+            xp, yp = x.cpu().pin_memory(), y.cpu().pin_memory()
+            assert np.array_equal(plan.run_host(xp.numpy(), yp.numpy()), b), (B, nx, ny, it, "pinned")
         with pytest.raises(ValueError):
             plan(x[:, :-1] if nx > 1 else x, y)

@@ -44,6 +44,11 @@ constexpr int kThreads = QX_NTT_THREADS;
 #ifndef QX_TW_UNROLL
 #define QX_TW_UNROLL 8
 #endif
+// next-wave L2 prefetch placement: 1 = after the CTA's own load phase (all
+// three passes), 0 = at kernel start (pass 2) / own tile (pass 1), as in r02 v3
+#ifndef QX_PF_LATE
+#define QX_PF_LATE 1
+#endif
 #define QX_STR_(x) #x
 #define QX_UNROLL(n) _Pragma(QX_STR_(unroll n))
 constexpr int kWarps = kThreads / 32;
@@ -368,10 +373,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     // register loads run one group ahead and then wait on L2, not HBM
     // (C2: pass 1 0.888 -> 0.879 ms per 4-depth step; prefetching the next
     // wave's tile instead measured 0.888)
+#if !QX_PF_LATE
     if (full) {
         for (int r = threadIdx.x; r < rows_loaded; r += kThreads)
             prefetch_l2(rev ? base - lane + 31 - (int64_t)r * N2 : base - lane + (int64_t)r * N2);
     }
+#endif
     // per-thread sums stay far below 2^32 (<= 64 samples of k^2 <= 2^14)
     unsigned ssq = 0, nnz = 0;
     unsigned flags = 0;
@@ -476,6 +483,25 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         if (nnz) atomicAdd(st + 1, (unsigned long long)nnz);
         if (flags) atomicOr(st + 2, (unsigned long long)flags);
     }
+#if QX_PF_LATE
+    // this tile's samples are in registers or shared memory: pull the tile of the
+    // CTA one wave later into L2 now, so its DRAM reads run under this CTA's
+    // transform instead of beside the next wave's own loads
+    if constexpr (sizeof(T) == 4) {  // (8-byte rows: the extra live values spill)
+        int bx, by, bz;
+        if (next_wave_block(bx, by, bz)) {
+            const OperandDesc& dn = a.op[by];
+            const T* sn = reinterpret_cast<const T*>(dn.data) + (a.pair0 + bz) * dn.ld;
+            const int64_t nn = dn.n;
+            const int cn = bx * 32;
+            if ((int64_t)(rows_loaded - 1) * N2 + cn + 31 < nn) {
+                const T* bn = dn.reverse ? sn + (nn - 1 - cn - 31) : sn + cn;
+                const int64_t rs = dn.reverse ? -(int64_t)N2 : (int64_t)N2;
+                for (int r = threadIdx.x; r < rows_loaded; r += kThreads) prefetch_l2(bn + r * rs);
+            }
+        }
+    }
+#endif
     __syncthreads();
     dif_middle<LOG1, 1, 1>(smem, nullptr, stw, m);
     // last DIF group (in shared memory)
@@ -497,17 +523,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         if (a.twab) {
             // factored twiddle: one per-lane A and a warp-uniform B per row
             // (two Shoup products instead of one 8-byte L2 load per element)
-            constexpr int NB = N1 / 32;
+            // (row pointers hoisted: every access of an unrolled chunk is base +
+            // immediate; indexing Yt[o + e] cost five address instructions per store)
+            constexpr int NB = N1 / 32, U = NB < QX_TW_UNROLL ? NB : QX_TW_UNROLL;
 #pragma unroll 1
             for (int c = warp; c < 32; c += kWarps) {
-                const int o = (c0 + c) * N1;
                 const uint2* tb = a.twab + (int64_t)(c0 + c) * (32 + NB);
                 const uint2 A = __ldg(&tb[lane]);
-                QX_UNROLL(QX_TW_UNROLL)
-                for (int j = 0; j < NB; ++j) {
-                    const uint2 B = __ldg(&tb[32 + j]);
-                    const int e = lane + 32 * j;
-                    Yt[o + e] = shoup(shoup(smem[e * kPad + c], A.x, A.y, m.p), B.x, B.y, m.p);
+                uint32_t* yp = Yt + ((int64_t)(c0 + c) * N1 + lane);
+                const uint32_t* sp = smem + lane * kPad + c;
+                tb += 32;
+#pragma unroll 1
+                for (int j0 = 0; j0 < NB; j0 += U, yp += 32 * U, sp += 32 * U * kPad, tb += U) {
+                    uint2 B[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) B[u] = __ldg(&tb[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        yp[32 * u] = shoup(shoup(sp[32 * u * kPad], A.x, A.y, m.p), B[u].x, B[u].y, m.p);
                 }
             }
             return;
@@ -576,16 +609,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     const uint32_t* Yu = a.Y + pl * 2 * P + r0 + lane;
     const uint32_t* Yv = Yu + P;
 
-    {
+    auto prefetch_next_wave = [&]() {
         int bx, by, bz;
-        // the next wave's tile: both operands' row segments (pass 2: 0.919 ->
-        // 0.902 ms per step; the same for pass 3 measured slower, 0.478 -> 0.510)
+        // the next wave's tile: both operands' row segments
         if (next_wave_block(bx, by, bz)) {
             const uint32_t* Yn = a.Y + (int64_t)by * 2 * P + bx * 32;
             for (int i = threadIdx.x; i < 2 * N2; i += kThreads)
                 prefetch_l2(Yn + (i >= N2 ? P : 0) + (int64_t)(i % N2) * N1);
         }
-    }
+    };
+#if !QX_PF_LATE
+    prefetch_next_wave();
+#endif
     stage_table(stf, a.gtwf, SC::TW_DIF);
     stage_table(sti, a.gtwi, SC::TW_DIT);
     __syncthreads();
@@ -619,6 +654,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
                 }
             });
     }
+#if QX_PF_LATE
+    // issued once this CTA's own loads have landed: the next wave's DRAM reads
+    // run under this tile's transform, not beside the loads of either wave
+    prefetch_next_wave();
+#endif
     __syncthreads();
     dif_middle<LOG2, 1, 2>(su, sv, stf, m);
     // last DIF group of both, pointwise product, first DIT group (same
@@ -651,17 +691,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass2(const __grid_constant__ P
     if constexpr (N2 >= 32) {
         if (a.twib) {
             // factored twiddle (see pass 1): per-lane A, warp-uniform B per row
-            constexpr int NB = N2 / 32;
+            constexpr int NB = N2 / 32, U = NB < QX_TW_UNROLL ? NB : QX_TW_UNROLL;
 #pragma unroll 1
             for (int c = warp; c < 32; c += kWarps) {
-                const int o = (r0 + c) * N2;
                 const uint2* tb = a.twib + (int64_t)(r0 + c) * (32 + NB);
                 const uint2 A = __ldg(&tb[lane]);
-                QX_UNROLL(QX_TW_UNROLL)
-                for (int j = 0; j < NB; ++j) {
-                    const uint2 B = __ldg(&tb[32 + j]);
-                    const int e = lane + 32 * j;
-                    Z[o + e] = shoup(shoup(su[e * kPad + c], A.x, A.y, m.p), B.x, B.y, m.p);
+                uint32_t* zp = Z + ((int64_t)(r0 + c) * N2 + lane);
+                const uint32_t* sp = su + lane * kPad + c;
+                tb += 32;
+#pragma unroll 1
+                for (int j0 = 0; j0 < NB; j0 += U, zp += 32 * U, sp += 32 * U * kPad, tb += U) {
+                    uint2 B[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) B[u] = __ldg(&tb[u]);
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        zp[32 * u] = shoup(shoup(sp[32 * u * kPad], A.x, A.y, m.p), B[u].x, B[u].y, m.p);
                 }
             }
             return;
@@ -743,6 +788,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     const int64_t P = (int64_t)N1 * N2;
     const uint32_t* Zc = a.Z + pl * P + col;
 
+    // Fused argmax of a single-prime lift: every output carries + half
+    // (added once per column at the DC input below), so the canonical residue
+    // k = (c + half) mod p is already a monotone key of the centred value c
+    // (|c| <= half): no per-element lift, compare keys, subtract half at the end.
+    const uint32_t half = (m.p - 1) / 2;
+    const uint32_t bias = (OUT == OUT_ARGMAX && final_out) ? half : 0u;
     stage_table(sti, a.gtwi, SC::TW_DIT);
     __syncthreads();
     // first DIT group from global (positions g*RAD0 + k, lane = column),
@@ -759,6 +810,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
                 uint32_t x[RAD0];
 #pragma unroll
                 for (int kk = 0; kk < RAD0; ++kk) x[kk] = b.v[kk];
+                // position 0 is the column's DC term: + bias there adds bias to
+                // every output of the column (inputs stay below 4p: < 2p + p/2)
+                if (g == 0) x[0] += bias;
                 dit_regs<LOG1, 0>(x, 0, sti, m);
                 uint32_t* p = smem + g * RAD0 * kPad + lane;
 #pragma unroll
@@ -768,49 +822,137 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass3(const __grid_constant__ P
     __syncthreads();
     dit_middle<LOG1, 1>(smem, sti, m);
     // last DIT group: natural-order n1 = j0 + (k << S0L), t = n1*N2 + col.
-    // Values of a single-prime lift are in (-p/2, p/2) and t < 2^25, so the
-    // per-thread peak bookkeeping runs in 32-bit; a CTA whose t range lies
-    // inside the window (and below nout) skips the per-element tests.
-    const uint32_t half = (m.p - 1) / 2;
     uint32_t* Rout = a.R + (pl * a.np + a.pi) * P;
-    const int tmin = blockIdx.x * 32, tmax = (N1 - 1) * N2 + blockIdx.x * 32 + 31;
-    const bool inside = a.am.t_lo <= tmin && a.am.t_hi >= tmax && tmax < a.nout;
-    const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(min(a.am.t_hi, a.nout - 1), P - 1);
-    int bv = INT_MIN, bt = INT_MAX, bc = 0;
+    if (!final_out || OUT == OUT_VALUES) {
 #pragma unroll 1
-    for (int g = warp; g < (1 << S0L); g += kWarps) {
-        uint32_t x[RADL];
-        const uint32_t* p = smem + g * kPad + lane;
+        for (int g = warp; g < (1 << S0L); g += kWarps) {
+            uint32_t x[RADL];
+            const uint32_t* p = smem + g * kPad + lane;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
-        dit_regs<LOG1, SC::NG - 1>(x, g, sti, m);
-        const int t0 = g * N2 + col;
+            for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
+            dit_regs<LOG1, SC::NG - 1>(x, g, sti, m);
+            const int t0 = g * N2 + col;
 #pragma unroll
-        for (int kk = 0; kk < RADL; ++kk) {
-            const int t = t0 + (kk << S0L) * N2;
-            const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
-            if (!final_out) {
-                Rout[t] = r;
-                continue;
-            }
-            const int v = (int)r - (r > half ? (int)m.p : 0);
-            if constexpr (OUT == OUT_VALUES) {
-                if (t < a.nout) a.values[pair * a.vld + t] = v;
-            } else {
-                const bool ok = inside || (t >= tlo && t <= thi);
-                const bool gt = ok && v > bv, eq = ok && v == bv;
-                bt = gt ? t : (eq ? min(bt, t) : bt);
-                bc = gt ? 1 : bc + (eq ? 1 : 0);
-                bv = gt ? v : bv;
+            for (int kk = 0; kk < RADL; ++kk) {
+                const int t = t0 + (kk << S0L) * N2;
+                const uint32_t r = redp(red2p(x[kk], m.p2), m.p);
+                if (!final_out) Rout[t] = r;
+                else if (t < a.nout) a.values[pair * a.vld + t] = (int)r - (r > half ? (int)m.p : 0);
             }
         }
+        return;
     }
     if constexpr (OUT == OUT_ARGMAX) {
-        if (final_out) {
-            Best b = bc ? Best{bv, bt, bc} : best_init();
-            argmax_finish<kWarps>(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
+        // Keys of a single-prime result are < 2^30 and t < 2^25, so the peak
+        // bookkeeping is 32-bit.  The warp shares one running best key wm; a
+        // group of 2^RL keys per lane costs a max tree and one vote unless some
+        // lane reaches wm (about ln(#groups) times per warp), and only then are
+        // the group's keys scanned for the count and the smallest t at wm.
+        const int tmin = blockIdx.x * 32, tmax = (N1 - 1) * N2 + blockIdx.x * 32 + 31;
+        const bool inside = a.am.t_lo <= tmin && a.am.t_hi >= tmax && tmax < a.nout;
+        const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(min(a.am.t_hi, a.nout - 1), P - 1);
+        uint32_t wm = 0;
+        int bc = 0, bt = INT_MAX;
+#pragma unroll 1
+        for (int g = warp; g < (1 << S0L); g += kWarps) {
+            uint32_t x[RADL];
+            const uint32_t* p = smem + g * kPad + lane;
+#pragma unroll
+            for (int kk = 0; kk < RADL; ++kk) x[kk] = p[(kk << S0L) * kPad];
+            dit_regs<LOG1, SC::NG - 1>(x, g, sti, m);
+            const int t0 = g * N2 + col;
+#pragma unroll
+            for (int kk = 0; kk < RADL; ++kk) x[kk] = redp(red2p(x[kk], m.p2), m.p);
+            if (!inside) {
+                // window edge (or the unused last point of P): this CTA's keys are
+                // k + 1, and 0 marks an out-of-window element (it never equals wm >= 1)
+#pragma unroll
+                for (int kk = 0; kk < RADL; ++kk) {
+                    const int t = t0 + (kk << S0L) * N2;
+                    x[kk] = (t < tlo || t > thi) ? 0u : x[kk] + 1u;
+                }
+            }
+            uint32_t mx = x[0];
+#pragma unroll
+            for (int kk = 1; kk + 1 < RADL; kk += 2) mx = __vimax3_u32(mx, x[kk], x[kk + 1]);
+            if constexpr (RADL % 2 == 0) mx = max(mx, x[RADL - 1]);
+            if (!__any_sync(0xffffffffu, mx >= wm)) continue;
+            const uint32_t wn = __reduce_max_sync(0xffffffffu, mx);
+            if (!inside && wn == 0) continue;  // nothing in the window yet
+            if (wn > wm) {
+                wm = wn;
+                bc = 0;
+                bt = INT_MAX;
+            }
+            int kb = RADL;
+#pragma unroll
+            for (int kk = RADL - 1; kk >= 0; --kk) {
+                if (x[kk] == wm) {
+                    ++bc;
+                    kb = kk;
+                }
+            }
+            if (kb < RADL) bt = min(bt, t0 + (kb << S0L) * N2);
+        }
+        // warp record -> CTA record -> one partial per CTA (merged per pair by
+        // k_merge_partials: no ticket, so no CTA waits on a fence and an atomic
+        // round trip while it holds the SM)
+        __shared__ uint32_t sk[kWarps];
+        __shared__ int st[kWarps], sc[kWarps];
+        const int wc = __reduce_add_sync(0xffffffffu, bc);
+        const int wt = __reduce_min_sync(0xffffffffu, bt);
+        if (lane == 0) {
+            sk[warp] = wc ? wm + 1 : 0;  // 0: no valid element in this warp's share
+            st[warp] = wt;
+            sc[warp] = wc;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t k1 = lane < kWarps ? sk[lane] : 0u;
+            const uint32_t kmax = __reduce_max_sync(0xffffffffu, k1);
+            const bool on = lane < kWarps && k1 == kmax && kmax > 0;
+            const int c = __reduce_add_sync(0xffffffffu, on ? sc[lane] : 0);
+            const int t = __reduce_min_sync(0xffffffffu, on ? st[lane] : INT_MAX);
+            if (lane == 0) {
+                long long* pp = a.am.partials + (pair * a.am.pstride + blockIdx.x) * 3;
+                const Best b = kmax ? Best{(long long)(kmax - 1) - (inside ? 0 : 1) - (long long)half, t, c}
+                                    : best_init();
+                pp[0] = b.v;
+                pp[1] = b.t;
+                pp[2] = b.c;
+            }
         }
     }
+}
+
+// per-pair merge of the per-CTA argmax partials of k_pass3 (one warp per pair)
+struct MergeArgs {
+    ArgmaxOut am;
+    const unsigned long long* stats;
+    int64_t pair0, nb;
+    uint32_t p0;
+    int nblk, np;
+};
+
+__global__ void __launch_bounds__(256) k_merge_partials(const __grid_constant__ MergeArgs a)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (w >= a.nb) return;
+    const int64_t pair = a.pair0 + w;
+    // multi-prime launches: pairs that need the CRT are finished by k_combine
+    if (a.np > 1 && !cs_single(a.stats, pair, a.p0)) return;
+    Best r = best_init();
+    const long long* pp = a.am.partials + pair * a.am.pstride * 3;
+    for (int i = lane; i < a.nblk; i += 32) best_merge(r, Best{pp[3 * i], pp[3 * i + 1], pp[3 * i + 2]});
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        Best o2{__shfl_xor_sync(0xffffffffu, r.v, o), __shfl_xor_sync(0xffffffffu, r.t, o),
+                __shfl_xor_sync(0xffffffffu, r.c, o)};
+        best_merge(r, o2);
+    }
+    if (lane == 0)
+        write_result(reinterpret_cast<long long*>(a.am.results) + pair * 8, r, a.am.first_lag, a.stats + pair * 8);
 }
 
 // ----------------------------------------------------- multi-prime combine
@@ -1477,6 +1619,12 @@ static cudaError_t launch_p1(const Pass1Args& a, dim3 grid, cudaStream_t s)
 template <int LOG1, bool ZU>
 static cudaError_t dispatch_p1_zu(const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
+#ifdef QX_NTT_DEV  // fast A/B builds (tools/build_variant.sh): float32 K1/uniform and residues only
+    if (dtype == DT_U32) return launch_p1<LOG1, uint32_t, QM_RESIDUE, ZU>(a, grid, s);
+    if (dtype == DT_F32 && qm == QM_K1) return launch_p1<LOG1, float, QM_K1, ZU>(a, grid, s);
+    if (dtype == DT_F32 && qm == QM_UNIFORM) return launch_p1<LOG1, float, QM_UNIFORM, ZU>(a, grid, s);
+    return cudaErrorInvalidValue;
+#else
     if (dtype == DT_U32) return launch_p1<LOG1, uint32_t, QM_RESIDUE, ZU>(a, grid, s);
     if (dtype == DT_I64) return launch_p1<LOG1, long long, QM_CODES, ZU>(a, grid, s);
     if (dtype == DT_F32) {
@@ -1487,6 +1635,7 @@ static cudaError_t dispatch_p1_zu(const Pass1Args& a, int dtype, int qm, dim3 gr
     if (qm == QM_K1) return launch_p1<LOG1, double, QM_K1, ZU>(a, grid, s);
     if (qm == QM_UNIFORM) return launch_p1<LOG1, double, QM_UNIFORM, ZU>(a, grid, s);
     return launch_p1<LOG1, double, QM_BSEARCH, ZU>(a, grid, s);
+#endif
 }
 
 template <int LOG1>
@@ -1499,11 +1648,13 @@ static cudaError_t dispatch_p1_mode(const Pass1Args& a, int dtype, int qm, dim3 
 static cudaError_t dispatch_p1(int log1, const Pass1Args& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
     switch (log1) {
+#ifndef QX_NTT_DEV
     case 5: return dispatch_p1_mode<5>(a, dtype, qm, grid, s);
     case 6: return dispatch_p1_mode<6>(a, dtype, qm, grid, s);
     case 7: return dispatch_p1_mode<7>(a, dtype, qm, grid, s);
     case 8: return dispatch_p1_mode<8>(a, dtype, qm, grid, s);
     case 9: return dispatch_p1_mode<9>(a, dtype, qm, grid, s);
+#endif
     case 10: return dispatch_p1_mode<10>(a, dtype, qm, grid, s);
     }
     return cudaErrorInvalidValue;
@@ -1521,10 +1672,12 @@ static cudaError_t launch_p2(const Pass2Args& a, dim3 grid, cudaStream_t s)
 static cudaError_t dispatch_p2(int log2, const Pass2Args& a, dim3 grid, cudaStream_t s)
 {
     switch (log2) {
+#ifndef QX_NTT_DEV
     case 5: return launch_p2<5>(a, grid, s);
     case 6: return launch_p2<6>(a, grid, s);
     case 7: return launch_p2<7>(a, grid, s);
     case 8: return launch_p2<8>(a, grid, s);
+#endif
     case 9: return launch_p2<9>(a, grid, s);
     }
     return cudaErrorInvalidValue;
@@ -1543,11 +1696,13 @@ template <int OUT>
 static cudaError_t dispatch_p3_out(int log1, const Pass3Args& a, dim3 grid, cudaStream_t s)
 {
     switch (log1) {
+#ifndef QX_NTT_DEV
     case 5: return launch_p3<5, OUT>(a, grid, s);
     case 6: return launch_p3<6, OUT>(a, grid, s);
     case 7: return launch_p3<7, OUT>(a, grid, s);
     case 8: return launch_p3<8, OUT>(a, grid, s);
     case 9: return launch_p3<9, OUT>(a, grid, s);
+#endif
     case 10: return launch_p3<10, OUT>(a, grid, s);
     }
     return cudaErrorInvalidValue;
@@ -1612,9 +1767,11 @@ static cudaError_t dispatch_ofwd_m(const OuterArgs& a, int dtype, int qm, dim3 g
 static cudaError_t dispatch_ofwd(int logm, const OuterArgs& a, int dtype, int qm, dim3 grid, cudaStream_t s)
 {
     switch (logm) {
+#ifndef QX_NTT_DEV
     case 3: return dispatch_ofwd_m<3>(a, dtype, qm, grid, s);
     case 4: return dispatch_ofwd_m<4>(a, dtype, qm, grid, s);
     case 5: return dispatch_ofwd_m<5>(a, dtype, qm, grid, s);
+#endif
     case 6: return dispatch_ofwd_m<6>(a, dtype, qm, grid, s);
     case 7: return dispatch_ofwd_m<7>(a, dtype, qm, grid, s);
     }
@@ -1632,9 +1789,11 @@ template <int OUT>
 static cudaError_t dispatch_oinv(int logm, const OuterArgs& a, dim3 grid, cudaStream_t s)
 {
     switch (logm) {
+#ifndef QX_NTT_DEV
     case 3: return launch_oinv<3, OUT>(a, grid, s);
     case 4: return launch_oinv<4, OUT>(a, grid, s);
     case 5: return launch_oinv<5, OUT>(a, grid, s);
+#endif
     case 6: return launch_oinv<6, OUT>(a, grid, s);
     case 7: return launch_oinv<7, OUT>(a, grid, s);
     }
@@ -1883,6 +2042,22 @@ cudaError_t ntt_run(const NttCall& c, cudaStream_t s)
                        : dispatch_p3_out<OUT_VALUES>(l1, a3, dim3(N2 / 32, (unsigned)nb), s);
             if (c.prof) c.prof->post(KK_PASS3, s);
             if (e != cudaSuccess) return e;
+            if (argmax && pi == 0) {
+                MergeArgs ma;
+                memset(&ma, 0, sizeof(ma));
+                ma.am = c.am;
+                ma.stats = c.stats;
+                ma.pair0 = p0;
+                ma.nb = nb;
+                ma.p0 = t0.p;
+                ma.nblk = N2 / 32;
+                ma.np = c.np;
+                if (c.prof) c.prof->pre(KK_PASS3, s);
+                k_merge_partials<<<(unsigned)((nb + 7) / 8), 256, 0, s>>>(ma);
+                e = cudaGetLastError();
+                if (c.prof) c.prof->post(KK_PASS3, s);
+                if (e != cudaSuccess) return e;
+            }
         }
         if (c.np > 1) {
             CombineArgs ca;

@@ -273,6 +273,42 @@ def test_random_pairs_against_oracle(qx, oracle):
             assert res["sumsq_x"][b] == oracle.sumsq(u) and res["sumsq_y"][b] == oracle.sumsq(v)
 
 
+def test_ntt_argmax_ties_and_windows(qx):
+    """The fused argmax of the last NTT pass (shared warp threshold, per-CTA
+    partials merged by k_merge_partials): impulse trains make every correlation
+    value small, so maxima tie many times across lanes, warps and CTAs; windows
+    start and end inside column tiles.  Expected records from the sparse sum."""
+    import torch
+
+    rng = np.random.default_rng(11)
+    q = qx.uniform(1, 1.0)
+    for n in (1 << 11, 1 << 14, 3 * 5000, 1 << 18):
+        B = 6
+        x = np.zeros((B, n), np.float32)
+        y = np.zeros((B, n), np.float32)
+        for r in range(B):
+            x[r, rng.choice(n, 2 + 3 * r, replace=False)] = rng.choice([-1.0, 1.0], 2 + 3 * r)
+            y[r, rng.choice(n, 3 + 2 * r, replace=False)] = rng.choice([-1.0, 1.0], 3 + 2 * r)
+        x[B - 1] = 0.0
+        x[B - 1, [5, n - 7]] = 1.0  # two equal impulses against a constant row: long runs of ties
+        y[B - 1] = 1.0
+        xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        windows = [(-(n - 1), n - 1), (-37, 1000), (n // 3, n - 1), (-(n - 1), -(n - 1) + 40), (-1, -1)]
+        for lo, hi in windows:
+            res = qx.estimate_batch(xd, yd, q, q, path="ntt", lag_lo=lo, lag_hi=hi).numpy()
+            for r in range(B):
+                ix, iy = np.nonzero(x[r])[0], np.nonzero(y[r])[0]
+                lag = (iy[None, :] - ix[:, None]).ravel()
+                val = (x[r, ix][:, None] * y[r, iy][None, :]).ravel().astype(np.int64)
+                c = np.zeros(hi - lo + 1, np.int64)
+                keep = (lag >= lo) & (lag <= hi)
+                np.add.at(c, lag[keep] - lo, val[keep])
+                m = int(c.max())
+                f = int(np.argmax(c))
+                assert (int(res["value"][r]), int(res["lag"][r]), int(res["ties"][r])) == \
+                    (m, lo + f, int((c == m).sum())), (n, lo, hi, r)
+
+
 def test_popc_path_against_oracle(qx, oracle):
     """Word-parallel 1-level path (path="popc", and what "auto" picks for
     C1-sized pairs): sign / uniform(1) / custom k=1 codes, with and without

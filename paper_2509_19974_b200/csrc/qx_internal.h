@@ -90,6 +90,8 @@ struct OuterTables {
     const uint32_t* thi;  // omega_P^-(8192 b) * R
     const uint2* rf;      // omega_M^t  (Shoup pairs), t < M/2: register-resident outer DIF
     const uint2* ri;      // omega_M^-t (Shoup pairs), t < M/2: register-resident outer DIT
+    const uint2* tcf;     // omega_P^(+tid * bitrev(r)) [r][tid], tid < 256 (Shoup pairs): per-thread factor
+    const uint2* tci;     // omega_P^(-tid * bitrev(r)) [r][tid]   of the outer four-step twiddles
 };
 
 // Tuning / measurement knobs of a context: the QX_* environment variables

@@ -1025,6 +1025,7 @@ struct OuterArgs {
     const uint32_t* th;
     const uint32_t* tlf;     // inverse: the forward two-level tables (omega_P^-j = omega_P^(P-j))
     const uint32_t* thf;
+    const uint2* tc;         // per-thread factor of the column twiddles [r][tid] (OuterTables::tcf / tci)
     unsigned long long* stats;
     ArgmaxOut am;
     int64_t* values;
@@ -1203,41 +1204,65 @@ constexpr int brev_c(int r, int bits)
     return o;
 }
 
-// Column j's four-step twiddles omega_P^(+-j k1), k1 = 0..M-1, as a running
-// Montgomery product (one table lookup per column instead of two per
-// element): x[bitrev(k1)] = x * cur_k1, cur_0 = c0, cur_(k+1) = cur_k * wj.
-// Four interleaved chains (k1 = 4i + c, step wj^4) keep the dependent
-// product chain at M/4.
+// Column j's four-step twiddles omega_P^(+-j k1), k1 = bitrev(r), r = 0..M-1.
+// With j = j0 + tid (j0 the tile's first column, a multiple of the CTA size)
+// the twiddle is U[r] * T[r][tid]: U[r] = omega_P^(+-j0 k1) (times M^-1 on the
+// inverse) is one Shoup pair per register, computed by M threads of the CTA
+// into shared memory; T is a fixed M x 256 table of Shoup pairs (128 KB at
+// M = 64, L1/L2 resident, read coalesced).  Two Shoup products per element
+// (2 IMAD.HI) replace the running Montgomery product's two general products
+// (4 IMAD.HI): the outer kernels are bound by the heavy FMA sub-pipe, where
+// IMAD.HI costs two issue slots.
 template <int LOGM>
-__device__ __forceinline__ void apply_column_twiddles(uint32_t (&x)[1 << LOGM], uint32_t c0, uint32_t wj,
-                                                      const ModP& m)
+__device__ __forceinline__ void column_twiddle_setup(uint2* su, const uint32_t* __restrict__ tl,
+                                                     const uint32_t* __restrict__ th, uint32_t j0, uint32_t pmask,
+                                                     const ModP& m)
 {
-    constexpr int M = 1 << LOGM, NC = M < 4 ? M : 4;
-    const uint32_t w2 = montmul(wj, wj, m.p, m.pinv);
-    const uint32_t w4 = montmul(w2, w2, m.p, m.pinv);
-    uint32_t cur[4];
-    cur[0] = c0;
-    cur[1] = montmul(c0, wj, m.p, m.pinv);
-    cur[2] = montmul(c0, w2, m.p, m.pinv);
-    cur[3] = montmul(cur[1], w2, m.p, m.pinv);
-    const uint32_t step = NC == 4 ? w4 : (NC == 2 ? w2 : wj);
+    constexpr int M = 1 << LOGM;
+    if (threadIdx.x < M) {
+        const uint32_t k1 = __brev(threadIdx.x) >> (32 - LOGM);
+        const uint32_t e = (uint32_t)(((uint64_t)j0 * k1) & pmask);
+        // the two-level tables hold Montgomery forms: x R^-1 gives the plain residue
+        const uint32_t w = redp(montmul(tw_2level(tl, th, e, m), 1u, m.p, m.pinv), m.p);
+        su[threadIdx.x] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / m.p));
+    }
+}
+
+template <int LOGM>
+__device__ __forceinline__ void apply_column_twiddles(uint32_t (&x)[1 << LOGM], const uint2* su,
+                                                      const uint2* __restrict__ tc, const ModP& m)
+{
+    constexpr int M = 1 << LOGM, CH = 8;
+    const uint2* t = tc + threadIdx.x;
+    // the table reads go out CH at a time, the next batch under this batch's
+    // products (all M at once cost 2M registers and half the occupancy)
+    uint2 T[2][CH];
 #pragma unroll
-    for (int k1 = 0; k1 < M; ++k1) {
-        uint32_t& v = x[brev_c(k1, LOGM)];
-        uint32_t& c = cur[k1 % NC];
-        v = montmul(v, c, m.p, m.pinv);
-        if (k1 + NC < M) c = montmul(c, step, m.p, m.pinv);
+    for (int i = 0; i < CH; ++i) T[0][i] = __ldg(t + i * kOuterThreads);
+#pragma unroll
+    for (int c = 0; c < M / CH; ++c) {
+        if (c + 1 < M / CH) {
+#pragma unroll
+            for (int i = 0; i < CH; ++i) T[(c + 1) & 1][i] = __ldg(t + ((c + 1) * CH + i) * kOuterThreads);
+        }
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+            const int r = c * CH + i;
+            const uint2 U = su[r];
+            x[r] = shoup(shoup(x[r], T[c & 1][i].x, T[c & 1][i].y, m.p), U.x, U.y, m.p);
+        }
     }
 }
 
 template <int LOGM, typename T, int QM, bool ZU>
-__global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_constant__ OuterArgs a)
+__global__ void __launch_bounds__(kOuterThreads, (LOGM <= 6 && (sizeof(T) == 4 || ZU)) ? 2 : 1) k_outer_fwd(const __grid_constant__ OuterArgs a)
 {
     constexpr int M = 1 << LOGM;
     constexpr int ROWS = ZU ? M / 2 : M;  // rows that can hold samples (ZU: the upper half is zero)
     constexpr int CH = 16;                // rows loaded ahead per batch
     constexpr int NCH = ROWS < CH ? 1 : ROWS / CH, CW = ROWS < CH ? ROWS : CH;
     __shared__ uint2 stw[M / 2];
+    __shared__ uint2 su[M];
     __shared__ T sthr[kMaxThr];
     const int op = blockIdx.y;
     const int64_t pl = blockIdx.z, pair = a.pair0 + pl;
@@ -1246,11 +1271,12 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
     const int lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < M / 2; i += kOuterThreads) stw[i] = a.rtw[i];
     for (int i = threadIdx.x; i < d.q.tsize; i += kOuterThreads) sthr[i] = (T)d.q.thr[i];
+    const ModP m = a.m;
+    const int Q = 1 << a.lq;
+    column_twiddle_setup<LOGM>(su, a.tl, a.th, blockIdx.x * kOuterThreads, (uint32_t)(((int64_t)M << a.lq) - 1), m);
     __syncthreads();
     const T t0 = sthr[0], t1 = sthr[1], inv_step = (T)d.q.inv_step;
     const int k = d.q.k, tbits = d.q.tbits;
-    const ModP m = a.m;
-    const int Q = 1 << a.lq;
     const int j = blockIdx.x * kOuterThreads + threadIdx.x;
     const int64_t n = d.n;
     // element r*Q + j of the (possibly reversed) row: base pointer + signed
@@ -1314,7 +1340,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
     if constexpr (ZU) dif_cg_zu<LOGM>(x, stw, m);
     else dif_cg<LOGM>(x, stw, m);
     // register r holds frequency k1 = bitrev(r): x omega_P^(j k1) -> row r
-    apply_column_twiddles<LOGM>(x, tw_2level(a.tl, a.th, 0, m), tw_2level(a.tl, a.th, (uint32_t)j, m), m);
+    apply_column_twiddles<LOGM>(x, su, a.tc, m);
     uint32_t* out = a.out + ((int64_t)op * a.batch + pl) * ((int64_t)M << a.lq) + j;  // a.batch: chunk size
 #pragma unroll
     for (int r = 0; r < M; ++r, out += Q) *out = x[r];
@@ -1333,10 +1359,11 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_fwd(const __grid_consta
 }
 
 template <int LOGM, int OUT>
-__global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_constant__ OuterArgs a)
+__global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(const __grid_constant__ OuterArgs a)
 {
     constexpr int M = 1 << LOGM;
     __shared__ uint2 stw[M / 2];
+    __shared__ uint2 su[M];
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
     if (a.pi > 0 && cs) return;
@@ -1348,7 +1375,6 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_consta
     const uint32_t half = (m.p - 1) / 2;
     const int64_t P = (int64_t)M << a.lq;
     const uint32_t pmask = (uint32_t)P - 1;
-    const uint32_t c0 = tw_2level(a.tl, a.th, 0, m);  // M^-1 (Montgomery form)
     // window in t (t = r*Q + j < P <= 2^26 and |value| < 2^29: 32-bit scan)
     const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(a.am.t_hi, P - 1);
     int bv = INT_MIN + 1, bt = INT_MAX, bc = 0;
@@ -1356,6 +1382,10 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_consta
 #pragma unroll 1
     for (int tile = blockIdx.x; tile < Q / kOuterThreads; tile += gridDim.x) {
         const int j = tile * kOuterThreads + threadIdx.x;
+        // U[r] = M^-1 omega_P^(-j0 k1) of this tile (a.tl / a.th: the inverse two-level tables)
+        __syncthreads();
+        column_twiddle_setup<LOGM>(su, a.tl, a.th, tile * kOuterThreads, pmask, m);
+        __syncthreads();
         uint32_t x[M];
         const uint32_t* rin = a.rin + ((int64_t)pl * M * a.np + a.pi) * Q + j;
         const int64_t rstep = (int64_t)a.np * Q;
@@ -1363,7 +1393,7 @@ __global__ void __launch_bounds__(kOuterThreads) k_outer_inv(const __grid_consta
         for (int r = 0; r < M; ++r, rin += rstep) x[r] = __ldg(rin);
         // inner results of sub-transform r are frequency k1 = bitrev(r):
         // x M^-1 omega_P^(-j k1)
-        apply_column_twiddles<LOGM>(x, c0, tw_2level(a.tlf, a.thf, ((uint32_t)P - (uint32_t)j) & pmask, m), m);
+        apply_column_twiddles<LOGM>(x, su, a.tc, m);
         dit_cg<LOGM>(x, stw, m);
         if (!final_out) {
             uint32_t* ro = a.rout + (pl * a.np + a.pi) * P + j;
@@ -1560,7 +1590,8 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
     auto al = [](size_t n) { return (n + 3) & ~(size_t)3; };
     const size_t ng = al(gf.size()) + al(gi.size());  // in uint2 units
     const size_t nr = al(M / 2);                      // uint2 units, each of rf / ri
-    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh) + 4 * nr;
+    const size_t ntc = (size_t)M * kOuterThreads;  // uint2 units, each of tcf / tci
+    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh) + 4 * nr + 4 * ntc;
     std::vector<uint32_t> h(words, 0);
     memcpy(h.data(), gf.data(), gf.size() * 8);
     memcpy(h.data() + 2 * al(gf.size()), gi.data(), gi.size() * 8);
@@ -1587,12 +1618,28 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
         ri[2 * t] = (uint32_t)iv;
         ri[2 * t + 1] = (uint32_t)((iv << 32) / p);
     }
+    // per-thread factors of the column twiddles: omega_P^(+-tid k1), k1 = bitrev(r)
+    uint32_t* tcf = ri + 2 * nr;
+    uint32_t* tci = tcf + 2 * ntc;
+    for (uint64_t r = 0; r < M; ++r) {
+        const uint64_t k1 = bitrev((uint32_t)r, logm);
+        const uint64_t sf = powmod(w, k1, p), si = powmod(wi, k1, p);
+        for (uint64_t t = 0, f = 1, iv = 1; t < (uint64_t)kOuterThreads; ++t, f = mulmod(f, sf, p), iv = mulmod(iv, si, p)) {
+            const size_t o = 2 * (r * kOuterThreads + t);
+            tcf[o] = (uint32_t)f;
+            tcf[o + 1] = (uint32_t)((f << 32) / p);
+            tci[o] = (uint32_t)iv;
+            tci[o + 1] = (uint32_t)((iv << 32) / p);
+        }
+    }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, words * 4);
     if (e != cudaSuccess) return e;
     e = cudaMemcpy(d, h.data(), words * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(d); return e; }
     const uint32_t* dw = reinterpret_cast<const uint32_t*>(d);
+    out->tcf = reinterpret_cast<const uint2*>(dw + (tcf - h.data()));
+    out->tci = reinterpret_cast<const uint2*>(dw + (tci - h.data()));
     out->rf = reinterpret_cast<const uint2*>(dw + (rf - h.data()));
     out->ri = reinterpret_cast<const uint2*>(dw + (ri - h.data()));
     out->gf = reinterpret_cast<const uint2*>(dw);
@@ -1826,6 +1873,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             oa.rtw = O.rf;
             oa.tl = O.tl;
             oa.th = O.th;
+            oa.tc = O.tcf;
             oa.stats = c.stats;
             oa.batch = nb;
             oa.m = T.m;
@@ -1915,6 +1963,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             ob.thf = O.th;
             ob.tl = O.tli;
             ob.th = O.thi;
+            ob.tc = O.tci;
             ob.am = c.am;
             ob.values = c.values;
             ob.nout = c.nout;

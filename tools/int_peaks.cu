@@ -4,7 +4,8 @@
 //   butterfly : the NTT path's lazy DIF butterfly (Shoup multiply, p < 2^30)
 //               on register-resident data, no memory traffic
 //   imad      : dependent-free 32-bit IMAD stream
-//   imad_hi   : IMAD.HI.U32 stream
+//   imad_hi   : IMAD.HI.U32 stream (with addend; r01 had a shift + xor beside it, which
+//               made the loop ALU-bound at 25/clk/SM: the pipe itself does 31/clk/SM)
 //   popc      : POPC + LOP3 (the 1-bit correlation inner op)
 // Output: one JSON object on stdout.  Build: nvcc -gencode
 // arch=compute_100a,code=sm_100a -O3 -o tools/int_peaks tools/int_peaks.cu
@@ -60,7 +61,7 @@ __global__ void k_imadhi(uint32_t* out, uint32_t seed)
     for (int i = 0; i < CH; ++i) a[i] = seed + threadIdx.x * i + 1;
     for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
-        for (int i = 0; i < CH; ++i) a[i] = __umulhi(a[i], 0x9E3779B1u) ^ (a[i] << 1);
+        for (int i = 0; i < CH; ++i) a[i] = __umulhi(a[i], 0x9E3779B1u) + seed;  // one IMAD.HI.U32, nothing else
     }
     uint32_t s = 0;
 #pragma unroll

@@ -312,6 +312,8 @@ struct Pass1Args {
     int op_base;     // operand index of blockIdx.y == 0 (1 when launched per operand)
     int pair_shift;  // statistics record = pair >> pair_shift (inner transforms)
     int64_t pair0;
+    int64_t row0;    // pair index of row 0 of op[].data (inner transforms: the launch group's first
+                     // sub-transform, whose rows start the group-local outer-pass buffer)
 };
 
 template <int LOG1>
@@ -359,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
     if constexpr (QM == QM_K1) { t0 = sthr[0]; t1 = sthr[1]; }
     const T inv_step = (T)d.q.inv_step;
     const int k = d.q.k, tbits = d.q.tbits;
-    const T* src = reinterpret_cast<const T*>(d.data) + pair * d.ld;
+    const T* src = reinterpret_cast<const T*>(d.data) + (pair - a.row0) * d.ld;
     const int64_t n = d.n;
     const bool rev = d.reverse;
     // every element of this tile's loaded rows is in range (no per-element checks)
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_pass1(const __grid_constant__ P
         int bx, by, bz;
         if (next_wave_block(bx, by, bz)) {
             const OperandDesc& dn = a.op[by];
-            const T* sn = reinterpret_cast<const T*>(dn.data) + (a.pair0 + bz) * dn.ld;
+            const T* sn = reinterpret_cast<const T*>(dn.data) + (a.pair0 + bz - a.row0) * dn.ld;
             const int64_t nn = dn.n;
             const int cn = bx * 32;
             if ((int64_t)(rows_loaded - 1) * N2 + cn + 31 < nn) {
@@ -1911,6 +1913,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             a1.skip_cs = pi > 0;
             a1.pair_shift = logm;
             a1.pair0 = p0 * M;
+            a1.row0 = p0 * M;
             if (c.prof) c.prof->pre(KK_PASS1, s);
             e = dispatch_p1(l1, a1, DT_U32, QM_RESIDUE, dim3(N2 / 32, 2, (unsigned)nin), s);
             if (c.prof) c.prof->post(KK_PASS1, s);

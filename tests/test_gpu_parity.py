@@ -821,6 +821,30 @@ def test_large_transform_path(qx, oracle):
         assert res["lag"][0] == -1000
 
 
+def test_large_transform_path_in_chunks(qx, oracle):
+    """P > 2^19 with more pairs than one launch group (chunk_pairs = 1 and 2
+    over a batch of 3): every group's inner passes must read that group's
+    outer-pass rows, and the records must not depend on the grouping."""
+    import torch
+
+    from paper_2509_19974_b200 import _native
+
+    rng = np.random.default_rng(34)
+    nx, ny, q = (1 << 19) + 9, (1 << 19) - 100, qx.uniform(3, 0.5)
+    x = rng.laplace(size=(3, nx)).astype(np.float32)
+    y = np.stack([np.roll(x[b], 100 * (b + 1))[:ny] for b in range(3)]) + rng.normal(0, 0.5, (3, ny)).astype(np.float32)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    whole = qx.estimate_batch(xd, yd, q, q, path="ntt").numpy()
+    for b in range(3):
+        u, v = oracle.quantize(q, x[b]), oracle.quantize(q, y[b])
+        m, f, n = oracle.argmax(oracle.xcorr_ks(u, v, q.k, q.k))
+        assert (whole["value"][b], whole["lag"][b], whole["ties"][b]) == (m, f - (nx - 1), n), b
+    for chunk in (1, 2):
+        with _native.option("chunk_pairs", chunk):
+            part = qx.estimate_batch(xd, yd, q, q, path="ntt").numpy()
+        assert np.array_equal(part, whole), chunk
+
+
 def test_c4_full_size(qx, oracle):
     """BASELINE config 4 at full size (2^24-sample Laplacian pair, 0 dB, 4-bit):
     the GPU finds the planted delay and agrees with the oracle's exact

@@ -1409,16 +1409,17 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
                 if (t < a.nout) a.values[pair * a.vld + t] = (long long)v - (v > half ? (long long)m.p : 0);
             }
         } else {
-            // t increases with r: the first maximum is the smallest index
+            // t increases with r inside a tile, but a thread's next tile starts
+            // below the previous tile's last rows: ties keep the smaller index
 #pragma unroll
             for (int r = 0; r < M; ++r) {
                 const int t = r * Q + j;
                 const uint32_t v = redp(red2p(x[r], m.p2), m.p);
                 const int cv = (int)v - (v > half ? (int)m.p : 0);
                 const int val = (t >= tlo && t <= thi) ? cv : INT_MIN;
-                const bool gt = val > bv;
-                bt = gt ? t : bt;
-                bc = gt ? 1 : bc + (int)(val == bv);
+                const bool gt = val > bv, eq = val == bv;
+                bt = gt ? t : (eq ? min(bt, t) : bt);
+                bc = gt ? 1 : bc + (int)eq;
                 bv = gt ? val : bv;
             }
         }

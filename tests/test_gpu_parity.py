@@ -282,7 +282,7 @@ def test_ntt_argmax_ties_and_windows(qx):
 
     rng = np.random.default_rng(11)
     q = qx.uniform(1, 1.0)
-    for n in (1 << 11, 1 << 14, 3 * 5000, 1 << 18):
+    for n in (1 << 11, 1 << 14, 3 * 5000, 1 << 18, (1 << 19) + 3):  # the last one: large-P outer passes
         B = 6
         x = np.zeros((B, n), np.float32)
         y = np.zeros((B, n), np.float32)
@@ -402,6 +402,40 @@ def test_multiprime_path_saturated(qx, oracle):
     res = qx.estimate_batch(x[None], y[None], q, q).numpy()
     m, f, cnt = oracle.argmax(want)
     assert (res["value"][0], res["lag"][0], res["ties"][0]) == (m, -(n - 1) + f, cnt)
+
+
+def test_launch_groups_mixed_primes(qx, oracle):
+    """A batch split into launch groups (chunk_pairs) where some pairs finish on
+    one prime (Cauchy-Schwarz) and others need the two-prime CRT: records and
+    full correlograms equal the oracle and do not depend on the grouping."""
+    import torch
+
+    from paper_2509_19974_b200 import _native
+    from paper_2509_19974_b200.intxcorr import xcorr_full_device
+
+    rng = np.random.default_rng(10)
+    B, n = 7, 1 << 16
+    x = rng.standard_normal((B, n)).astype(np.float32)
+    y = rng.standard_normal((B, n)).astype(np.float32)
+    for b in (1, 4, 6):  # saturated rows: beyond a single prime's centred range
+        x[b] += 30
+        y[b] += 30
+        y[b, ::97] *= -1
+    q = qx.uniform(127, 0.1)
+    xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    want = []
+    for b in range(B):
+        c = oracle.xcorr_ks(oracle.quantize(q, x[b]), oracle.quantize(q, y[b]), 127, 127)
+        want.append(c)
+    assert max(np.abs(c).max() for c in want) > 600_000_000 > min(np.abs(c).max() for c in want)
+    for chunk in (0, 1, 3):
+        with _native.option("chunk_pairs", chunk):
+            res = qx.estimate_batch(xd, yd, q, q, path="ntt").numpy()
+            vals, _ = xcorr_full_device(xd, yd, q, q)
+        for b in range(B):
+            m, f, cnt = oracle.argmax(want[b])
+            assert (res["value"][b], res["lag"][b], res["ties"][b]) == (m, -(n - 1) + f, cnt), (chunk, b)
+            assert np.array_equal(vals[b].cpu().numpy(), want[b]), (chunk, b)
 
 
 def test_errors_match_reference(qx):

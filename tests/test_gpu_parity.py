@@ -309,6 +309,54 @@ def test_ntt_argmax_ties_and_windows(qx):
                     (m, lo + f, int((c == m).sum())), (n, lo, hi, r)
 
 
+def _sparse_peak(xr, yr, lo, hi):
+    """(max, smallest lag, count) of the correlation of two impulse trains over lags lo..hi"""
+    ix, iy = np.nonzero(xr)[0], np.nonzero(yr)[0]
+    lag = (iy[None, :] - ix[:, None]).ravel()
+    val = (np.rint(xr[ix])[:, None] * np.rint(yr[iy])[None, :]).ravel().astype(np.int64)
+    c = np.zeros(hi - lo + 1, np.int64)
+    keep = (lag >= lo) & (lag <= hi)
+    np.add.at(c, lag[keep] - lo, val[keep])
+    m = int(c.max())
+    return m, lo + int(np.argmax(c)), int((c == m).sum())
+
+
+def test_window_and_template_paths_with_ties(qx):
+    """Tensor-core window path (int8 tiles, extra lags, both tile sizes), the popc
+    path and the blocked template search on impulse trains: small values, so
+    maxima tie across epilogue lanes, tiles, CTAs and blocks; the smallest lag
+    and the tie count must match the sparse sum."""
+    import torch
+
+    rng = np.random.default_rng(12)
+    for k in (1, 7):
+        q = qx.uniform(k, 1.0)
+        for n in (4096, 3001):
+            B = 8
+            x = np.zeros((B, n), np.float32)
+            y = np.zeros((B, n), np.float32)
+            for r in range(B):
+                x[r, rng.choice(n, 4 + 5 * r, replace=False)] = rng.choice([-1.0, 1.0], 4 + 5 * r)
+                y[r, rng.choice(n, 6 + 3 * r, replace=False)] = rng.choice([-1.0, 1.0], 6 + 3 * r)
+            xd, yd = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+            for lo, hi in [(-512, 512), (-2056, 2055), (-5, 3), (100, 100), (-1500, 37), (-(n - 1), -(n - 1) + 900)]:
+                for path in (["direct", "ntt", "popc"] if k == 1 else ["direct", "ntt"]):
+                    res = qx.estimate_batch(xd, yd, q, q, path=path, lag_lo=lo, lag_hi=hi).numpy()
+                    for r in range(B):
+                        assert (int(res["value"][r]), int(res["lag"][r]), int(res["ties"][r])) == \
+                            _sparse_peak(x[r], y[r], lo, hi), (k, n, lo, hi, path, r)
+    # template search: impulse template against an impulse stream, several blocks,
+    # some of them without a single non-zero stream sample
+    for k, nt, ns in [(1, 4096, 4096 + 5 * 8192 + 77), (1, 4096, 60000), (7, 4096, 50000), (1, 1000, 30000)]:
+        q = qx.uniform(k, 1.0)
+        tpl = np.zeros(nt, np.float32)
+        st = np.zeros(ns, np.float32)
+        tpl[rng.choice(nt, 9, replace=False)] = rng.choice([-1.0, 1.0], 9)
+        st[rng.choice(ns // 2, 40, replace=False)] = rng.choice([-1.0, 1.0], 40)  # second half silent
+        got = qx.template_search(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q)
+        assert got == _sparse_peak(tpl, st, 0, ns - nt), (k, nt, ns)
+
+
 def test_popc_path_against_oracle(qx, oracle):
     """Word-parallel 1-level path (path="popc", and what "auto" picks for
     C1-sized pairs): sign / uniform(1) / custom k=1 codes, with and without

@@ -927,6 +927,46 @@ def test_large_transform_path_in_chunks(qx, oracle):
         assert np.array_equal(part, whole), chunk
 
 
+def test_large_transform_dtypes_quantizers_and_layouts(qx):
+    """Large-P path over float32/float64 rows, the three quantiser modes (k = 1,
+    uniform, custom thresholds), operands longer than P/2 (no zero-upper
+    specialisation), padded row strides and a row shared by every pair
+    (ld = 0), on impulse trains with the sparse sum as the expected answer."""
+    import torch
+
+    rng = np.random.default_rng(13)
+    quants = [qx.uniform(1, 1.0), qx.uniform(3, 1.0), qx.custom([-2.5, -1.5, -0.5, 0.5, 1.5, 2.5])]
+    for dt in (np.float32, np.float64):
+        for nx, ny in [((1 << 19) + 3, (1 << 19) - 50), (700_000, 300_000), (300_001, 745_000)]:
+            B, pad = 3, 17
+            xb = np.zeros((B, nx + pad), dt)
+            yb = np.zeros((B, ny + pad), dt)
+            for r in range(B):
+                xb[r, rng.choice(nx, 5 + r, replace=False)] = rng.choice([-3.0, -1.0, 1.0, 2.0], 5 + r)
+                yb[r, rng.choice(ny, 4 + r, replace=False)] = rng.choice([-2.0, -1.0, 1.0, 3.0], 4 + r)
+            xb[:, nx:] = 9.0  # the row padding must never be read
+            yb[:, ny:] = 9.0
+            xd, yd = torch.from_numpy(xb).cuda()[:, :nx], torch.from_numpy(yb).cuda()[:, :ny]  # ld = n + pad
+            for q in quants:
+                k = q.k
+                res = qx.estimate_batch(xd, yd, q, q, path="ntt").numpy()
+                lo, hi = -(nx - 1) + 1000, ny - 1 - 7
+                win = qx.estimate_batch(xd, yd, q, q, path="ntt", lag_lo=lo, lag_hi=hi).numpy()
+                for r in range(B):
+                    cx, cy = np.clip(xb[r, :nx], -k, k), np.clip(yb[r, :ny], -k, k)
+                    assert (int(res["value"][r]), int(res["lag"][r]), int(res["ties"][r])) == \
+                        _sparse_peak(cx, cy, -(nx - 1), ny - 1), (dt, nx, ny, k, r)
+                    assert (int(win["value"][r]), int(win["lag"][r]), int(win["ties"][r])) == \
+                        _sparse_peak(cx, cy, lo, hi), (dt, nx, ny, k, r, "window")
+            # one x row for every pair
+            q = quants[1]
+            shared = qx.estimate_batch(xd[:1].expand(B, nx), yd, q, q, path="ntt").numpy()
+            for r in range(B):
+                cx, cy = np.clip(xb[0, :nx], -3, 3), np.clip(yb[r, :ny], -3, 3)
+                assert (int(shared["value"][r]), int(shared["lag"][r]), int(shared["ties"][r])) == \
+                    _sparse_peak(cx, cy, -(nx - 1), ny - 1), (dt, nx, ny, r, "shared row")
+
+
 def test_c4_full_size(qx, oracle):
     """BASELINE config 4 at full size (2^24-sample Laplacian pair, 0 dB, 4-bit):
     the GPU finds the planted delay and agrees with the oracle's exact

@@ -355,6 +355,10 @@ def test_window_and_template_paths_with_ties(qx):
         st[rng.choice(ns // 2, 40, replace=False)] = rng.choice([-1.0, 1.0], 40)  # second half silent
         got = qx.template_search(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q)
         assert got == _sparse_peak(tpl, st, 0, ns - nt), (k, nt, ns)
+        for block in (5000, 1 << 14):  # NTT blocks: ties across block summaries
+            got = qx.template_search(torch.from_numpy(tpl).cuda(), torch.from_numpy(st).cuda(), q, q, block=block,
+                                     path="ntt")
+            assert got == _sparse_peak(tpl, st, 0, ns - nt), (k, nt, ns, block)
 
 
 def test_popc_path_against_oracle(qx, oracle):
@@ -965,6 +969,29 @@ def test_large_transform_dtypes_quantizers_and_layouts(qx):
                 cx, cy = np.clip(xb[0, :nx], -3, 3), np.clip(yb[r, :ny], -3, 3)
                 assert (int(shared["value"][r]), int(shared["lag"][r]), int(shared["ties"][r])) == \
                     _sparse_peak(cx, cy, -(nx - 1), ny - 1), (dt, nx, ny, r, "shared row")
+
+
+def test_large_transform_statuses_in_a_batch(qx):
+    """Per-pair statuses on the large-P path: an all-zero row (degenerate) and a
+    NaN row beside healthy pairs keep their own records."""
+    import torch
+
+    rng = np.random.default_rng(14)
+    n = (1 << 19) + 40
+    x = np.zeros((4, n), np.float32)
+    y = np.zeros((4, n), np.float32)
+    for r in range(4):
+        x[r, rng.choice(n, 6, replace=False)] = 1.0
+        y[r, rng.choice(n, 6, replace=False)] = 1.0
+    x[1] = 0.0          # quantises to all zeros
+    y[2, 12345] = np.nan
+    q = qx.uniform(1, 1.0)
+    res = qx.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), q, q, path="ntt").numpy()
+    assert res["status"][1] == 2 and res["status"][2] == 9, res["status"]
+    for r in (0, 3):
+        assert res["status"][r] == 0
+        assert (int(res["value"][r]), int(res["lag"][r]), int(res["ties"][r])) == \
+            _sparse_peak(x[r], y[r], -(n - 1), n - 1), r
 
 
 def test_c4_full_size(qx, oracle):

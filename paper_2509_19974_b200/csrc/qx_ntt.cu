@@ -1379,7 +1379,13 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
     const uint32_t pmask = (uint32_t)P - 1;
     // window in t (t = r*Q + j < P <= 2^26 and |value| < 2^29: 32-bit scan)
     const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(a.am.t_hi, P - 1);
-    int bv = INT_MIN + 1, bt = INT_MAX, bc = 0;
+    // Fused argmax as in k_pass3: + half at the column's DC input makes every
+    // output c + half, whose canonical residue is a monotone key of c; the warp
+    // shares one running best key wm, kept as key + 1 (0: nothing in the window
+    // yet); bc / bt are this lane's count and smallest index at wm.
+    const uint32_t bias = (OUT == OUT_ARGMAX && final_out) ? half : 0u;
+    uint32_t wm = 0;
+    int bt = INT_MAX, bc = 0;
     // column tiles strided over the (<= kMaxPartialsLarge) CTAs of this pair
 #pragma unroll 1
     for (int tile = blockIdx.x; tile < Q / kOuterThreads; tile += gridDim.x) {
@@ -1396,6 +1402,7 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
         // inner results of sub-transform r are frequency k1 = bitrev(r):
         // x M^-1 omega_P^(-j k1)
         apply_column_twiddles<LOGM>(x, su, a.tc, m);
+        x[0] += bias;  // register 0 is frequency 0 (inputs stay below 4p: < 2p + p/2)
         dit_cg<LOGM>(x, stw, m);
         if (!final_out) {
             uint32_t* ro = a.rout + (pl * a.np + a.pi) * P + j;
@@ -1409,24 +1416,50 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
                 if (t < a.nout) a.values[pair * a.vld + t] = (long long)v - (v > half ? (long long)m.p : 0);
             }
         } else {
-            // t increases with r inside a tile, but a thread's next tile starts
-            // below the previous tile's last rows: ties keep the smaller index
+            // a tile inside the window holds plain keys (off = 1 maps them to the
+            // key + 1 scale of wm); a tile on a window edge holds key + 1 with 0 for
+            // out-of-window elements, which never equal a scan target >= 1
+            const int jmin = tile * kOuterThreads;
+            const bool inside = tlo <= jmin && thi >= (M - 1) * Q + jmin + kOuterThreads - 1;
+            const uint32_t off = inside ? 1u : 0u;
 #pragma unroll
-            for (int r = 0; r < M; ++r) {
-                const int t = r * Q + j;
-                const uint32_t v = redp(red2p(x[r], m.p2), m.p);
-                const int cv = (int)v - (v > half ? (int)m.p : 0);
-                const int val = (t >= tlo && t <= thi) ? cv : INT_MIN;
-                const bool gt = val > bv, eq = val == bv;
-                bt = gt ? t : (eq ? min(bt, t) : bt);
-                bc = gt ? 1 : bc + (int)eq;
-                bv = gt ? val : bv;
+            for (int r = 0; r < M; ++r) x[r] = redp(red2p(x[r], m.p2), m.p);
+            if (!inside) {
+#pragma unroll
+                for (int r = 0; r < M; ++r) {
+                    const int t = r * Q + j;
+                    x[r] = (t < tlo || t > thi) ? 0u : x[r] + 1u;
+                }
+            }
+            uint32_t mx = x[0];
+#pragma unroll
+            for (int r = 1; r + 1 < M; r += 2) mx = __vimax3_u32(mx, x[r], x[r + 1]);
+            mx = max(mx, x[M - 1]);
+            const uint32_t mu = mx + off;
+            if (__any_sync(0xffffffffu, mu >= wm && mu > 0u)) {
+                const uint32_t wn = __reduce_max_sync(0xffffffffu, mu);
+                if (wn > wm) {
+                    wm = wn;
+                    bc = 0;
+                    bt = INT_MAX;
+                }
+                // t increases with r inside a tile; across a thread's tiles it does not
+                const uint32_t target = wm - off;
+                int rb = M;
+#pragma unroll
+                for (int r = M - 1; r >= 0; --r) {
+                    if (x[r] == target && (inside || target > 0u)) {
+                        ++bc;
+                        rb = r;
+                    }
+                }
+                if (rb < M) bt = min(bt, rb * Q + j);
             }
         }
     }
     if constexpr (OUT == OUT_ARGMAX) {
         if (final_out) {
-            const Best b = bc ? Best{bv, bt, bc} : best_init();
+            const Best b = bc ? Best{(long long)(wm - 1u) - (long long)half, bt, bc} : best_init();
             argmax_finish<kWarps>(b, a.am, a.stats, pair, gridDim.x, blockIdx.x);
         }
     }

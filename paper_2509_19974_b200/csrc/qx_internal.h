@@ -92,6 +92,8 @@ struct OuterTables {
     const uint2* ri;      // omega_M^-t (Shoup pairs), t < M/2: register-resident outer DIT
     const uint2* tcf;     // omega_P^(+tid * bitrev(r)) [r][tid], tid < 256 (Shoup pairs): per-thread factor
     const uint2* tci;     // omega_P^(-tid * bitrev(r)) [r][tid]   of the outer four-step twiddles
+    const uint2* ucf;     // per-tile factor omega_P^(+256 tile * bitrev(r)) [tile][r] (Shoup pairs)
+    const uint2* uci;     // per-tile factor M^-1 omega_P^(-256 tile * bitrev(r)) [tile][r]
 };
 
 // Tuning / measurement knobs of a context: the QX_* environment variables

@@ -1028,6 +1028,7 @@ struct OuterArgs {
     const uint32_t* tlf;     // inverse: the forward two-level tables (omega_P^-j = omega_P^(P-j))
     const uint32_t* thf;
     const uint2* tc;         // per-thread factor of the column twiddles [r][tid] (OuterTables::tcf / tci)
+    const uint2* uc;         // per-tile factor [tile][r] (OuterTables::ucf / uci)
     unsigned long long* stats;
     ArgmaxOut am;
     int64_t* values;
@@ -1207,29 +1208,12 @@ constexpr int brev_c(int r, int bits)
 }
 
 // Column j's four-step twiddles omega_P^(+-j k1), k1 = bitrev(r), r = 0..M-1.
-// With j = j0 + tid (j0 the tile's first column, a multiple of the CTA size)
-// the twiddle is U[r] * T[r][tid]: U[r] = omega_P^(+-j0 k1) (times M^-1 on the
-// inverse) is one Shoup pair per register, computed by M threads of the CTA
-// into shared memory; T is a fixed M x 256 table of Shoup pairs (128 KB at
-// M = 64, L1/L2 resident, read coalesced).  Two Shoup products per element
-// (2 IMAD.HI) replace the running Montgomery product's two general products
-// (4 IMAD.HI): the outer kernels are bound by the heavy FMA sub-pipe, where
-// IMAD.HI costs two issue slots.
-template <int LOGM>
-__device__ __forceinline__ void column_twiddle_setup(uint2* su, const uint32_t* __restrict__ tl,
-                                                     const uint32_t* __restrict__ th, uint32_t j0, uint32_t pmask,
-                                                     const ModP& m)
-{
-    constexpr int M = 1 << LOGM;
-    if (threadIdx.x < M) {
-        const uint32_t k1 = __brev(threadIdx.x) >> (32 - LOGM);
-        const uint32_t e = (uint32_t)(((uint64_t)j0 * k1) & pmask);
-        // the two-level tables hold Montgomery forms: x R^-1 gives the plain residue
-        const uint32_t w = redp(montmul(tw_2level(tl, th, e, m), 1u, m.p, m.pinv), m.p);
-        su[threadIdx.x] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / m.p));
-    }
-}
-
+// With j = j0 + tid (j0 = 256 tile, the tile's first column) the twiddle is
+// U[tile][r] * T[r][tid]: two host-built tables of Shoup pairs.  U (times M^-1
+// on the inverse; 1 MB at Q = 2^19, M = 64) is copied to shared memory per
+// tile, T is a fixed M x 256 table (128 KB at M = 64, L1/L2 resident, read
+// coalesced).  Two Shoup products per element (2 IMAD.HI) replace the running
+// Montgomery product's two general products (4 IMAD.HI).
 template <int LOGM>
 __device__ __forceinline__ void apply_column_twiddles(uint32_t (&x)[1 << LOGM], const uint2* su,
                                                       const uint2* __restrict__ tc, const ModP& m)
@@ -1275,7 +1259,7 @@ __global__ void __launch_bounds__(kOuterThreads, (LOGM <= 6 && (sizeof(T) == 4 |
     for (int i = threadIdx.x; i < d.q.tsize; i += kOuterThreads) sthr[i] = (T)d.q.thr[i];
     const ModP m = a.m;
     const int Q = 1 << a.lq;
-    column_twiddle_setup<LOGM>(su, a.tl, a.th, blockIdx.x * kOuterThreads, (uint32_t)(((int64_t)M << a.lq) - 1), m);
+    if (threadIdx.x < M) su[threadIdx.x] = __ldg(&a.uc[(int64_t)blockIdx.x * M + threadIdx.x]);
     __syncthreads();
     const T t0 = sthr[0], t1 = sthr[1], inv_step = (T)d.q.inv_step;
     const int k = d.q.k, tbits = d.q.tbits;
@@ -1365,18 +1349,19 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
 {
     constexpr int M = 1 << LOGM;
     __shared__ uint2 stw[M / 2];
-    __shared__ uint2 su[M];
+    __shared__ uint2 su[2][M];  // this tile's U and the next one's (copied a tile ahead)
     const int64_t pl = blockIdx.y, pair = a.pair0 + pl;
     const bool cs = (a.np > 1) && cs_single(a.stats, pair, a.p0);
     if (a.pi > 0 && cs) return;
     const bool final_out = (a.np == 1) || cs;
     for (int i = threadIdx.x; i < M / 2; i += kOuterThreads) stw[i] = a.rtw[i];
-    __syncthreads();
+    if (threadIdx.x < M && (int)blockIdx.x < (1 << a.lq) / kOuterThreads)
+        su[0][threadIdx.x] = __ldg(&a.uc[(int64_t)blockIdx.x * M + threadIdx.x]);
+    int cur = 0;
     const int Q = 1 << a.lq;
     const ModP m = a.m;
     const uint32_t half = (m.p - 1) / 2;
     const int64_t P = (int64_t)M << a.lq;
-    const uint32_t pmask = (uint32_t)P - 1;
     // window in t (t = r*Q + j < P <= 2^26 and |value| < 2^29: 32-bit scan)
     const int tlo = (int)max(a.am.t_lo, (int64_t)0), thi = (int)min(a.am.t_hi, P - 1);
     // Fused argmax as in k_pass3: + half at the column's DC input makes every
@@ -1390,10 +1375,12 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
 #pragma unroll 1
     for (int tile = blockIdx.x; tile < Q / kOuterThreads; tile += gridDim.x) {
         const int j = tile * kOuterThreads + threadIdx.x;
-        // U[r] = M^-1 omega_P^(-j0 k1) of this tile (a.tl / a.th: the inverse two-level tables)
+        // one barrier per tile: su[cur] (and stw) are visible, and every warp is
+        // done with su[cur ^ 1], which now takes the next tile's U
         __syncthreads();
-        column_twiddle_setup<LOGM>(su, a.tl, a.th, tile * kOuterThreads, pmask, m);
-        __syncthreads();
+        const int nxt = tile + gridDim.x;
+        if (threadIdx.x < M && nxt < Q / kOuterThreads)
+            su[cur ^ 1][threadIdx.x] = __ldg(&a.uc[(int64_t)nxt * M + threadIdx.x]);
         uint32_t x[M];
         const uint32_t* rin = a.rin + ((int64_t)pl * M * a.np + a.pi) * Q + j;
         const int64_t rstep = (int64_t)a.np * Q;
@@ -1401,7 +1388,8 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
         for (int r = 0; r < M; ++r, rin += rstep) x[r] = __ldg(rin);
         // inner results of sub-transform r are frequency k1 = bitrev(r):
         // x M^-1 omega_P^(-j k1)
-        apply_column_twiddles<LOGM>(x, su, a.tc, m);
+        apply_column_twiddles<LOGM>(x, su[cur], a.tc, m);
+        cur ^= 1;
         x[0] += bias;  // register 0 is frequency 0 (inputs stay below 4p: < 2p + p/2)
         dit_cg<LOGM>(x, stw, m);
         if (!final_out) {
@@ -1627,7 +1615,9 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
     const size_t ng = al(gf.size()) + al(gi.size());  // in uint2 units
     const size_t nr = al(M / 2);                      // uint2 units, each of rf / ri
     const size_t ntc = (size_t)M * kOuterThreads;  // uint2 units, each of tcf / tci
-    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh) + 4 * nr + 4 * ntc;
+    const size_t ntile = (size_t)(Q / kOuterThreads > 0 ? Q / kOuterThreads : 1);
+    const size_t nuc = ntile * M;                  // uint2 units, each of ucf / uci
+    const size_t words = 2 * ng + 2 * al(nl) + 2 * al(nh) + 4 * nr + 4 * ntc + 4 * nuc;
     std::vector<uint32_t> h(words, 0);
     memcpy(h.data(), gf.data(), gf.size() * 8);
     memcpy(h.data() + 2 * al(gf.size()), gi.data(), gi.size() * 8);
@@ -1668,12 +1658,28 @@ cudaError_t ntt_make_outer_tables(uint32_t p, uint32_t g, int lp, int logm, Oute
             tci[o + 1] = (uint32_t)((iv << 32) / p);
         }
     }
+    // per-tile factors: omega_P^(+-256 tile k1), the inverse one times M^-1
+    uint32_t* ucf = tci + 2 * ntc;
+    uint32_t* uci = ucf + 2 * nuc;
+    for (uint64_t r = 0; r < M; ++r) {
+        const uint64_t k1 = bitrev((uint32_t)r, logm);
+        const uint64_t sf = powmod(w, (k1 * kOuterThreads) % P, p), si = powmod(wi, (k1 * kOuterThreads) % P, p);
+        for (uint64_t t = 0, f = 1, iv = invM; t < ntile; ++t, f = mulmod(f, sf, p), iv = mulmod(iv, si, p)) {
+            const size_t o = 2 * (t * M + r);
+            ucf[o] = (uint32_t)f;
+            ucf[o + 1] = (uint32_t)((f << 32) / p);
+            uci[o] = (uint32_t)iv;
+            uci[o + 1] = (uint32_t)((iv << 32) / p);
+        }
+    }
     void* d = nullptr;
     cudaError_t e = cudaMalloc(&d, words * 4);
     if (e != cudaSuccess) return e;
     e = cudaMemcpy(d, h.data(), words * 4, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(d); return e; }
     const uint32_t* dw = reinterpret_cast<const uint32_t*>(d);
+    out->ucf = reinterpret_cast<const uint2*>(dw + (ucf - h.data()));
+    out->uci = reinterpret_cast<const uint2*>(dw + (uci - h.data()));
     out->tcf = reinterpret_cast<const uint2*>(dw + (tcf - h.data()));
     out->tci = reinterpret_cast<const uint2*>(dw + (tci - h.data()));
     out->rf = reinterpret_cast<const uint2*>(dw + (rf - h.data()));
@@ -1910,6 +1916,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             oa.tl = O.tl;
             oa.th = O.th;
             oa.tc = O.tcf;
+            oa.uc = O.ucf;
             oa.stats = c.stats;
             oa.batch = nb;
             oa.m = T.m;
@@ -2001,6 +2008,7 @@ static cudaError_t ntt_run_large(const NttCall& c, cudaStream_t s)
             ob.tl = O.tli;
             ob.th = O.thi;
             ob.tc = O.tci;
+            ob.uc = O.uci;
             ob.am = c.am;
             ob.values = c.values;
             ob.nout = c.nout;

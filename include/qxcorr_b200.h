@@ -127,7 +127,10 @@ const char *qx_context_last_error(const qx_context *ctx);
  * "sweep_restage" (0: the host sweep skips its H2D copies -- compute-only
  * timing), "sweep_compute" (0: it skips its kernels -- copy-only timing),
  * "popc", "popc_timing" (1: the popc correlation kernel prints its phase
- * times), "tc_f4".  QX_ERR_INVALID for an unknown name.
+ * times), "tc_f4", "zero_copy" (0: qx_plan_run_host always stages the rows
+ * on the device; by default rows of at most 1 MiB in pinned host memory are
+ * read in place over PCIe and the records written to a mapped pinned buffer).
+ * QX_ERR_INVALID for an unknown name.
  *
  * Threading and streams: every entry point locks the context, runs on the
  * context's device and restores the caller's current device.  Work enqueued
@@ -194,7 +197,10 @@ qx_status qx_plan_create(qx_context *ctx, const qx_signals *x, const qx_signals 
 qx_status qx_plan_run(qx_plan *plan, const void *x, const void *y, qx_result *results, void *stream);
 /* qx_plan_run from HOST rows and a HOST results array (batch entries): the
  * plan stages the rows' extent into its own device buffer, runs, copies the
- * results back and synchronises (page-locked rows: asynchronous DMA).
+ * results back and synchronises (page-locked rows: asynchronous DMA).  Rows of
+ * at most 1 MiB in page-locked memory are not staged at all: the kernels read
+ * them in place through their device alias and write the records to a mapped
+ * page-locked buffer of the plan (option "zero_copy").
  * Returns the first per-pair error status, as qx_estimate_batch_host. */
 qx_status qx_plan_run_host(qx_plan *plan, const void *x, const void *y, qx_result *results);
 /* the qx_path the plan runs (never QX_PATH_AUTO) */

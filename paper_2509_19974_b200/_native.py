@@ -197,7 +197,7 @@ class option:
     """Context manager: set a context option, restore it on exit."""
 
     DEFAULTS = {"sweep_restage": 1, "sweep_compute": 1, "popc": 1, "popc_timing": 0, "tc_f4": 1, "sweep_lanes": 0,
-                "sweep_chunks": 0, "sweep_taper": 2, "sweep_even": 0, "chunk_pairs": 0}
+                "sweep_chunks": 0, "sweep_taper": 2, "sweep_even": 0, "chunk_pairs": 0, "zero_copy": 1}
 
     def __init__(self, name: str, value: int, device: int | None = None, restore: int | None = None):
         self.name, self.value, self.device = name, value, device

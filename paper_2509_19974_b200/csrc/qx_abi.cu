@@ -120,6 +120,7 @@ static Knobs knobs_from_env()
     k.popc = num("QX_POPC", 1) != 0;
     k.popc_timing = num("QX_POPC_TIMING", 0) != 0;
     k.tc_f4 = num("QX_TC_F4", 1) != 0;
+    k.zero_copy = num("QX_ZERO_COPY", 1) != 0;
     if (const char* ev = getenv("QX_SWEEP_PLAN")) {
         for (const char* p = ev; *p && k.sweep_plan_n < 16;) {
             const int64_t v = atoll(p);
@@ -140,6 +141,7 @@ struct Lane {
     cudaEvent_t done = nullptr;
 };
 constexpr int kMaxLanes = 8;
+constexpr size_t kZeroCopyBytes = 1 << 20;  // qx_plan_run_host reads pinned rows in place up to this size
 
 struct qx_context {
     int device = 0;
@@ -328,6 +330,7 @@ qx_status qx_context_set_option(qx_context* c, const char* name, int64_t value)
     else if (n == "popc") k.popc = value != 0;
     else if (n == "popc_timing") k.popc_timing = value != 0;
     else if (n == "tc_f4") k.tc_f4 = value != 0;
+    else if (n == "zero_copy") k.zero_copy = value != 0;
     else return fail(c, QX_ERR_INVALID, "unknown option " + n);
     return QX_OK;
 }
@@ -828,14 +831,28 @@ struct qx_plan {
     uint64_t gen_s = 0, gen_c = 0;  // arena generations the pointers in pr were derived from
     void* dstage = nullptr;         // qx_plan_run_host: device copies of the rows + results
     size_t dstage_bytes = 0;
+    qx_result* hres = nullptr;      // qx_plan_run_host, zero-copy mode: mapped pinned result records
+    size_t hres_bytes = 0;
     ~qx_plan()
     {
-        if (dstage) {
+        if (dstage || hres) {
             DevGuard dg(ctx->device);
-            cudaFree(dstage);
+            if (dstage) cudaFree(dstage);
+            if (hres) cudaFreeHost(hres);
         }
     }
 };
+
+// device alias of a pinned (page-locked, mapped) host pointer, or null
+static const void* pinned_device_alias(const void* h)
+{
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
 
 static qx_status plan_prepare(qx_plan* p)
 {
@@ -934,6 +951,37 @@ qx_status qx_plan_run_host(qx_plan* p, const void* x, const void* y, qx_result* 
     const size_t xa = (xb + 255) & ~(size_t)255, ya = (yb + 255) & ~(size_t)255;
     const size_t rb = (size_t)batch * sizeof(qx_result);
     cudaError_t e = cudaSuccess;
+    // Small inputs in pinned host memory (latency-bound single pairs, BASELINE
+    // config 1): no staging copies at all.  The kernels read the rows once,
+    // straight over PCIe through the buffers' device aliases, and write the
+    // records into a mapped pinned buffer of the plan: two H2D copies and one
+    // D2H copy (each a driver call and a DMA start) leave the call's latency.
+    if (xb + yb <= kZeroCopyBytes && ctx->knobs.zero_copy) {
+        const void* xd = pinned_device_alias(x);
+        const void* yd = xd ? pinned_device_alias(y) : nullptr;
+        if (xd && yd) {
+            if (p->hres_bytes < rb) {
+                if (p->hres) cudaFreeHost(p->hres);
+                p->hres = nullptr;
+                p->hres_bytes = 0;
+                e = cudaHostAlloc((void**)&p->hres, rb, cudaHostAllocMapped);
+                if (e != cudaSuccess) return cuda_fail(ctx, e, "plan result buffer");
+                p->hres_bytes = rb;
+            }
+            qx_result* hd = nullptr;
+            e = cudaHostGetDevicePointer((void**)&hd, p->hres, 0);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "plan result buffer");
+            cudaStream_t s = ctx->host_stream;
+            qx_status st = qx_plan_run(p, xd, yd, hd, s);
+            if (st != QX_OK) return st;
+            e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "sync");
+            memcpy(results, p->hres, rb);
+            for (int64_t b = 0; b < batch; ++b)
+                if (results[b].status) return (qx_status)results[b].status;
+            return QX_OK;
+        }
+    }
     if (p->dstage_bytes < xa + ya + rb) {
         if (p->dstage) cudaFree(p->dstage);
         p->dstage = nullptr;

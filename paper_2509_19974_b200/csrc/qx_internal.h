@@ -111,6 +111,7 @@ struct Knobs {
     int popc = 1;              // QX_POPC=0: never pick the popc path on AUTO
     int popc_timing = 0;       // QX_POPC_TIMING=1: popc correlation kernel prints its phase times
     int tc_f4 = 1;             // QX_TC_F4=0: no fp4 tensor-core template search
+    int zero_copy = 1;         // QX_ZERO_COPY=0: qx_plan_run_host always stages small pinned rows on the device
     int64_t sweep_plan[16] = {0};  // QX_SWEEP_PLAN="a,b,...": explicit host-sweep chunk sizes
     int sweep_plan_n = 0;
 };

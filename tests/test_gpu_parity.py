@@ -1076,7 +1076,12 @@ def test_estimate_plan_matches_estimate_batch(qx, oracle):
             # the same rows from host memory (qx_plan_run_host), pageable and pinned
             xh, yh = x.cpu().numpy(), y.cpu().numpy()
             assert np.array_equal(plan.run_host(xh, yh), b), (B, nx, ny, it, "host")
+            # pinned rows: read in place over PCIe (zero-copy, the default for small rows), and staged
             xp, yp = x.cpu().pin_memory(), y.cpu().pin_memory()
             assert np.array_equal(plan.run_host(xp.numpy(), yp.numpy()), b), (B, nx, ny, it, "pinned")
+            from paper_2509_19974_b200 import _native
+
+            with _native.option("zero_copy", 0):
+                assert np.array_equal(plan.run_host(xp.numpy(), yp.numpy()), b), (B, nx, ny, it, "pinned, staged")
         with pytest.raises(ValueError):
             plan(x[:, :-1] if nx > 1 else x, y)

@@ -80,8 +80,9 @@ class C1(Workload):
         G.check_c1(int(r["lag"]), int(r["value"]))
 
     def e2e_step(self):
-        # the serving form from host rows: one qx_plan_run_host call per pair (H2D of both rows from
-        # page-locked buffers, the popc launch, D2H of the 64-B result, one synchronisation)
+        # the serving form from host rows: one qx_plan_run_host call per pair (both rows read from
+        # page-locked buffers over PCIe by the popc launch itself, the 64-B result written to a mapped
+        # page-locked buffer, one synchronisation)
         if not hasattr(self, "xh"):
             import torch
             self.xh = torch.from_numpy(self.x).pin_memory().numpy()
@@ -400,12 +401,14 @@ def run(args):
     # e2e: the public host API with host buffers, copies inside the timed region
     e2e = None
     if not args.no_e2e:
-        for _ in range(3):
+        # C1 is one 50-us call per step: warm up past the first calls on fresh page-locked
+        # buffers (slower, as in the C2 line's e2e) and time enough calls for a stable mean
+        for _ in range(60 if wl.name == "c1" else 3):
             wl.e2e_step()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        n_e2e = max(3, min(args.steps, 10)) if wl.name != "c1" else max(3, args.steps)
+        n_e2e = max(3, min(args.steps, 10)) if wl.name != "c1" else max(200, args.steps)
         t0 = time.perf_counter()
         for _ in range(n_e2e):
             wl.e2e_step()
@@ -416,6 +419,10 @@ def run(args):
         hb, db = wl.e2e_bytes()
         e2e = {"value": wl.units * n_e2e / float(dt.item()), "unit": wl.unit, "h2d_bytes_per_step": int(hb),
                "d2h_bytes_per_step": int(db), "steps": n_e2e, "path": "public host API, pinned host buffers"}
+        if wl.name == "c1":
+            e2e["path"] = ("EstimatePlan.run_host (qx_plan_run_host): page-locked rows read in place over PCIe "
+                           "(zero-copy), the record written to a mapped page-locked buffer, one synchronisation")
+            e2e["h2d_bytes_per_step"] = int(hb)  # read by the kernel over PCIe, no staging copy
         if hasattr(wl, "e2e_pageable"):
             # the same estimate from pageable numpy rows (a caller that does not pin)
             for _ in range(3):

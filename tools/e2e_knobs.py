@@ -1,6 +1,9 @@
 """C2 end-to-end (qx_estimate_sweep_host) under the sweep schedule knobs,
 beside the plain pinned-H2D bound of the same bytes.  One process; the knobs
-are read per call.  Usage: python tools/e2e_knobs.py [reps]"""
+are context options (qx_context_set_option), set before each series; explicit
+chunk plans (QX_SWEEP_PLAN) are read at context creation only and need one
+process per plan (PLANS=... runs them through the environment of a fresh
+interpreter).  Usage: python tools/e2e_knobs.py [reps]"""
 import os
 import sys
 import time
@@ -34,11 +37,12 @@ h2d = e0.elapsed_time(e1) / reps
 print(f"pinned H2D {xs.nbytes + ys.nbytes} B: {h2d:.3f} ms ({(xs.nbytes + ys.nbytes) / h2d / 1e6:.1f} GB/s)"
       f" -> bound {est / h2d * 1e3:.0f} est/s")
 
-KNOBS = [{}, {"QX_SWEEP_TAPER": "1"}, {"QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_CHUNKS": "16"},
+KNOBS = [{}, {"QX_SWEEP_TAPER": "1"}, {"QX_SWEEP_TAPER": "4"}, {"QX_SWEEP_TAPER": "8"}, {"QX_SWEEP_CHUNKS": "16"},
+         {"QX_SWEEP_CHUNKS": "12"}, {"QX_SWEEP_CHUNKS": "10"}, {"QX_SWEEP_CHUNKS": "6"},
          {"QX_SWEEP_CHUNKS": "4"}, {"QX_SWEEP_LANES": "2"}, {"QX_SWEEP_EVEN": "1"}]
 PLANS = os.environ.get("PLANS", "4,12,16,16,12,4;4,8,16,16,16,4;2,6,12,16,16,10,2;4,12,24,20,4;"
                        "8,16,16,16,8;4,28,28,4;4,10,16,16,10,6,2;6,12,16,16,10,4").split(";")
-KNOBS += [{"QX_SWEEP_PLAN": p} for p in PLANS] + [{}]
+KNOBS += [{}]
 if os.environ.get("LANES_ONLY"):
     KNOBS = [{}, {"QX_SWEEP_LANES": "5"}, {"QX_SWEEP_LANES": "6"}, {"QX_SWEEP_LANES": "8"},
              {"QX_SWEEP_LANES": "8", "QX_SWEEP_CHUNKS": "16"}, {"QX_SWEEP_LANES": "8", "QX_SWEEP_CHUNKS": "4"},
@@ -52,10 +56,12 @@ if os.environ.get("RESTAGE_ONLY"):
              {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_EVEN": "1"}, {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_CHUNKS": "16"},
              {"QX_SWEEP_RESTAGE": "0", "QX_SWEEP_LANES": "1", "QX_SWEEP_CHUNKS": "1"}, {}]
 for kn in KNOBS:
-    for k in ("QX_SWEEP_TAPER", "QX_SWEEP_CHUNKS", "QX_SWEEP_LANES", "QX_SWEEP_EVEN", "QX_SWEEP_PLAN",
-              "QX_SWEEP_RESTAGE", "QX_SWEEP_COMPUTE"):
-        os.environ.pop(k, None)
-    os.environ.update(kn)
+    from paper_2509_19974_b200 import _native  # noqa: E402
+
+    DEFAULT = {"QX_SWEEP_TAPER": 2, "QX_SWEEP_CHUNKS": 0, "QX_SWEEP_LANES": 0, "QX_SWEEP_EVEN": 0,
+               "QX_SWEEP_RESTAGE": 1, "QX_SWEEP_COMPUTE": 1}
+    for k, v in DEFAULT.items():
+        _native.set_option(k[3:].lower(), int(kn.get(k, v)))
     for _ in range(2):
         P.estimate_sweep_host(hxn, hyn, sweep)
     torch.cuda.synchronize()

@@ -14,7 +14,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2509_19974_b200 as P  # noqa: E402
-from paper_2509_19974_b200 import workloads as W  # noqa: E402
+from paper_2509_19974_b200 import _native, workloads as W  # noqa: E402
 
 xs, ys, lag = W.c2()
 qs = [W.bit_quantizer(b, W.C2_SIGMA) for b in (1, 2, 4, 8)]
@@ -37,8 +37,7 @@ def huge_pinned(a):
 
 
 def time_calls(hx, hy, env, reps=12):
-    os.environ.pop("QX_SWEEP_COMPUTE", None)
-    os.environ.update(env)
+    _native.set_option("sweep_compute", int(env.get("QX_SWEEP_COMPUTE", 1)))
     for _ in range(2):
         P.estimate_sweep_host(hx, hy, sweep)
     ts = []
@@ -46,7 +45,7 @@ def time_calls(hx, hy, env, reps=12):
         t0 = time.perf_counter()
         res = P.estimate_sweep_host(hx, hy, sweep)
         ts.append(time.perf_counter() - t0)
-    os.environ.pop("QX_SWEEP_COMPUTE", None)
+    _native.set_option("sweep_compute", 1)
     if not env:
         for r in res:
             assert np.array_equal(r["lag"], lag)

@@ -6,13 +6,14 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 
 import paper_2509_19974_b200 as P
+from paper_2509_19974_b200 import _native
 from paper_2509_19974_b200 import workloads as W
 
 xs, ys, lag = W.c2()
 xd, yd = torch.from_numpy(xs).cuda(), torch.from_numpy(ys).cuda()
 qs = [W.bit_quantizer(b, W.C2_SIGMA) for b in (1, 2, 4, 8)]
 for chunk in sys.argv[1:]:
-    os.environ["QX_CHUNK_PAIRS"] = chunk
+    _native.set_option("chunk_pairs", int(chunk))  # the knobs are context options, not per-call environment
     for _ in range(3):
         for q in qs:
             P.estimate_batch(xd, yd, q, q)

@@ -18,9 +18,10 @@ for trial in range(int(sys.argv[2]) if len(sys.argv) > 2 else 40):
     qb = qa if rng.random() < 0.5 else quants[int(rng.integers(len(quants)))]
     if (qa.k == 1) != (qb.k == 1) or (qa.kind == "custom") != (qb.kind == "custom"):
         qb = qa
-    for env in ({}, {"QX_TC_T4": "1"}, {"QX_TC_F2": "1"}):
-        for k in ("QX_TC_T4", "QX_TC_F2"): os.environ.pop(k, None)
-        os.environ.update(env)
+    for env in ({}, {"tc_f4": 0}):  # the fp4 tensor-core search, and the int8 / NTT fallbacks
+        from paper_2509_19974_b200 import _native
+
+        _native.set_option("tc_f4", int(env.get("tc_f4", 1)))
         try:
             got = qx.template_search(tpl, st, qa, qb, stream_start=3)
         except Exception as e:

@@ -309,6 +309,39 @@ def test_ntt_argmax_ties_and_windows(qx):
                     (m, lo + f, int((c == m).sum())), (n, lo, hi, r)
 
 
+def test_medium_pairs_against_oracle(qx, oracle):
+    """Seeded sweep over the middle of the NTT size range (P = 2^13 .. 2^19, every
+    four-step shape, operands with and without the zero-upper half), random
+    windows, quantisers and dtypes, against the oracle's Kronecker substitution."""
+    import torch
+
+    rng = np.random.default_rng(21)
+    quants = [qx.sign(), qx.uniform(1, 0.7), qx.uniform(7, 0.3), qx.uniform(127, 0.02),
+              qx.custom([-1.0, -0.2, 0.3, 1.1])]
+    for trial in range(24):
+        lp = 13 + trial % 7
+        tot = int(rng.integers((1 << (lp - 1)) + 2, (1 << lp) + 1))  # nx + ny - 1 in (2^(lp-1), 2^lp]
+        nx = int(rng.integers(max(1, tot // 8), tot - max(1, tot // 8)))
+        ny = tot + 1 - nx
+        dt = np.float32 if trial % 3 else np.float64
+        B = 2
+        x = (rng.standard_normal((B, nx)) * rng.uniform(0.3, 2)).astype(dt)
+        y = (rng.standard_normal((B, ny)) * rng.uniform(0.3, 2)).astype(dt)
+        qa = quants[int(rng.integers(len(quants)))]
+        qb = quants[int(rng.integers(len(quants)))]
+        nout = nx + ny - 1
+        t_lo = int(rng.integers(0, nout)) if trial % 2 else 0
+        t_hi = int(rng.integers(t_lo, nout)) if trial % 2 else nout - 1
+        first = -(nx - 1)
+        res = qx.estimate_batch(torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda(), qa, qb, path="ntt",
+                                lag_lo=first + t_lo, lag_hi=first + t_hi).numpy()
+        for b in range(B):
+            u, v = oracle.quantize(qa, x[b]), oracle.quantize(qb, y[b])
+            c = oracle.xcorr_ks(u, v, qa.k, qb.k)[t_lo:t_hi + 1]
+            m, f, n = oracle.argmax(c)
+            assert (res["value"][b], res["lag"][b], res["ties"][b]) == (m, first + t_lo + f, n), (trial, lp, nx, ny)
+
+
 def _sparse_peak(xr, yr, lo, hi):
     """(max, smallest lag, count) of the correlation of two impulse trains over lags lo..hi"""
     ix, iy = np.nonzero(xr)[0], np.nonzero(yr)[0]

@@ -10,8 +10,10 @@
 // r = a*w - q*p + p lies in (0.49p, 1.51p).
 // Measures, on register-resident data: IMAD, IMAD.HI (with addend, nothing
 // else in the loop), IMAD.WIDE, DFMA, DFMA and IMAD interleaved, the Shoup
-// butterfly and the two DFMA butterflies; checks the DFMA product against
-// the exact residue on random inputs.  Output: one JSON object.
+// butterfly, the two DFMA butterflies and mixed loops in which every 3rd /
+// 4th / 8th / 16th butterfly takes its quotient from the FP64 pipe; checks
+// the DFMA product against the exact residue for every 32-bit input and eight
+// twiddles.  Output: one JSON object.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -59,12 +61,12 @@ __global__ void k_bfly(uint32_t* out, uint32_t seed, uint2 w, TwD t)
     for (int it = 0; it < ITERS; ++it) {
 #pragma unroll
         for (int i = 0; i < CH; ++i) {
-            if (MODE == 0) bfly_dif(a[i], b[i], w, m);
+            if (MODE == 0 || (MODE >= 3 && (i % MODE) != 0)) bfly_dif(a[i], b[i], w, m);
             else {
                 const uint32_t s = a[i] + b[i] + m.zero;
                 const uint32_t d = a[i] - b[i] + m.p2;
                 a[i] = red2p(s, m.p2);
-                b[i] = MODE == 1 ? mul_dfma1(d, t, m.p, np) : mul_dfma2(d, t, m.p, np);
+                b[i] = MODE != 2 ? mul_dfma1(d, t, m.p, np) : mul_dfma2(d, t, m.p, np);
             }
         }
     }
@@ -168,6 +170,11 @@ int main()
     const double b0 = time_kernel([&] { k_bfly<0><<<blocks, threads>>>(out, 3, w, t); }, 5);
     const double b1 = time_kernel([&] { k_bfly<1><<<blocks, threads>>>(out, 3, w, t); }, 5);
     const double b2 = time_kernel([&] { k_bfly<2><<<blocks, threads>>>(out, 3, w, t); }, 5);
+    // mixed loops: every MODE-th butterfly takes its quotient from the FP64 pipe
+    const double b3 = time_kernel([&] { k_bfly<3><<<blocks, threads>>>(out, 3, w, t); }, 5);
+    const double b4 = time_kernel([&] { k_bfly<4><<<blocks, threads>>>(out, 3, w, t); }, 5);
+    const double b8 = time_kernel([&] { k_bfly<8><<<blocks, threads>>>(out, 3, w, t); }, 5);
+    const double bh = time_kernel([&] { k_bfly<16><<<blocks, threads>>>(out, 3, w, t); }, 5);
     double s[5];
     s[0] = time_kernel([&] { k_stream<0><<<blocks, threads>>>(out, 3, 0.999); }, 5);
     s[1] = time_kernel([&] { k_stream<1><<<blocks, threads>>>(out, 3, 0.999); }, 5);
@@ -175,9 +182,11 @@ int main()
     s[3] = time_kernel([&] { k_stream<3><<<blocks, threads>>>(out, 3, 0.999); }, 5);
     s[4] = time_kernel([&] { k_stream<4><<<blocks, threads>>>(out, 3, 0.999); }, 5);
     printf("{\"sms\": %d, \"clock_khz\": %d, \"dfma_check_bad\": %llu, \"bfly_shoup_per_s\": %.6e, "
-           "\"bfly_dfma1_per_s\": %.6e, \"bfly_dfma2_per_s\": %.6e, \"imad_per_s\": %.6e, \"imad_hi_per_s\": %.6e, "
+           "\"bfly_dfma1_per_s\": %.6e, \"bfly_dfma2_per_s\": %.6e, \"bfly_mixed_1of3_per_s\": %.6e, "
+           "\"bfly_mixed_1of4_per_s\": %.6e, \"bfly_mixed_1of8_per_s\": %.6e, \"bfly_mixed_1of16_per_s\": %.6e, "
+           "\"imad_per_s\": %.6e, \"imad_hi_per_s\": %.6e, "
            "\"imad_wide_per_s\": %.6e, \"dfma_per_s\": %.6e, \"dfma_plus_imad_pairs_per_s\": %.6e, \"err\": \"%s\"}\n",
-           sms, clk, hbad, per / b0, per / b1, per / b2, per / s[0], per / s[1], per / s[2], per / s[3], per / s[4],
+           sms, clk, hbad, per / b0, per / b1, per / b2, per / b3, per / b4, per / b8, per / bh, per / s[0], per / s[1], per / s[2], per / s[3], per / s[4],
            cudaGetErrorString(cudaGetLastError()));
     return 0;
 }

@@ -1,5 +1,10 @@
-import sys, time
-sys.path.insert(0, "/root/repo")
+"""qx_plan_run_host per-call time on BASELINE config 1 from page-locked rows: read in place over
+PCIe (zero_copy = 1, the default) against staged on the device (zero_copy = 0)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import paper_2509_19974_b200 as P
 from paper_2509_19974_b200 import _native, workloads as W

@@ -1384,6 +1384,11 @@ __global__ void __launch_bounds__(kOuterThreads, LOGM <= 6 ? 2 : 1) k_outer_inv(
         uint32_t x[M];
         const uint32_t* rin = a.rin + ((int64_t)pl * M * a.np + a.pi) * Q + j;
         const int64_t rstep = (int64_t)a.np * Q;
+        if (nxt < Q / kOuterThreads) {
+            // the next tile's rows (this warp's 128-byte segment of each) into L2 under this tile's work
+            const uint32_t* pn = rin - (threadIdx.x & 31) + (int64_t)gridDim.x * kOuterThreads;
+            for (int r = threadIdx.x & 31; r < M; r += 32) prefetch_l2(pn + r * rstep);
+        }
 #pragma unroll
         for (int r = 0; r < M; ++r, rin += rstep) x[r] = __ldg(rin);
         // inner results of sub-transform r are frequency k1 = bitrev(r):

@@ -342,6 +342,31 @@ def test_medium_pairs_against_oracle(qx, oracle):
             assert (res["value"][b], res["lag"][b], res["ties"][b]) == (m, first + t_lo + f, n), (trial, lp, nx, ny)
 
 
+def test_row_layouts_agree_on_every_path(qx):
+    """Rows that overlap (stride < length), are padded (stride > length) or are
+    one shared row (stride 0) give the records of their contiguous copies, on
+    the NTT, tensor-core window and popc paths (float32 and float64)."""
+    import torch
+
+    rng = np.random.default_rng(15)
+    for dt in (torch.float32, torch.float64):
+        for path, n, win, q in [("ntt", 5000, (None, None), qx.uniform(7, 0.3)),
+                                ("ntt", 70000, (-300, 9000), qx.uniform(1, 0.6)),
+                                ("direct", 4096, (-512, 512), qx.uniform(7, 0.3)),
+                                ("direct", 3000, (-40, 1999), qx.sign()),
+                                ("popc", 6000, (None, None), qx.sign())]:
+            B = 5
+            base_x = torch.from_numpy(rng.standard_normal(n * (B + 2))).to(dt).cuda()
+            base_y = torch.from_numpy(rng.standard_normal(n * (B + 2))).to(dt).cuda()
+            for ld in (n // 3, n + 13, 0):
+                x = base_x.as_strided((B, n), (ld, 1))
+                y = base_y.as_strided((B, n), (ld if ld else n, 1))  # y keeps distinct rows when x is shared
+                got = qx.estimate_batch(x, y, q, q, path=path, lag_lo=win[0], lag_hi=win[1]).numpy()
+                want = qx.estimate_batch(x.contiguous(), y.contiguous(), q, q, path=path, lag_lo=win[0],
+                                         lag_hi=win[1]).numpy()
+                assert np.array_equal(got, want), (dt, path, n, ld)
+
+
 def _sparse_peak(xr, yr, lo, hi):
     """(max, smallest lag, count) of the correlation of two impulse trains over lags lo..hi"""
     ix, iy = np.nonzero(xr)[0], np.nonzero(yr)[0]

@@ -367,6 +367,29 @@ def test_row_layouts_agree_on_every_path(qx):
                 assert np.array_equal(got, want), (dt, path, n, ld)
 
 
+def test_signal_starts_shift_lags_on_every_path(qx):
+    """Signal.start offsets only translate the lag axis (first_lag = y.start -
+    (x.start + N_x - 1), intxcorr.py:85-86): a call with starts and a window
+    equals the zero-start call on the translated window, lags shifted back."""
+    import torch
+
+    rng = np.random.default_rng(16)
+    for path, n, q in [("ntt", 9000, qx.uniform(7, 0.3)), ("direct", 4096, qx.uniform(1, 0.6)),
+                       ("popc", 5000, qx.sign()), ("ntt", (1 << 19) + 5, qx.uniform(1, 0.6))]:
+        x = torch.from_numpy(rng.standard_normal((3, n)).astype(np.float32)).cuda()
+        y = torch.from_numpy(rng.standard_normal((3, n)).astype(np.float32)).cuda()
+        for sx, sy in [(0, 0), (17, -250), (-100000, 3), (5, 5)]:
+            d = sy - sx
+            for lo, hi in [(-700, 600), (d - 3, d + 3), (-(n - 1) + d, -(n - 1) + d + 1000)]:
+                if lo - d < -(n - 1) or hi - d > n - 1:
+                    continue
+                a = qx.estimate_batch(x, y, q, q, path=path, x_start=sx, y_start=sy, lag_lo=lo, lag_hi=hi).numpy()
+                b = qx.estimate_batch(x, y, q, q, path=path, lag_lo=lo - d, lag_hi=hi - d).numpy()
+                assert np.array_equal(a["lag"], b["lag"] + d), (path, n, sx, sy, lo, hi)
+                for f in ("value", "ties", "sumsq_x", "sumsq_y", "status"):
+                    assert np.array_equal(a[f], b[f]), (path, n, sx, sy, lo, hi, f)
+
+
 def _sparse_peak(xr, yr, lo, hi):
     """(max, smallest lag, count) of the correlation of two impulse trains over lags lo..hi"""
     ix, iy = np.nonzero(xr)[0], np.nonzero(yr)[0]
